@@ -1,0 +1,168 @@
+/* fastvol_b200.h -- C ABI of the B200 batched pricing / Greeks / implied-vol
+ * library (libfastvol_b200.so, built from paper_2604_27210_b200/csrc).
+ *
+ * Drop-in boundary for the reference's batch engine (fastvol 0.1.0,
+ * /root/reference/pkg/src/fastvol/batch.py).  Each entry point replaces one
+ * `fill(start, stop)` loop + `_run_chunked(fill, n)` pair of the reference;
+ * the SPEC's intended binding shape (bind_batch_price,
+ * bind_batch_iv(model, method, buffers) -> (iv, status), bind_all_greeks ->
+ * five buffers) maps onto:
+ *
+ *   fv_batch_price   <- batch.py:181-203  batch_price   (fill :195-198)
+ *   fv_batch_iv      <- batch.py:206-247  batch_iv      (fill :223-241)
+ *   fv_batch_greeks  <- batch.py:250-280  batch_greeks  (fill :263-274)
+ *   fv_price_greeks  <- batch_price + batch_greeks on the same columns, one
+ *                       fused pass (shared d1/d2/Phi/phi), two error records
+ *
+ * Columns are structure-of-arrays: a column is a pointer
+ * plus an element stride; stride 0 broadcasts element 0 (the reference's
+ * length-1 columns, batch.py:91-101).  Flags are int8 +1 (call) / -1 (put)
+ * (the result of batch.py:parse_flags).  All pointers of one call live in the
+ * same memory space: either all device memory (kernels run in place on the
+ * current device, on the stream set by fv_set_stream) or all host memory
+ * (pinned or pageable; the library pipelines H2D / kernel / D2H in chunks).
+ *
+ * Semantics are the reference's, bit for bit:
+ *   - validation (batch.py:104-124, :144-147): the first failing check in the
+ *     reference's order, at its lowest row, is reported as FV_ERR_BATCH with
+ *     fv_error.kind / index / column (BatchError(kind, index, detail));
+ *   - per-row numeric failures stay in-band: NaN + status code;
+ *   - a row whose reference execution raises a Python exception (e.g.
+ *     OverflowError from math.exp) aborts the batch: FV_ERR_PYEXC with the
+ *     lowest such row in fv_error.index and the exception in fv_error.kind.
+ * Reentrant; no global mutable state besides the per-thread stream setting
+ * and a per-device workspace cache (mutex-protected).
+ */
+#ifndef FASTVOL_B200_H
+#define FASTVOL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FV_API __attribute__((visibility("default")))
+
+/* models (fastvol/models.py:27-48) */
+#define FV_MODEL_BLACK76 0
+#define FV_MODEL_BLACK_SCHOLES 1
+#define FV_MODEL_BLACK_SCHOLES_MERTON 2
+
+/* IV methods (batch.py:212) */
+#define FV_METHOD_HALLEY 0
+#define FV_METHOD_LBR 1
+
+/* IV status codes (fastvol/solver.py:14-19, in declaration order) */
+#define FV_STATUS_CONVERGED 0
+#define FV_STATUS_FELL_BACK_TO_BISECTION 1
+#define FV_STATUS_BELOW_INTRINSIC 2
+#define FV_STATUS_ABOVE_UPPER_BOUND 3
+#define FV_STATUS_MAX_ITERATIONS 4
+/* Greeks status codes (batch.py:270-274) */
+#define FV_STATUS_OK 0
+#define FV_STATUS_STEP_FUNCTION_EDGE 1
+
+/* return codes */
+#define FV_OK 0
+#define FV_ERR_BATCH 1   /* BatchError: kind = FV_CHECK_*, index, column */
+#define FV_ERR_PYEXC 2   /* reference raised: kind = FV_EXC_*, index = row */
+#define FV_ERR_CUDA 3    /* CUDA runtime failure (message has the text) */
+#define FV_ERR_ARG 4     /* bad arguments (mixed memory spaces, bad model...) */
+
+/* validation checks, in the reference's evaluation order (fv_error.kind for
+ * FV_ERR_BATCH).  BadFlag: a flag that is not +1/-1 (parse_flags). */
+#define FV_CHECK_BAD_FLAG 0
+#define FV_CHECK_NONFINITE_UNDERLYING 1
+#define FV_CHECK_NONFINITE_STRIKE 2
+#define FV_CHECK_NONFINITE_T 3
+#define FV_CHECK_NONFINITE_R 4
+#define FV_CHECK_NONFINITE_Q 5
+#define FV_CHECK_NONFINITE_LAST 6     /* sigma (price/greeks) or price (iv) */
+#define FV_CHECK_POSITIVE_UNDERLYING 7
+#define FV_CHECK_POSITIVE_STRIKE 8
+#define FV_CHECK_NONNEG_T 9
+#define FV_CHECK_NONNEG_SIGMA 10
+#define FV_CHECK_DIVIDEND 11          /* q != 0 with a non-BSM model */
+#define FV_NCHECK 12
+
+/* Python exceptions the reference can raise mid-batch (fv_error.kind for
+ * FV_ERR_PYEXC) */
+#define FV_EXC_MATH_RANGE 1     /* OverflowError('math range error') */
+#define FV_EXC_MATH_DOMAIN 2    /* ValueError('math domain error') */
+#define FV_EXC_ZERO_DIV 3       /* ZeroDivisionError('float division by zero') */
+#define FV_EXC_POW_RANGE 4      /* OverflowError(34, 'Numerical result out of range') */
+#define FV_EXC_DOM_FK 5         /* DomainError('F and K must be positive') */
+#define FV_EXC_DOM_ATM_BETA 6   /* DomainError('atm_inverse requires beta in (0, 1), got <value>') */
+#define FV_EXC_DOM_INVCDF_P 7   /* DomainError('inv_norm_cdf requires p in (0, 1), got <value>') */
+#define FV_EXC_DOM_NB_X 8       /* DomainError('normalized_black requires x <= 0, got <value>') */
+#define FV_EXC_DOM_NB_S 9       /* DomainError('normalized_black requires s > 0, got <value>') */
+#define FV_EXC_DOM_OBJ_S 10     /* DomainError('objective_branch requires s > 0, got <value>') */
+
+typedef struct fv_col {
+  const void* data;   /* double* (flag column: int8_t*) */
+  int64_t stride;     /* in elements; 0 = broadcast data[0] */
+} fv_col;
+
+typedef struct fv_error {
+  int32_t code;        /* FV_OK / FV_ERR_* */
+  int32_t kind;        /* FV_CHECK_* or FV_EXC_* */
+  int64_t index;       /* first offending row */
+  int32_t column;      /* FV_ERR_BATCH: 0 flag, 1 underlying, 2 strike, 3 t, 4 r, 5 q, 6 sigma/price */
+  int32_t value_is_numpy; /* FV_EXC_DOM_* with a value: the reference value was a numpy.float64 */
+  double value;        /* the value a DomainError message quotes */
+  char message[256];   /* human-readable, reference wording where it exists */
+} fv_error;
+
+/* batch_price (batch.py:181-203): price[i] for every row. */
+FV_API int fv_batch_price(int model, fv_col flag, fv_col underlying, fv_col strike, fv_col t,
+                          fv_col r, fv_col q, fv_col sigma, int64_t n, double* price,
+                          fv_error* err);
+
+/* batch_iv (batch.py:206-247): iv[i] (NaN unless status is converged or
+ * fell_back_to_bisection) and status[i] (FV_STATUS_*).  region may be NULL;
+ * otherwise it receives the LBR region (0 far_low, 1 near_low, 2 near_high,
+ * 3 far_high, -1 none: bounds/ATM/Halley) for diagnostics. */
+FV_API int fv_batch_iv(int model, int method, fv_col flag, fv_col underlying, fv_col strike,
+                       fv_col t, fv_col r, fv_col q, fv_col price, int64_t n, double* iv,
+                       int8_t* status, int8_t* region, fv_error* err);
+
+/* batch_greeks (batch.py:250-280): per-day theta, per-1% vega/rho
+ * (greeks.py:93-96); status FV_STATUS_OK / FV_STATUS_STEP_FUNCTION_EDGE. */
+FV_API int fv_batch_greeks(int model, fv_col flag, fv_col underlying, fv_col strike, fv_col t,
+                           fv_col r, fv_col q, fv_col sigma, int64_t n, double* delta,
+                           double* gamma, double* theta, double* rho, double* vega,
+                           int8_t* status, fv_error* err);
+
+/* Fused batch_price + batch_greeks over the same columns.  Any output may be
+ * NULL (not computed).  err_price / err_greeks get the outcome each separate
+ * reference call would have had; the return code is the worse of the two. */
+FV_API int fv_price_greeks(int model, fv_col flag, fv_col underlying, fv_col strike, fv_col t,
+                           fv_col r, fv_col q, fv_col sigma, int64_t n, double* price,
+                           double* delta, double* gamma, double* theta, double* rho,
+                           double* vega, int8_t* status, fv_error* err_price,
+                           fv_error* err_greeks);
+
+/* Stream used by device-pointer calls made from the calling thread
+ * (cudaStream_t; NULL = the library's own non-blocking stream). */
+FV_API int fv_set_stream(void* stream);
+
+/* Number of CUDA devices visible; library version string. */
+FV_API int fv_device_count(void);
+FV_API const char* fv_version(void);
+
+/* Host-pointer calls: rows per pipelined chunk (default 1<<22). */
+FV_API int fv_set_chunk_rows(int64_t rows);
+
+/* Kernels launched by this thread's last call (instrumentation for the
+ * bench's gpu_launches count). */
+FV_API int64_t fv_last_launch_count(void);
+
+/* Diagnostics: measured DFMA instruction rate of the current device (the
+ * FP64-pipe roofline denominator for this path). */
+FV_API int fv_probe_fp64_peak(double* dfma_per_s, double* seconds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTVOL_B200_H */

@@ -1,0 +1,101 @@
+"""ctypes binding of libfastvol_b200.so (the C ABI in include/fastvol_b200.h).
+
+There is no CPU fallback: if the CUDA library is missing or no GPU is visible,
+every compute entry point raises (the reference's CPU path lives in the
+reference; this package is the GPU drop-in for it).
+"""
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfastvol_b200.so")
+
+FV_OK, FV_ERR_BATCH, FV_ERR_PYEXC, FV_ERR_CUDA, FV_ERR_ARG = 0, 1, 2, 3, 4
+
+
+class fv_col(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("stride", ctypes.c_int64)]
+
+
+class fv_error(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_int32), ("kind", ctypes.c_int32), ("index", ctypes.c_int64),
+                ("column", ctypes.c_int32), ("value_is_numpy", ctypes.c_int32),
+                ("value", ctypes.c_double), ("message", ctypes.c_char * 256)]
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA extension is not built or cannot run here."""
+
+
+_lock = threading.Lock()
+_lib = None
+
+_COL = fv_col
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_ERR = ctypes.POINTER(fv_error)
+
+SIGNATURES = {
+    "fv_batch_price": ([ctypes.c_int] + [_COL] * 7 + [_I64, _P, _ERR], ctypes.c_int),
+    "fv_batch_iv": ([ctypes.c_int, ctypes.c_int] + [_COL] * 7 + [_I64, _P, _P, _P, _ERR],
+                    ctypes.c_int),
+    "fv_batch_greeks": ([ctypes.c_int] + [_COL] * 7 + [_I64] + [_P] * 6 + [_ERR], ctypes.c_int),
+    "fv_price_greeks": ([ctypes.c_int] + [_COL] * 7 + [_I64] + [_P] * 7 + [_ERR, _ERR],
+                        ctypes.c_int),
+    "fv_set_stream": ([_P], ctypes.c_int),
+    "fv_device_count": ([], ctypes.c_int),
+    "fv_version": ([], ctypes.c_char_p),
+    "fv_set_chunk_rows": ([_I64], ctypes.c_int),
+    "fv_last_launch_count": ([], _I64),
+    "fv_probe_fp64_peak": ([_P, _P], ctypes.c_int),
+}
+
+
+def load(path=LIB_PATH):
+    """Load the shared library (no device needed); raises NativeUnavailable."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                "or `python -m paper_2604_27210_b200._build`")
+        lib = ctypes.CDLL(path)
+        for name, (args, res) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+        return lib
+
+
+def lib_for_compute():
+    """The library, after checking a CUDA device is present (fails loudly)."""
+    lib = load()
+    if lib.fv_device_count() < 1:
+        raise NativeUnavailable("no CUDA device visible: the fastvol B200 path has no CPU fallback")
+    return lib
+
+
+def col(arr):
+    """fv_col for a 1-D numpy array / torch tensor (stride in elements); a
+    single-element column is a stride-0 broadcast (batch.py:95-96)."""
+    if hasattr(arr, "data_ptr"):             # torch tensor
+        stride = arr.stride(0) if (arr.dim() == 1 and arr.numel() > 1) else 0
+        return fv_col(arr.data_ptr(), stride)
+    a = np.asarray(arr)
+    stride = a.strides[0] // a.dtype.itemsize if (a.ndim == 1 and a.size > 1) else 0
+    return fv_col(a.ctypes.data, stride)
+
+
+def ptr(arr):
+    if arr is None:
+        return None
+    if hasattr(arr, "data_ptr"):
+        return arr.data_ptr()
+    return np.asarray(arr).ctypes.data

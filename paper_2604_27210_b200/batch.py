@@ -1,0 +1,396 @@
+"""Drop-in replacement for the reference batch engine, fastvol/batch.py.
+
+Same entry points, signatures, broadcasting, 'c'/'p' flag parsing, ChainTable
+results, status strings, BatchError kinds/indices/messages and Python
+exceptions as /root/reference/pkg/src/fastvol/batch.py:33-334.  What changes
+is underneath: the reference's per-row Python ``fill`` loops run under
+``_run_chunked`` (batch.py:166-178); here each batch is ONE call into the
+C ABI (include/fastvol_b200.h), which validates and computes on the B200 in a
+single fused pass.  There is no CPU fallback.
+"""
+
+import json
+import math
+import os
+from dataclasses import dataclass
+from typing import Dict, Sequence, Union
+
+import numpy as np
+
+from . import _native
+from .errors import DomainError
+from .models import Model, as_model
+from .solver import GREEK_STATUS_NAMES, IV_STATUS_NAMES
+
+ENV_THREADS = "FASTVOL_THREADS"
+MIN_CHUNK = 1024
+INPUT_COLUMNS = ("flag", "underlying", "strike", "t", "r", "q", "sigma", "price")
+GREEK_COLUMNS = ("delta", "gamma", "theta", "rho", "vega")
+
+_IV_STATUS = np.array(IV_STATUS_NAMES, dtype=object)
+_GREEK_STATUS = np.array(GREEK_STATUS_NAMES, dtype=object)
+_CHECK_KIND = ["BadFlag"] + ["NonFiniteInput"] * 6 + ["DomainError"] * 5
+_CHECK_COLUMN = ["flag", "underlying", "strike", "t", "r", "q", None,
+                 "underlying", "strike", "t", "sigma", "q"]
+
+
+class BatchError(Exception):
+    """Pre-kernel batch rejection; ``index`` is the first offending row
+    (batch.py:33-40)."""
+
+    def __init__(self, kind: str, index: int, detail: str):
+        self.kind = kind
+        self.index = index
+        self.detail = detail
+        super().__init__(f"{kind} at row {index}: {detail}")
+
+
+@dataclass
+class ChainTable:
+    """Columnar batch of contracts (batch.py:43-62)."""
+
+    columns: Dict[str, np.ndarray]
+
+    def __post_init__(self):
+        lengths = {c.shape[0] for c in self.columns.values()}
+        if len(lengths) > 1:
+            raise BatchError("ShapeMismatch", 0, f"column lengths differ: {sorted(lengths)}")
+
+    @property
+    def length(self) -> int:
+        for col in self.columns.values():
+            return col.shape[0]
+        return 0
+
+    def __getitem__(self, name: str) -> np.ndarray:
+        return self.columns[name]
+
+
+# ---------------------------------------------------------------------------
+# front end (batch.py:65-148 semantics; validation runs fused on the device)
+# ---------------------------------------------------------------------------
+def broadcast(lengths: Sequence[int]) -> int:
+    """Common batch length under scalar-extends-to-N rules (batch.py:65-75)."""
+    n = max(lengths, default=1)
+    if 0 in lengths:
+        n = 0
+    for i, length in enumerate(lengths):
+        if length not in (1, n):
+            raise BatchError("ShapeMismatch", i, f"length {length} incompatible with batch size {n}")
+    return n
+
+
+def _flag_error(i, f):
+    return BatchError("BadFlag", i, f"option flag must be 'c' or 'p', got {f!r}")
+
+
+def parse_flags(flags: Union[str, Sequence[str]]) -> np.ndarray:
+    """Case-insensitive 'c'/'p' -> int8 +1/-1 (batch.py:78-88), vectorised for
+    string arrays; the first bad element raises BadFlag with its repr."""
+    if isinstance(flags, str):
+        flags = [flags]
+    arr = flags if isinstance(flags, np.ndarray) else None
+    if arr is None:
+        try:
+            arr = np.asarray(flags)
+        except (ValueError, TypeError):
+            arr = None
+    if arr is not None and arr.ndim == 1 and arr.dtype.kind in "US":
+        if arr.dtype.kind == "S":              # bytes never compare equal to 'c'
+            if len(arr):
+                raise _flag_error(0, flags[0])
+            return np.empty(0, dtype=np.int8)
+        is_c = (arr == "c") | (arr == "C")
+        bad = ~(is_c | (arr == "p") | (arr == "P"))
+        if bad.any():
+            i = int(np.flatnonzero(bad)[0])
+            raise _flag_error(i, flags[i])
+        return np.where(is_c, 1, -1).astype(np.int8)
+    out = np.empty(len(flags), dtype=np.int8)
+    for i, f in enumerate(flags):
+        if f == "c" or f == "C":
+            out[i] = 1
+        elif f == "p" or f == "P":
+            out[i] = -1
+        else:
+            raise _flag_error(i, f)
+    return out
+
+
+def _as_column(values, n: int, name: str) -> np.ndarray:
+    arr = np.atleast_1d(np.asarray(values, dtype=np.float64))
+    if arr.ndim != 1:
+        raise BatchError("ShapeMismatch", 0, f"column {name} is not 1-D")
+    if arr.shape[0] == 1 and n != 1:
+        arr = np.broadcast_to(arr, (n,))
+    if arr.shape[0] != n:
+        raise BatchError("ShapeMismatch", 0, f"column {name} has length {arr.shape[0]}, expected {n}")
+    return arr
+
+
+def validate(table: Dict[str, np.ndarray]) -> None:
+    """Host-side restatement of batch.py:104-124 (public helper; the batch
+    entry points run the same checks fused into the GPU pass instead)."""
+    for name, col in table.items():
+        if col.dtype.kind != "f":
+            continue
+        bad = np.flatnonzero(~np.isfinite(col))
+        if bad.size:
+            raise BatchError("NonFiniteInput", int(bad[0]), f"column {name} is not finite")
+    for name in ("underlying", "strike"):
+        if name in table:
+            bad = np.flatnonzero(~(table[name] > 0.0))
+            if bad.size:
+                raise BatchError("DomainError", int(bad[0]), f"column {name} must be positive")
+    for name in ("t", "sigma"):
+        if name in table:
+            bad = np.flatnonzero(table[name] < 0.0)
+            if bad.size:
+                raise BatchError("DomainError", int(bad[0]), f"column {name} must be >= 0")
+
+
+def _assemble(model: Model, flag, underlying, strike, t, r, q=0.0, sigma=None, price=None):
+    """batch.py:127-148 up to (not including) validate: flags, lengths,
+    columns.  Returns (n, table)."""
+    theta = parse_flags(flag)
+    raw = {"underlying": underlying, "strike": strike, "t": t, "r": r, "q": q}
+    if sigma is not None:
+        raw["sigma"] = sigma
+    if price is not None:
+        raw["price"] = price
+    lengths = [theta.shape[0]] + [np.atleast_1d(np.asarray(v, dtype=np.float64)).shape[0]
+                                  for v in raw.values()]
+    n = broadcast(lengths)
+    table = {"flag": theta if theta.shape[0] == n else np.broadcast_to(theta, (n,))}
+    for name, values in raw.items():
+        table[name] = _as_column(values, n, name)
+    return n, table
+
+
+def worker_count() -> int:
+    """FASTVOL_THREADS validation kept for parity (batch.py:151-163); the GPU
+    path does not use host worker threads."""
+    env = os.environ.get(ENV_THREADS)
+    if env is not None:
+        try:
+            w = int(env)
+        except ValueError as exc:
+            raise BatchError("DomainError", 0, f"{ENV_THREADS} must be a positive integer") from exc
+        if w < 1:
+            raise BatchError("DomainError", 0, f"{ENV_THREADS} must be a positive integer")
+        return w
+    return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# native dispatch
+# ---------------------------------------------------------------------------
+def _native_col(a):
+    """A 1-D column for the C ABI: broadcast views become stride-0 columns
+    (never materialised), other views are made contiguous."""
+    if a.ndim == 1 and a.shape[0] > 1 and a.strides[0] == 0:
+        return a, _native.fv_col(a.ctypes.data, 0)
+    if a.ndim == 1 and a.shape[0] == 1:
+        return a, _native.fv_col(a.ctypes.data, 0)
+    c = np.ascontiguousarray(a)
+    return c, _native.fv_col(c.ctypes.data, 1)
+
+
+def _columns(table, last):
+    keep, cols = [], []
+    for name in ("flag", "underlying", "strike", "t", "r", "q", last):
+        arr = table[name]
+        if name == "flag":
+            arr = np.asarray(arr, dtype=np.int8)
+        a, c = _native_col(arr)
+        keep.append(a)
+        cols.append(c)
+    return keep, cols
+
+
+def _value_repr(err):
+    return repr(np.float64(err.value)) if err.value_is_numpy else repr(float(err.value))
+
+
+def _raise_for(err, table, last_name):
+    """Turn an fv_error into the exception the reference raises."""
+    if err.code == _native.FV_ERR_BATCH:
+        kind = _CHECK_KIND[err.kind]
+        col = _CHECK_COLUMN[err.kind] or last_name
+        if err.kind == 0:
+            raise BatchError("BadFlag", int(err.index), "option flag must be 'c' or 'p'")
+        if kind == "NonFiniteInput":
+            detail = f"column {col} is not finite"
+        elif err.kind in (7, 8):
+            detail = f"column {col} must be positive"
+        elif err.kind in (9, 10):
+            detail = f"column {col} must be >= 0"
+        else:
+            raise BatchError("DomainError", int(err.index),
+                             f"model {table['__model__']} does not accept a dividend yield")
+        raise BatchError(kind, int(err.index), detail)
+    if err.code == _native.FV_ERR_PYEXC:
+        k = err.kind
+        if k == 1:
+            raise OverflowError("math range error")
+        if k == 2:
+            raise ValueError("math domain error")
+        if k == 3:
+            raise ZeroDivisionError("float division by zero")
+        if k == 4:
+            raise OverflowError(34, "Numerical result out of range")
+        if k == 5:
+            raise DomainError("F and K must be positive")
+        if k == 6:
+            raise DomainError(f"atm_inverse requires beta in (0, 1), got {_value_repr(err)}")
+        if k == 7:
+            raise DomainError(f"inv_norm_cdf requires p in (0, 1), got {_value_repr(err)}")
+        if k == 8:
+            raise DomainError(f"normalized_black requires x <= 0, got {_value_repr(err)}")
+        if k == 9:
+            raise DomainError(f"normalized_black requires s > 0, got {_value_repr(err)}")
+        if k == 10:
+            raise DomainError(f"objective_branch requires s > 0, got {_value_repr(err)}")
+    raise RuntimeError("fastvol_b200: " + err.message.decode(errors="replace"))
+
+
+def _ok_or_raise(rc, err, table, model, last):
+    """Reference order: validation BatchError (_assemble), then the
+    FASTVOL_THREADS check (_run_chunked -> worker_count), then the first
+    raising row's exception (fill)."""
+    if rc == _native.FV_ERR_BATCH:
+        table = dict(table)
+        table["__model__"] = model.value
+        _raise_for(err, table, last)
+    worker_count()
+    if rc != _native.FV_OK:
+        _raise_for(err, table, last)
+
+
+# ---------------------------------------------------------------------------
+# public batch API (batch.py:181-280)
+# ---------------------------------------------------------------------------
+def batch_price(model, flag, underlying, strike, t, r, q=0.0, sigma=None) -> ChainTable:
+    """Price every row; returns the input columns plus ``price``."""
+    model = as_model(model)
+    n, table = _assemble(model, flag, underlying, strike, t, r, q, sigma=sigma)
+    if "sigma" not in table:
+        validate_order_then(table, model, need="sigma")
+        raise BatchError("DomainError", 0, "batch_price requires sigma")
+    out = np.empty(n, dtype=np.float64)
+    if n:
+        lib = _native.lib_for_compute()
+        keep, cols = _columns(table, "sigma")
+        err = _native.fv_error()
+        rc = lib.fv_batch_price(model.code, *cols, n, out.ctypes.data, err)
+        _ok_or_raise(rc, err, table, model, "sigma")
+    cols_out = dict(table)
+    cols_out["price"] = out
+    return ChainTable(cols_out)
+
+
+def batch_iv(model, method: str, flag, underlying, strike, t, r, price=None, q=0.0) -> ChainTable:
+    """Invert the price column row by row (Halley or LBR); failed rows carry
+    NaN plus an in-band status string."""
+    if method not in ("halley", "lbr"):
+        raise BatchError("DomainError", 0, f"unknown IV method {method!r}")
+    model = as_model(model)
+    n, table = _assemble(model, flag, underlying, strike, t, r, q, price=price)
+    if "price" not in table:
+        validate_order_then(table, model, need="price")
+        raise BatchError("DomainError", 0, "batch_iv requires price")
+    iv = np.empty(n, dtype=np.float64)
+    codes = np.empty(n, dtype=np.int8)
+    if n:
+        lib = _native.lib_for_compute()
+        keep, cols = _columns(table, "price")
+        err = _native.fv_error()
+        rc = lib.fv_batch_iv(model.code, 1 if method == "lbr" else 0, *cols, n, iv.ctypes.data,
+                             codes.ctypes.data, None, err)
+        _ok_or_raise(rc, err, table, model, "price")
+    cols_out = dict(table)
+    cols_out["iv"] = iv
+    cols_out["status"] = _IV_STATUS[codes]
+    return ChainTable(cols_out)
+
+
+def batch_greeks(model, flag, underlying, strike, t, r, q=0.0, sigma=None) -> ChainTable:
+    """All five Greeks per row; zero-vol / zero-time rows carry NaNs plus a
+    ``step_function_edge`` status."""
+    model = as_model(model)
+    n, table = _assemble(model, flag, underlying, strike, t, r, q, sigma=sigma)
+    if "sigma" not in table:
+        validate_order_then(table, model, need="sigma")
+        raise BatchError("DomainError", 0, "batch_greeks requires sigma")
+    outs = {name: np.empty(n, dtype=np.float64) for name in GREEK_COLUMNS}
+    codes = np.empty(n, dtype=np.int8)
+    if n:
+        lib = _native.lib_for_compute()
+        keep, cols = _columns(table, "sigma")
+        err = _native.fv_error()
+        rc = lib.fv_batch_greeks(model.code, *cols, n, *[outs[g].ctypes.data for g in GREEK_COLUMNS],
+                                 codes.ctypes.data, err)
+        _ok_or_raise(rc, err, table, model, "sigma")
+    cols_out = dict(table)
+    cols_out.update(outs)
+    cols_out["status"] = _GREEK_STATUS[codes]
+    return ChainTable(cols_out)
+
+
+def validate_order_then(table, model, need):
+    """A batch without its sigma/price column still runs the reference's
+    validate() and dividend check first (batch.py:145-147 precede the
+    'requires sigma/price' error)."""
+    validate(table)
+    if model is not Model.BLACK_SCHOLES_MERTON and np.any(table["q"] != 0.0):
+        idx = int(np.flatnonzero(table["q"] != 0.0)[0])
+        raise BatchError("DomainError", idx, f"model {model.value} does not accept a dividend yield")
+
+
+# ---------------------------------------------------------------------------
+# serialization (batch.py:287-334), unchanged semantics
+# ---------------------------------------------------------------------------
+def _cell_text(value) -> str:
+    if isinstance(value, (float, np.floating)):
+        return repr(float(value))
+    if isinstance(value, (np.int8, np.integer, int)):
+        return "c" if int(value) > 0 else "p"
+    return str(value)
+
+
+def _plain_text(value) -> str:
+    if isinstance(value, (float, np.floating)):
+        return f"{float(value):.8g}"
+    if isinstance(value, (np.int8, np.integer, int)):
+        return "c" if int(value) > 0 else "p"
+    return str(value)
+
+
+def format_output(table: ChainTable, fmt: str = "csv") -> str:
+    """Serialize a table to csv, json, or a plain aligned listing."""
+    names = list(table.columns)
+    n = table.length
+    if fmt == "csv":
+        lines = [",".join(names)]
+        for i in range(n):
+            lines.append(",".join(_cell_text(table[c][i]) for c in names))
+        return "\n".join(lines) + "\n"
+    if fmt == "json":
+        obj = {}
+        for name in names:
+            col = table[name]
+            if col.dtype.kind == "f":
+                obj[name] = [None if not math.isfinite(v) else float(v) for v in col]
+            elif name == "flag":
+                obj[name] = ["c" if v > 0 else "p" for v in col]
+            else:
+                obj[name] = [str(v) for v in col]
+        return json.dumps(obj)
+    if fmt == "plain":
+        cells = [[_plain_text(table[c][i]) for c in names] for i in range(n)]
+        widths = [max([len(name)] + [len(row[j]) for row in cells]) for j, name in enumerate(names)]
+        lines = ["  ".join(name.ljust(widths[j]) for j, name in enumerate(names))]
+        for row in cells:
+            lines.append("  ".join(cell.ljust(widths[j]) for j, cell in enumerate(row)))
+        return "\n".join(lines) + "\n"
+    raise BatchError("DomainError", 0, f"unknown output format {fmt!r}")

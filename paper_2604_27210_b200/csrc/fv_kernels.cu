@@ -1,0 +1,1038 @@
+// fv_kernels.cu -- sm_100a kernels + the C ABI (include/fastvol_b200.h) for
+// the batched pricing / Greeks / implied-vol path.
+//
+// Execution model (one quote = one unit of independent fp64 work):
+//   * persistent grid-stride kernels, grid = SMs x resident CTAs, each thread
+//     owns a PAIR of adjacent quotes so structure-of-arrays columns are read
+//     with 128-bit (double2 / char2) coalesced loads and written back the same
+//     way; broadcast (stride-0) columns are a single cached load;
+//   * the reference's batch validation (batch.py:104-124, :144-147) is fused
+//     into the compute pass: each row's failed checks go to a per-check
+//     atomicMin, so the first failing row per check comes out of the same HBM
+//     read that feeds the solver;
+//   * rows whose reference execution would raise a Python exception publish
+//     (row << 8 | code) through one atomicMin -- the lowest raising row wins,
+//     exactly as _run_chunked surfaces it (batch.py:166-178);
+//   * Halley IV (solver.py:49-161) runs in two phases: phase 1 (setup + <= 16
+//     Halley steps) finishes ~96% of quotes and appends the rest, with their
+//     bracket state, to a compact queue (warp-aggregated atomics); phase 2
+//     runs the <= 128-step bisection tail on that dense queue, so lanes that
+//     finished early do not idle behind the tail;
+//   * host-pointer calls stream through chunked pinned/pageable H2D ->
+//     kernel -> D2H on NSLOT streams so copies overlap compute.
+// All arithmetic is fv_quote.h / fv_libm.h (bit-faithful to the reference);
+// compile with -fmad=false.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <vector>
+
+#include "fv_quote.h"
+#include "../../include/fastvol_b200.h"
+
+#define FV_VERSION "fastvol_b200 0.1.0 (sm_100a)"
+#define FV_NSLOT 3
+
+// ---------------------------------------------------------------------------
+// device-side column access
+// ---------------------------------------------------------------------------
+struct DCol {
+  const double* p;
+  int64_t stride;
+  int mode;  // 0 broadcast, 1 contiguous + 16B aligned (double2), 2 generic strided
+};
+struct DFlag {
+  const int8_t* p;
+  int64_t stride;
+  int mode;  // 0 broadcast, 1 contiguous + 2B aligned (char2), 2 generic
+};
+
+__device__ __forceinline__ void ld2(const DCol& c, int64_t i, bool two, double& a, double& b) {
+  if (c.mode == 0) {
+    a = __ldg(c.p);
+    b = a;
+  } else if (c.mode == 1 && two) {
+    double2 v = __ldg(reinterpret_cast<const double2*>(c.p + i));
+    a = v.x;
+    b = v.y;
+  } else {
+    a = __ldg(c.p + i * c.stride);
+    b = two ? __ldg(c.p + (i + 1) * c.stride) : 0.0;
+  }
+}
+__device__ __forceinline__ void ldf2(const DFlag& c, int64_t i, bool two, int& a, int& b) {
+  if (c.mode == 0) {
+    a = c.p[0];
+    b = a;
+  } else if (c.mode == 1 && two) {
+    char2 v = *reinterpret_cast<const char2*>(c.p + i);
+    a = v.x;
+    b = v.y;
+  } else {
+    a = c.p[i * c.stride];
+    b = two ? c.p[(i + 1) * c.stride] : 0;
+  }
+}
+__device__ __forceinline__ void st2(double* p, int64_t i, bool two, bool vec, double a, double b) {
+  if (!p) return;
+  if (two && vec) {
+    *reinterpret_cast<double2*>(p + i) = make_double2(a, b);
+  } else {
+    p[i] = a;
+    if (two) p[i + 1] = b;
+  }
+}
+__device__ __forceinline__ void st2i8(int8_t* p, int64_t i, bool two, int a, int b) {
+  if (!p) return;
+  if (two && (((uintptr_t)(p + i)) & 1) == 0) {
+    *reinterpret_cast<char2*>(p + i) = make_char2((signed char)a, (signed char)b);
+  } else {
+    p[i] = (int8_t)a;
+    if (two) p[i + 1] = (int8_t)b;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// status block shared by all kernels of one call
+// ---------------------------------------------------------------------------
+struct FvDevStatus {
+  unsigned long long check_first[FV_NCHECK];
+  unsigned long long exc_first;    // (row << 8) | code: price / iv / greeks
+  unsigned long long exc2_first;   // second stream (fused greeks)
+  unsigned long long pad[2];
+};
+
+struct KArgs {
+  int model;
+  int has_sigma;       // last column is sigma (price/greeks) rather than price (iv)
+  uint32_t check_mask; // checks evaluated per row (broadcast columns are host-checked)
+  DFlag flag;
+  DCol un, k, t, r, q, last;
+  int64_t n;           // rows in this launch
+  int64_t row0;        // global index of local row 0
+  int out_vec;         // all double outputs 16B aligned
+  double* o0;          // price | iv
+  double* o1;          // delta
+  double* o2;          // gamma
+  double* o3;          // theta
+  double* o4;          // rho
+  double* o5;          // vega
+  int8_t* status;
+  int8_t* region;
+  FvDevStatus* st;
+};
+
+__device__ __forceinline__ uint32_t row_checks(const KArgs& a, int fl, double un, double k,
+                                               double t, double r, double q, double last) {
+  uint32_t b = 0;
+  b |= (uint32_t)(fl != 1 && fl != -1) << FV_CHECK_BAD_FLAG;
+  b |= (uint32_t)(!fv_isfinite(un)) << FV_CHECK_NONFINITE_UNDERLYING;
+  b |= (uint32_t)(!fv_isfinite(k)) << FV_CHECK_NONFINITE_STRIKE;
+  b |= (uint32_t)(!fv_isfinite(t)) << FV_CHECK_NONFINITE_T;
+  b |= (uint32_t)(!fv_isfinite(r)) << FV_CHECK_NONFINITE_R;
+  b |= (uint32_t)(!fv_isfinite(q)) << FV_CHECK_NONFINITE_Q;
+  b |= (uint32_t)(!fv_isfinite(last)) << FV_CHECK_NONFINITE_LAST;
+  b |= (uint32_t)(!(un > 0.0)) << FV_CHECK_POSITIVE_UNDERLYING;
+  b |= (uint32_t)(!(k > 0.0)) << FV_CHECK_POSITIVE_STRIKE;
+  b |= (uint32_t)(t < 0.0) << FV_CHECK_NONNEG_T;
+  b |= (uint32_t)(a.has_sigma && last < 0.0) << FV_CHECK_NONNEG_SIGMA;
+  b |= (uint32_t)(a.model != FV_MODEL_BLACK_SCHOLES_MERTON && q != 0.0) << FV_CHECK_DIVIDEND;
+  return b & a.check_mask;
+}
+
+__device__ __noinline__ void publish_checks(FvDevStatus* st, uint32_t bits, int64_t row) {
+  while (bits) {
+    int c = __ffs(bits) - 1;
+    bits &= bits - 1;
+    atomicMin(&st->check_first[c], (unsigned long long)row);
+  }
+}
+__device__ __forceinline__ void publish_exc(unsigned long long* slot, int code, int64_t row) {
+  if (code) atomicMin(slot, ((unsigned long long)row << 8) | (unsigned long long)code);
+}
+
+// Loads the pair (i, i+1) of every input column.
+struct Pair {
+  int fl[2];
+  double un[2], k[2], t[2], r[2], q[2], last[2];
+};
+__device__ __forceinline__ void load_pair(const KArgs& a, int64_t i, bool two, Pair& p) {
+  ldf2(a.flag, i, two, p.fl[0], p.fl[1]);
+  ld2(a.un, i, two, p.un[0], p.un[1]);
+  ld2(a.k, i, two, p.k[0], p.k[1]);
+  ld2(a.t, i, two, p.t[0], p.t[1]);
+  ld2(a.r, i, two, p.r[0], p.r[1]);
+  ld2(a.q, i, two, p.q[0], p.q[1]);
+  ld2(a.last, i, two, p.last[0], p.last[1]);
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_price(KArgs a) {
+  const int64_t npair = (a.n + 1) >> 1;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = 2 * j;
+    const bool two = i + 1 < a.n;
+    Pair p;
+    load_pair(a, i, two, p);
+    double out[2] = {0.0, 0.0};
+#pragma unroll 1
+    for (int u = 0; u < (two ? 2 : 1); ++u) {
+      uint32_t bad = row_checks(a, p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u], p.q[u], p.last[u]);
+      if (bad) { publish_checks(a.st, bad, a.row0 + i + u); out[u] = __builtin_nan(""); continue; }
+      FvExc e = {0, 0, 0.0};
+      out[u] = fv_price_row(a.model, (double)p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u], p.q[u],
+                            p.last[u], e);
+      publish_exc(&a.st->exc_first, e.code, a.row0 + i + u);
+    }
+    st2(a.o0, i, two, a.out_vec, out[0], out[1]);
+  }
+}
+
+template <bool kPrice, bool kGreeks>
+__global__ void __launch_bounds__(256) k_price_greeks(KArgs a) {
+  const int64_t npair = (a.n + 1) >> 1;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = 2 * j;
+    const bool two = i + 1 < a.n;
+    Pair p;
+    load_pair(a, i, two, p);
+    FvGreeks g[2];
+#pragma unroll 1
+    for (int u = 0; u < (two ? 2 : 1); ++u) {
+      uint32_t bad = row_checks(a, p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u], p.q[u], p.last[u]);
+      if (bad) {
+        publish_checks(a.st, bad, a.row0 + i + u);
+        g[u].price = g[u].delta = g[u].gamma = g[u].theta = g[u].rho = g[u].vega = __builtin_nan("");
+        g[u].status = 0;
+        continue;
+      }
+      FvExc ep = {0, 0, 0.0}, eg = {0, 0, 0.0};
+      g[u] = fv_price_greeks_row(a.model, (double)p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u],
+                                 p.q[u], p.last[u], kPrice, kGreeks, ep, eg);
+      if (kPrice) publish_exc(&a.st->exc_first, ep.code, a.row0 + i + u);
+      if (kGreeks) publish_exc(&a.st->exc2_first, eg.code, a.row0 + i + u);
+    }
+    if (!two) g[1] = g[0];
+    if (kPrice) st2(a.o0, i, two, a.out_vec, g[0].price, g[1].price);
+    if (kGreeks) {
+      st2(a.o1, i, two, a.out_vec, g[0].delta, g[1].delta);
+      st2(a.o2, i, two, a.out_vec, g[0].gamma, g[1].gamma);
+      st2(a.o3, i, two, a.out_vec, g[0].theta, g[1].theta);
+      st2(a.o4, i, two, a.out_vec, g[0].rho, g[1].rho);
+      st2(a.o5, i, two, a.out_vec, g[0].vega, g[1].vega);
+      st2i8(a.status, i, two, g[0].status, g[1].status);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_lbr(KArgs a) {
+  const int64_t npair = (a.n + 1) >> 1;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = 2 * j;
+    const bool two = i + 1 < a.n;
+    Pair p;
+    load_pair(a, i, two, p);
+    double iv[2] = {0.0, 0.0};
+    int stt[2] = {0, 0}, reg[2] = {-1, -1};
+#pragma unroll 1
+    for (int u = 0; u < (two ? 2 : 1); ++u) {
+      uint32_t bad = row_checks(a, p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u], p.q[u], p.last[u]);
+      if (bad) {
+        publish_checks(a.st, bad, a.row0 + i + u);
+        iv[u] = __builtin_nan(""); stt[u] = FV_IV_MAX_ITER; reg[u] = -1;
+        continue;
+      }
+      FvExc e = {0, 0, 0.0};
+      FvLbrOut o = fv_lbr_batch_row(a.model, (double)p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u],
+                                    p.q[u], p.last[u], e);
+      publish_exc(&a.st->exc_first, e.code, a.row0 + i + u);
+      iv[u] = o.sigma; stt[u] = o.status; reg[u] = o.region;
+    }
+    st2(a.o0, i, two, a.out_vec, iv[0], iv[1]);
+    st2i8(a.status, i, two, stt[0], stt[1]);
+    st2i8(a.region, i, two, reg[0], reg[1]);
+  }
+}
+
+// Halley phase-2 queue entry
+struct HQ {
+  FvHalleyCtx c;
+  FvHalleyState s;
+  int64_t row;   // local row
+};
+
+__device__ __forceinline__ unsigned int warp_append(unsigned int* counter, bool want) {
+  unsigned mask = __ballot_sync(0xffffffffu, want);
+  unsigned int base = 0;
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(mask) - 1;
+  if (mask) {
+    if (lane == leader) base = atomicAdd(counter, (unsigned int)__popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+  }
+  return base + __popc(mask & ((1u << lane) - 1));
+}
+
+__global__ void __launch_bounds__(256) k_halley1(KArgs a, HQ* queue, unsigned int* qlen) {
+  const int64_t npair = (a.n + 1) >> 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // the loop trip count is uniform per warp so warp_append's ballot sees the
+  // whole warp; lanes past the end participate with want = false.
+  const int64_t nloop = (npair + stride - 1) / stride;
+  for (int64_t it = 0; it < nloop; ++it) {
+    const int64_t j = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool active = j < npair;
+    const int64_t i = 2 * j;
+    const bool two = active && (i + 1 < a.n);
+    double iv[2] = {0.0, 0.0};
+    int stt[2] = {0, 0};
+    bool need[2] = {false, false};
+    FvHalleyCtx cx[2];
+    FvHalleyState sx[2];
+    if (active) {
+      Pair p;
+      load_pair(a, i, two, p);
+#pragma unroll 1
+      for (int u = 0; u < (two ? 2 : 1); ++u) {
+        uint32_t bad = row_checks(a, p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u], p.q[u], p.last[u]);
+        if (bad) {
+          publish_checks(a.st, bad, a.row0 + i + u);
+          iv[u] = __builtin_nan(""); stt[u] = FV_IV_MAX_ITER;
+          continue;
+        }
+        FvExc e = {0, 0, 0.0};
+        int status;
+        double sig;
+        int done = fv_halley_phase1(a.model, (double)p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u],
+                                    p.q[u], p.last[u], cx[u], sx[u], &status, &sig, e);
+        publish_exc(&a.st->exc_first, e.code, a.row0 + i + u);
+        if (done || e.code) {
+          iv[u] = (status == FV_IV_CONVERGED || status == FV_IV_FELL_BACK) ? sig : __builtin_nan("");
+          stt[u] = status;
+        } else {
+          need[u] = true;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      unsigned int slot = warp_append(qlen, need[u]);
+      if (need[u]) {
+        HQ h;
+        h.c = cx[u]; h.s = sx[u]; h.row = i + u;
+        queue[slot] = h;
+      }
+    }
+    if (active) {
+      // queued rows are overwritten by phase 2
+      st2(a.o0, i, two, a.out_vec, iv[0], iv[1]);
+      st2i8(a.status, i, two, stt[0], stt[1]);
+      if (a.region) st2i8(a.region, i, two, -1, -1);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_halley2(KArgs a, const HQ* queue, const unsigned int* qlen) {
+  const unsigned int n = *qlen;
+  for (unsigned int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    HQ h = queue[j];
+    FvExc e = {0, 0, 0.0};
+    int status;
+    double sig;
+    fv_halley_phase2(h.c, h.s, &status, &sig, e);
+    publish_exc(&a.st->exc_first, e.code, a.row0 + h.row);
+    a.o0[h.row] = (status == FV_IV_CONVERGED || status == FV_IV_FELL_BACK) ? sig : __builtin_nan("");
+    a.status[h.row] = (int8_t)status;
+  }
+}
+
+// One-row re-run that records the full exception (value + numpy-ness) for
+// DomainError messages that quote a value.
+struct ExplainOut { int code; int np; double val; };
+__global__ void k_explain(KArgs a, int method, int64_t local_row, ExplainOut* out) {
+  Pair p;
+  load_pair(a, local_row, false, p);
+  FvExc e = {0, 0, 0.0};
+  if (method == FV_METHOD_LBR) {
+    fv_lbr_batch_row(a.model, (double)p.fl[0], p.un[0], p.k[0], p.t[0], p.r[0], p.q[0], p.last[0], e);
+  } else {
+    FvHalleyCtx c; FvHalleyState s; int status; double sig;
+    if (!fv_halley_phase1(a.model, (double)p.fl[0], p.un[0], p.k[0], p.t[0], p.r[0], p.q[0],
+                          p.last[0], c, s, &status, &sig, e) && !e.code)
+      fv_halley_phase2(c, s, &status, &sig, e);
+  }
+  out->code = e.code; out->np = e.np; out->val = e.val;
+}
+
+// FP64-pipe peak probe: 8 independent DFMA chains per thread (the roofline
+// denominator for this FP64-bound path; MEASURED_PEAKS.json has no fp64 entry).
+__global__ void __launch_bounds__(256) k_fp64_probe(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-9, x2 = x0 + 2e-9, x3 = x0 + 3e-9;
+  double x4 = x0 + 4e-9, x5 = x0 + 5e-9, x6 = x0 + 6e-9, x7 = x0 + 7e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      x0 = __fma_rn(x0, a, b); x1 = __fma_rn(x1, a, b); x2 = __fma_rn(x2, a, b);
+      x3 = __fma_rn(x3, a, b); x4 = __fma_rn(x4, a, b); x5 = __fma_rn(x5, a, b);
+      x6 = __fma_rn(x6, a, b); x7 = __fma_rn(x7, a, b);
+    }
+  }
+  double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 12345.678) out[blockIdx.x * blockDim.x + threadIdx.x] = s;  // keep live
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+namespace {
+
+thread_local cudaStream_t t_user_stream = nullptr;
+thread_local int64_t t_launches = 0;
+int64_t g_chunk_rows = 1 << 22;
+
+struct DevWork {
+  int dev = -1;
+  int sm_count = 0;
+  cudaStream_t streams[FV_NSLOT] = {};
+  FvDevStatus* st = nullptr;            // device
+  FvDevStatus* st_host = nullptr;       // pinned mirror
+  unsigned int* qlen = nullptr;         // [FV_NSLOT]
+  HQ* queue[FV_NSLOT] = {};
+  int64_t queue_cap[FV_NSLOT] = {};
+  // chunk buffers for host-pointer calls
+  char* chunk[FV_NSLOT] = {};
+  int64_t chunk_cap_rows[FV_NSLOT] = {};
+  ExplainOut* explain = nullptr;
+  int blocks_price = 0, blocks_greeks = 0, blocks_lbr = 0, blocks_h1 = 0, blocks_h2 = 0;
+  std::mutex mu;
+};
+
+std::mutex g_mu;
+std::vector<DevWork*> g_work;
+
+#define CK(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) return _e; } while (0)
+
+int occupancy_blocks(const void* fn, int sm) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
+  if (per_sm < 1) per_sm = 1;
+  return per_sm * sm;
+}
+
+cudaError_t get_work(DevWork** out) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(g_mu);
+  if ((int)g_work.size() <= dev) g_work.resize(dev + 1, nullptr);
+  if (!g_work[dev]) {
+    DevWork* w = new DevWork();
+    w->dev = dev;
+    CK(cudaDeviceGetAttribute(&w->sm_count, cudaDevAttrMultiProcessorCount, dev));
+    for (int s = 0; s < FV_NSLOT; ++s) CK(cudaStreamCreateWithFlags(&w->streams[s], cudaStreamNonBlocking));
+    CK(cudaMalloc(&w->st, sizeof(FvDevStatus)));
+    CK(cudaMallocHost(&w->st_host, sizeof(FvDevStatus)));
+    CK(cudaMalloc(&w->qlen, sizeof(unsigned int) * FV_NSLOT));
+    CK(cudaMalloc(&w->explain, sizeof(ExplainOut)));
+    w->blocks_price = occupancy_blocks((const void*)k_price, w->sm_count);
+    w->blocks_greeks = occupancy_blocks((const void*)k_price_greeks<true, true>, w->sm_count);
+    w->blocks_lbr = occupancy_blocks((const void*)k_lbr, w->sm_count);
+    w->blocks_h1 = occupancy_blocks((const void*)k_halley1, w->sm_count);
+    w->blocks_h2 = occupancy_blocks((const void*)k_halley2, w->sm_count);
+    g_work[dev] = w;
+  }
+  *out = g_work[dev];
+  return cudaSuccess;
+}
+
+cudaError_t ensure_queue(DevWork* w, int slot, int64_t rows) {
+  if (w->queue_cap[slot] >= rows) return cudaSuccess;
+  if (w->queue[slot]) cudaFree(w->queue[slot]);
+  int64_t cap = rows < 1024 ? 1024 : rows;
+  CK(cudaMalloc(&w->queue[slot], sizeof(HQ) * cap));
+  w->queue_cap[slot] = cap;
+  return cudaSuccess;
+}
+
+enum Kind { KIND_PRICE, KIND_IV, KIND_GREEKS, KIND_PRICE_GREEKS };
+
+struct Call {
+  Kind kind;
+  int model, method;
+  fv_col cols[7];      // flag, under, strike, t, r, q, last
+  int64_t n;
+  double* outs[6];     // price|iv, delta, gamma, theta, rho, vega
+  int8_t* status;
+  int8_t* region;
+  bool want_price, want_greeks;
+};
+
+int64_t blocks_for(int64_t max_blocks, int64_t n) {
+  int64_t need = ((n + 1) / 2 + 255) / 256;
+  if (need < 1) need = 1;
+  return need < max_blocks ? need : max_blocks;
+}
+
+cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStream_t s) {
+  if (a.n <= 0) return cudaSuccess;
+  switch (c.kind) {
+    case KIND_PRICE:
+      k_price<<<blocks_for(w->blocks_price, a.n), 256, 0, s>>>(a);
+      ++t_launches;
+      break;
+    case KIND_GREEKS:
+      k_price_greeks<false, true><<<blocks_for(w->blocks_greeks, a.n), 256, 0, s>>>(a);
+      ++t_launches;
+      break;
+    case KIND_PRICE_GREEKS:
+      if (c.want_price && c.want_greeks)
+        k_price_greeks<true, true><<<blocks_for(w->blocks_greeks, a.n), 256, 0, s>>>(a);
+      else if (c.want_greeks)
+        k_price_greeks<false, true><<<blocks_for(w->blocks_greeks, a.n), 256, 0, s>>>(a);
+      else
+        k_price_greeks<true, false><<<blocks_for(w->blocks_greeks, a.n), 256, 0, s>>>(a);
+      ++t_launches;
+      break;
+    case KIND_IV:
+      if (c.method == FV_METHOD_LBR) {
+        k_lbr<<<blocks_for(w->blocks_lbr, a.n), 256, 0, s>>>(a);
+        ++t_launches;
+      } else {
+        CK(ensure_queue(w, slot, a.n));
+        CK(cudaMemsetAsync(w->qlen + slot, 0, sizeof(unsigned int), s));
+        k_halley1<<<blocks_for(w->blocks_h1, a.n), 256, 0, s>>>(a, w->queue[slot], w->qlen + slot);
+        k_halley2<<<w->blocks_h2, 256, 0, s>>>(a, w->queue[slot], w->qlen + slot);
+        t_launches += 2;
+      }
+      break;
+  }
+  return cudaGetLastError();
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+const char* check_name(int c, bool has_sigma, char* buf, size_t len) {
+  static const char* cols[] = {"underlying", "strike", "t", "r", "q"};
+  switch (c) {
+    case FV_CHECK_BAD_FLAG: snprintf(buf, len, "option flag must be +1 (call) or -1 (put)"); break;
+    case FV_CHECK_NONFINITE_UNDERLYING: case FV_CHECK_NONFINITE_STRIKE: case FV_CHECK_NONFINITE_T:
+    case FV_CHECK_NONFINITE_R: case FV_CHECK_NONFINITE_Q:
+      snprintf(buf, len, "column %s is not finite", cols[c - 1]); break;
+    case FV_CHECK_NONFINITE_LAST:
+      snprintf(buf, len, "column %s is not finite", has_sigma ? "sigma" : "price"); break;
+    case FV_CHECK_POSITIVE_UNDERLYING: snprintf(buf, len, "column underlying must be positive"); break;
+    case FV_CHECK_POSITIVE_STRIKE: snprintf(buf, len, "column strike must be positive"); break;
+    case FV_CHECK_NONNEG_T: snprintf(buf, len, "column t must be >= 0"); break;
+    case FV_CHECK_NONNEG_SIGMA: snprintf(buf, len, "column sigma must be >= 0"); break;
+    case FV_CHECK_DIVIDEND: snprintf(buf, len, "model does not accept a dividend yield"); break;
+    default: snprintf(buf, len, "check %d", c);
+  }
+  return buf;
+}
+
+const int kCheckColumn[FV_NCHECK] = {0, 1, 2, 3, 4, 5, 6, 1, 2, 3, 6, 5};
+
+void fill_exc_message(fv_error* e) {
+  const char* txt = "";
+  switch (e->kind) {
+    case FV_EXC_MATH_RANGE: txt = "OverflowError: math range error"; break;
+    case FV_EXC_MATH_DOMAIN: txt = "ValueError: math domain error"; break;
+    case FV_EXC_ZERO_DIV: txt = "ZeroDivisionError: float division by zero"; break;
+    case FV_EXC_POW_RANGE: txt = "OverflowError: (34, 'Numerical result out of range')"; break;
+    case FV_EXC_DOM_FK: txt = "DomainError: F and K must be positive"; break;
+    case FV_EXC_DOM_ATM_BETA: txt = "DomainError: atm_inverse requires beta in (0, 1)"; break;
+    case FV_EXC_DOM_INVCDF_P: txt = "DomainError: inv_norm_cdf requires p in (0, 1)"; break;
+    case FV_EXC_DOM_NB_X: txt = "DomainError: normalized_black requires x <= 0"; break;
+    case FV_EXC_DOM_NB_S: txt = "DomainError: normalized_black requires s > 0"; break;
+    case FV_EXC_DOM_OBJ_S: txt = "DomainError: objective_branch requires s > 0"; break;
+  }
+  snprintf(e->message, sizeof(e->message), "%s (row %lld)", txt, (long long)e->index);
+}
+
+void set_ok(fv_error* e) {
+  if (!e) return;
+  memset(e, 0, sizeof(*e));
+  e->index = -1;
+}
+int set_cuda_err(fv_error* e, cudaError_t ce) {
+  if (e) {
+    memset(e, 0, sizeof(*e));
+    e->code = FV_ERR_CUDA;
+    e->index = -1;
+    snprintf(e->message, sizeof(e->message), "CUDA error: %s", cudaGetErrorString(ce));
+  }
+  return FV_ERR_CUDA;
+}
+int set_arg_err(fv_error* e, const char* msg) {
+  if (e) {
+    memset(e, 0, sizeof(*e));
+    e->code = FV_ERR_ARG;
+    e->index = -1;
+    snprintf(e->message, sizeof(e->message), "%s", msg);
+  }
+  return FV_ERR_ARG;
+}
+
+// Host-side checks for broadcast columns (row 0 is their only row).
+uint32_t bcast_checks(const Call& c, const double vals[7], int flag_val, const bool bc[7]) {
+  uint32_t b = 0;
+  bool has_sigma = c.kind != KIND_IV;
+  if (bc[0]) b |= (uint32_t)(flag_val != 1 && flag_val != -1) << FV_CHECK_BAD_FLAG;
+  for (int col = 1; col <= 6; ++col)
+    if (bc[col]) b |= (uint32_t)(!fv_isfinite(vals[col])) << (FV_CHECK_NONFINITE_UNDERLYING + col - 1);
+  if (bc[1]) b |= (uint32_t)(!(vals[1] > 0.0)) << FV_CHECK_POSITIVE_UNDERLYING;
+  if (bc[2]) b |= (uint32_t)(!(vals[2] > 0.0)) << FV_CHECK_POSITIVE_STRIKE;
+  if (bc[3]) b |= (uint32_t)(vals[3] < 0.0) << FV_CHECK_NONNEG_T;
+  if (bc[6] && has_sigma) b |= (uint32_t)(vals[6] < 0.0) << FV_CHECK_NONNEG_SIGMA;
+  if (bc[5]) b |= (uint32_t)(c.model != FV_MODEL_BLACK_SCHOLES_MERTON && vals[5] != 0.0) << FV_CHECK_DIVIDEND;
+  return b;
+}
+
+// Resolve the device status into the two fv_error records.
+int finish(DevWork* w, const Call& c, const KArgs& a0, uint32_t bcast_bits, cudaStream_t s,
+           fv_error* e1, fv_error* e2) {
+  FvDevStatus& st = *w->st_host;
+  bool has_sigma = c.kind != KIND_IV;
+  // BatchError: first check in order that failed anywhere
+  for (int ck = 0; ck < FV_NCHECK; ++ck) {
+    unsigned long long row = st.check_first[ck];
+    if (bcast_bits & (1u << ck)) row = 0;
+    if (row != ~0ull) {
+      fv_error* outs[2] = {e1, e2};
+      for (fv_error* e : outs) {
+        if (!e) continue;
+        memset(e, 0, sizeof(*e));
+        e->code = FV_ERR_BATCH;
+        e->kind = ck;
+        e->index = (int64_t)row;
+        e->column = kCheckColumn[ck];
+        char detail[128];
+        check_name(ck, has_sigma, detail, sizeof(detail));
+        const char* kindname = ck == FV_CHECK_BAD_FLAG ? "BadFlag"
+                               : (ck <= FV_CHECK_NONFINITE_LAST ? "NonFiniteInput" : "DomainError");
+        snprintf(e->message, sizeof(e->message), "%s at row %lld: %s", kindname, (long long)row, detail);
+      }
+      return FV_ERR_BATCH;
+    }
+  }
+  int rc = FV_OK;
+  unsigned long long ex[2] = {st.exc_first, st.exc2_first};
+  fv_error* outs[2] = {e1, e2};
+  for (int k = 0; k < 2; ++k) {
+    fv_error* e = outs[k];
+    if (e) set_ok(e);
+    if (ex[k] == ~0ull) continue;
+    rc = FV_ERR_PYEXC;
+    if (!e) continue;
+    e->code = FV_ERR_PYEXC;
+    e->kind = (int)(ex[k] & 0xff);
+    e->index = (int64_t)(ex[k] >> 8);
+    if (e->kind >= FV_EXC_DOM_ATM_BETA && c.kind == KIND_IV && a0.n > 0) {
+      // re-run the row once to recover the value the message quotes
+      k_explain<<<1, 1, 0, s>>>(a0, c.method, e->index - a0.row0, w->explain);
+      ++t_launches;
+      ExplainOut eo;
+      cudaMemcpyAsync(&eo, w->explain, sizeof(eo), cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      e->value = eo.val;
+      e->value_is_numpy = eo.np;
+    }
+    fill_exc_message(e);
+  }
+  return rc;
+}
+
+DCol make_dcol(const fv_col& c, const void* base_override) {
+  DCol d;
+  d.p = (const double*)(base_override ? base_override : c.data);
+  d.stride = c.stride;
+  if (c.stride == 0) d.mode = 0;
+  else if (c.stride == 1 && (((uintptr_t)d.p) & 15) == 0) d.mode = 1;
+  else d.mode = 2;
+  return d;
+}
+DFlag make_dflag(const fv_col& c, const void* base_override) {
+  DFlag d;
+  d.p = (const int8_t*)(base_override ? base_override : c.data);
+  d.stride = c.stride;
+  if (c.stride == 0) d.mode = 0;
+  else if (c.stride == 1 && (((uintptr_t)d.p) & 1) == 0) d.mode = 1;
+  else d.mode = 2;
+  return d;
+}
+
+KArgs base_args(const Call& c, DevWork* w) {
+  KArgs a;
+  memset(&a, 0, sizeof(a));
+  a.model = c.model;
+  a.has_sigma = c.kind != KIND_IV;
+  uint32_t mask = (1u << FV_NCHECK) - 1;
+  if (!a.has_sigma) mask &= ~(1u << FV_CHECK_NONNEG_SIGMA);
+  // broadcast columns are checked on the host (once), not per row
+  const int col_checks[7][3] = {{FV_CHECK_BAD_FLAG, -1, -1},
+                                {FV_CHECK_NONFINITE_UNDERLYING, FV_CHECK_POSITIVE_UNDERLYING, -1},
+                                {FV_CHECK_NONFINITE_STRIKE, FV_CHECK_POSITIVE_STRIKE, -1},
+                                {FV_CHECK_NONFINITE_T, FV_CHECK_NONNEG_T, -1},
+                                {FV_CHECK_NONFINITE_R, -1, -1},
+                                {FV_CHECK_NONFINITE_Q, FV_CHECK_DIVIDEND, -1},
+                                {FV_CHECK_NONFINITE_LAST, FV_CHECK_NONNEG_SIGMA, -1}};
+  for (int col = 0; col < 7; ++col)
+    if (c.cols[col].stride == 0)
+      for (int j = 0; j < 3; ++j)
+        if (col_checks[col][j] >= 0) mask &= ~(1u << col_checks[col][j]);
+  a.check_mask = mask;
+  a.st = w->st;
+  a.status = c.status;
+  a.region = c.region;
+  return a;
+}
+
+bool outs_aligned(const Call& c, double* const* outs) {
+  for (int i = 0; i < 6; ++i)
+    if (outs[i] && (((uintptr_t)outs[i]) & 15)) return false;
+  (void)c;
+  return true;
+}
+
+int run_device(DevWork* w, const Call& c, cudaStream_t s, uint32_t bcast_bits, fv_error* e1,
+               fv_error* e2) {
+  cudaError_t ce;
+  KArgs a = base_args(c, w);
+  a.flag = make_dflag(c.cols[0], nullptr);
+  a.un = make_dcol(c.cols[1], nullptr);
+  a.k = make_dcol(c.cols[2], nullptr);
+  a.t = make_dcol(c.cols[3], nullptr);
+  a.r = make_dcol(c.cols[4], nullptr);
+  a.q = make_dcol(c.cols[5], nullptr);
+  a.last = make_dcol(c.cols[6], nullptr);
+  a.n = c.n;
+  a.row0 = 0;
+  a.o0 = c.outs[0]; a.o1 = c.outs[1]; a.o2 = c.outs[2];
+  a.o3 = c.outs[3]; a.o4 = c.outs[4]; a.o5 = c.outs[5];
+  a.out_vec = outs_aligned(c, c.outs);
+  if ((ce = cudaMemsetAsync(w->st, 0xff, sizeof(FvDevStatus), s)) != cudaSuccess) return set_cuda_err(e1, ce);
+  if ((ce = launch(w, c, a, 0, s)) != cudaSuccess) return set_cuda_err(e1, ce);
+  if ((ce = cudaMemcpyAsync(w->st_host, w->st, sizeof(FvDevStatus), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return set_cuda_err(e1, ce);
+  if ((ce = cudaStreamSynchronize(s)) != cudaSuccess) return set_cuda_err(e1, ce);
+  return finish(w, c, a, bcast_bits, s, e1, e2);
+}
+
+// Host-pointer path: chunked H2D -> kernel -> D2H, FV_NSLOT streams.
+int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_error* e2) {
+  cudaError_t ce;
+  const int64_t chunk = g_chunk_rows;
+  const int64_t n = c.n;
+  // column element sizes and whether each is streamed
+  const size_t in_sz[7] = {1, 8, 8, 8, 8, 8, 8};
+  int nout = 0;
+  for (int i = 0; i < 6; ++i) if (c.outs[i]) ++nout;
+  bool has_status = c.status != nullptr, has_region = c.region != nullptr;
+  // per-slot layout: [inputs (streamed cols)] [outputs] [status] [region], 256B aligned
+  auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  size_t slot_bytes = 0;
+  size_t off_in[7], off_out[6], off_status = 0, off_region = 0;
+  for (int col = 0; col < 7; ++col) {
+    off_in[col] = slot_bytes;
+    if (c.cols[col].stride != 0) slot_bytes += align(in_sz[col] * chunk);
+  }
+  for (int i = 0; i < 6; ++i) { off_out[i] = slot_bytes; if (c.outs[i]) slot_bytes += align(8 * chunk); }
+  off_status = slot_bytes; if (has_status) slot_bytes += align(chunk);
+  off_region = slot_bytes; if (has_region) slot_bytes += align(chunk);
+  for (int s = 0; s < FV_NSLOT; ++s) {
+    if (w->chunk_cap_rows[s] < (int64_t)slot_bytes) {
+      if (w->chunk[s]) cudaFree(w->chunk[s]);
+      if ((ce = cudaMalloc(&w->chunk[s], slot_bytes)) != cudaSuccess) return set_cuda_err(e1, ce);
+      w->chunk_cap_rows[s] = (int64_t)slot_bytes;
+    }
+  }
+  if ((ce = cudaMemsetAsync(w->st, 0xff, sizeof(FvDevStatus), w->streams[0])) != cudaSuccess)
+    return set_cuda_err(e1, ce);
+  cudaEvent_t ready;
+  cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  cudaEventRecord(ready, w->streams[0]);
+  for (int s = 1; s < FV_NSLOT; ++s) cudaStreamWaitEvent(w->streams[s], ready, 0);
+  KArgs a_first;
+  memset(&a_first, 0, sizeof(a_first));
+  int64_t nchunks = (n + chunk - 1) / chunk;
+  for (int64_t ci = 0; ci < nchunks; ++ci) {
+    int slot = (int)(ci % FV_NSLOT);
+    cudaStream_t s = w->streams[slot];
+    int64_t r0 = ci * chunk, rn = (r0 + chunk < n ? chunk : n - r0);
+    char* base = w->chunk[slot];
+    void* dev_in[7];
+    for (int col = 0; col < 7; ++col) {
+      if (c.cols[col].stride == 0) { dev_in[col] = nullptr; continue; }
+      dev_in[col] = base + off_in[col];
+      const char* src = (const char*)c.cols[col].data + r0 * in_sz[col];
+      if ((ce = cudaMemcpyAsync(dev_in[col], src, rn * in_sz[col], cudaMemcpyHostToDevice, s)) != cudaSuccess) {
+        cudaEventDestroy(ready);
+        return set_cuda_err(e1, ce);
+      }
+    }
+    KArgs a = base_args(c, w);
+    a.flag = make_dflag(c.cols[0], dev_in[0]);
+    a.un = make_dcol(c.cols[1], dev_in[1]);
+    a.k = make_dcol(c.cols[2], dev_in[2]);
+    a.t = make_dcol(c.cols[3], dev_in[3]);
+    a.r = make_dcol(c.cols[4], dev_in[4]);
+    a.q = make_dcol(c.cols[5], dev_in[5]);
+    a.last = make_dcol(c.cols[6], dev_in[6]);
+    a.n = rn;
+    a.row0 = r0;
+    double* douts[6];
+    for (int i = 0; i < 6; ++i) douts[i] = c.outs[i] ? (double*)(base + off_out[i]) : nullptr;
+    a.o0 = douts[0]; a.o1 = douts[1]; a.o2 = douts[2]; a.o3 = douts[3]; a.o4 = douts[4]; a.o5 = douts[5];
+    a.out_vec = 1;
+    a.status = has_status ? (int8_t*)(base + off_status) : nullptr;
+    a.region = has_region ? (int8_t*)(base + off_region) : nullptr;
+    if (ci == 0) a_first = a;
+    if ((ce = launch(w, c, a, slot, s)) != cudaSuccess) { cudaEventDestroy(ready); return set_cuda_err(e1, ce); }
+    for (int i = 0; i < 6; ++i)
+      if (c.outs[i]) cudaMemcpyAsync(c.outs[i] + r0, douts[i], 8 * rn, cudaMemcpyDeviceToHost, s);
+    if (has_status) cudaMemcpyAsync(c.status + r0, a.status, rn, cudaMemcpyDeviceToHost, s);
+    if (has_region) cudaMemcpyAsync(c.region + r0, a.region, rn, cudaMemcpyDeviceToHost, s);
+  }
+  for (int s = 1; s < FV_NSLOT; ++s) {
+    cudaEventRecord(ready, w->streams[s]);
+    cudaStreamWaitEvent(w->streams[0], ready, 0);
+  }
+  cudaEventDestroy(ready);
+  cudaStream_t s0 = w->streams[0];
+  if ((ce = cudaMemcpyAsync(w->st_host, w->st, sizeof(FvDevStatus), cudaMemcpyDeviceToHost, s0)) != cudaSuccess)
+    return set_cuda_err(e1, ce);
+  if ((ce = cudaStreamSynchronize(s0)) != cudaSuccess) return set_cuda_err(e1, ce);
+  for (int s = 1; s < FV_NSLOT; ++s)
+    if ((ce = cudaStreamSynchronize(w->streams[s])) != cudaSuccess) return set_cuda_err(e1, ce);
+  if ((ce = cudaGetLastError()) != cudaSuccess) return set_cuda_err(e1, ce);
+  // exceptions in later chunks: the explain kernel needs that chunk's inputs;
+  // re-stage the offending row alone.
+  FvDevStatus& st = *w->st_host;
+  unsigned long long ex = st.exc_first;
+  KArgs ax = a_first;
+  if (ex != ~0ull && c.kind == KIND_IV && (int)(ex & 0xff) >= FV_EXC_DOM_ATM_BETA) {
+    int64_t row = (int64_t)(ex >> 8);
+    char* base = w->chunk[0];
+    void* dev_in[7];
+    for (int col = 0; col < 7; ++col) {
+      if (c.cols[col].stride == 0) { dev_in[col] = nullptr; continue; }
+      dev_in[col] = base + off_in[col];
+      cudaMemcpy(dev_in[col], (const char*)c.cols[col].data + row * in_sz[col], in_sz[col], cudaMemcpyHostToDevice);
+    }
+    ax.flag = make_dflag(c.cols[0], dev_in[0]);
+    ax.un = make_dcol(c.cols[1], dev_in[1]);
+    ax.k = make_dcol(c.cols[2], dev_in[2]);
+    ax.t = make_dcol(c.cols[3], dev_in[3]);
+    ax.r = make_dcol(c.cols[4], dev_in[4]);
+    ax.q = make_dcol(c.cols[5], dev_in[5]);
+    ax.last = make_dcol(c.cols[6], dev_in[6]);
+    ax.n = 1;
+    ax.row0 = row;
+  }
+  return finish(w, c, ax, bcast_bits, s0, e1, e2);
+}
+
+// For host calls, broadcast columns must be readable on the device.
+int dispatch(Call c, fv_error* e1, fv_error* e2) {
+  t_launches = 0;
+  set_ok(e1);
+  set_ok(e2);
+  if (c.n < 0) return set_arg_err(e1, "n must be >= 0");
+  if (c.model < 0 || c.model > 2) return set_arg_err(e1, "unknown model");
+  if (c.kind == KIND_IV && c.method != FV_METHOD_HALLEY && c.method != FV_METHOD_LBR)
+    return set_arg_err(e1, "unknown IV method");
+  for (int i = 0; i < 7; ++i)
+    if (!c.cols[i].data) return set_arg_err(e1, "null input column");
+  DevWork* w = nullptr;
+  cudaError_t ce = get_work(&w);
+  if (ce != cudaSuccess) return set_cuda_err(e1, ce);
+  std::lock_guard<std::mutex> g(w->mu);
+  // memory space: all device or all host
+  int ndev = 0, nptr = 0;
+  for (int i = 0; i < 7; ++i) { ++nptr; ndev += is_device_ptr(c.cols[i].data); }
+  for (int i = 0; i < 6; ++i) if (c.outs[i]) { ++nptr; ndev += is_device_ptr(c.outs[i]); }
+  if (c.status) { ++nptr; ndev += is_device_ptr(c.status); }
+  if (c.region) { ++nptr; ndev += is_device_ptr(c.region); }
+  bool device = ndev == nptr;
+  if (ndev != 0 && !device) return set_arg_err(e1, "all pointers of a call must be device pointers or all host pointers");
+  // broadcast scalars: checked once on the host; for host calls they are
+  // copied into a small device buffer.
+  bool bc[7];
+  double vals[7] = {0, 0, 0, 0, 0, 0, 0};
+  int flag_val = 0;
+  for (int i = 0; i < 7; ++i) bc[i] = c.cols[i].stride == 0;
+  double* dscal = nullptr;
+  int8_t* dflag = nullptr;
+  if (bc[0]) {
+    if (device) cudaMemcpy(&flag_val, c.cols[0].data, 1, cudaMemcpyDeviceToHost), flag_val = (int)(int8_t)flag_val;
+    else flag_val = *(const int8_t*)c.cols[0].data;
+  }
+  for (int i = 1; i < 7; ++i)
+    if (bc[i]) {
+      if (device) cudaMemcpy(&vals[i], c.cols[i].data, 8, cudaMemcpyDeviceToHost);
+      else vals[i] = *(const double*)c.cols[i].data;
+    }
+  uint32_t bbits = c.n > 0 ? bcast_checks(c, vals, flag_val, bc) : 0;
+  if (!device) {
+    // device copies of the broadcast scalars (8 doubles, one allocation per call)
+    if ((ce = cudaMalloc(&dscal, 8 * 8)) != cudaSuccess) return set_cuda_err(e1, ce);
+    double tmp[8] = {0};
+    int8_t f8 = (int8_t)flag_val;
+    memcpy(&tmp[7], &f8, 1);
+    for (int i = 1; i < 7; ++i) tmp[i] = vals[i];
+    cudaMemcpy(dscal, tmp, sizeof(tmp), cudaMemcpyHostToDevice);
+    dflag = (int8_t*)(dscal + 7);
+    for (int i = 0; i < 7; ++i)
+      if (bc[i]) c.cols[i].data = (i == 0) ? (const void*)dflag : (const void*)(dscal + i);
+  }
+  int rc;
+  if (device) {
+    cudaStream_t s = t_user_stream ? t_user_stream : w->streams[0];
+    rc = run_device(w, c, s, bbits, e1, e2);
+  } else {
+    rc = run_host(w, c, bbits, e1, e2);
+  }
+  if (dscal) cudaFree(dscal);
+  return rc;
+}
+
+Call make_call(Kind kind, int model, int method, fv_col flag, fv_col un, fv_col k, fv_col t,
+               fv_col r, fv_col q, fv_col last, int64_t n) {
+  Call c;
+  memset(&c, 0, sizeof(c));
+  c.kind = kind; c.model = model; c.method = method;
+  c.cols[0] = flag; c.cols[1] = un; c.cols[2] = k; c.cols[3] = t;
+  c.cols[4] = r; c.cols[5] = q; c.cols[6] = last;
+  c.n = n;
+  return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+FV_API int fv_batch_price(int model, fv_col flag, fv_col underlying, fv_col strike, fv_col t,
+                          fv_col r, fv_col q, fv_col sigma, int64_t n, double* price,
+                          fv_error* err) {
+  Call c = make_call(KIND_PRICE, model, 0, flag, underlying, strike, t, r, q, sigma, n);
+  c.outs[0] = price;
+  if (!price && n > 0) return set_arg_err(err, "null output");
+  return dispatch(c, err, nullptr);
+}
+
+FV_API int fv_batch_iv(int model, int method, fv_col flag, fv_col underlying, fv_col strike,
+                       fv_col t, fv_col r, fv_col q, fv_col price, int64_t n, double* iv,
+                       int8_t* status, int8_t* region, fv_error* err) {
+  Call c = make_call(KIND_IV, model, method, flag, underlying, strike, t, r, q, price, n);
+  c.outs[0] = iv;
+  c.status = status;
+  c.region = region;
+  if ((!iv || !status) && n > 0) return set_arg_err(err, "null output");
+  return dispatch(c, err, nullptr);
+}
+
+FV_API int fv_batch_greeks(int model, fv_col flag, fv_col underlying, fv_col strike, fv_col t,
+                           fv_col r, fv_col q, fv_col sigma, int64_t n, double* delta,
+                           double* gamma, double* theta, double* rho, double* vega,
+                           int8_t* status, fv_error* err) {
+  Call c = make_call(KIND_GREEKS, model, 0, flag, underlying, strike, t, r, q, sigma, n);
+  c.outs[1] = delta; c.outs[2] = gamma; c.outs[3] = theta; c.outs[4] = rho; c.outs[5] = vega;
+  c.status = status;
+  c.want_greeks = true;
+  if ((!delta || !gamma || !theta || !rho || !vega || !status) && n > 0)
+    return set_arg_err(err, "null output");
+  fv_error unused;
+  return dispatch(c, &unused, err);
+}
+
+FV_API int fv_price_greeks(int model, fv_col flag, fv_col underlying, fv_col strike, fv_col t,
+                           fv_col r, fv_col q, fv_col sigma, int64_t n, double* price,
+                           double* delta, double* gamma, double* theta, double* rho,
+                           double* vega, int8_t* status, fv_error* err_price,
+                           fv_error* err_greeks) {
+  Call c = make_call(KIND_PRICE_GREEKS, model, 0, flag, underlying, strike, t, r, q, sigma, n);
+  c.outs[0] = price;
+  c.outs[1] = delta; c.outs[2] = gamma; c.outs[3] = theta; c.outs[4] = rho; c.outs[5] = vega;
+  c.status = status;
+  c.want_price = price != nullptr;
+  c.want_greeks = delta || gamma || theta || rho || vega || status;
+  if (!c.want_price && !c.want_greeks) return set_arg_err(err_price, "no outputs requested");
+  if (c.want_greeks && (!delta || !gamma || !theta || !rho || !vega || !status))
+    return set_arg_err(err_price, "Greeks outputs must be all set or all NULL");
+  fv_error ep, eg;
+  int rc = dispatch(c, &ep, &eg);
+  if (err_price) *err_price = ep;
+  if (err_greeks) *err_greeks = eg;
+  if (rc == FV_ERR_PYEXC) {
+    bool any = (c.want_price && ep.code) || (c.want_greeks && eg.code);
+    if (!any) rc = FV_OK;
+    if (!c.want_price && err_price) set_ok(err_price);
+    if (!c.want_greeks && err_greeks) set_ok(err_greeks);
+  }
+  return rc;
+}
+
+FV_API int fv_set_stream(void* stream) {
+  t_user_stream = (cudaStream_t)stream;
+  return FV_OK;
+}
+
+FV_API int fv_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) { cudaGetLastError(); return 0; }
+  return n;
+}
+
+FV_API const char* fv_version(void) { return FV_VERSION; }
+
+FV_API int fv_set_chunk_rows(int64_t rows) {
+  if (rows < 1024) return FV_ERR_ARG;
+  g_chunk_rows = rows;
+  return FV_OK;
+}
+
+FV_API int64_t fv_last_launch_count(void) { return t_launches; }
+
+// Measured FP64 DFMA issue rate of the current device (DFMA instructions per
+// second across the chip), timed with CUDA events.
+FV_API int fv_probe_fp64_peak(double* dfma_per_s, double* seconds) {
+  int dev = 0, sm = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FV_ERR_CUDA;
+  cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_fp64_probe, 256, 0);
+  if (per_sm < 1) per_sm = 1;
+  int blocks = sm * per_sm;
+  double* out = nullptr;
+  if (cudaMalloc(&out, sizeof(double) * blocks * 256) != cudaSuccess) return FV_ERR_CUDA;
+  const int iters = 4096;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  k_fp64_probe<<<blocks, 256>>>(out, 64, 0.999999, 1e-7);          // warm-up
+  cudaEventRecord(e0);
+  k_fp64_probe<<<blocks, 256>>>(out, iters, 0.999999, 1e-7);
+  cudaEventRecord(e1);
+  cudaError_t ce = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  cudaFree(out);
+  if (ce != cudaSuccess) return FV_ERR_CUDA;
+  double dfma = (double)blocks * 256.0 * iters * 16.0 * 8.0;
+  if (dfma_per_s) *dfma_per_s = dfma / (ms * 1e-3);
+  if (seconds) *seconds = ms * 1e-3;
+  return FV_OK;
+}
+
+}  // extern "C"

@@ -27,8 +27,10 @@
 
 #if defined(__CUDACC__)
 #define FV_HD __host__ __device__ __forceinline__
+#define FV_HDM __host__ __device__ __forceinline__
 #else
 #define FV_HD static inline
+#define FV_HDM inline
 #endif
 
 // ---- tables: host copy (static arrays) + device copy (global memory) -------

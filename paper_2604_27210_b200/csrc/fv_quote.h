@@ -1,0 +1,721 @@
+// fv_quote.h -- per-quote device code for the batched pricing / Greeks /
+// implied-vol path, __host__ __device__ (the CUDA kernels in fv_kernels.cu
+// instantiate it; tests/native/quote_hostcheck.cpp compiles the same source
+// for CPU pre-checks against the oracle).
+//
+// Restates, bit for bit, the reference's per-row arithmetic:
+//   pricing.py:23-61 (black_kernel, price_black76, price_bsm)
+//   greeks.py:45-98  (_core)
+//   solver.py:40-161 (_raw_vega, implied_vol_halley)
+//   lbr.py:48-486    (normalized Black, normalize_quote, anchors/regions,
+//                     initial guesses, objective branches, Householder(3))
+//   distributions.py:19-95 (norm_cdf, norm_pdf, AS241 inverse)
+// on top of fv_libm.h (glibc/scipy-faithful exp/log/pow/erfc/erfcx).
+//
+// Differences from the Python are restricted to bit-neutral restructuring:
+//   * common subexpressions computed once (the second _anchors() call of
+//     initial_guess, lbr.py:325; the duplicated normalized_black_log in the
+//     far-low Newton step, lbr.py:293/:299; log(F/K) and sqrt(t) inside the
+//     Halley loop, solver.py:45/:122; the per-quote constants exp(+-x/2),
+//     b_max - beta and ln(beta) of the far-high / far-low objectives; the
+//     exp(-(h^2+t^2)/2) shared by normalized_black and normalized_vega);
+//   * the discarded LBR residual (lbr.py:429, :484) is not evaluated -- it
+//     cannot raise for any quote that reaches it (|x| <= 1419.6 there, so its
+//     b_max = exp(x/2) > 0);
+//   * Python exceptions are reported as codes (fv_exc) instead of unwinding;
+//     every raising site is kept, with the Python-float vs numpy.float64
+//     operand typing that decides whether a division by zero raises.
+#pragma once
+#include "fv_libm.h"
+
+// ---- exception codes (same numbering as oracle/fvoracle.cpp) ---------------
+#define FV_EXC_NONE 0
+#define FV_EXC_MATH_RANGE 1     // OverflowError('math range error')
+#define FV_EXC_MATH_DOMAIN 2    // ValueError('math domain error')
+#define FV_EXC_ZERO_DIV 3       // ZeroDivisionError('float division by zero')
+#define FV_EXC_POW_RANGE 4      // OverflowError(34, 'Numerical result out of range')
+#define FV_EXC_DOM_FK 5         // DomainError('F and K must be positive')
+#define FV_EXC_DOM_ATM_BETA 6   // DomainError('atm_inverse requires beta in (0, 1), got ...')
+#define FV_EXC_DOM_INVCDF_P 7   // DomainError('inv_norm_cdf requires p in (0, 1), got ...')
+#define FV_EXC_DOM_NB_X 8       // DomainError('normalized_black requires x <= 0, got ...')
+#define FV_EXC_DOM_NB_S 9       // DomainError('normalized_black requires s > 0, got ...')
+#define FV_EXC_DOM_OBJ_S 10     // DomainError('objective_branch requires s > 0, got ...')
+
+// ---- statuses (solver.py:14-19; batch.py:270-274) --------------------------
+#define FV_IV_CONVERGED 0
+#define FV_IV_FELL_BACK 1
+#define FV_IV_BELOW_INTRINSIC 2
+#define FV_IV_ABOVE_UPPER 3
+#define FV_IV_MAX_ITER 4
+#define FV_GK_OK 0
+#define FV_GK_EDGE 1
+
+#define FV_REGION_NONE (-1)
+#define FV_FAR_LOW 0
+#define FV_NEAR_LOW 1
+#define FV_NEAR_HIGH 2
+#define FV_FAR_HIGH 3
+
+struct FvExc {
+  int code;
+  int np;      // value is a numpy.float64 (repr "np.float64(...)")
+  double val;  // value quoted by DomainError messages
+  FV_HDM void raise(int c) { if (code == FV_EXC_NONE) { code = c; } }
+  FV_HDM void raise_v(int c, double v, int is_np) {
+    if (code == FV_EXC_NONE) { code = c; val = v; np = is_np; }
+  }
+};
+
+// ---- CPython semantics -----------------------------------------------------
+FV_HD double py_exp(double x, FvExc& e) {           // math.exp (math_1, can_overflow)
+  double r = fv_exp(x);
+  if (fv_isinf(r) && fv_isfinite(x)) e.raise(FV_EXC_MATH_RANGE);
+  return r;
+}
+FV_HD double py_log(double x, FvExc& e) {           // math.log (m_log)
+  if (fv_isfinite(x)) {
+    if (x > 0.0) return fv_log(x);
+    e.raise(FV_EXC_MATH_DOMAIN);
+    return x == 0.0 ? -__builtin_inf() : __builtin_nan("");
+  }
+  if (fv_isnan(x) || x > 0.0) return x;
+  e.raise(FV_EXC_MATH_DOMAIN);
+  return __builtin_nan("");
+}
+FV_HD double py_sqrt(double x, FvExc& e) {          // math.sqrt
+  double r = sqrt(x);
+  if (fv_isnan(r) && !fv_isnan(x)) e.raise(FV_EXC_MATH_DOMAIN);
+  return r;
+}
+// float / float raises on a zero divisor; any numpy.float64 operand does not.
+FV_HD double py_div(double a, double b, bool np, FvExc& e) {
+  if (!np && b == 0.0) e.raise(FV_EXC_ZERO_DIV);
+  return a / b;
+}
+// x ** n, n in {2,3,4}: float_pow for Python floats (OverflowError on an
+// infinite result from finite x), npy_pow for numpy scalars; both reach
+// glibc pow for finite x != 0 (|x| via CPython's sign handling).
+FV_HD double py_powi(double x, int n, bool np, FvExc& e) {
+  if (!fv_isfinite(x) || x == 0.0) {
+    if (fv_isnan(x)) return x;
+    if (x == 0.0) return (n & 1) ? x : 0.0;
+    return (x < 0.0 && (n & 1)) ? -__builtin_inf() : __builtin_inf();
+  }
+  double r = fv_pow_pos(fv_fabs(x), (double)n);
+  if (x < 0.0 && (n & 1)) r = -r;
+  if (!np && fv_isinf(r)) e.raise(FV_EXC_POW_RANGE);
+  return r;
+}
+FV_HD double py_max(double a, double b) { return (b > a) ? b : a; }   // builtins.max
+FV_HD double py_min(double a, double b) { return (b < a) ? b : a; }   // builtins.min
+
+// ---- distributions.py ------------------------------------------------------
+FV_HD double fv_norm_cdf(double x) { return 0.5 * fv_erfc(-x / FV_SQRT_TWO); }
+FV_HD double fv_norm_pdf(double x) { return FV_INV_SQRT_TWO_PI * fv_exp(-0.5 * x * x); }
+
+FV_HD double as241_poly(double c0, double c1, double c2, double c3, double c4, double c5,
+                        double c6, double c7, double r) {
+  double acc = 0.0;                              // distributions.py:56-60 (Horner from 0.0)
+  acc = acc * r + c7; acc = acc * r + c6; acc = acc * r + c5; acc = acc * r + c4;
+  acc = acc * r + c3; acc = acc * r + c2; acc = acc * r + c1; acc = acc * r + c0;
+  return acc;
+}
+#define FV_AS241_POLY(L, r) as241_poly(FV_AS241_##L##0, FV_AS241_##L##1, FV_AS241_##L##2, \
+  FV_AS241_##L##3, FV_AS241_##L##4, FV_AS241_##L##5, FV_AS241_##L##6, FV_AS241_##L##7, r)
+
+// inv_norm_cdf (distributions.py:63-95).  p_np: p is a numpy scalar.  On
+// return *x_np is the type of the result (for the caller's later divisions).
+FV_HD double fv_inv_norm_cdf(double p, bool p_np, bool* x_np, FvExc& e) {
+  if (!(0.0 < p && p < 1.0)) { e.raise_v(FV_EXC_DOM_INVCDF_P, p, p_np); *x_np = p_np; return __builtin_nan(""); }
+  double q = p - 0.5;
+  double x;
+  bool xnp;
+  if (fv_fabs(q) <= 0.425) {
+    double r = 0.180625 - q * q;
+    x = q * FV_AS241_POLY(A, r) / FV_AS241_POLY(B, r);
+    xnp = p_np;
+  } else {
+    double r = (q < 0.0) ? p : (1.0 - p);
+    r = py_sqrt(-py_log(r, e), e);
+    double val;
+    if (r <= 5.0) {
+      r = r - 1.6;
+      val = py_div(FV_AS241_POLY(C, r), FV_AS241_POLY(D, r), false, e);
+    } else {
+      r = r - 5.0;
+      val = py_div(FV_AS241_POLY(E, r), FV_AS241_POLY(F, r), false, e);
+    }
+    x = (q < 0.0) ? -val : val;
+    xnp = false;
+  }
+  double pdf = fv_norm_pdf(x);
+  if (pdf > 0.0) {
+    double err = fv_norm_cdf(x) - p;
+    double u = py_div(err, pdf, p_np, e);
+    bool unp = p_np;
+    x = x - py_div(u, 1.0 + 0.5 * x * u, unp || xnp, e);
+    xnp = xnp || unp;
+  }
+  *x_np = xnp;
+  return x;
+}
+
+// ---- pricing.py black_kernel (:23-33) ---------------------------------------
+// lnFK = log(F/K) computed by the caller (bit-identical each call); fk_bad:
+// F/K <= 0 so math.log raises once the kernel reaches it.
+FV_HD double fv_black_kernel(double th, double Fw, double K, double disc, double s,
+                             double lnFK, bool fk_bad, FvExc& e) {
+  double intrinsic = py_max(th * (Fw - K), 0.0);
+  double cap = (th > 0.0) ? Fw : K;
+  if (s < 1e-12) return disc * intrinsic;
+  if (fk_bad) e.raise(FV_EXC_MATH_DOMAIN);
+  double d1 = (lnFK + 0.5 * s * s) / s;
+  double d2 = d1 - s;
+  double raw = th * (Fw * fv_norm_cdf(th * d1) - K * fv_norm_cdf(th * d2));
+  return disc * py_min(py_max(raw, intrinsic), cap);
+}
+
+// math.log(F / K) evaluated once per quote; *bad: the call raises
+// ValueError('math domain error') whenever the reference reaches it.
+FV_HD double fv_log_fk(double FK, bool* bad) {
+  FvExc tmp = {0, 0, 0.0};
+  double v = py_log(FK, tmp);
+  *bad = tmp.code != FV_EXC_NONE;
+  return v;
+}
+
+// batch_price row (batch.py:195-198): model 0 = Black-76, else spot (BS/BSM).
+FV_HD double fv_price_row(int model, double th, double un, double K, double t, double r,
+                          double q, double sigma, FvExc& e) {
+  double Fw = un;
+  if (model != 0) Fw = un * py_exp((r - q) * t, e);
+  double disc = py_exp(-r * t, e);
+  double s = sigma * sqrt(t);
+  bool bad;
+  double lnFK = fv_log_fk(Fw / K, &bad);
+  return fv_black_kernel(th, Fw, K, disc, s, lnFK, bad, e);
+}
+
+// ---- fused price + Greeks (pricing.py:56-61 + greeks.py:45-98) -------------
+// One pass over d1/d2/Phi/phi for both reference calls (batch_price and
+// batch_greeks); each keeps its own exception record (ep / eg).
+struct FvGreeks { double price, delta, gamma, theta, rho, vega; int status; };
+
+FV_HD FvGreeks fv_price_greeks_row(int model, double th, double un, double K, double t,
+                                   double r, double q, double sigma, bool want_price,
+                                   bool want_greeks, FvExc& ep, FvExc& eg) {
+  FvGreeks o;
+  const double nan = __builtin_nan("");
+  o.price = nan; o.delta = nan; o.gamma = nan; o.theta = nan; o.rho = nan; o.vega = nan;
+  o.status = FV_GK_OK;
+  bool fwd = (model == 0);
+  double sqrt_t = sqrt(t);
+  double s = sigma * sqrt_t;
+  // pricing: F (spot), disc ; greeks: disc, edge check, F, carry_disc
+  double eFq = 1.0;
+  FvExc e0 = {0, 0, 0.0};
+  if (!fwd) eFq = py_exp((r - q) * t, e0);          // both reference calls evaluate this
+  double disc = fv_exp(-r * t);
+  bool disc_ovf = fv_isinf(disc) && fv_isfinite(-r * t);
+  double Fw = fwd ? un : un * eFq;
+  // batch_price: F (spot) -> disc -> kernel
+  if (want_price) {
+    if (e0.code) ep.raise(e0.code);
+    if (disc_ovf) ep.raise(FV_EXC_MATH_RANGE);
+  }
+  // batch_greeks: disc -> (edge) -> F -> carry_disc -> log
+  bool edge = s < 1e-12;
+  double carry_disc = disc;
+  if (want_greeks) {
+    if (disc_ovf) eg.raise(FV_EXC_MATH_RANGE);
+    if (!edge && !fwd) {
+      if (e0.code) eg.raise(e0.code);
+      carry_disc = py_exp(-q * t, eg);
+    }
+    if (edge && eg.code == FV_EXC_NONE) o.status = FV_GK_EDGE;
+  }
+  double intrinsic = py_max(th * (Fw - K), 0.0);
+  double cap = (th > 0.0) ? Fw : K;
+  if (s < 1e-12) {
+    o.price = disc * intrinsic;
+    return o;
+  }
+  bool bad;
+  double lnFK = fv_log_fk(Fw / K, &bad);
+  if (bad) { if (want_price) ep.raise(FV_EXC_MATH_DOMAIN); if (want_greeks) eg.raise(FV_EXC_MATH_DOMAIN); }
+  double d1 = (lnFK + 0.5 * s * s) / s;
+  double d2 = d1 - s;
+  double cdf_td1 = fv_norm_cdf(th * d1);
+  double cdf_td2 = fv_norm_cdf(th * d2);
+  double raw = th * (Fw * cdf_td1 - K * cdf_td2);
+  o.price = disc * py_min(py_max(raw, intrinsic), cap);
+  if (!want_greeks) return o;
+  double under = fwd ? Fw : un;
+  double pdf_d1 = fv_norm_pdf(d1);
+  o.delta = th * carry_disc * cdf_td1;
+  o.gamma = carry_disc * pdf_d1 / (under * s);
+  double vega = carry_disc * under * pdf_d1 * sqrt_t;
+  double theta_cal, rho;
+  if (fwd) {
+    double value = disc * th * (Fw * cdf_td1 - K * cdf_td2);
+    theta_cal = r * value - disc * Fw * pdf_d1 * sigma / (2.0 * sqrt_t);
+    rho = -t * value;
+  } else {
+    theta_cal = (-under * carry_disc * pdf_d1 * sigma / (2.0 * sqrt_t)
+                 - th * (r * K * disc * cdf_td2 - q * under * carry_disc * cdf_td1));
+    rho = th * K * t * disc * cdf_td2;
+  }
+  o.theta = theta_cal / 365.0;
+  o.rho = rho / 100.0;
+  o.vega = vega / 100.0;
+  return o;
+}
+
+// ---- solver.py implied_vol_halley (:49-161), two phases ---------------------
+// Phase 1 (setup + <= 16 Halley steps) either finishes the quote or hands a
+// compact state to phase 2 (<= 128 bisection steps), so the ~4% of quotes
+// that need the long bisection tail run on their own, warp-dense.
+struct FvHalleyCtx {       // per-quote constants
+  double th, Fw, K, disc, sqrt_t, lnFK, target, tol_price;
+  bool fk_bad;
+};
+struct FvHalleyState { double sigma, fval, lo, hi; int iterations; };
+
+FV_HD double fv_halley_f(const FvHalleyCtx& c, double sigma, FvExc& e) {
+  return fv_black_kernel(c.th, c.Fw, c.K, c.disc, sigma * c.sqrt_t, c.lnFK, c.fk_bad, e) - c.target;
+}
+
+// Returns 1 if the quote is finished (status/sigma/iterations set), 0 if it
+// needs the bisection phase (ctx/state filled).
+FV_HD int fv_halley_phase1(int model, double th, double un, double K, double t, double r,
+                           double q, double target, FvHalleyCtx& c, FvHalleyState& st,
+                           int* status, double* sigma_out, FvExc& e) {
+  const double nan = __builtin_nan("");
+  *sigma_out = nan;
+  st.iterations = 0;
+  double Fw = (model == 0) ? un : un * py_exp((r - q) * t, e);
+  double discount = py_exp(-r * t, e);
+  double sqrt_t = sqrt(t);
+  if (e.code) { *status = FV_IV_MAX_ITER; return 1; }
+  double disc_intrinsic = discount * py_max(th * (Fw - K), 0.0);
+  double disc_cap = discount * ((th > 0.0) ? Fw : K);
+  double tie_tol = 1e-12 * py_max(1.0, disc_cap);
+  if (!fv_isfinite(target)) { *status = FV_IV_BELOW_INTRINSIC; return 1; }
+  if (target <= disc_intrinsic + tie_tol) { *status = FV_IV_BELOW_INTRINSIC; return 1; }
+  if (target > disc_cap + tie_tol) { *status = FV_IV_ABOVE_UPPER; return 1; }
+  double tol_price = py_min(tie_tol, 1e-10 * (target - disc_intrinsic));
+  if (t <= 0.0) { *status = FV_IV_ABOVE_UPPER; return 1; }
+  c.th = th; c.Fw = Fw; c.K = K; c.disc = discount; c.sqrt_t = sqrt_t;
+  c.lnFK = fv_log_fk(Fw / K, &c.fk_bad);
+  c.target = target; c.tol_price = tol_price;
+
+  double lo = 1e-9, hi = 10.0;
+  double f_lo = fv_halley_f(c, lo, e);
+  if (e.code) { *status = FV_IV_MAX_ITER; return 1; }
+  if (f_lo >= 0.0) {
+    if (fv_fabs(f_lo) <= tol_price) { *status = FV_IV_CONVERGED; *sigma_out = lo; return 1; }
+    *status = FV_IV_BELOW_INTRINSIC; return 1;
+  }
+  double f_hi = fv_halley_f(c, hi, e);
+  while (f_hi < 0.0 && hi < 100.0) {
+    hi = py_min(2.0 * hi, 100.0);
+    f_hi = fv_halley_f(c, hi, e);
+  }
+  if (f_hi < 0.0) { *status = FV_IV_MAX_ITER; return 1; }
+  double sigma = sqrt(FV_TWO_PI / t) * target / un;
+  sigma = py_min(py_max(sigma, 0.05), 2.0);
+  sigma = py_min(py_max(sigma, lo), hi);
+  double fval = fv_halley_f(c, sigma, e);
+  if (fval > 0.0) hi = py_min(hi, sigma);
+  else if (fval < 0.0) lo = py_max(lo, sigma);
+  int iterations = 0;
+  for (int it = 0; it < 16; ++it) {
+    if (fv_fabs(fval) <= tol_price) {
+      *status = FV_IV_CONVERGED; *sigma_out = sigma; st.iterations = iterations; return 1;
+    }
+    // _raw_vega (solver.py:40-46) and the d1/d2 of :121-123 share s and d1
+    double s = sigma * sqrt_t;
+    double vega = 0.0, d1 = 0.0;
+    if (!(s < 1e-12)) {
+      if (c.fk_bad) e.raise(FV_EXC_MATH_DOMAIN);
+      d1 = (c.lnFK + 0.5 * s * s) / s;
+      vega = discount * Fw * fv_norm_pdf(d1) * sqrt_t;
+    }
+    double cand = nan;
+    if (vega > 0.0) {
+      double d2 = d1 - s;
+      double vomma = vega * d1 * d2 / sigma;
+      double denom = 2.0 * vega * vega - fval * vomma;
+      if (denom != 0.0) cand = sigma - 2.0 * fval * vega / denom;
+    }
+    bool accepted = false;
+    double f_cand = 0.0;
+    if (fv_isfinite(cand) && lo < cand && cand < hi) {
+      f_cand = fv_halley_f(c, cand, e);
+      if (fv_fabs(f_cand) < fv_fabs(fval)) accepted = true;
+    }
+    if (!accepted) {
+      cand = 0.5 * (lo + hi);
+      f_cand = fv_halley_f(c, cand, e);
+    }
+    if (e.code) { *status = FV_IV_MAX_ITER; return 1; }
+    if (f_cand > 0.0) hi = cand;
+    else if (f_cand < 0.0) lo = cand;
+    double step = cand - sigma;
+    sigma = cand; fval = f_cand;
+    iterations += 1;
+    if (fv_fabs(step) <= 1e-12 * py_max(1.0, sigma)) {
+      *status = FV_IV_CONVERGED; *sigma_out = sigma; st.iterations = iterations; return 1;
+    }
+  }
+  st.sigma = sigma; st.fval = fval; st.lo = lo; st.hi = hi; st.iterations = iterations;
+  return 0;
+}
+
+// Phase 2: solver.py:146-161.
+FV_HD void fv_halley_phase2(const FvHalleyCtx& c, FvHalleyState st, int* status,
+                            double* sigma_out, FvExc& e) {
+  double sigma = st.sigma, fval = st.fval, lo = st.lo, hi = st.hi;
+  for (int it = 0; it < 128; ++it) {
+    if (fv_fabs(fval) <= c.tol_price || (hi - lo) <= 1e-12 * py_max(1.0, sigma)) {
+      *status = FV_IV_FELL_BACK; *sigma_out = sigma; return;
+    }
+    sigma = 0.5 * (lo + hi);
+    fval = fv_halley_f(c, sigma, e);
+    if (fval > 0.0) hi = sigma;
+    else lo = sigma;
+  }
+  if (fv_fabs(fval) <= c.tol_price || (hi - lo) <= 1e-12 * py_max(1.0, sigma)) {
+    *status = FV_IV_FELL_BACK; *sigma_out = sigma; return;
+  }
+  *status = FV_IV_MAX_ITER; *sigma_out = __builtin_nan("");
+}
+
+// ---- lbr.py: normalized Black --------------------------------------------
+// normalized_black (:112-129) for Python-float x (x_work) and s of numpy-ness
+// s_np.  *E (if non-null) receives exp(-(h^2+t^2)/2) -- the factor
+// normalized_vega (:152-156) shares -- computed here when the branch needs it.
+FV_HD double fv_normalized_black(double x, double s, bool s_np, FvExc& e, double* E, int* branch) {
+  if (x > 0.0) { e.raise_v(FV_EXC_DOM_NB_X, x, 0); return __builtin_nan(""); }
+  if (!(s > 0.0)) { e.raise_v(FV_EXC_DOM_NB_S, s, s_np); return __builtin_nan(""); }
+  double h = py_div(x, s, s_np, e);
+  double t = 0.5 * s;
+  if (h < -10.0 && t < FV_SMALL_T_THRESHOLD + (-10.0 - h)) {
+    // _asymptotic_black (:65-71)
+    if (branch) *branch = 0;
+    double th_ = py_div(t, h, s_np, e);
+    double ee = th_ * th_;
+    double rr = (h + t) * (h - t);
+    double hr = py_div(h, rr, s_np, e);
+    double qq = hr * hr;
+    double c0 = 0.0;
+    for (int j = 17; j >= 0; --j) {
+      // column j of _ASYM_PASCAL: P[0..j][j] (zeros above the diagonal are
+      // bit-neutral in numpy's Horner since e is finite and >= 0)
+      int base = j * (j + 1) / 2;
+      double cj = FV_TAB(fv_asym_pascal, base + j) + ee * 0.0;
+      for (int i = j - 1; i >= 0; --i) cj = FV_TAB(fv_asym_pascal, base + i) + cj * ee;
+      double wj = FV_TAB(fv_asym_facts, j) * cj;
+      c0 = (j == 17) ? (wj + qq * 0.0) : (wj + c0 * qq);
+    }
+    double Ev = fv_exp(-0.5 * (h * h + t * t));
+    if (E) *E = Ev;
+    double b = FV_INV_SQRT_TWO_PI * Ev * py_div(t, rr, s_np, e) * c0;
+    return py_max(b, 0.0);
+  }
+  if (t < FV_SMALL_T_THRESHOLD) {
+    // _small_t_black (:74-103)
+    if (branch) *branch = 1;
+    double a = 1.0 + h * FV_HALF_SQRT_TWO_PI * fv_erfcx(-h / FV_SQRT_TWO);
+    double w = t * t;
+    double h2 = h * h;
+    double c1 = (-1.0 + 3.0 * a + a * h2) / 6.0;
+    double c2 = (-7.0 + 15.0 * a + h2 * (-1.0 + 10.0 * a + a * h2)) / 120.0;
+    double c3 = (-57.0 + 105.0 * a + h2 * (-18.0 + 105.0 * a + h2 * (-1.0 + 21.0 * a + a * h2))) / 5040.0;
+    double c4 = (-561.0 + 945.0 * a + h2 * (-285.0 + 1260.0 * a + h2 * (-33.0 + 378.0 * a
+                 + h2 * (-1.0 + 36.0 * a + a * h2)))) / 362880.0;
+    double c5 = (-6555.0 + 10395.0 * a + h2 * (-4680.0 + 17325.0 * a + h2 * (-840.0 + 6930.0 * a
+                 + h2 * (-52.0 + 990.0 * a + h2 * (-1.0 + 55.0 * a + a * h2))))) / 39916800.0;
+    double c6 = (-89055.0 + 135135.0 * a + h2 * (-82845.0 + 270270.0 * a + h2 * (-20370.0 + 135135.0 * a
+                 + h2 * (-1926.0 + 25740.0 * a + h2 * (-75.0 + 2145.0 * a
+                 + h2 * (-1.0 + 78.0 * a + a * h2)))))) / 6227020800.0;
+    double expansion = 2.0 * t * (a + w * (c1 + w * (c2 + w * (c3 + w * (c4 + w * (c5 + w * c6))))));
+    double Ev = fv_exp(-0.5 * (h * h + t * t));
+    if (E) *E = Ev;
+    double b = FV_INV_SQRT_TWO_PI * Ev * expansion;
+    return py_max(b, 0.0);
+  }
+  if (h + t > 0.85) {
+    if (branch) *branch = 2;
+    double b_max = fv_exp(0.5 * x);
+    double b = fv_norm_cdf(h + t) * b_max - py_div(fv_norm_cdf(h - t), b_max, false, e);
+    if (E) *E = fv_exp(-0.5 * (h * h + t * t));
+    return py_max(b, 0.0);
+  }
+  // _erfcx_black (:106-109)
+  if (branch) *branch = 3;
+  double Ev = fv_exp(-0.5 * (h * h + t * t));
+  if (E) *E = Ev;
+  double b = 0.5 * Ev * (fv_erfcx(-(h + t) / FV_SQRT_TWO) - fv_erfcx(-(h - t) / FV_SQRT_TWO));
+  return py_max(b, 0.0);
+}
+
+// normalized_black_log (:140-149); *E receives -(h^2+t^2)/2 * 1 (the exponent)
+FV_HD double fv_normalized_black_log(double x, double s, bool s_np, FvExc& e) {
+  double h = py_div(x, s, s_np, e);
+  double t = 0.5 * s;
+  double diff = fv_erfcx(-(h + t) / FV_SQRT_TWO) - fv_erfcx(-(h - t) / FV_SQRT_TWO);
+  if (diff <= 0.0) return -__builtin_inf();
+  return -0.5 * (h * h + t * t) + py_log(0.5 * diff, e);
+}
+
+// normalized_black_complement (:132-137) with the per-quote exp(+-x/2)
+FV_HD double fv_complement(double x, double s, bool s_np, double ep, double em, FvExc& e) {
+  double h = py_div(x, s, s_np, e);
+  double t = 0.5 * s;
+  return ep * fv_norm_cdf(-h - t) + em * fv_norm_cdf(h - t);
+}
+
+// ---- lbr.py: implied_vol_lbr (:410-486) -----------------------------------
+struct FvLbrOut { double sigma; int status; int region; int iterations; };
+
+FV_HD FvLbrOut fv_lbr_row(double th, double Fw, double K, double t, double r, double px, FvExc& e) {
+  const double nan = __builtin_nan("");
+  FvLbrOut o;
+  o.sigma = nan; o.status = FV_IV_MAX_ITER; o.region = FV_REGION_NONE; o.iterations = 0;
+  // normalize_quote (:174-207); F, K, t, price are numpy scalars
+  if (!(Fw > 0.0 && K > 0.0)) { e.raise(FV_EXC_DOM_FK); return o; }
+  double xq = py_log(Fw / K, e);
+  double beta0 = px * py_exp(r * t, e) / sqrt(Fw * K);
+  double e_hx = py_exp(0.5 * xq, e);
+  double e_mhx = py_exp(-0.5 * xq, e);
+  if (e.code) return o;
+  double parity = e_hx - e_mhx;
+  double beta;
+  if (th > 0.0) beta = (xq > 0.0) ? beta0 - parity : beta0;
+  else beta = (xq < 0.0) ? beta0 + parity : beta0;
+  double x = -fv_fabs(xq);
+  double b_max = fv_exp(0.5 * x);
+  if (beta <= 1e-300) { o.status = FV_IV_BELOW_INTRINSIC; return o; }
+  if (beta >= b_max * (1.0 - 1e-15)) { o.status = FV_IV_ABOVE_UPPER; return o; }
+  double sqrt_t = sqrt(t);
+  py_exp(-r * t, e);                             // scale = sqrt(F K) exp(-r t): only its overflow
+  if (e.code) return o;
+
+  if (fv_fabs(x) < 1e-12) {                      // ATM shortcut (:427-430)
+    if (!(0.0 < beta && beta < 1.0)) { e.raise_v(FV_EXC_DOM_ATM_BETA, beta, 1); return o; }
+    bool znp;
+    double z = fv_inv_norm_cdf(0.5 * (1.0 - beta), true, &znp, e);
+    if (e.code) return o;
+    double s = -2.0 * z;
+    o.sigma = s / sqrt_t; o.status = FV_IV_CONVERGED;
+    return o;
+  }
+
+  // anchors (:231-238), computed once (initial_guess recomputes them, :325)
+  double s_c = py_sqrt(2.0 * fv_fabs(x), e);
+  double s_lo = s_c * 0.5;
+  double s_hi = s_c / 0.5;
+  double E_lo = 0.0, E_c = 0.0, E_hi = 0.0;
+  double b_lo = fv_normalized_black(x, s_lo, false, e, &E_lo, nullptr);
+  double b_c = fv_normalized_black(x, s_c, false, e, &E_c, nullptr);
+  double b_hi = fv_normalized_black(x, s_hi, false, e, &E_hi, nullptr);
+  if (e.code) return o;
+  int region;
+  if (beta < b_lo) region = FV_FAR_LOW;
+  else if (beta < b_c) region = FV_NEAR_LOW;
+  else if (beta < b_hi) region = FV_NEAR_HIGH;
+  else region = FV_FAR_HIGH;
+  o.region = region;
+
+  double ep = b_max;                              // exp(0.5 x), x = x_work
+  double em = 0.0;                                // exp(-0.5 x)
+  double comp_beta = b_max - beta;
+  double lo, hi;
+  if (region == FV_FAR_LOW) { lo = 0.0; hi = s_lo; }
+  else if (region == FV_NEAR_LOW) { lo = s_lo; hi = s_c; }
+  else if (region == FV_NEAR_HIGH) { lo = s_c; hi = s_hi; }
+  else {
+    lo = s_hi; hi = 2.0 * s_hi;
+    em = py_exp(-0.5 * x, e);
+    while (fv_complement(x, hi, false, ep, em, e) > comp_beta && hi < 1e6) hi *= 2.0;
+    if (e.code) return o;
+  }
+  lo *= 1.0 - 1e-6;
+  hi *= 1.0 + 1e-6;
+  bool lo_np = false, hi_np = false;
+
+  // initial_guess (:321-332)
+  double s;
+  bool s_np = false;
+  double ln_beta = 0.0;
+  if (region == FV_FAR_LOW) {
+    // _far_low_guess (:283-309)
+    ln_beta = py_log(beta, e);
+    double s_cap = s_lo;
+    s = py_div(fv_fabs(x), py_sqrt(-2.0 * ln_beta, e), false, e);
+    s = py_min(py_max(s, 1e-6 * s_cap), 0.999 * s_cap);
+    double v = py_log(s, e);
+    double v_hi = py_log(s_cap, e);
+    for (int it = 0; it < 5; ++it) {
+      if (e.code) return o;
+      double ln_b = fv_normalized_black_log(x, s, false, e);
+      double g = ln_b - ln_beta;
+      if (g > 0.0) v_hi = py_min(v_hi, v);
+      double xs = py_div(x, s, false, e);
+      double arg = FV_LOG_INV_SQRT_TWO_PI - 0.5 * (py_powi(xs, 2, false, e) + 0.25 * s * s) - ln_b;
+      double dg_dv = s * py_exp(arg, e);
+      if (e.code) return o;
+      if (!(fv_isfinite(dg_dv) && dg_dv > 0.0)) break;
+      double v_new = v - g / dg_dv;
+      if (!fv_isfinite(v_new)) break;
+      if (v_new >= v_hi) v_new = 0.5 * (v + v_hi);
+      v = v_new;
+      s = py_exp(v, e);
+    }
+  } else if (region == FV_FAR_HIGH) {
+    // _far_high_guess (:312-318)
+    double p = (b_max - beta) / (2.0 * b_max);    // numpy scalar (beta)
+    bool p_np = true;
+    if (5e-324 > p) { p = 5e-324; p_np = false; }
+    if (FV_HALF_ONE_MINUS_EPS < p) { p = FV_HALF_ONE_MINUS_EPS; p_np = false; }
+    bool z_np;
+    double z = fv_inv_norm_cdf(p, p_np, &z_np, e);
+    if (e.code) return o;
+    s = -z + py_sqrt(z * z + 2.0 * fv_fabs(x), e);
+    s_np = z_np;
+  } else {
+    // _hermite_inverse (:265-280), all Python floats
+    double b0, b1, s0, s1, E0, E1;
+    if (region == FV_NEAR_LOW) { b0 = b_lo; b1 = b_c; s0 = s_lo; s1 = s_c; E0 = E_lo; E1 = E_c; }
+    else { b0 = b_c; b1 = b_hi; s0 = s_c; s1 = s_hi; E0 = E_c; E1 = E_hi; }
+    double m0 = py_div(b0, FV_INV_SQRT_TWO_PI * E0, false, e);
+    double m1 = py_div(b1, FV_INV_SQRT_TWO_PI * E1, false, e);
+    double lb1 = py_log(b1, e);
+    double lb0 = py_log(b0, e);
+    double du = lb1 - lb0;
+    double u = py_div(py_log(beta, e) - lb0, du, false, e);
+    if (e.code) return o;
+    double u2 = u * u;
+    double u3 = u2 * u;
+    s = ((2.0 * u3 - 3.0 * u2 + 1.0) * s0 + (u3 - 2.0 * u2 + u) * du * m0
+         + (-2.0 * u3 + 3.0 * u2) * s1 + (u3 - u2) * du * m1);
+    if (!(py_min(s0, s1) <= s && s <= py_max(s0, s1))) s = s0 + u * (s1 - s0);
+  }
+  if (!(lo < s && s < hi)) { s = 0.5 * (lo + hi); s_np = false; }
+
+  // Householder(3) iterations (:454-483)
+  bool increasing = region != FV_FAR_LOW;
+  double ln_comp_beta = 0.0;
+  bool comp_beta_bad = false;
+  if (region == FV_FAR_HIGH) {
+    comp_beta_bad = !(comp_beta > 0.0 && fv_isfinite(comp_beta));
+    ln_comp_beta = comp_beta_bad ? 0.0 : fv_log(comp_beta);
+    if (comp_beta_bad) {                          // math.log's special cases
+      FvExc tmp = {0, 0, 0.0};
+      ln_comp_beta = py_log(comp_beta, tmp);
+      comp_beta_bad = tmp.code != 0;
+    }
+  }
+  int iterations = 0;
+  bool converged = false;
+  for (int it = 0; it < 8; ++it) {
+    // objective_branch (:346-389)
+    if (!(s > 0.0)) { e.raise_v(FV_EXC_DOM_OBJ_S, s, s_np); return o; }
+    double h = py_div(x, s, s_np, e);
+    double t = 0.5 * s;
+    double s3 = s * s * s;
+    double r2 = py_div(x * x, s3, s_np, e) - 0.25 * s;
+    double s4 = py_powi(s, 4, s_np, e);
+    double r3 = r2 * r2 - py_div(3.0 * x * x, s4, s_np, e) - 0.25;
+    double g, g1, g2, g3;
+    bool g_np, g1_np, g23_np;
+    if (region == FV_FAR_LOW) {
+      double ln_b = fv_normalized_black_log(x, s, s_np, e);
+      double ln_bp = FV_LOG_INV_SQRT_TWO_PI - 0.5 * (h * h + 0.25 * s * s);
+      double up = py_exp(ln_bp - ln_b, e);
+      double up3 = py_powi(up, 3, false, e);
+      double upp = up * r2 - up * up;
+      double uppp = up * r3 - 3.0 * up * up * r2 + 2.0 * up3;
+      double inv = py_div(1.0, ln_b, false, e);
+      double inv2 = inv * inv;
+      g = inv - py_div(1.0, ln_beta, false, e);
+      g1 = -up * inv2;
+      g2 = -upp * inv2 + 2.0 * up * up * inv2 * inv;
+      g3 = (-uppp * inv2 + 6.0 * up * upp * inv2 * inv - 6.0 * up3 * inv2 * inv2);
+      g_np = false; g1_np = false; g23_np = s_np;
+    } else if (region == FV_FAR_HIGH) {
+      double bp = FV_INV_SQRT_TWO_PI * fv_exp(-0.5 * (h * h + t * t));
+      double comp = ep * fv_norm_cdf(-h - t) + em * fv_norm_cdf(h - t);
+      double w = py_div(bp, comp, false, e);
+      if (comp_beta_bad) e.raise(FV_EXC_MATH_DOMAIN);
+      double lcomp = py_log(comp, e);
+      double w3 = py_powi(w, 3, false, e);
+      g = ln_comp_beta - lcomp;
+      g1 = w;
+      g2 = w * r2 + w * w;
+      g3 = w * r3 + 3.0 * w * w * r2 + 2.0 * w3;
+      g_np = false; g1_np = false; g23_np = s_np;
+    } else {
+      double Ev = 0.0;
+      double b = fv_normalized_black(x, s, s_np, e, &Ev, nullptr);
+      double bp = FV_INV_SQRT_TWO_PI * Ev;
+      g = b - beta; g1 = bp; g2 = bp * r2; g3 = bp * r3;
+      g_np = true; g1_np = false; g23_np = s_np;
+    }
+    if (e.code) return o;
+    if (g == 0.0) { converged = true; break; }
+    bool below = increasing ? (g < 0.0) : (g > 0.0);
+    if (below) { if (s > lo) { lo = s; lo_np = s_np; } }
+    else { if (s < hi) { hi = s; hi_np = s_np; } }
+    // householder3_step (:392-402)
+    double ds;
+    bool ds_np;
+    if (g1 == 0.0 || !fv_isfinite(g1)) { ds = nan; ds_np = false; }
+    else {
+      double nu = -g / g1;
+      double eta = g2 / g1;
+      double gam = py_div(g3, 6.0 * g1, g23_np || g1_np, e);
+      bool num_np = g_np || g1_np || g23_np;
+      ds = py_div(nu * (1.0 + 0.5 * nu * eta), 1.0 + nu * (eta + nu * gam), num_np, e);
+      ds_np = num_np;
+      if (e.code) return o;
+    }
+    if (fv_isfinite(ds) && fv_fabs(ds) <= 1e-14 * py_max(1.0, s)) {
+      s = s + ds; s_np = s_np || ds_np;
+      iterations += 1;
+      converged = true;
+      break;
+    }
+    double cand = s + ds;
+    bool cand_np = s_np || ds_np;
+    if (!fv_isfinite(cand) || !(lo < cand && cand < hi)) {
+      cand = 0.5 * (lo + hi);
+      cand_np = lo_np || hi_np;
+      ds = cand - s;
+    }
+    s = cand; s_np = cand_np;
+    iterations += 1;
+    if (fv_fabs(ds) <= 1e-14 * py_max(1.0, s)) { converged = true; break; }
+  }
+  o.sigma = s / sqrt_t;
+  o.status = converged ? FV_IV_CONVERGED : FV_IV_MAX_ITER;
+  o.iterations = iterations;
+  return o;
+}
+
+// batch_iv LBR row (batch.py:227-238): spot models forward the underlying.
+FV_HD FvLbrOut fv_lbr_batch_row(int model, double th, double un, double K, double t, double r,
+                                double q, double px, FvExc& e) {
+  FvLbrOut o;
+  o.sigma = __builtin_nan(""); o.status = FV_IV_MAX_ITER; o.region = FV_REGION_NONE; o.iterations = 0;
+  double Fw = un;
+  if (model != 0) {
+    Fw = un * py_exp((r - q) * t, e);
+    if (e.code) return o;
+  }
+  if (!(t > 0.0)) { o.status = FV_IV_BELOW_INTRINSIC; return o; }
+  o = fv_lbr_row(th, Fw, K, t, r, px, e);
+  if (o.status != FV_IV_CONVERGED && o.status != FV_IV_FELL_BACK) o.sigma = __builtin_nan("");
+  return o;
+}

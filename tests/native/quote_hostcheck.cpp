@@ -1,0 +1,60 @@
+// Host build of paper_2604_27210_b200/csrc/fv_quote.h (the device per-quote
+// code) for CPU pre-checks against the oracle / golden fixtures.  Test
+// infrastructure only: the product runs the CUDA build of the same header.
+// Build: g++ -O2 -ffp-contract=off -fno-fast-math -shared -fPIC
+#include "../../paper_2604_27210_b200/csrc/fv_quote.h"
+
+extern "C" {
+
+void qh_price(int model, const int8_t* flag, const double* un, const double* k, const double* t,
+              const double* r, const double* q, const double* sg, int64_t n, double* out,
+              int8_t* exc) {
+  for (int64_t i = 0; i < n; ++i) {
+    FvExc e = {0, 0, 0.0};
+    out[i] = fv_price_row(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], sg[i], e);
+    exc[i] = (int8_t)e.code;
+  }
+}
+
+void qh_price_greeks(int model, const int8_t* flag, const double* un, const double* k,
+                     const double* t, const double* r, const double* q, const double* sg,
+                     int64_t n, double* price, double* g5, int8_t* status, int8_t* excp,
+                     int8_t* excg) {
+  for (int64_t i = 0; i < n; ++i) {
+    FvExc ep = {0, 0, 0.0}, eg = {0, 0, 0.0};
+    FvGreeks o = fv_price_greeks_row(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], sg[i],
+                                     true, true, ep, eg);
+    price[i] = o.price;
+    g5[5 * i + 0] = o.delta; g5[5 * i + 1] = o.gamma; g5[5 * i + 2] = o.theta;
+    g5[5 * i + 3] = o.rho; g5[5 * i + 4] = o.vega;
+    status[i] = (int8_t)o.status;
+    excp[i] = (int8_t)ep.code; excg[i] = (int8_t)eg.code;
+  }
+}
+
+void qh_iv(int model, int method, const int8_t* flag, const double* un, const double* k,
+           const double* t, const double* r, const double* q, const double* px, int64_t n,
+           double* iv, int8_t* status, int8_t* region, int8_t* exc, double* exc_val,
+           int8_t* exc_np) {
+  for (int64_t i = 0; i < n; ++i) {
+    FvExc e = {0, 0, 0.0};
+    if (method == 1) {
+      FvLbrOut o = fv_lbr_batch_row(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], px[i], e);
+      iv[i] = o.sigma; status[i] = (int8_t)o.status; region[i] = (int8_t)o.region;
+    } else {
+      FvHalleyCtx c; FvHalleyState st; int status_; double sig;
+      int done = fv_halley_phase1(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], px[i],
+                                  c, st, &status_, &sig, e);
+      if (!done) fv_halley_phase2(c, st, &status_, &sig, e);
+      iv[i] = (status_ == FV_IV_CONVERGED || status_ == FV_IV_FELL_BACK) ? sig : __builtin_nan("");
+      status[i] = (int8_t)status_; region[i] = -1;
+    }
+    exc[i] = (int8_t)e.code; exc_val[i] = e.val; exc_np[i] = (int8_t)e.np;
+  }
+}
+
+double qh_normalized_black(double x, double s, int* branch) {
+  FvExc e = {0, 0, 0.0};
+  return fv_normalized_black(x, s, false, e, nullptr, branch);
+}
+}

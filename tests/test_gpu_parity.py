@@ -1,0 +1,287 @@
+"""GPU parity: the CUDA path (C ABI via the drop-in batch API, and via device
+pointers) against the golden fixtures from the live reference and against the
+CPU oracle on larger seeded workloads.  Bit-exact everywhere: IV values and NaN
+masks, statuses, LBR regions, prices, Greeks, exception rows, BatchErrors."""
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+from _helpers import assert_bits, bits_equal, load
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fv():
+    import paper_2604_27210_b200 as fv
+    from paper_2604_27210_b200 import _native
+    _native.lib_for_compute()
+    return fv
+
+
+IV_FIXTURES = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "lbr_*.npz"))
+                     + glob.glob(os.path.join(GOLDEN, "halley_c*.npz")))
+IV_CODES = {"converged": 0, "fell_back_to_bisection": 1, "below_intrinsic": 2,
+            "above_upper_bound": 3, "max_iterations": 4}
+
+
+def _chars(flag):
+    return np.where(np.asarray(flag) > 0, "c", "p")
+
+
+@pytest.mark.parametrize("name", IV_FIXTURES)
+def test_iv_golden(fv, name):
+    g = load(os.path.join(GOLDEN, name))
+    tb = fv.batch_iv(str(g["model"]), str(g["method"]), _chars(g["flag"]), g["underlying"],
+                     g["strike"], g["t"], g["r"], price=g["price"], q=g["q"])
+    codes = np.array([IV_CODES[s] for s in tb["status"]], np.int8)
+    ctx = {k: g[k] for k in ("flag", "underlying", "strike", "t", "r", "price")}
+    assert_bits(codes, g["status"], f"{name} status", ctx)
+    assert_bits(tb["iv"], g["iv"], f"{name} iv", ctx)
+
+
+def _iv_native(model, method, flag, un, k, t, r, q, px, device):
+    """Direct C-ABI call (host or device pointers) returning iv, status, region."""
+    from paper_2604_27210_b200 import _native
+    lib = _native.lib_for_compute()
+    n = len(flag)
+    cols = [np.ascontiguousarray(flag, np.int8)] + [np.ascontiguousarray(c, np.float64)
+                                                    for c in (un, k, t, r, q, px)]
+    if device:
+        import torch
+        dcols = [torch.from_numpy(c).cuda() for c in cols]
+        iv = torch.empty(n, dtype=torch.float64, device="cuda")
+        st = torch.empty(n, dtype=torch.int8, device="cuda")
+        reg = torch.empty(n, dtype=torch.int8, device="cuda")
+        err = _native.fv_error()
+        rc = lib.fv_batch_iv(model, method, *[_native.col(c) for c in dcols], n, iv.data_ptr(),
+                             st.data_ptr(), reg.data_ptr(), err)
+        return rc, err, iv.cpu().numpy(), st.cpu().numpy(), reg.cpu().numpy()
+    iv = np.empty(n)
+    st = np.empty(n, np.int8)
+    reg = np.empty(n, np.int8)
+    err = _native.fv_error()
+    rc = lib.fv_batch_iv(model, method, *[_native.col(c) for c in cols], n, iv.ctypes.data,
+                         st.ctypes.data, reg.ctypes.data, err)
+    return rc, err, iv, st, reg
+
+
+@pytest.mark.parametrize("device", [False, True])
+@pytest.mark.parametrize("name", ["lbr_c1.npz", "lbr_c4.npz", "lbr_c5.npz", "lbr_grid.npz"])
+def test_lbr_regions_golden(fv, name, device):
+    g = load(os.path.join(GOLDEN, name))
+    rc, err, iv, st, reg = _iv_native(0, 1, g["flag"], g["underlying"], g["strike"], g["t"],
+                                      g["r"], g["q"], g["price"], device)
+    assert rc == 0, err.message
+    assert_bits(st, g["status"], f"{name} status")
+    assert_bits(iv, g["iv"], f"{name} iv")
+    assert_bits(reg, g["region"], f"{name} region")
+
+
+def test_halley_grid_golden(fv):
+    g = load(os.path.join(GOLDEN, "halley_grid.npz"))
+    for m in ("black", "bs", "bsm"):
+        tb = fv.batch_iv(m, "halley", _chars(g[f"{m}_flag"]), g[f"{m}_underlying"],
+                         g[f"{m}_strike"], g[f"{m}_t"], g[f"{m}_r"], price=g[f"{m}_price"],
+                         q=g[f"{m}_q"])
+        codes = np.array([IV_CODES[s] for s in tb["status"]], np.int8)
+        assert_bits(codes, g[f"{m}_status"], f"halley grid {m} status")
+        assert_bits(tb["iv"], g[f"{m}_iv"], f"halley grid {m} iv")
+
+
+@pytest.mark.parametrize("model", ["bsm", "bs", "black"])
+def test_price_greeks_golden(fv, model):
+    g = load(os.path.join(GOLDEN, "price_greeks.npz"))
+    q = g["q"] if model == "bsm" else 0.0
+    args = (model, _chars(g["flag"]), g["underlying"], g["strike"], g["t"], g["r"], q)
+    p = fv.batch_price(*args, sigma=g["sigma"])
+    assert_bits(p["price"], g[f"{model}_price"], f"{model} price")
+    gk = fv.batch_greeks(*args, sigma=g["sigma"])
+    codes = np.array([{"ok": 0, "step_function_edge": 1}[s] for s in gk["status"]], np.int8)
+    assert_bits(codes, g[f"{model}_status"], f"{model} greeks status")
+    for name in ("delta", "gamma", "theta", "rho", "vega"):
+        assert_bits(gk[name], g[f"{model}_{name}"], f"{model} {name}")
+
+
+def test_fused_price_greeks_device(fv):
+    import torch
+    from paper_2604_27210_b200 import _native
+    lib = _native.lib_for_compute()
+    g = load(os.path.join(GOLDEN, "price_greeks.npz"))
+    n = len(g["flag"])
+    cols = [torch.from_numpy(np.ascontiguousarray(g["flag"], np.int8)).cuda()] + [
+        torch.from_numpy(np.ascontiguousarray(g[k])).cuda()
+        for k in ("underlying", "strike", "t", "r", "q", "sigma")]
+    outs = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(6)]
+    st = torch.empty(n, dtype=torch.int8, device="cuda")
+    ep, eg = _native.fv_error(), _native.fv_error()
+    rc = lib.fv_price_greeks(2, *[_native.col(c) for c in cols], n, *[o.data_ptr() for o in outs],
+                             st.data_ptr(), ep, eg)
+    assert rc == 0, (ep.message, eg.message)
+    assert_bits(outs[0].cpu().numpy(), g["bsm_price"], "fused price")
+    for j, name in enumerate(("delta", "gamma", "theta", "rho", "vega")):
+        assert_bits(outs[j + 1].cpu().numpy(), g[f"bsm_{name}"], f"fused {name}")
+    assert_bits(st.cpu().numpy(), g["bsm_status"], "fused status")
+
+
+def _outcome(fn):
+    try:
+        return {"value": fn()}
+    except Exception as e:  # noqa: BLE001
+        name = type(e).__name__
+        return {"exc": name, "msg": str(e)}
+
+
+def test_exception_rows(fv):
+    """Each fuzzed extreme row alone: same value or same exception + message."""
+    cases = json.load(open(os.path.join(GOLDEN, "exceptions.json")))
+    n_checked = 0
+    for c in cases:
+        a = c["in"]
+        m = a["model"]
+        fl = ["c" if a["flag"] > 0 else "p"]
+        base = (m, fl, [a["underlying"]], [a["strike"]], [a["t"]], [a["r"]])
+        calls = {
+            "price": lambda: {"price": float(fv.batch_price(*base, [a["q"]], sigma=[a["sigma"]])["price"][0])},
+            "greeks": lambda: (lambda tb: {g: float(tb[g][0]) for g in ("delta", "gamma", "theta", "rho", "vega")})(
+                fv.batch_greeks(*base, [a["q"]], sigma=[a["sigma"]])),
+            "lbr": lambda: (lambda tb: {"iv": float(tb["iv"][0]), "status": str(tb["status"][0])})(
+                fv.batch_iv(m, "lbr", *base[1:], price=[a["price"]], q=[a["q"]])),
+            "halley": lambda: (lambda tb: {"iv": float(tb["iv"][0]), "status": str(tb["status"][0])})(
+                fv.batch_iv(m, "halley", *base[1:], price=[a["price"]], q=[a["q"]])),
+        }
+        for key, fn in calls.items():
+            if key not in c:
+                continue
+            want = c[key]
+            got = _outcome(fn)
+            if "exc" in want:
+                assert got.get("exc") == want["exc"] and got.get("msg") == want["msg"], (key, a, got, want)
+            else:
+                assert "value" in got, (key, a, got, want)
+                for k, v in want.items():
+                    gv = got["value"][k]
+                    if isinstance(v, str):
+                        assert gv == v, (key, a, got, want)
+                    else:
+                        assert bits_equal(gv, v), (key, a, got, want)
+            n_checked += 1
+    assert n_checked > 5000
+
+
+def test_validation_errors(fv):
+    cases = json.load(open(os.path.join(GOLDEN, "validation.json")))
+    for c in cases:
+        fn = getattr(fv, c["fn"])
+        try:
+            fn(c["model"], **c["kwargs"])
+            got = {"ok": True}
+        except fv.BatchError as e:
+            got = {"kind": e.kind, "index": e.index, "detail": e.detail, "msg": str(e)}
+        assert got == c["out"], (c, got)
+
+
+def first_exception_batch(which):
+    """Two raising rows in one LBR batch; ``which`` picks the order."""
+    n = 5000
+    F = np.full(n, 100.0)
+    K = np.full(n, 100.0)
+    t = np.full(n, 1.0)
+    r = np.zeros(n)
+    px = np.full(n, 5.0)
+    a, b = (2000, 3000) if which == 0 else (3000, 2000)
+    F[a], K[a] = 1e-300, 1e300       # log(F/K) of 0: ValueError('math domain error')
+    r[b] = 1000.0                    # exp(r t) overflow: OverflowError('math range error')
+    return n, F, K, t, r, px
+
+
+@pytest.mark.parametrize("which,exc", [(0, ValueError), (1, OverflowError)])
+def test_first_exception_row_wins(fv, which, exc):
+    """A batch with several raising rows raises the lowest one (batch.py:166-178)."""
+    n, F, K, t, r, px = first_exception_batch(which)
+    with pytest.raises(exc, match="math (domain|range) error"):
+        fv.batch_iv("black", "lbr", ["c"] * n, F, K, t, r, price=px)
+
+
+# --------------------------------------------------------------------------
+# larger seeded workloads: GPU vs the CPU oracle (bit-exact)
+# --------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def oracle_mod():
+    from oracle import fvoracle
+    fvoracle.lib()
+    return fvoracle
+
+
+def test_c1_lbr_vs_oracle(fv, oracle_mod):
+    from paper_2604_27210_b200 import workloads as W
+    flag, S, K, t, r, q, sig = W.chain_draws(400_000, seed=7)
+    px = oracle_mod.rows_price("black", flag, S, K, t, r, 0.0, sig)["price"]
+    want = oracle_mod.rows_iv("black", "lbr", flag, S, K, t, r, 0.0, px)
+    rc, err, iv, st, reg = _iv_native(0, 1, flag, S, K, t, r, np.zeros_like(S), px, True)
+    assert rc == 0, err.message
+    assert_bits(st, want["status_code"], "C1 status")
+    assert_bits(iv, want["iv"], "C1 iv")
+    assert_bits(reg, want["region"], "C1 region")
+
+
+def test_c2_halley_vs_oracle(fv, oracle_mod):
+    from paper_2604_27210_b200 import workloads as W
+    flag, S, K, t, r, q, sig = W.chain_draws(100_000, seed=8)
+    px = oracle_mod.rows_price("bsm", flag, S, K, t, r, q, sig)["price"]
+    want = oracle_mod.rows_iv("bsm", "halley", flag, S, K, t, r, q, px)
+    rc, err, iv, st, reg = _iv_native(2, 0, flag, S, K, t, r, q, px, True)
+    assert rc == 0, err.message
+    assert_bits(st, want["status_code"], "C2 status")
+    assert_bits(iv, want["iv"], "C2 iv")
+
+
+def test_c5_wings_vs_oracle(fv, oracle_mod):
+    from paper_2604_27210_b200 import workloads as W
+    flag, F, K, t, r, s, kind, side = W.c5_params(200_000, seed=9)
+    px0 = oracle_mod.rows_price("black", flag, F, K, t, r, 0.0, s)["price"]
+    px = W.c5_prices(flag, F, K, t, r, kind, side, px0)
+    for method, mcode in (("lbr", 1), ("halley", 0)):
+        want = oracle_mod.rows_iv("black", method, flag, F, K, t, r, 0.0, px)
+        rc, err, iv, st, reg = _iv_native(0, mcode, flag, F, K, t, r, np.zeros_like(F), px, True)
+        assert rc == 0, err.message
+        assert_bits(st, want["status_code"], f"C5 {method} status")
+        assert_bits(iv, want["iv"], f"C5 {method} iv")
+
+
+def test_c4_chain_sample_vs_oracle(fv, oracle_mod):
+    from paper_2604_27210_b200 import workloads as W
+    rng = np.random.default_rng(4)
+    starts = rng.integers(0, W.C4_ROWS - 2000, 40)
+    parts = [W.c4_params(int(s0), int(s0) + 2000) for s0 in starts]
+    flag, F, K, t, r, s = (np.concatenate([p[j] for p in parts]) for j in range(6))
+    px = oracle_mod.rows_price("black", flag, F, K, t, r, 0.0, s)["price"]
+    want = oracle_mod.rows_iv("black", "lbr", flag, F, K, t, r, 0.0, px)
+    rc, err, iv, st, reg = _iv_native(0, 1, flag, F, K, t, r, np.zeros_like(F), px, False)
+    assert rc == 0, err.message
+    assert_bits(st, want["status_code"], "C4 status")
+    assert_bits(iv, want["iv"], "C4 iv")
+    assert_bits(reg, want["region"], "C4 region")
+
+
+def test_host_chunked_pipeline_matches_device(fv):
+    """Host-pointer calls (chunked H2D/kernel/D2H over 3 streams) give the same
+    bits as device-resident calls, including row offsets across chunks."""
+    from paper_2604_27210_b200 import _native
+    from paper_2604_27210_b200 import workloads as W
+    lib = _native.load()
+    flag, S, K, t, r, q, sig = W.chain_draws(300_001, seed=11)
+    px = fv.batch_price("black", W.flag_chars(flag), S, K, t, r, sigma=sig)["price"]
+    lib.fv_set_chunk_rows(65_536)
+    try:
+        a = _iv_native(0, 1, flag, S, K, t, r, np.zeros_like(S), px, False)
+    finally:
+        lib.fv_set_chunk_rows(1 << 22)
+    b = _iv_native(0, 1, flag, S, K, t, r, np.zeros_like(S), px, True)
+    assert a[0] == 0 and b[0] == 0
+    assert_bits(a[2], b[2], "iv host vs device")
+    assert_bits(a[3], b[3], "status host vs device")

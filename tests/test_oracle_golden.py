@@ -136,3 +136,11 @@ def test_validation_errors(oracle):
         except oracle.OracleBatchError as e:
             got = {"kind": e.kind, "index": e.index, "detail": e.detail, "msg": str(e)}
         assert got == c["out"], (c, got)
+
+
+@pytest.mark.parametrize("which,exc", [(0, ValueError), (1, OverflowError)])
+def test_first_exception_row_wins_oracle(oracle, which, exc):
+    from test_gpu_parity import first_exception_batch
+    n, F, K, t, r, px = first_exception_batch(which)
+    with pytest.raises(exc, match="math (domain|range) error"):
+        oracle.batch_iv("black", "lbr", ["c"] * n, F, K, t, r, price=px)
