@@ -232,43 +232,6 @@ __global__ void __launch_bounds__(256) k_price_greeks(KArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_lbr(KArgs a) {
-  const int64_t npair = (a.n + 1) >> 1;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = 2 * j;
-    const bool two = i + 1 < a.n;
-    Pair p;
-    load_pair(a, i, two, p);
-    double iv[2] = {0.0, 0.0};
-    int stt[2] = {0, 0}, reg[2] = {-1, -1};
-#pragma unroll 1
-    for (int u = 0; u < (two ? 2 : 1); ++u) {
-      uint32_t bad = row_checks(a, p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u], p.q[u], p.last[u]);
-      if (bad) {
-        publish_checks(a.st, bad, a.row0 + i + u);
-        iv[u] = __builtin_nan(""); stt[u] = FV_IV_MAX_ITER; reg[u] = -1;
-        continue;
-      }
-      FvExc e = {0, 0, 0.0};
-      FvLbrOut o = fv_lbr_batch_row(a.model, (double)p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u],
-                                    p.q[u], p.last[u], e);
-      publish_exc(&a.st->exc_first, e.code, a.row0 + i + u);
-      iv[u] = o.sigma; stt[u] = o.status; reg[u] = o.region;
-    }
-    st2(a.o0, i, two, a.out_vec, iv[0], iv[1]);
-    st2i8(a.status, i, two, stt[0], stt[1]);
-    st2i8(a.region, i, two, reg[0], reg[1]);
-  }
-}
-
-// Halley phase-2 queue entry
-struct HQ {
-  FvHalleyCtx c;
-  FvHalleyState s;
-  int64_t row;   // local row
-};
-
 __device__ __forceinline__ unsigned int warp_append(unsigned int* counter, bool want) {
   unsigned mask = __ballot_sync(0xffffffffu, want);
   unsigned int base = 0;
@@ -280,6 +243,159 @@ __device__ __forceinline__ unsigned int warp_append(unsigned int* counter, bool 
   }
   return base + __popc(mask & ((1u << lane) - 1));
 }
+
+// LBR as classify + region-uniform solve passes.  k_lbr_classify normalizes
+// every quote, finishes the ones that need no iteration (bounds, ATM,
+// exceptions) and sorts the rest into three queues (far-low, near, far-high)
+// with their anchors; each k_lbr_solve<R> then runs one region's guess +
+// Householder(3) code over a dense queue, so warps are region-uniform and
+// each kernel's instruction footprint stays small.
+struct LbrQueues {
+  FvLbrState* state;     // [chunk] per local row
+  int32_t* q[4];         // 0..2: local rows per region class; 3: rows pending anchors
+  unsigned int* count;   // [4]
+};
+
+__device__ __forceinline__ int region_class(int region) {
+  return region == FV_FAR_LOW ? 0 : (region == FV_FAR_HIGH ? 2 : 1);
+}
+
+// Pass 1: validation + normalize_quote + bounds + ATM (small code, one pass
+// over the input columns).  Finished quotes are written out; the rest get
+// (x, beta, sqrt_t) in the state block and their row in the pending queue.
+__global__ void __launch_bounds__(256) k_lbr_normalize(KArgs a, LbrQueues lq) {
+  const int64_t npair = (a.n + 1) >> 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nloop = (npair + stride - 1) / stride;
+  for (int64_t it = 0; it < nloop; ++it) {
+    const int64_t j = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool active = j < npair;
+    const int64_t i = 2 * j;
+    const bool two = active && (i + 1 < a.n);
+    double iv[2] = {0.0, 0.0};
+    int stt[2] = {FV_IV_MAX_ITER, FV_IV_MAX_ITER};
+    Pair p;
+    if (active) load_pair(a, i, two, p);
+    // uniform trip count so the queue ballot sees the full warp
+#pragma unroll 1
+    for (int u = 0; u < 2; ++u) {
+      const bool valid = active && (u == 0 || two);
+      bool pending = false;
+      double ivu = __builtin_nan("");
+      int stu = FV_IV_MAX_ITER;
+      FvLbrState st;
+      if (valid) {
+        const int fl = u ? p.fl[1] : p.fl[0];
+        const double un = u ? p.un[1] : p.un[0], k = u ? p.k[1] : p.k[0];
+        const double t = u ? p.t[1] : p.t[0], r = u ? p.r[1] : p.r[0];
+        const double q = u ? p.q[1] : p.q[0], px = u ? p.last[1] : p.last[0];
+        uint32_t bad = row_checks(a, fl, un, k, t, r, q, px);
+        if (bad) {
+          publish_checks(a.st, bad, a.row0 + i + u);
+        } else {
+          FvExc e = {0, 0, 0.0};
+          FvLbrOut o;
+          o.sigma = __builtin_nan(""); o.status = FV_IV_MAX_ITER; o.region = -1; o.iterations = 0;
+          double Fw = un;
+          bool done = true;
+          if (a.model != 0) Fw = un * py_exp((r - q) * t, e);     // batch.py:229
+          if (e.code) {
+          } else if (!(t > 0.0)) {
+            o.status = FV_IV_BELOW_INTRINSIC;                      // batch.py:230-236
+          } else {
+            done = fv_lbr_normalize((double)fl, Fw, k, t, r, px, st, o, e) != 0;
+          }
+          publish_exc(&a.st->exc_first, e.code, a.row0 + i + u);
+          if (done || e.code) {
+            ivu = (o.status == FV_IV_CONVERGED) ? o.sigma : __builtin_nan("");
+            stu = o.status;
+          } else {
+            pending = true;
+          }
+        }
+      }
+      unsigned int slot = warp_append(lq.count + 3, pending);
+      if (pending) {
+        lq.q[3][slot] = (int32_t)(i + u);
+        FvLbrState* d = lq.state + (i + u);
+        d->x = st.x; d->beta = st.beta; d->sqrt_t = st.sqrt_t;
+      }
+      if (u) { iv[1] = ivu; stt[1] = stu; }
+      else { iv[0] = ivu; stt[0] = stu; }
+    }
+    if (active) {
+      st2(a.o0, i, two, a.out_vec, iv[0], iv[1]);
+      st2i8(a.status, i, two, stt[0], stt[1]);
+      st2i8(a.region, i, two, -1, -1);
+    }
+  }
+}
+
+// Pass 2: anchors + region over the pending queue; appends each quote to its
+// region class queue.
+__global__ void __launch_bounds__(256) k_lbr_anchors(KArgs a, LbrQueues lq) {
+  const unsigned int n = lq.count[3];
+  const unsigned int stride = gridDim.x * blockDim.x;
+  const unsigned int nloop = (n + stride - 1) / stride;
+  for (unsigned int it = 0; it < nloop; ++it) {
+    const unsigned int j = it * stride + blockIdx.x * blockDim.x + threadIdx.x;
+    int cls = -1, region = -1;
+    int32_t row = 0;
+    FvLbrState st;
+    if (j < n) {
+      row = lq.q[3][j];
+      st = lq.state[row];
+      FvExc e = {0, 0, 0.0};
+      FvLbrOut o;
+      o.region = -1;
+      if (fv_lbr_anchors(st, o, e)) {
+        publish_exc(&a.st->exc_first, e.code, a.row0 + row);
+        a.o0[row] = __builtin_nan("");
+        a.status[row] = (int8_t)FV_IV_MAX_ITER;
+      } else {
+        region = o.region;
+        cls = region_class(region);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      unsigned int slot = warp_append(lq.count + c, cls == c);
+      if (cls == c) {
+        // entry = local row * 2 + near-high bit (the near class holds both)
+        lq.q[c][slot] = (int32_t)(2 * row + (region == FV_NEAR_HIGH ? 1 : 0));
+        FvLbrState* d = lq.state + row;
+        d->s_c = st.s_c; d->b0 = st.b0; d->b1 = st.b1; d->E0 = st.E0; d->E1 = st.E1;
+      }
+    }
+    if (j < n && a.region && cls >= 0) a.region[row] = (int8_t)region;
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256, 4) k_lbr_solve(KArgs a, LbrQueues lq) {
+  const int c = R == FV_FAR_LOW ? 0 : (R == FV_FAR_HIGH ? 2 : 1);
+  const unsigned int n = lq.count[c];
+  const int32_t* q = lq.q[c];
+  for (unsigned int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int32_t ent = q[j];
+    const int32_t row = ent >> 1;
+    const FvLbrState st = lq.state[row];
+    const int region = (R == FV_NEAR_LOW) ? ((ent & 1) ? FV_NEAR_HIGH : FV_NEAR_LOW) : R;
+    FvExc e = {0, 0, 0.0};
+    FvLbrOut o = fv_lbr_solve<R>(region, st, e);
+    publish_exc(&a.st->exc_first, e.code, a.row0 + row);
+    a.o0[row] = (o.status == FV_IV_CONVERGED) ? o.sigma : __builtin_nan("");
+    a.status[row] = (int8_t)o.status;
+  }
+}
+
+// Halley phase-2 queue entry
+struct HQ {
+  FvHalleyCtx c;
+  FvHalleyState s;
+  int64_t row;   // local row
+};
+
 
 __global__ void __launch_bounds__(256) k_halley1(KArgs a, HQ* queue, unsigned int* qlen) {
   const int64_t npair = (a.n + 1) >> 1;
@@ -411,7 +527,13 @@ struct DevWork {
   char* chunk[FV_NSLOT] = {};
   int64_t chunk_cap_rows[FV_NSLOT] = {};
   ExplainOut* explain = nullptr;
-  int blocks_price = 0, blocks_greeks = 0, blocks_lbr = 0, blocks_h1 = 0, blocks_h2 = 0;
+  // LBR classify -> solve workspace (per slot)
+  FvLbrState* lbr_state[FV_NSLOT] = {};
+  int32_t* lbr_q[FV_NSLOT] = {};        // 4 queues of lbr_cap entries each
+  unsigned int* lbr_count = nullptr;    // [FV_NSLOT][4]
+  int64_t lbr_cap[FV_NSLOT] = {};
+  int blocks_price = 0, blocks_greeks = 0, blocks_h1 = 0, blocks_h2 = 0;
+  int blocks_lbr_norm = 0, blocks_lbr_anch = 0, blocks_lbr_fl = 0, blocks_lbr_near = 0, blocks_lbr_fh = 0;
   std::mutex mu;
 };
 
@@ -443,7 +565,12 @@ cudaError_t get_work(DevWork** out) {
     CK(cudaMalloc(&w->explain, sizeof(ExplainOut)));
     w->blocks_price = occupancy_blocks((const void*)k_price, w->sm_count);
     w->blocks_greeks = occupancy_blocks((const void*)k_price_greeks<true, true>, w->sm_count);
-    w->blocks_lbr = occupancy_blocks((const void*)k_lbr, w->sm_count);
+    CK(cudaMalloc(&w->lbr_count, sizeof(unsigned int) * 4 * FV_NSLOT));
+    w->blocks_lbr_norm = occupancy_blocks((const void*)k_lbr_normalize, w->sm_count);
+    w->blocks_lbr_anch = occupancy_blocks((const void*)k_lbr_anchors, w->sm_count);
+    w->blocks_lbr_fl = occupancy_blocks((const void*)k_lbr_solve<FV_FAR_LOW>, w->sm_count);
+    w->blocks_lbr_near = occupancy_blocks((const void*)k_lbr_solve<FV_NEAR_LOW>, w->sm_count);
+    w->blocks_lbr_fh = occupancy_blocks((const void*)k_lbr_solve<FV_FAR_HIGH>, w->sm_count);
     w->blocks_h1 = occupancy_blocks((const void*)k_halley1, w->sm_count);
     w->blocks_h2 = occupancy_blocks((const void*)k_halley2, w->sm_count);
     g_work[dev] = w;
@@ -459,6 +586,41 @@ cudaError_t ensure_queue(DevWork* w, int slot, int64_t rows) {
   CK(cudaMalloc(&w->queue[slot], sizeof(HQ) * cap));
   w->queue_cap[slot] = cap;
   return cudaSuccess;
+}
+
+// rows per LBR classify/solve round (bounds the state workspace: 64 B/row)
+const int64_t kLbrChunk = 1 << 25;
+
+cudaError_t ensure_lbr(DevWork* w, int slot, int64_t rows) {
+  if (w->lbr_cap[slot] >= rows) return cudaSuccess;
+  if (w->lbr_state[slot]) cudaFree(w->lbr_state[slot]);
+  if (w->lbr_q[slot]) cudaFree(w->lbr_q[slot]);
+  w->lbr_state[slot] = nullptr;
+  w->lbr_q[slot] = nullptr;
+  w->lbr_cap[slot] = 0;
+  int64_t cap = rows < 4096 ? 4096 : rows;
+  CK(cudaMalloc(&w->lbr_state[slot], sizeof(FvLbrState) * cap));
+  CK(cudaMalloc(&w->lbr_q[slot], sizeof(int32_t) * 4 * cap));
+  w->lbr_cap[slot] = cap;
+  return cudaSuccess;
+}
+
+// Rows [off, off + len) of a launch as a launch of its own.
+DCol dcol_at(DCol c, int64_t off) { if (c.mode != 0) c.p += off * c.stride; return c; }
+DFlag dflag_at(DFlag c, int64_t off) { if (c.mode != 0) c.p += off * c.stride; return c; }
+KArgs sub_args(const KArgs& a, int64_t off, int64_t len) {
+  KArgs b = a;
+  b.flag = dflag_at(a.flag, off);
+  b.un = dcol_at(a.un, off); b.k = dcol_at(a.k, off); b.t = dcol_at(a.t, off);
+  b.r = dcol_at(a.r, off); b.q = dcol_at(a.q, off); b.last = dcol_at(a.last, off);
+  double** outs[6] = {&b.o0, &b.o1, &b.o2, &b.o3, &b.o4, &b.o5};
+  for (double** o : outs) if (*o) *o += off;
+  if (b.status) b.status += off;
+  if (b.region) b.region += off;
+  b.n = len;
+  b.row0 = a.row0 + off;
+  if (off & 1) b.out_vec = 0;
+  return b;
 }
 
 enum Kind { KIND_PRICE, KIND_IV, KIND_GREEKS, KIND_PRICE_GREEKS };
@@ -502,8 +664,23 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
       break;
     case KIND_IV:
       if (c.method == FV_METHOD_LBR) {
-        k_lbr<<<blocks_for(w->blocks_lbr, a.n), 256, 0, s>>>(a);
-        ++t_launches;
+        const int64_t chunk = a.n < kLbrChunk ? a.n : kLbrChunk;
+        CK(ensure_lbr(w, slot, chunk));
+        for (int64_t off = 0; off < a.n; off += chunk) {
+          KArgs b = sub_args(a, off, (a.n - off) < chunk ? (a.n - off) : chunk);
+          LbrQueues lq;
+          lq.state = w->lbr_state[slot];
+          for (int c3 = 0; c3 < 4; ++c3) lq.q[c3] = w->lbr_q[slot] + c3 * w->lbr_cap[slot];
+          lq.count = w->lbr_count + 4 * slot;
+          CK(cudaMemsetAsync(lq.count, 0, 4 * sizeof(unsigned int), s));
+          k_lbr_normalize<<<blocks_for(w->blocks_lbr_norm, b.n), 256, 0, s>>>(b, lq);
+          int64_t cap1 = (b.n + 255) / 256;
+          k_lbr_anchors<<<cap1 < w->blocks_lbr_anch ? cap1 : w->blocks_lbr_anch, 256, 0, s>>>(b, lq);
+          k_lbr_solve<FV_FAR_LOW><<<cap1 < w->blocks_lbr_fl ? cap1 : w->blocks_lbr_fl, 256, 0, s>>>(b, lq);
+          k_lbr_solve<FV_NEAR_LOW><<<cap1 < w->blocks_lbr_near ? cap1 : w->blocks_lbr_near, 256, 0, s>>>(b, lq);
+          k_lbr_solve<FV_FAR_HIGH><<<cap1 < w->blocks_lbr_fh ? cap1 : w->blocks_lbr_fh, 256, 0, s>>>(b, lq);
+          t_launches += 5;
+        }
       } else {
         CK(ensure_queue(w, slot, a.n));
         CK(cudaMemsetAsync(w->qlen + slot, 0, sizeof(unsigned int), s));

@@ -28,9 +28,13 @@
 #if defined(__CUDACC__)
 #define FV_HD __host__ __device__ __forceinline__
 #define FV_HDM __host__ __device__ __forceinline__
+// Out-of-line on the device: the LBR kernel calls these from many sites and
+// inlining all of them blows the instruction cache (ncu: stall_no_instruction).
+#define FV_HDN __host__ __device__ __noinline__
 #else
 #define FV_HD static inline
 #define FV_HDM inline
+#define FV_HDN static
 #endif
 
 // ---- tables: host copy (static arrays) + device copy (global memory) -------
@@ -43,6 +47,8 @@
 #include "fv_tables.h"
 #undef FV_TABLE
 #endif
+
+#include "fv_consts.h"
 
 #if defined(__CUDA_ARCH__)
 #define FV_TAB(name, i) (__ldg(&name##_d[(i)]))
@@ -81,7 +87,7 @@ FV_HD double fv_fabs(double x) { return fv_asdouble(fv_asuint64(x) & 0x7ffffffff
 // exp: glibc 2.39 sysdeps/ieee754/dbl-64/e_exp.c as built into __exp_fma.
 // exp(x) = 2^(k/128) * exp(r); table scale*(1+tail); degree-5 polynomial.
 // ---------------------------------------------------------------------------
-FV_HD double fv_exp_specialcase(double tmp, uint64_t sbits, uint64_t ki) {
+FV_HDN double fv_exp_specialcase(double tmp, uint64_t sbits, uint64_t ki) {
   if ((ki & 0x80000000ull) == 0) {
     // k > 0: the exponent of scale might have overflowed by <= 460.
     sbits -= 1009ull << 52;
@@ -170,7 +176,7 @@ FV_HD double fv_exp(double x) { return fv_exp_core<false>(x, 0.0, 0); }
 // ---------------------------------------------------------------------------
 // log: glibc 2.39 sysdeps/ieee754/dbl-64/e_log.c as built into __log_fma.
 // ---------------------------------------------------------------------------
-FV_HD double fv_log(double x) {
+FV_HDN double fv_log(double x) {
   uint64_t ix = fv_asuint64(x);
   uint32_t top = (uint32_t)(ix >> 48);
   if (ix - 0x3fee000000000000ull < 0x3090000000000ull) {  // |x - 1| < ~0x1p-4
@@ -228,7 +234,7 @@ FV_HD double fv_log(double x) {
 // and > 0 (float_pow strips the sign, zero, inf, nan and 1.0 itself) and y a
 // small positive integer (2, 3, 4 at lbr.py:298, :342, :369, :376, :386).
 // ---------------------------------------------------------------------------
-FV_HD double fv_pow_pos(double x, double y) {
+FV_HDN double fv_pow_pos(double x, double y) {
   uint64_t ix = fv_asuint64(x);
   if ((ix >> 52) == 0) {                       // subnormal x: normalize
     ix = fv_asuint64(x * 0x1p52);
@@ -275,7 +281,7 @@ FV_HD double fv_pow_pos(double x, double y) {
 // erfc: glibc 2.39 sysdeps/ieee754/dbl-64/s_erf.c (fdlibm-derived, Estrin-style
 // pairs), built WITHOUT fma; its two exp calls resolve to __exp_fma (fv_exp).
 // ---------------------------------------------------------------------------
-FV_HD double fv_erfc(double x) {
+FV_HDN double fv_erfc(double x) {
   uint64_t ux = fv_asuint64(x);
   int32_t hx = (int32_t)(ux >> 32);
   int32_t ix = hx & 0x7fffffff;
@@ -339,7 +345,7 @@ FV_HD double fv_erfc(double x) {
       R = ((R1 + s2 * R2) + s4 * R3) + s6 * R4;
       S = (((S1 + s2 * S2) + s4 * S3) + s6 * S4) + s8 * FV_ERFC_SA8;
     } else {               // |x| >= 1/0.35
-      if (hx < 0 && ix >= 0x40180000) return 2.0 - 1e-300;  // x < -6
+      if (hx < 0 && ix >= 0x40180000) return FV_K_TWO_M_TINY;  // x < -6: two - tiny
       double R1 = s * FV_ERFC_RB1 + FV_ERFC_RB0;
       double s2 = s * s;
       double S1 = s * FV_ERFC_SB1 + 1.0;
@@ -361,7 +367,7 @@ FV_HD double fv_erfc(double x) {
     return 2.0 - r / ax;
   }
   if (hx > 0) return 0.0;  // tiny*tiny
-  return 2.0 - 1e-300;
+  return FV_K_TWO_M_TINY;
 }
 
 // ---------------------------------------------------------------------------
@@ -382,17 +388,17 @@ FV_HD double fv_erfcx_y100(double y100) {
   return c0 + (c1 + (c2 + (c3 + (c4 + (c5 + c6 * t) * t) * t) * t) * t) * t;
 }
 
-FV_HD double fv_erfcx(double x) {
+FV_HDN double fv_erfcx(double x) {
   if (x >= 0.0) {
     if (x > 50.0) {
-      const double ispi = 0.56418958354775628694807945156;  // 1/sqrt(pi)
+      const double ispi = FV_K_ISPI;  // 1/sqrt(pi)
       if (x > 5e7) return ispi / x;
       return ispi * ((x * x) * (x * x + 4.5) + 2.0) / (x * ((x * x) * (x * x + 5.0) + 3.75));
     }
     return fv_erfcx_y100(400.0 / (4.0 + x));
   }
   if (fv_isnan(x)) return x;
-  if (x < -26.7) return __builtin_inf();
-  if (x < -6.1) return 2.0 * fv_exp(x * x);
+  if (x < FV_K_M26P7) return __builtin_inf();
+  if (x < FV_K_M6P1) return 2.0 * fv_exp(x * x);
   return 2.0 * fv_exp(x * x) - fv_erfcx_y100(400.0 / (4.0 - x));
 }

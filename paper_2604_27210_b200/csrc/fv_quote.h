@@ -123,15 +123,19 @@ FV_HD double as241_poly(double c0, double c1, double c2, double c3, double c4, d
 #define FV_AS241_POLY(L, r) as241_poly(FV_AS241_##L##0, FV_AS241_##L##1, FV_AS241_##L##2, \
   FV_AS241_##L##3, FV_AS241_##L##4, FV_AS241_##L##5, FV_AS241_##L##6, FV_AS241_##L##7, r)
 
-// inv_norm_cdf (distributions.py:63-95).  p_np: p is a numpy scalar.  On
-// return *x_np is the type of the result (for the caller's later divisions).
-FV_HD double fv_inv_norm_cdf(double p, bool p_np, bool* x_np, FvExc& e) {
-  if (!(0.0 < p && p < 1.0)) { e.raise_v(FV_EXC_DOM_INVCDF_P, p, p_np); *x_np = p_np; return __builtin_nan(""); }
+// inv_norm_cdf (distributions.py:63-95).  p_np: p is a numpy scalar.  Out of
+// line on the device, so it returns (x, type of x, exception code) by value;
+// the DomainError value is p (the caller's).
+struct IncRes { double x; int x_np; int code; };
+FV_HDN IncRes fv_inv_norm_cdf_impl(double p, bool p_np) {
+  IncRes o;
+  FvExc e = {0, 0, 0.0};
+  if (!(0.0 < p && p < 1.0)) { o.x = __builtin_nan(""); o.x_np = p_np; o.code = FV_EXC_DOM_INVCDF_P; return o; }
   double q = p - 0.5;
   double x;
   bool xnp;
-  if (fv_fabs(q) <= 0.425) {
-    double r = 0.180625 - q * q;
+  if (fv_fabs(q) <= FV_K_0P425) {
+    double r = FV_K_0P180625 - q * q;
     x = q * FV_AS241_POLY(A, r) / FV_AS241_POLY(B, r);
     xnp = p_np;
   } else {
@@ -139,7 +143,7 @@ FV_HD double fv_inv_norm_cdf(double p, bool p_np, bool* x_np, FvExc& e) {
     r = py_sqrt(-py_log(r, e), e);
     double val;
     if (r <= 5.0) {
-      r = r - 1.6;
+      r = r - FV_K_1P6;
       val = py_div(FV_AS241_POLY(C, r), FV_AS241_POLY(D, r), false, e);
     } else {
       r = r - 5.0;
@@ -156,8 +160,15 @@ FV_HD double fv_inv_norm_cdf(double p, bool p_np, bool* x_np, FvExc& e) {
     x = x - py_div(u, 1.0 + 0.5 * x * u, unp || xnp, e);
     xnp = xnp || unp;
   }
-  *x_np = xnp;
-  return x;
+  o.x = x; o.x_np = xnp; o.code = e.code;
+  return o;
+}
+FV_HD double fv_inv_norm_cdf(double p, bool p_np, bool* x_np, FvExc& e) {
+  IncRes o = fv_inv_norm_cdf_impl(p, p_np);
+  if (o.code == FV_EXC_DOM_INVCDF_P) e.raise_v(o.code, p, p_np);
+  else if (o.code) e.raise(o.code);
+  *x_np = o.x_np != 0;
+  return o.x;
 }
 
 // ---- pricing.py black_kernel (:23-33) ---------------------------------------
@@ -167,7 +178,7 @@ FV_HD double fv_black_kernel(double th, double Fw, double K, double disc, double
                              double lnFK, bool fk_bad, FvExc& e) {
   double intrinsic = py_max(th * (Fw - K), 0.0);
   double cap = (th > 0.0) ? Fw : K;
-  if (s < 1e-12) return disc * intrinsic;
+  if (s < FV_K_1EM12) return disc * intrinsic;
   if (fk_bad) e.raise(FV_EXC_MATH_DOMAIN);
   double d1 = (lnFK + 0.5 * s * s) / s;
   double d2 = d1 - s;
@@ -224,7 +235,7 @@ FV_HD FvGreeks fv_price_greeks_row(int model, double th, double un, double K, do
     if (disc_ovf) ep.raise(FV_EXC_MATH_RANGE);
   }
   // batch_greeks: disc -> (edge) -> F -> carry_disc -> log
-  bool edge = s < 1e-12;
+  bool edge = s < FV_K_1EM12;
   double carry_disc = disc;
   if (want_greeks) {
     if (disc_ovf) eg.raise(FV_EXC_MATH_RANGE);
@@ -236,7 +247,7 @@ FV_HD FvGreeks fv_price_greeks_row(int model, double th, double un, double K, do
   }
   double intrinsic = py_max(th * (Fw - K), 0.0);
   double cap = (th > 0.0) ? Fw : K;
-  if (s < 1e-12) {
+  if (s < FV_K_1EM12) {
     o.price = disc * intrinsic;
     return o;
   }
@@ -299,17 +310,17 @@ FV_HD int fv_halley_phase1(int model, double th, double un, double K, double t, 
   if (e.code) { *status = FV_IV_MAX_ITER; return 1; }
   double disc_intrinsic = discount * py_max(th * (Fw - K), 0.0);
   double disc_cap = discount * ((th > 0.0) ? Fw : K);
-  double tie_tol = 1e-12 * py_max(1.0, disc_cap);
+  double tie_tol = FV_K_1EM12 * py_max(1.0, disc_cap);
   if (!fv_isfinite(target)) { *status = FV_IV_BELOW_INTRINSIC; return 1; }
   if (target <= disc_intrinsic + tie_tol) { *status = FV_IV_BELOW_INTRINSIC; return 1; }
   if (target > disc_cap + tie_tol) { *status = FV_IV_ABOVE_UPPER; return 1; }
-  double tol_price = py_min(tie_tol, 1e-10 * (target - disc_intrinsic));
+  double tol_price = py_min(tie_tol, FV_K_1EM10 * (target - disc_intrinsic));
   if (t <= 0.0) { *status = FV_IV_ABOVE_UPPER; return 1; }
   c.th = th; c.Fw = Fw; c.K = K; c.disc = discount; c.sqrt_t = sqrt_t;
   c.lnFK = fv_log_fk(Fw / K, &c.fk_bad);
   c.target = target; c.tol_price = tol_price;
 
-  double lo = 1e-9, hi = 10.0;
+  double lo = FV_K_1EM9, hi = 10.0;
   double f_lo = fv_halley_f(c, lo, e);
   if (e.code) { *status = FV_IV_MAX_ITER; return 1; }
   if (f_lo >= 0.0) {
@@ -323,7 +334,7 @@ FV_HD int fv_halley_phase1(int model, double th, double un, double K, double t, 
   }
   if (f_hi < 0.0) { *status = FV_IV_MAX_ITER; return 1; }
   double sigma = sqrt(FV_TWO_PI / t) * target / un;
-  sigma = py_min(py_max(sigma, 0.05), 2.0);
+  sigma = py_min(py_max(sigma, FV_K_0P05), 2.0);
   sigma = py_min(py_max(sigma, lo), hi);
   double fval = fv_halley_f(c, sigma, e);
   if (fval > 0.0) hi = py_min(hi, sigma);
@@ -336,7 +347,7 @@ FV_HD int fv_halley_phase1(int model, double th, double un, double K, double t, 
     // _raw_vega (solver.py:40-46) and the d1/d2 of :121-123 share s and d1
     double s = sigma * sqrt_t;
     double vega = 0.0, d1 = 0.0;
-    if (!(s < 1e-12)) {
+    if (!(s < FV_K_1EM12)) {
       if (c.fk_bad) e.raise(FV_EXC_MATH_DOMAIN);
       d1 = (c.lnFK + 0.5 * s * s) / s;
       vega = discount * Fw * fv_norm_pdf(d1) * sqrt_t;
@@ -364,7 +375,7 @@ FV_HD int fv_halley_phase1(int model, double th, double un, double K, double t, 
     double step = cand - sigma;
     sigma = cand; fval = f_cand;
     iterations += 1;
-    if (fv_fabs(step) <= 1e-12 * py_max(1.0, sigma)) {
+    if (fv_fabs(step) <= FV_K_1EM12 * py_max(1.0, sigma)) {
       *status = FV_IV_CONVERGED; *sigma_out = sigma; st.iterations = iterations; return 1;
     }
   }
@@ -377,7 +388,7 @@ FV_HD void fv_halley_phase2(const FvHalleyCtx& c, FvHalleyState st, int* status,
                             double* sigma_out, FvExc& e) {
   double sigma = st.sigma, fval = st.fval, lo = st.lo, hi = st.hi;
   for (int it = 0; it < 128; ++it) {
-    if (fv_fabs(fval) <= c.tol_price || (hi - lo) <= 1e-12 * py_max(1.0, sigma)) {
+    if (fv_fabs(fval) <= c.tol_price || (hi - lo) <= FV_K_1EM12 * py_max(1.0, sigma)) {
       *status = FV_IV_FELL_BACK; *sigma_out = sigma; return;
     }
     sigma = 0.5 * (lo + hi);
@@ -385,7 +396,7 @@ FV_HD void fv_halley_phase2(const FvHalleyCtx& c, FvHalleyState st, int* status,
     if (fval > 0.0) hi = sigma;
     else lo = sigma;
   }
-  if (fv_fabs(fval) <= c.tol_price || (hi - lo) <= 1e-12 * py_max(1.0, sigma)) {
+  if (fv_fabs(fval) <= c.tol_price || (hi - lo) <= FV_K_1EM12 * py_max(1.0, sigma)) {
     *status = FV_IV_FELL_BACK; *sigma_out = sigma; return;
   }
   *status = FV_IV_MAX_ITER; *sigma_out = __builtin_nan("");
@@ -395,14 +406,18 @@ FV_HD void fv_halley_phase2(const FvHalleyCtx& c, FvHalleyState st, int* status,
 // normalized_black (:112-129) for Python-float x (x_work) and s of numpy-ness
 // s_np.  *E (if non-null) receives exp(-(h^2+t^2)/2) -- the factor
 // normalized_vega (:152-156) shares -- computed here when the branch needs it.
-FV_HD double fv_normalized_black(double x, double s, bool s_np, FvExc& e, double* E, int* branch) {
-  if (x > 0.0) { e.raise_v(FV_EXC_DOM_NB_X, x, 0); return __builtin_nan(""); }
-  if (!(s > 0.0)) { e.raise_v(FV_EXC_DOM_NB_S, s, s_np); return __builtin_nan(""); }
+struct NbRes { double b; double E; int code; int branch; };
+FV_HDN NbRes fv_normalized_black_impl(double x, double s, bool s_np) {
+  NbRes o;
+  o.E = 0.0; o.code = 0; o.branch = -1;
+  FvExc e = {0, 0, 0.0};
+  if (x > 0.0) { o.b = __builtin_nan(""); o.code = FV_EXC_DOM_NB_X; return o; }
+  if (!(s > 0.0)) { o.b = __builtin_nan(""); o.code = FV_EXC_DOM_NB_S; return o; }
   double h = py_div(x, s, s_np, e);
   double t = 0.5 * s;
   if (h < -10.0 && t < FV_SMALL_T_THRESHOLD + (-10.0 - h)) {
     // _asymptotic_black (:65-71)
-    if (branch) *branch = 0;
+    o.branch = 0;
     double th_ = py_div(t, h, s_np, e);
     double ee = th_ * th_;
     double rr = (h + t) * (h - t);
@@ -419,13 +434,13 @@ FV_HD double fv_normalized_black(double x, double s, bool s_np, FvExc& e, double
       c0 = (j == 17) ? (wj + qq * 0.0) : (wj + c0 * qq);
     }
     double Ev = fv_exp(-0.5 * (h * h + t * t));
-    if (E) *E = Ev;
+    o.E = Ev;
     double b = FV_INV_SQRT_TWO_PI * Ev * py_div(t, rr, s_np, e) * c0;
-    return py_max(b, 0.0);
+    o.b = py_max(b, 0.0); o.code = e.code; return o;
   }
   if (t < FV_SMALL_T_THRESHOLD) {
     // _small_t_black (:74-103)
-    if (branch) *branch = 1;
+    o.branch = 1;
     double a = 1.0 + h * FV_HALF_SQRT_TWO_PI * fv_erfcx(-h / FV_SQRT_TWO);
     double w = t * t;
     double h2 = h * h;
@@ -441,28 +456,57 @@ FV_HD double fv_normalized_black(double x, double s, bool s_np, FvExc& e, double
                  + h2 * (-1.0 + 78.0 * a + a * h2)))))) / 6227020800.0;
     double expansion = 2.0 * t * (a + w * (c1 + w * (c2 + w * (c3 + w * (c4 + w * (c5 + w * c6))))));
     double Ev = fv_exp(-0.5 * (h * h + t * t));
-    if (E) *E = Ev;
+    o.E = Ev;
     double b = FV_INV_SQRT_TWO_PI * Ev * expansion;
-    return py_max(b, 0.0);
+    o.b = py_max(b, 0.0); o.code = e.code; return o;
   }
-  if (h + t > 0.85) {
-    if (branch) *branch = 2;
+  if (h + t > FV_K_0P85) {
+    o.branch = 2;
     double b_max = fv_exp(0.5 * x);
     double b = fv_norm_cdf(h + t) * b_max - py_div(fv_norm_cdf(h - t), b_max, false, e);
-    if (E) *E = fv_exp(-0.5 * (h * h + t * t));
-    return py_max(b, 0.0);
+    o.E = fv_exp(-0.5 * (h * h + t * t));
+    o.b = py_max(b, 0.0); o.code = e.code; return o;
   }
   // _erfcx_black (:106-109)
-  if (branch) *branch = 3;
+  o.branch = 3;
   double Ev = fv_exp(-0.5 * (h * h + t * t));
-  if (E) *E = Ev;
+  o.E = Ev;
   double b = 0.5 * Ev * (fv_erfcx(-(h + t) / FV_SQRT_TWO) - fv_erfcx(-(h - t) / FV_SQRT_TWO));
-  return py_max(b, 0.0);
+  o.b = py_max(b, 0.0); o.code = e.code; return o;
 }
 
-// normalized_black_log (:140-149); *E receives -(h^2+t^2)/2 * 1 (the exponent)
-FV_HD double fv_normalized_black_log(double x, double s, bool s_np, FvExc& e) {
+FV_HD double fv_normalized_black(double x, double s, bool s_np, FvExc& e, double* E, int* branch) {
+  NbRes o = fv_normalized_black_impl(x, s, s_np);
+  if (o.code == FV_EXC_DOM_NB_X) e.raise_v(o.code, x, 0);
+  else if (o.code == FV_EXC_DOM_NB_S) e.raise_v(o.code, s, s_np);
+  else if (o.code) e.raise(o.code);
+  if (E) *E = o.E;
+  if (branch) *branch = o.branch;
+  return o.b;
+}
+
+// normalized_black_log (:140-149)
+struct DRes { double v; int code; };
+FV_HDN DRes fv_normalized_black_log_impl(double x, double s, bool s_np) {
+  FvExc e = {0, 0, 0.0};
+  DRes o;
   double h = py_div(x, s, s_np, e);
+  double t = 0.5 * s;
+  double diff = fv_erfcx(-(h + t) / FV_SQRT_TWO) - fv_erfcx(-(h - t) / FV_SQRT_TWO);
+  if (diff <= 0.0) { o.v = -__builtin_inf(); o.code = e.code; return o; }
+  o.v = -0.5 * (h * h + t * t) + py_log(0.5 * diff, e);
+  o.code = e.code;
+  return o;
+}
+FV_HD double fv_normalized_black_log(double x, double s, bool s_np, FvExc& e) {
+  DRes o = fv_normalized_black_log_impl(x, s, s_np);
+  if (o.code) e.raise(o.code);
+  return o.v;
+}
+// Inline form for the far-low kernel, with h = x / s supplied by the caller
+// (the same division the caller needs anyway; its ZeroDivisionError check is
+// the caller's).
+FV_HD double fv_nbl_h(double h, double s, FvExc& e) {
   double t = 0.5 * s;
   double diff = fv_erfcx(-(h + t) / FV_SQRT_TWO) - fv_erfcx(-(h - t) / FV_SQRT_TWO);
   if (diff <= 0.0) return -__builtin_inf();
@@ -470,49 +514,76 @@ FV_HD double fv_normalized_black_log(double x, double s, bool s_np, FvExc& e) {
 }
 
 // normalized_black_complement (:132-137) with the per-quote exp(+-x/2)
-FV_HD double fv_complement(double x, double s, bool s_np, double ep, double em, FvExc& e) {
+FV_HDN DRes fv_complement_impl(double x, double s, bool s_np, double ep, double em) {
+  FvExc e = {0, 0, 0.0};
+  DRes o;
   double h = py_div(x, s, s_np, e);
   double t = 0.5 * s;
-  return ep * fv_norm_cdf(-h - t) + em * fv_norm_cdf(h - t);
+  o.v = ep * fv_norm_cdf(-h - t) + em * fv_norm_cdf(h - t);
+  o.code = e.code;
+  return o;
+}
+FV_HD double fv_complement(double x, double s, bool s_np, double ep, double em, FvExc& e) {
+  DRes o = fv_complement_impl(x, s, s_np, ep, em);
+  if (o.code) e.raise(o.code);
+  return o.v;
 }
 
 // ---- lbr.py: implied_vol_lbr (:410-486) -----------------------------------
+// Split in two so the GPU can run it as a classify pass plus region-uniform
+// solve passes (csrc/fv_kernels.cu); fv_lbr_row glues them back together in
+// the reference's order for single-row use.
 struct FvLbrOut { double sigma; int status; int region; int iterations; };
 
-FV_HD FvLbrOut fv_lbr_row(double th, double Fw, double K, double t, double r, double px, FvExc& e) {
+// Per-quote state handed from classify to solve (anchors computed once).
+struct FvLbrState {
+  double x, beta, sqrt_t, s_c;   // x = x_work, beta = beta_work, s_c = sqrt(2|x|)
+  double b0, b1, E0, E1;         // NEAR_LOW: (b_lo, b_c, E_lo, E_c); NEAR_HIGH: (b_c, b_hi, E_c, E_hi)
+};
+
+// normalize_quote + ATM shortcut (:416-430).  Returns 1 when the quote is
+// finished (o filled: bounds, ATM, exception), else 0 with st.x / st.beta /
+// st.sqrt_t set for fv_lbr_anchors.
+FV_HD int fv_lbr_normalize(double th, double Fw, double K, double t, double r, double px,
+                           FvLbrState& st, FvLbrOut& o, FvExc& e) {
   const double nan = __builtin_nan("");
-  FvLbrOut o;
   o.sigma = nan; o.status = FV_IV_MAX_ITER; o.region = FV_REGION_NONE; o.iterations = 0;
   // normalize_quote (:174-207); F, K, t, price are numpy scalars
-  if (!(Fw > 0.0 && K > 0.0)) { e.raise(FV_EXC_DOM_FK); return o; }
+  if (!(Fw > 0.0 && K > 0.0)) { e.raise(FV_EXC_DOM_FK); return 1; }
   double xq = py_log(Fw / K, e);
   double beta0 = px * py_exp(r * t, e) / sqrt(Fw * K);
   double e_hx = py_exp(0.5 * xq, e);
   double e_mhx = py_exp(-0.5 * xq, e);
-  if (e.code) return o;
+  if (e.code) return 1;
   double parity = e_hx - e_mhx;
   double beta;
   if (th > 0.0) beta = (xq > 0.0) ? beta0 - parity : beta0;
   else beta = (xq < 0.0) ? beta0 + parity : beta0;
   double x = -fv_fabs(xq);
   double b_max = fv_exp(0.5 * x);
-  if (beta <= 1e-300) { o.status = FV_IV_BELOW_INTRINSIC; return o; }
-  if (beta >= b_max * (1.0 - 1e-15)) { o.status = FV_IV_ABOVE_UPPER; return o; }
+  if (beta <= FV_K_1EM300) { o.status = FV_IV_BELOW_INTRINSIC; return 1; }
+  if (beta >= b_max * FV_K_ONE_M_1EM15) { o.status = FV_IV_ABOVE_UPPER; return 1; }
   double sqrt_t = sqrt(t);
   py_exp(-r * t, e);                             // scale = sqrt(F K) exp(-r t): only its overflow
-  if (e.code) return o;
+  if (e.code) return 1;
 
-  if (fv_fabs(x) < 1e-12) {                      // ATM shortcut (:427-430)
-    if (!(0.0 < beta && beta < 1.0)) { e.raise_v(FV_EXC_DOM_ATM_BETA, beta, 1); return o; }
+  if (fv_fabs(x) < FV_K_1EM12) {                      // ATM shortcut (:427-430)
+    if (!(0.0 < beta && beta < 1.0)) { e.raise_v(FV_EXC_DOM_ATM_BETA, beta, 1); return 1; }
     bool znp;
     double z = fv_inv_norm_cdf(0.5 * (1.0 - beta), true, &znp, e);
-    if (e.code) return o;
+    if (e.code) return 1;
     double s = -2.0 * z;
     o.sigma = s / sqrt_t; o.status = FV_IV_CONVERGED;
-    return o;
+    return 1;
   }
+  st.x = x; st.beta = beta; st.sqrt_t = sqrt_t;
+  return 0;
+}
 
-  // anchors (:231-238), computed once (initial_guess recomputes them, :325)
+// anchors (:231-238) + _region (:241-248), computed once (initial_guess
+// recomputes them, :325).  Returns 1 if an exception was raised.
+FV_HD int fv_lbr_anchors(FvLbrState& st, FvLbrOut& o, FvExc& e) {
+  const double x = st.x, beta = st.beta;
   double s_c = py_sqrt(2.0 * fv_fabs(x), e);
   double s_lo = s_c * 0.5;
   double s_hi = s_c / 0.5;
@@ -520,49 +591,72 @@ FV_HD FvLbrOut fv_lbr_row(double th, double Fw, double K, double t, double r, do
   double b_lo = fv_normalized_black(x, s_lo, false, e, &E_lo, nullptr);
   double b_c = fv_normalized_black(x, s_c, false, e, &E_c, nullptr);
   double b_hi = fv_normalized_black(x, s_hi, false, e, &E_hi, nullptr);
-  if (e.code) return o;
+  if (e.code) return 1;
   int region;
   if (beta < b_lo) region = FV_FAR_LOW;
   else if (beta < b_c) region = FV_NEAR_LOW;
   else if (beta < b_hi) region = FV_NEAR_HIGH;
   else region = FV_FAR_HIGH;
   o.region = region;
+  st.s_c = s_c;
+  if (region == FV_NEAR_HIGH) { st.b0 = b_c; st.b1 = b_hi; st.E0 = E_c; st.E1 = E_hi; }
+  else { st.b0 = b_lo; st.b1 = b_c; st.E0 = E_lo; st.E1 = E_c; }
+  return 0;
+}
 
-  double ep = b_max;                              // exp(0.5 x), x = x_work
-  double em = 0.0;                                // exp(-0.5 x)
-  double comp_beta = b_max - beta;
+FV_HD int fv_lbr_classify(double th, double Fw, double K, double t, double r, double px,
+                          FvLbrState& st, FvLbrOut& o, FvExc& e) {
+  if (fv_lbr_normalize(th, Fw, K, t, r, px, st, o, e)) return 1;
+  return fv_lbr_anchors(st, o, e);
+}
+
+// Bracket, initial guess and Householder(3) iterations for one region
+// (:434-486).  R is the region (NEAR_LOW stands for both near regions, whose
+// code is identical; `region` then picks the anchor pair at run time).
+template <int R>
+FV_HD FvLbrOut fv_lbr_solve(int region, const FvLbrState& st, FvExc& e) {
+  const double nan = __builtin_nan("");
+  FvLbrOut o;
+  o.sigma = nan; o.status = FV_IV_MAX_ITER; o.region = region; o.iterations = 0;
+  const double x = st.x, beta = st.beta, s_c = st.s_c;
+  const double s_lo = s_c * 0.5;
+  const double s_hi = s_c / 0.5;
+
   double lo, hi;
-  if (region == FV_FAR_LOW) { lo = 0.0; hi = s_lo; }
-  else if (region == FV_NEAR_LOW) { lo = s_lo; hi = s_c; }
-  else if (region == FV_NEAR_HIGH) { lo = s_c; hi = s_hi; }
-  else {
+  double ep = 0.0, em = 0.0, comp_beta = 0.0, b_max = 0.0;
+  if (R == FV_FAR_LOW) { lo = 0.0; hi = s_lo; }
+  else if (R == FV_FAR_HIGH) {
+    b_max = fv_exp(0.5 * x);                      // quote.b_max, exp(0.5 x)
+    ep = b_max;
+    comp_beta = b_max - beta;
     lo = s_hi; hi = 2.0 * s_hi;
     em = py_exp(-0.5 * x, e);
     while (fv_complement(x, hi, false, ep, em, e) > comp_beta && hi < 1e6) hi *= 2.0;
     if (e.code) return o;
-  }
-  lo *= 1.0 - 1e-6;
-  hi *= 1.0 + 1e-6;
+  } else if (region == FV_NEAR_LOW) { lo = s_lo; hi = s_c; }
+  else { lo = s_c; hi = s_hi; }
+  lo *= FV_K_ONE_M_1EM6;
+  hi *= FV_K_ONE_P_1EM6;
   bool lo_np = false, hi_np = false;
 
   // initial_guess (:321-332)
   double s;
   bool s_np = false;
   double ln_beta = 0.0;
-  if (region == FV_FAR_LOW) {
+  if (R == FV_FAR_LOW) {
     // _far_low_guess (:283-309)
     ln_beta = py_log(beta, e);
     double s_cap = s_lo;
     s = py_div(fv_fabs(x), py_sqrt(-2.0 * ln_beta, e), false, e);
-    s = py_min(py_max(s, 1e-6 * s_cap), 0.999 * s_cap);
+    s = py_min(py_max(s, FV_K_1EM6 * s_cap), FV_K_0P999 * s_cap);
     double v = py_log(s, e);
     double v_hi = py_log(s_cap, e);
     for (int it = 0; it < 5; ++it) {
       if (e.code) return o;
-      double ln_b = fv_normalized_black_log(x, s, false, e);
+      double xs = py_div(x, s, false, e);        // h of normalized_black_log == x / s of :298
+      double ln_b = fv_nbl_h(xs, s, e);
       double g = ln_b - ln_beta;
       if (g > 0.0) v_hi = py_min(v_hi, v);
-      double xs = py_div(x, s, false, e);
       double arg = FV_LOG_INV_SQRT_TWO_PI - 0.5 * (py_powi(xs, 2, false, e) + 0.25 * s * s) - ln_b;
       double dg_dv = s * py_exp(arg, e);
       if (e.code) return o;
@@ -573,11 +667,11 @@ FV_HD FvLbrOut fv_lbr_row(double th, double Fw, double K, double t, double r, do
       v = v_new;
       s = py_exp(v, e);
     }
-  } else if (region == FV_FAR_HIGH) {
+  } else if (R == FV_FAR_HIGH) {
     // _far_high_guess (:312-318)
     double p = (b_max - beta) / (2.0 * b_max);    // numpy scalar (beta)
     bool p_np = true;
-    if (5e-324 > p) { p = 5e-324; p_np = false; }
+    if (FV_K_MIN_SUB > p) { p = FV_K_MIN_SUB; p_np = false; }
     if (FV_HALF_ONE_MINUS_EPS < p) { p = FV_HALF_ONE_MINUS_EPS; p_np = false; }
     bool z_np;
     double z = fv_inv_norm_cdf(p, p_np, &z_np, e);
@@ -586,9 +680,9 @@ FV_HD FvLbrOut fv_lbr_row(double th, double Fw, double K, double t, double r, do
     s_np = z_np;
   } else {
     // _hermite_inverse (:265-280), all Python floats
-    double b0, b1, s0, s1, E0, E1;
-    if (region == FV_NEAR_LOW) { b0 = b_lo; b1 = b_c; s0 = s_lo; s1 = s_c; E0 = E_lo; E1 = E_c; }
-    else { b0 = b_c; b1 = b_hi; s0 = s_c; s1 = s_hi; E0 = E_c; E1 = E_hi; }
+    const double b0 = st.b0, b1 = st.b1, E0 = st.E0, E1 = st.E1;
+    const double s0 = (region == FV_NEAR_LOW) ? s_lo : s_c;
+    const double s1 = (region == FV_NEAR_LOW) ? s_c : s_hi;
     double m0 = py_div(b0, FV_INV_SQRT_TWO_PI * E0, false, e);
     double m1 = py_div(b1, FV_INV_SQRT_TWO_PI * E1, false, e);
     double lb1 = py_log(b1, e);
@@ -605,18 +699,15 @@ FV_HD FvLbrOut fv_lbr_row(double th, double Fw, double K, double t, double r, do
   if (!(lo < s && s < hi)) { s = 0.5 * (lo + hi); s_np = false; }
 
   // Householder(3) iterations (:454-483)
-  bool increasing = region != FV_FAR_LOW;
+  const bool increasing = R != FV_FAR_LOW;
   double ln_comp_beta = 0.0;
   bool comp_beta_bad = false;
-  if (region == FV_FAR_HIGH) {
-    comp_beta_bad = !(comp_beta > 0.0 && fv_isfinite(comp_beta));
-    ln_comp_beta = comp_beta_bad ? 0.0 : fv_log(comp_beta);
-    if (comp_beta_bad) {                          // math.log's special cases
-      FvExc tmp = {0, 0, 0.0};
-      ln_comp_beta = py_log(comp_beta, tmp);
-      comp_beta_bad = tmp.code != 0;
-    }
+  if (R == FV_FAR_HIGH) {
+    FvExc tmp = {0, 0, 0.0};
+    ln_comp_beta = py_log(comp_beta, tmp);
+    comp_beta_bad = tmp.code != 0;
   }
+  const double inv_ln_beta = (R == FV_FAR_LOW) ? 1.0 / ln_beta : 0.0;
   int iterations = 0;
   bool converged = false;
   for (int it = 0; it < 8; ++it) {
@@ -630,8 +721,8 @@ FV_HD FvLbrOut fv_lbr_row(double th, double Fw, double K, double t, double r, do
     double r3 = r2 * r2 - py_div(3.0 * x * x, s4, s_np, e) - 0.25;
     double g, g1, g2, g3;
     bool g_np, g1_np, g23_np;
-    if (region == FV_FAR_LOW) {
-      double ln_b = fv_normalized_black_log(x, s, s_np, e);
+    if (R == FV_FAR_LOW) {
+      double ln_b = fv_nbl_h(h, s, e);            // its h = x / s is the h above
       double ln_bp = FV_LOG_INV_SQRT_TWO_PI - 0.5 * (h * h + 0.25 * s * s);
       double up = py_exp(ln_bp - ln_b, e);
       double up3 = py_powi(up, 3, false, e);
@@ -639,12 +730,13 @@ FV_HD FvLbrOut fv_lbr_row(double th, double Fw, double K, double t, double r, do
       double uppp = up * r3 - 3.0 * up * up * r2 + 2.0 * up3;
       double inv = py_div(1.0, ln_b, false, e);
       double inv2 = inv * inv;
-      g = inv - py_div(1.0, ln_beta, false, e);
+      if (ln_beta == 0.0) e.raise(FV_EXC_ZERO_DIV);
+      g = inv - inv_ln_beta;                      // 1.0 / ln_beta, loop-invariant
       g1 = -up * inv2;
       g2 = -upp * inv2 + 2.0 * up * up * inv2 * inv;
       g3 = (-uppp * inv2 + 6.0 * up * upp * inv2 * inv - 6.0 * up3 * inv2 * inv2);
       g_np = false; g1_np = false; g23_np = s_np;
-    } else if (region == FV_FAR_HIGH) {
+    } else if (R == FV_FAR_HIGH) {
       double bp = FV_INV_SQRT_TWO_PI * fv_exp(-0.5 * (h * h + t * t));
       double comp = ep * fv_norm_cdf(-h - t) + em * fv_norm_cdf(h - t);
       double w = py_div(bp, comp, false, e);
@@ -681,7 +773,7 @@ FV_HD FvLbrOut fv_lbr_row(double th, double Fw, double K, double t, double r, do
       ds_np = num_np;
       if (e.code) return o;
     }
-    if (fv_isfinite(ds) && fv_fabs(ds) <= 1e-14 * py_max(1.0, s)) {
+    if (fv_isfinite(ds) && fv_fabs(ds) <= FV_K_1EM14 * py_max(1.0, s)) {
       s = s + ds; s_np = s_np || ds_np;
       iterations += 1;
       converged = true;
@@ -696,12 +788,21 @@ FV_HD FvLbrOut fv_lbr_row(double th, double Fw, double K, double t, double r, do
     }
     s = cand; s_np = cand_np;
     iterations += 1;
-    if (fv_fabs(ds) <= 1e-14 * py_max(1.0, s)) { converged = true; break; }
+    if (fv_fabs(ds) <= FV_K_1EM14 * py_max(1.0, s)) { converged = true; break; }
   }
-  o.sigma = s / sqrt_t;
+  o.sigma = s / st.sqrt_t;
   o.status = converged ? FV_IV_CONVERGED : FV_IV_MAX_ITER;
   o.iterations = iterations;
   return o;
+}
+
+FV_HD FvLbrOut fv_lbr_row(double th, double Fw, double K, double t, double r, double px, FvExc& e) {
+  FvLbrState st;
+  FvLbrOut o;
+  if (fv_lbr_classify(th, Fw, K, t, r, px, st, o, e)) return o;
+  if (o.region == FV_FAR_LOW) return fv_lbr_solve<FV_FAR_LOW>(o.region, st, e);
+  if (o.region == FV_FAR_HIGH) return fv_lbr_solve<FV_FAR_HIGH>(o.region, st, e);
+  return fv_lbr_solve<FV_NEAR_LOW>(o.region, st, e);
 }
 
 // batch_iv LBR row (batch.py:227-238): spot models forward the underlying.
