@@ -6,6 +6,28 @@
 // the literal values (fv_tables.h).  Values are unchanged bit for bit.
 #pragma once
 
+// Divisors the reference divides by, with yh = RN(1/c) and yl = RN(1/c - yh)
+// for fv_div_const (Markstein-corrected reciprocal product; see fv_libm.h).
+#define FV_DIV_SQRT2_C 0x1.6a09e667f3bcdp+0
+#define FV_DIV_SQRT2_YH 0x1.6a09e667f3bccp-1
+#define FV_DIV_SQRT2_YL 0x1.08b2fb1366eaap-56
+#define FV_DIV_6_YH 0x1.5555555555555p-3
+#define FV_DIV_6_YL 0x1.5555555555555p-57
+#define FV_DIV_120_YH 0x1.1111111111111p-7
+#define FV_DIV_120_YL 0x1.1111111111111p-63
+#define FV_DIV_5040_YH 0x1.a01a01a01a01ap-13
+#define FV_DIV_5040_YL 0x1.a01a01a01a01ap-73
+#define FV_DIV_362880_YH 0x1.71de3a556c734p-19
+#define FV_DIV_362880_YL -0x1.c154f8ddc6c00p-73
+#define FV_DIV_39916800_YH 0x1.ae64567f544e4p-26
+#define FV_DIV_39916800_YL -0x1.c062e06d1f209p-80
+#define FV_DIV_6227020800_YH 0x1.6124613a86d09p-33
+#define FV_DIV_6227020800_YL 0x1.f28e0cc748ebep-87
+#define FV_DIV_365_YH 0x1.6719f3601671ap-9
+#define FV_DIV_365_YL -0x1.93fd31cc193fdp-66
+#define FV_DIV_100_YH 0x1.47ae147ae147bp-7
+#define FV_DIV_100_YL -0x1.eb851eb851eb8p-63
+
 #define FV_K_1EM300 1e-300
 #define FV_K_ONE_M_1EM15 (1.0 - 1e-15)
 #define FV_K_1EM12 1e-12
@@ -28,6 +50,25 @@
 #define FV_K_TWO_M_TINY (2.0 - 1e-300)
 
 struct FvK {
+  double DIV_SQRT2_C;
+  double DIV_SQRT2_YH;
+  double DIV_SQRT2_YL;
+  double DIV_6_YH;
+  double DIV_6_YL;
+  double DIV_120_YH;
+  double DIV_120_YL;
+  double DIV_5040_YH;
+  double DIV_5040_YL;
+  double DIV_362880_YH;
+  double DIV_362880_YL;
+  double DIV_39916800_YH;
+  double DIV_39916800_YL;
+  double DIV_6227020800_YH;
+  double DIV_6227020800_YL;
+  double DIV_365_YH;
+  double DIV_365_YL;
+  double DIV_100_YH;
+  double DIV_100_YL;
   double ERFC_ERX;
   double ERFC_ONE_M_ERX;
   double ERFC_PA0;
@@ -194,6 +235,25 @@ struct FvK {
 
 #if defined(__CUDACC__)
 static __constant__ FvK fv_kc = {
+    FV_DIV_SQRT2_C,
+    FV_DIV_SQRT2_YH,
+    FV_DIV_SQRT2_YL,
+    FV_DIV_6_YH,
+    FV_DIV_6_YL,
+    FV_DIV_120_YH,
+    FV_DIV_120_YL,
+    FV_DIV_5040_YH,
+    FV_DIV_5040_YL,
+    FV_DIV_362880_YH,
+    FV_DIV_362880_YL,
+    FV_DIV_39916800_YH,
+    FV_DIV_39916800_YL,
+    FV_DIV_6227020800_YH,
+    FV_DIV_6227020800_YL,
+    FV_DIV_365_YH,
+    FV_DIV_365_YL,
+    FV_DIV_100_YH,
+    FV_DIV_100_YL,
     FV_ERFC_ERX,
     FV_ERFC_ONE_M_ERX,
     FV_ERFC_PA0,
@@ -360,6 +420,44 @@ static __constant__ FvK fv_kc = {
 #endif
 
 #if defined(__CUDA_ARCH__)
+#undef FV_DIV_SQRT2_C
+#define FV_DIV_SQRT2_C (fv_kc.DIV_SQRT2_C)
+#undef FV_DIV_SQRT2_YH
+#define FV_DIV_SQRT2_YH (fv_kc.DIV_SQRT2_YH)
+#undef FV_DIV_SQRT2_YL
+#define FV_DIV_SQRT2_YL (fv_kc.DIV_SQRT2_YL)
+#undef FV_DIV_6_YH
+#define FV_DIV_6_YH (fv_kc.DIV_6_YH)
+#undef FV_DIV_6_YL
+#define FV_DIV_6_YL (fv_kc.DIV_6_YL)
+#undef FV_DIV_120_YH
+#define FV_DIV_120_YH (fv_kc.DIV_120_YH)
+#undef FV_DIV_120_YL
+#define FV_DIV_120_YL (fv_kc.DIV_120_YL)
+#undef FV_DIV_5040_YH
+#define FV_DIV_5040_YH (fv_kc.DIV_5040_YH)
+#undef FV_DIV_5040_YL
+#define FV_DIV_5040_YL (fv_kc.DIV_5040_YL)
+#undef FV_DIV_362880_YH
+#define FV_DIV_362880_YH (fv_kc.DIV_362880_YH)
+#undef FV_DIV_362880_YL
+#define FV_DIV_362880_YL (fv_kc.DIV_362880_YL)
+#undef FV_DIV_39916800_YH
+#define FV_DIV_39916800_YH (fv_kc.DIV_39916800_YH)
+#undef FV_DIV_39916800_YL
+#define FV_DIV_39916800_YL (fv_kc.DIV_39916800_YL)
+#undef FV_DIV_6227020800_YH
+#define FV_DIV_6227020800_YH (fv_kc.DIV_6227020800_YH)
+#undef FV_DIV_6227020800_YL
+#define FV_DIV_6227020800_YL (fv_kc.DIV_6227020800_YL)
+#undef FV_DIV_365_YH
+#define FV_DIV_365_YH (fv_kc.DIV_365_YH)
+#undef FV_DIV_365_YL
+#define FV_DIV_365_YL (fv_kc.DIV_365_YL)
+#undef FV_DIV_100_YH
+#define FV_DIV_100_YH (fv_kc.DIV_100_YH)
+#undef FV_DIV_100_YL
+#define FV_DIV_100_YL (fv_kc.DIV_100_YL)
 #undef FV_ERFC_ERX
 #define FV_ERFC_ERX (fv_kc.ERFC_ERX)
 #undef FV_ERFC_ONE_M_ERX

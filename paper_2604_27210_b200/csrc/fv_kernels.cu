@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(256, 4) k_lbr_solve(KArgs a, LbrQueues lq) {
     const FvLbrState st = lq.state[row];
     const int region = (R == FV_NEAR_LOW) ? ((ent & 1) ? FV_NEAR_HIGH : FV_NEAR_LOW) : R;
     FvExc e = {0, 0, 0.0};
-    FvLbrOut o = fv_lbr_solve<R>(region, st, e);
+    FvLbrOut o = (R == FV_FAR_LOW) ? fv_lbr_far_low_fused(st, e) : fv_lbr_solve<R>(region, st, e);
     publish_exc(&a.st->exc_first, e.code, a.row0 + row);
     a.o0[row] = (o.status == FV_IV_CONVERGED) ? o.sigma : __builtin_nan("");
     a.status[row] = (int8_t)o.status;

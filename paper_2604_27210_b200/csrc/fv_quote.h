@@ -72,9 +72,10 @@ FV_HD double py_exp(double x, FvExc& e) {           // math.exp (math_1, can_ove
   if (fv_isinf(r) && fv_isfinite(x)) e.raise(FV_EXC_MATH_RANGE);
   return r;
 }
-FV_HD double py_log(double x, FvExc& e) {           // math.log (m_log)
+template <bool kInl>
+FV_HD double py_log_t(double x, FvExc& e) {         // math.log (m_log)
   if (fv_isfinite(x)) {
-    if (x > 0.0) return fv_log(x);
+    if (x > 0.0) return kInl ? fv_log_i(x) : fv_log(x);
     e.raise(FV_EXC_MATH_DOMAIN);
     return x == 0.0 ? -__builtin_inf() : __builtin_nan("");
   }
@@ -82,6 +83,7 @@ FV_HD double py_log(double x, FvExc& e) {           // math.log (m_log)
   e.raise(FV_EXC_MATH_DOMAIN);
   return __builtin_nan("");
 }
+FV_HD double py_log(double x, FvExc& e) { return py_log_t<false>(x, e); }
 FV_HD double py_sqrt(double x, FvExc& e) {          // math.sqrt
   double r = sqrt(x);
   if (fv_isnan(r) && !fv_isnan(x)) e.raise(FV_EXC_MATH_DOMAIN);
@@ -95,22 +97,25 @@ FV_HD double py_div(double a, double b, bool np, FvExc& e) {
 // x ** n, n in {2,3,4}: float_pow for Python floats (OverflowError on an
 // infinite result from finite x), npy_pow for numpy scalars; both reach
 // glibc pow for finite x != 0 (|x| via CPython's sign handling).
-FV_HD double py_powi(double x, int n, bool np, FvExc& e) {
+template <bool kInl>
+FV_HD double py_powi_t(double x, int n, bool np, FvExc& e) {
   if (!fv_isfinite(x) || x == 0.0) {
     if (fv_isnan(x)) return x;
     if (x == 0.0) return (n & 1) ? x : 0.0;
     return (x < 0.0 && (n & 1)) ? -__builtin_inf() : __builtin_inf();
   }
-  double r = fv_pow_pos(fv_fabs(x), (double)n);
+  double r = kInl ? fv_pow_pos_i(fv_fabs(x), (double)n) : fv_pow_pos(fv_fabs(x), (double)n);
   if (x < 0.0 && (n & 1)) r = -r;
   if (!np && fv_isinf(r)) e.raise(FV_EXC_POW_RANGE);
   return r;
 }
+FV_HD double py_powi(double x, int n, bool np, FvExc& e) { return py_powi_t<false>(x, n, np, e); }
 FV_HD double py_max(double a, double b) { return (b > a) ? b : a; }   // builtins.max
 FV_HD double py_min(double a, double b) { return (b < a) ? b : a; }   // builtins.min
 
 // ---- distributions.py ------------------------------------------------------
-FV_HD double fv_norm_cdf(double x) { return 0.5 * fv_erfc(-x / FV_SQRT_TWO); }
+FV_HD double fv_norm_cdf(double x) { return 0.5 * fv_erfc(FV_DIV_SQRT2(-x)); }
+FV_HD double fv_norm_cdf_i(double x) { return 0.5 * fv_erfc_i(FV_DIV_SQRT2(-x)); }
 FV_HD double fv_norm_pdf(double x) { return FV_INV_SQRT_TWO_PI * fv_exp(-0.5 * x * x); }
 
 FV_HD double as241_poly(double c0, double c1, double c2, double c3, double c4, double c5,
@@ -276,9 +281,9 @@ FV_HD FvGreeks fv_price_greeks_row(int model, double th, double un, double K, do
                  - th * (r * K * disc * cdf_td2 - q * under * carry_disc * cdf_td1));
     rho = th * K * t * disc * cdf_td2;
   }
-  o.theta = theta_cal / 365.0;
-  o.rho = rho / 100.0;
-  o.vega = vega / 100.0;
+  o.theta = FV_DIV_INT(theta_cal, 365);
+  o.rho = FV_DIV_INT(rho, 100);
+  o.vega = FV_DIV_INT(vega, 100);
   return o;
 }
 
@@ -441,19 +446,19 @@ FV_HDN NbRes fv_normalized_black_impl(double x, double s, bool s_np) {
   if (t < FV_SMALL_T_THRESHOLD) {
     // _small_t_black (:74-103)
     o.branch = 1;
-    double a = 1.0 + h * FV_HALF_SQRT_TWO_PI * fv_erfcx(-h / FV_SQRT_TWO);
+    double a = 1.0 + h * FV_HALF_SQRT_TWO_PI * fv_erfcx(FV_DIV_SQRT2(-h));
     double w = t * t;
     double h2 = h * h;
-    double c1 = (-1.0 + 3.0 * a + a * h2) / 6.0;
-    double c2 = (-7.0 + 15.0 * a + h2 * (-1.0 + 10.0 * a + a * h2)) / 120.0;
-    double c3 = (-57.0 + 105.0 * a + h2 * (-18.0 + 105.0 * a + h2 * (-1.0 + 21.0 * a + a * h2))) / 5040.0;
-    double c4 = (-561.0 + 945.0 * a + h2 * (-285.0 + 1260.0 * a + h2 * (-33.0 + 378.0 * a
-                 + h2 * (-1.0 + 36.0 * a + a * h2)))) / 362880.0;
-    double c5 = (-6555.0 + 10395.0 * a + h2 * (-4680.0 + 17325.0 * a + h2 * (-840.0 + 6930.0 * a
-                 + h2 * (-52.0 + 990.0 * a + h2 * (-1.0 + 55.0 * a + a * h2))))) / 39916800.0;
-    double c6 = (-89055.0 + 135135.0 * a + h2 * (-82845.0 + 270270.0 * a + h2 * (-20370.0 + 135135.0 * a
+    double c1 = FV_DIV_INT(-1.0 + 3.0 * a + a * h2, 6);
+    double c2 = FV_DIV_INT(-7.0 + 15.0 * a + h2 * (-1.0 + 10.0 * a + a * h2), 120);
+    double c3 = FV_DIV_INT(-57.0 + 105.0 * a + h2 * (-18.0 + 105.0 * a + h2 * (-1.0 + 21.0 * a + a * h2)), 5040);
+    double c4 = FV_DIV_INT(-561.0 + 945.0 * a + h2 * (-285.0 + 1260.0 * a + h2 * (-33.0 + 378.0 * a
+                 + h2 * (-1.0 + 36.0 * a + a * h2))), 362880);
+    double c5 = FV_DIV_INT(-6555.0 + 10395.0 * a + h2 * (-4680.0 + 17325.0 * a + h2 * (-840.0 + 6930.0 * a
+                 + h2 * (-52.0 + 990.0 * a + h2 * (-1.0 + 55.0 * a + a * h2)))), 39916800);
+    double c6 = FV_DIV_INT(-89055.0 + 135135.0 * a + h2 * (-82845.0 + 270270.0 * a + h2 * (-20370.0 + 135135.0 * a
                  + h2 * (-1926.0 + 25740.0 * a + h2 * (-75.0 + 2145.0 * a
-                 + h2 * (-1.0 + 78.0 * a + a * h2)))))) / 6227020800.0;
+                 + h2 * (-1.0 + 78.0 * a + a * h2))))), 6227020800);
     double expansion = 2.0 * t * (a + w * (c1 + w * (c2 + w * (c3 + w * (c4 + w * (c5 + w * c6))))));
     double Ev = fv_exp(-0.5 * (h * h + t * t));
     o.E = Ev;
@@ -471,7 +476,7 @@ FV_HDN NbRes fv_normalized_black_impl(double x, double s, bool s_np) {
   o.branch = 3;
   double Ev = fv_exp(-0.5 * (h * h + t * t));
   o.E = Ev;
-  double b = 0.5 * Ev * (fv_erfcx(-(h + t) / FV_SQRT_TWO) - fv_erfcx(-(h - t) / FV_SQRT_TWO));
+  double b = 0.5 * Ev * (fv_erfcx(FV_DIV_SQRT2(-(h + t))) - fv_erfcx(FV_DIV_SQRT2(-(h - t))));
   o.b = py_max(b, 0.0); o.code = e.code; return o;
 }
 
@@ -492,7 +497,7 @@ FV_HDN DRes fv_normalized_black_log_impl(double x, double s, bool s_np) {
   DRes o;
   double h = py_div(x, s, s_np, e);
   double t = 0.5 * s;
-  double diff = fv_erfcx(-(h + t) / FV_SQRT_TWO) - fv_erfcx(-(h - t) / FV_SQRT_TWO);
+  double diff = fv_erfcx(FV_DIV_SQRT2(-(h + t))) - fv_erfcx(FV_DIV_SQRT2(-(h - t)));
   if (diff <= 0.0) { o.v = -__builtin_inf(); o.code = e.code; return o; }
   o.v = -0.5 * (h * h + t * t) + py_log(0.5 * diff, e);
   o.code = e.code;
@@ -506,11 +511,13 @@ FV_HD double fv_normalized_black_log(double x, double s, bool s_np, FvExc& e) {
 // Inline form for the far-low kernel, with h = x / s supplied by the caller
 // (the same division the caller needs anyway; its ZeroDivisionError check is
 // the caller's).
+template <bool kInl>
 FV_HD double fv_nbl_h(double h, double s, FvExc& e) {
   double t = 0.5 * s;
-  double diff = fv_erfcx(-(h + t) / FV_SQRT_TWO) - fv_erfcx(-(h - t) / FV_SQRT_TWO);
+  double a1 = FV_DIV_SQRT2(-(h + t)), a2 = FV_DIV_SQRT2(-(h - t));
+  double diff = kInl ? (fv_erfcx_i(a1) - fv_erfcx_i(a2)) : (fv_erfcx(a1) - fv_erfcx(a2));
   if (diff <= 0.0) return -__builtin_inf();
-  return -0.5 * (h * h + t * t) + py_log(0.5 * diff, e);
+  return -0.5 * (h * h + t * t) + py_log_t<kInl>(0.5 * diff, e);
 }
 
 // normalized_black_complement (:132-137) with the per-quote exp(+-x/2)
@@ -615,6 +622,8 @@ FV_HD int fv_lbr_classify(double th, double Fw, double K, double t, double r, do
 // code is identical; `region` then picks the anchor pair at run time).
 template <int R>
 FV_HD FvLbrOut fv_lbr_solve(int region, const FvLbrState& st, FvExc& e) {
+  // far-low (the bulk of a chain's OTM quotes) inlines its libm calls
+  constexpr bool kInl = (R == FV_FAR_LOW);
   const double nan = __builtin_nan("");
   FvLbrOut o;
   o.sigma = nan; o.status = FV_IV_MAX_ITER; o.region = region; o.iterations = 0;
@@ -654,10 +663,10 @@ FV_HD FvLbrOut fv_lbr_solve(int region, const FvLbrState& st, FvExc& e) {
     for (int it = 0; it < 5; ++it) {
       if (e.code) return o;
       double xs = py_div(x, s, false, e);        // h of normalized_black_log == x / s of :298
-      double ln_b = fv_nbl_h(xs, s, e);
+      double ln_b = fv_nbl_h<kInl>(xs, s, e);
       double g = ln_b - ln_beta;
       if (g > 0.0) v_hi = py_min(v_hi, v);
-      double arg = FV_LOG_INV_SQRT_TWO_PI - 0.5 * (py_powi(xs, 2, false, e) + 0.25 * s * s) - ln_b;
+      double arg = FV_LOG_INV_SQRT_TWO_PI - 0.5 * (py_powi_t<kInl>(xs, 2, false, e) + 0.25 * s * s) - ln_b;
       double dg_dv = s * py_exp(arg, e);
       if (e.code) return o;
       if (!(fv_isfinite(dg_dv) && dg_dv > 0.0)) break;
@@ -717,15 +726,15 @@ FV_HD FvLbrOut fv_lbr_solve(int region, const FvLbrState& st, FvExc& e) {
     double t = 0.5 * s;
     double s3 = s * s * s;
     double r2 = py_div(x * x, s3, s_np, e) - 0.25 * s;
-    double s4 = py_powi(s, 4, s_np, e);
+    double s4 = py_powi_t<kInl>(s, 4, s_np, e);
     double r3 = r2 * r2 - py_div(3.0 * x * x, s4, s_np, e) - 0.25;
     double g, g1, g2, g3;
     bool g_np, g1_np, g23_np;
     if (R == FV_FAR_LOW) {
-      double ln_b = fv_nbl_h(h, s, e);            // its h = x / s is the h above
+      double ln_b = fv_nbl_h<kInl>(h, s, e);      // its h = x / s is the h above
       double ln_bp = FV_LOG_INV_SQRT_TWO_PI - 0.5 * (h * h + 0.25 * s * s);
       double up = py_exp(ln_bp - ln_b, e);
-      double up3 = py_powi(up, 3, false, e);
+      double up3 = py_powi_t<kInl>(up, 3, false, e);
       double upp = up * r2 - up * up;
       double uppp = up * r3 - 3.0 * up * up * r2 + 2.0 * up3;
       double inv = py_div(1.0, ln_b, false, e);
@@ -796,11 +805,134 @@ FV_HD FvLbrOut fv_lbr_solve(int region, const FvLbrState& st, FvExc& e) {
   return o;
 }
 
+// Far-low region (:434-486 with _far_low_guess :283-309 and the 1/ln b
+// objective :362-377), restructured for the GPU's instruction cache: the five
+// safeguarded Newton steps of the guess and the <= 8 Householder(3) steps run
+// as ONE step loop, so each heavy routine (normalized_black_log, pow, exp) has
+// a single inlined call site and the loop body stays a few KB.  Every value is
+// computed by the same expression as in the reference; where the two phases
+// check exceptions in different orders, each check keeps its own record and
+// they are merged in the reference's order.  Bit-identical to
+// fv_lbr_solve<FV_FAR_LOW> (tests/test_quote_host.py checks both).
+FV_HD FvLbrOut fv_lbr_far_low_fused(const FvLbrState& st, FvExc& e) {
+  const double nan = __builtin_nan("");
+  FvLbrOut o;
+  o.sigma = nan; o.status = FV_IV_MAX_ITER; o.region = FV_FAR_LOW; o.iterations = 0;
+  const double x = st.x, beta = st.beta;
+  const double s_lo = st.s_c * 0.5;
+  double lo = 0.0, hi = s_lo;
+  lo *= FV_K_ONE_M_1EM6;
+  hi *= FV_K_ONE_P_1EM6;
+  // _far_low_guess prologue (:286-291)
+  const double ln_beta = py_log_t<true>(beta, e);
+  const double s_cap = s_lo;
+  double s = py_div(fv_fabs(x), py_sqrt(-2.0 * ln_beta, e), false, e);
+  s = py_min(py_max(s, FV_K_1EM6 * s_cap), FV_K_0P999 * s_cap);
+  double v = py_log_t<true>(s, e);
+  double v_hi = py_log_t<true>(s_cap, e);
+  if (e.code) return o;
+  const double xx = x * x;
+  const double x3 = 3.0 * x * x;
+  const double inv_ln_beta = 1.0 / ln_beta;
+  int nk = 0;                 // Newton steps taken
+  bool newton = true;
+  int iterations = 0;
+  bool converged = false;
+  for (int step = 0; step < 13; ++step) {
+    if (!newton) {
+      if (iterations == 8) break;
+      if (!(s > 0.0)) { e.raise_v(FV_EXC_DOM_OBJ_S, s, 0); return o; }     // :358-359
+    }
+    FvExc e_h = {0, 0, 0.0}, e_r = {0, 0, 0.0}, e_nb = {0, 0, 0.0}, e_pw = {0, 0, 0.0};
+    const double h = py_div(x, s, false, e_h);                 // x / s (:144 / :298 / :154)
+    double r2 = 0.0, r3 = 0.0;
+    if (!newton) r2 = py_div(xx, s * s * s, false, e_r) - 0.25 * s;   // :341
+    // pow site: (x/s)**2 (:298) or s**4 (:342)
+    const double pw = py_powi_t<true>(newton ? h : s, newton ? 2 : 4, false, e_pw);
+    if (!newton) r3 = r2 * r2 - py_div(x3, pw, false, e_pw) - 0.25;  // :342
+    const double ln_b = fv_nbl_h<true>(h, s, e_nb);            // normalized_black_log(x, s)
+    // reference order: Newton = nbl, (x/s)**2 ; iteration = x/s, ratios, nbl
+    e.raise(e_h.code);
+    if (newton) { e.raise(e_nb.code); e.raise(e_pw.code); }
+    else { e.raise(e_r.code); e.raise(e_pw.code); e.raise(e_nb.code); }
+    if (e.code) return o;
+    // exp site: dg_dv's exponent (:297-299) or b'/b (:366-367)
+    const double q = newton ? pw : h * h;
+    const double ex = py_exp(FV_LOG_INV_SQRT_TWO_PI - 0.5 * (q + 0.25 * s * s) - ln_b, e);
+    if (e.code) return o;
+    if (newton) {
+      // rest of the Newton step (:293-308)
+      const double g = ln_b - ln_beta;
+      if (g > 0.0) v_hi = py_min(v_hi, v);
+      const double dg_dv = s * ex;
+      bool stop = !(fv_isfinite(dg_dv) && dg_dv > 0.0);
+      if (!stop) {
+        double v_new = v - g / dg_dv;
+        if (!fv_isfinite(v_new)) stop = true;
+        else {
+          if (v_new >= v_hi) v_new = 0.5 * (v + v_hi);
+          v = v_new;
+          s = py_exp(v, e);
+          if (e.code) return o;
+        }
+      }
+      if (stop || ++nk == 5) {
+        newton = false;                                         // initial_guess done
+        if (!(lo < s && s < hi)) s = 0.5 * (lo + hi);           // :451-452
+      }
+      continue;
+    }
+    // Householder(3) step on the far-low objective (:363-377, :457-483)
+    const double up = ex;
+    const double up3 = py_powi_t<true>(up, 3, false, e);
+    const double upp = up * r2 - up * up;
+    const double uppp = up * r3 - 3.0 * up * up * r2 + 2.0 * up3;
+    const double inv = py_div(1.0, ln_b, false, e);
+    const double inv2 = inv * inv;
+    if (ln_beta == 0.0) e.raise(FV_EXC_ZERO_DIV);
+    const double g = inv - inv_ln_beta;
+    const double g1 = -up * inv2;
+    const double g2 = -upp * inv2 + 2.0 * up * up * inv2 * inv;
+    const double g3 = (-uppp * inv2 + 6.0 * up * upp * inv2 * inv - 6.0 * up3 * inv2 * inv2);
+    if (e.code) return o;
+    if (g == 0.0) { converged = true; break; }
+    if (g > 0.0) { if (s > lo) lo = s; }                        // decreasing objective
+    else { if (s < hi) hi = s; }
+    double ds;
+    if (g1 == 0.0 || !fv_isfinite(g1)) ds = nan;
+    else {
+      const double nu = -g / g1;
+      const double eta = g2 / g1;
+      const double gam = py_div(g3, 6.0 * g1, false, e);
+      ds = py_div(nu * (1.0 + 0.5 * nu * eta), 1.0 + nu * (eta + nu * gam), false, e);
+      if (e.code) return o;
+    }
+    if (fv_isfinite(ds) && fv_fabs(ds) <= FV_K_1EM14 * py_max(1.0, s)) {
+      s = s + ds;
+      iterations += 1;
+      converged = true;
+      break;
+    }
+    double cand = s + ds;
+    if (!fv_isfinite(cand) || !(lo < cand && cand < hi)) {
+      cand = 0.5 * (lo + hi);
+      ds = cand - s;
+    }
+    s = cand;
+    iterations += 1;
+    if (fv_fabs(ds) <= FV_K_1EM14 * py_max(1.0, s)) { converged = true; break; }
+  }
+  o.sigma = s / st.sqrt_t;
+  o.status = converged ? FV_IV_CONVERGED : FV_IV_MAX_ITER;
+  o.iterations = iterations;
+  return o;
+}
+
 FV_HD FvLbrOut fv_lbr_row(double th, double Fw, double K, double t, double r, double px, FvExc& e) {
   FvLbrState st;
   FvLbrOut o;
   if (fv_lbr_classify(th, Fw, K, t, r, px, st, o, e)) return o;
-  if (o.region == FV_FAR_LOW) return fv_lbr_solve<FV_FAR_LOW>(o.region, st, e);
+  if (o.region == FV_FAR_LOW) return fv_lbr_far_low_fused(st, e);
   if (o.region == FV_FAR_HIGH) return fv_lbr_solve<FV_FAR_HIGH>(o.region, st, e);
   return fv_lbr_solve<FV_NEAR_LOW>(o.region, st, e);
 }

@@ -58,3 +58,30 @@ double qh_normalized_black(double x, double s, int* branch) {
   return fv_normalized_black(x, s, false, e, nullptr, branch);
 }
 }
+
+extern "C" {
+// Bit-compare the fused far-low solver against the reference-order one on
+// the far-low quotes of a batch; returns the number of mismatching rows.
+int64_t qh_far_low_fused_check(const int8_t* flag, const double* F, const double* k,
+                               const double* t, const double* r, const double* px, int64_t n,
+                               int64_t* nfar) {
+  int64_t bad = 0, nf = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    FvExc e = {0, 0, 0.0};
+    FvLbrState st; FvLbrOut o;
+    if (!(t[i] > 0.0)) continue;
+    if (fv_lbr_classify((double)flag[i], F[i], k[i], t[i], r[i], px[i], st, o, e)) continue;
+    if (o.region != FV_FAR_LOW) continue;
+    ++nf;
+    FvExc e1 = {0, 0, 0.0}, e2 = {0, 0, 0.0};
+    FvLbrOut a = fv_lbr_solve<FV_FAR_LOW>(FV_FAR_LOW, st, e1);
+    FvLbrOut b = fv_lbr_far_low_fused(st, e2);
+    uint64_t ua, ub; memcpy(&ua, &a.sigma, 8); memcpy(&ub, &b.sigma, 8);
+    bool same = (ua == ub || (a.sigma != a.sigma && b.sigma != b.sigma)) && a.status == b.status &&
+                a.iterations == b.iterations && e1.code == e2.code;
+    if (!same) ++bad;
+  }
+  *nfar = nf;
+  return bad;
+}
+}
