@@ -158,6 +158,18 @@ FV_API int fv_set_chunk_rows(int64_t rows);
  * bench's gpu_launches count). */
 FV_API int64_t fv_last_launch_count(void);
 
+/* Raw outcome of the calling thread's last batch call: per validation check
+ * (FV_CHECK_* order) the first failing row or -1; the first raising row and
+ * its FV_EXC_* code for the price/iv stream [0] and the Greeks stream [1]
+ * (-1 / 0 when none).  Lets a caller that shards one logical batch over
+ * several calls/devices reproduce the reference's single first error. */
+FV_API int fv_last_outcome(int64_t* check_rows /*[FV_NCHECK]*/, int64_t* exc_rows /*[2]*/,
+                           int32_t* exc_codes /*[2]*/);
+
+/* Self-test: the exact constant-division used by the kernels against the
+ * device's IEEE division on n random inputs x 9 divisors; mismatches out. */
+FV_API int fv_selftest_div_const(int64_t n, uint64_t seed, int64_t* mismatches);
+
 /* Diagnostics: measured DFMA instruction rate of the current device (the
  * FP64-pipe roofline denominator for this path). */
 FV_API int fv_probe_fp64_peak(double* dfma_per_s, double* seconds);

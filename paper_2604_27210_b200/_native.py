@@ -52,6 +52,8 @@ SIGNATURES = {
     "fv_set_chunk_rows": ([_I64], ctypes.c_int),
     "fv_last_launch_count": ([], _I64),
     "fv_probe_fp64_peak": ([_P, _P], ctypes.c_int),
+    "fv_last_outcome": ([_P, _P, _P], ctypes.c_int),
+    "fv_selftest_div_const": ([_I64, ctypes.c_uint64, _P], ctypes.c_int),
 }
 
 
@@ -99,3 +101,12 @@ def ptr(arr):
     if hasattr(arr, "data_ptr"):
         return arr.data_ptr()
     return np.asarray(arr).ctypes.data
+
+
+def last_outcome(lib):
+    """(check_rows[12], exc_rows[2], exc_codes[2]) of this thread's last call."""
+    cr = np.empty(12, np.int64)
+    er = np.empty(2, np.int64)
+    ec = np.empty(2, np.int32)
+    lib.fv_last_outcome(cr.ctypes.data, er.ctypes.data, ec.ctypes.data)
+    return cr, er, ec

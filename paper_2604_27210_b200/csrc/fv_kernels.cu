@@ -505,6 +505,37 @@ __global__ void __launch_bounds__(256) k_fp64_probe(double* out, int iters, doub
   if (s == 12345.678) out[blockIdx.x * blockDim.x + threadIdx.x] = s;  // keep live
 }
 
+// Self-test: fv_div_const against the hardware IEEE division on the device
+// for every constant divisor the path uses (random 64-bit patterns, biased
+// to moderate exponents, plus the full range).
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__global__ void k_selftest_div_const(int64_t n, uint64_t seed, unsigned long long* bad) {
+  const double cs[9] = {FV_DIV_SQRT2_C, 6.0, 120.0, 5040.0, 362880.0, 39916800.0, 6227020800.0, 365.0, 100.0};
+  const double yh[9] = {FV_DIV_SQRT2_YH, FV_DIV_6_YH, FV_DIV_120_YH, FV_DIV_5040_YH, FV_DIV_362880_YH,
+                        FV_DIV_39916800_YH, FV_DIV_6227020800_YH, FV_DIV_365_YH, FV_DIV_100_YH};
+  const double yl[9] = {FV_DIV_SQRT2_YL, FV_DIV_6_YL, FV_DIV_120_YL, FV_DIV_5040_YL, FV_DIV_362880_YL,
+                        FV_DIV_39916800_YL, FV_DIV_6227020800_YL, FV_DIV_365_YL, FV_DIV_100_YL};
+  unsigned long long local = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t u = splitmix64(seed + (uint64_t)i);
+    uint64_t e = (i & 7) ? (uint64_t)(1023 + (int)((u >> 52) % 128) - 64) : ((u >> 52) & 0x7ff);
+    uint64_t bits = (u & 0x800fffffffffffffull) | (e << 52);
+    double x = __longlong_as_double((long long)bits);
+#pragma unroll 1
+    for (int k = 0; k < 9; ++k) {
+      double a = fv_div_const(x, cs[k], yh[k], yl[k]);
+      double b = __ddiv_rn(x, cs[k]);
+      if (__double_as_longlong(a) != __double_as_longlong(b) && !(a != a && b != b)) ++local;
+    }
+  }
+  if (local) atomicAdd(bad, local);
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -512,6 +543,11 @@ namespace {
 
 thread_local cudaStream_t t_user_stream = nullptr;
 thread_local int64_t t_launches = 0;
+// raw outcome of this thread's last call (for sharded callers that merge
+// the first-failure rows of several shards)
+thread_local int64_t t_check_rows[FV_NCHECK];
+thread_local int64_t t_exc_row[2] = {-1, -1};
+thread_local int32_t t_exc_code[2] = {0, 0};
 int64_t g_chunk_rows = 1 << 22;
 
 struct DevWork {
@@ -782,6 +818,16 @@ int finish(DevWork* w, const Call& c, const KArgs& a0, uint32_t bcast_bits, cuda
            fv_error* e1, fv_error* e2) {
   FvDevStatus& st = *w->st_host;
   bool has_sigma = c.kind != KIND_IV;
+  for (int ck = 0; ck < FV_NCHECK; ++ck) {
+    unsigned long long row = st.check_first[ck];
+    if (bcast_bits & (1u << ck)) row = 0;
+    t_check_rows[ck] = row == ~0ull ? -1 : (int64_t)row;
+  }
+  for (int k = 0; k < 2; ++k) {
+    unsigned long long ex = k ? st.exc2_first : st.exc_first;
+    t_exc_row[k] = ex == ~0ull ? -1 : (int64_t)(ex >> 8);
+    t_exc_code[k] = ex == ~0ull ? 0 : (int32_t)(ex & 0xff);
+  }
   // BatchError: first check in order that failed anywhere
   for (int ck = 0; ck < FV_NCHECK; ++ck) {
     unsigned long long row = st.check_first[ck];
@@ -1181,6 +1227,25 @@ FV_API int fv_set_chunk_rows(int64_t rows) {
 }
 
 FV_API int64_t fv_last_launch_count(void) { return t_launches; }
+
+FV_API int fv_selftest_div_const(int64_t n, uint64_t seed, int64_t* mismatches) {
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, sizeof(*d)) != cudaSuccess) return FV_ERR_CUDA;
+  cudaMemset(d, 0, sizeof(*d));
+  k_selftest_div_const<<<148 * 8, 256>>>(n, seed, d);
+  unsigned long long h = 0;
+  cudaError_t ce = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (ce != cudaSuccess) return FV_ERR_CUDA;
+  *mismatches = (int64_t)h;
+  return FV_OK;
+}
+
+FV_API int fv_last_outcome(int64_t* check_rows, int64_t* exc_rows, int32_t* exc_codes) {
+  for (int c = 0; c < FV_NCHECK; ++c) check_rows[c] = t_check_rows[c];
+  for (int k = 0; k < 2; ++k) { exc_rows[k] = t_exc_row[k]; exc_codes[k] = t_exc_code[k]; }
+  return FV_OK;
+}
 
 // Measured FP64 DFMA issue rate of the current device (DFMA instructions per
 // second across the chip), timed with CUDA events.

@@ -1,0 +1,114 @@
+"""Quote-sharded execution across GPUs (one process per GPU, torch.distributed).
+
+Every output row of the reference batch is a pure function of its input row
+(batch.py:4-7), so a chain shards by contiguous row ranges with no exchange
+on the data path.  The only cross-rank traffic is
+  * one small all-reduce (MIN) of each shard's first-failure rows, so every
+    rank raises exactly the error the single-process reference would
+    (validation checks in the reference's order first, then the lowest
+    raising row -- batch.py:104-148, :166-178), and
+  * optionally, an all-gather of the result shards when the caller asks for
+    the whole result on every rank (NCCL over NVLink / NVSwitch).
+
+``run_sharded`` holds the merge logic and is backend-agnostic (tested on CPU
+with gloo); ``batch_iv_sharded`` binds it to the CUDA C ABI.
+"""
+
+import numpy as np
+
+NCHECK = 12
+NO_ROW = np.iinfo(np.int64).max
+
+
+def shard_bounds(n, world, rank):
+    """Contiguous shard [lo, hi) of n rows for ``rank`` of ``world`` (the
+    first n % world ranks get one extra row)."""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def _status_vector(check_rows, exc_row, exc_code, offset):
+    """Local outcome -> global keys: per-check first global row, then the
+    first raising global row packed with its code (row * 256 + code)."""
+    v = np.full(NCHECK + 1, NO_ROW, dtype=np.int64)
+    for c in range(NCHECK):
+        if check_rows[c] >= 0:
+            v[c] = offset + int(check_rows[c])
+    if exc_row >= 0:
+        v[NCHECK] = (offset + int(exc_row)) * 256 + int(exc_code)
+    return v
+
+
+def merge_status(vec):
+    """Global outcome from the MIN-reduced status vector:
+    ('batch', check, row) | ('exc', code, row) | None."""
+    for c in range(NCHECK):
+        if vec[c] != NO_ROW:
+            return ("batch", c, int(vec[c]))
+    if vec[NCHECK] != NO_ROW:
+        return ("exc", int(vec[NCHECK] % 256), int(vec[NCHECK] // 256))
+    return None
+
+
+def run_sharded(compute, n, group=None, device=None, gather=False):
+    """Run ``compute(lo, hi) -> (outputs: dict of 1-D arrays/tensors,
+    check_rows[12], exc_row, exc_code)`` on this rank's shard, agree on the
+    global outcome with one MIN all-reduce, and optionally all-gather the
+    outputs.  Returns (outputs, outcome) where outputs are this rank's shard
+    (or the full arrays with ``gather=True``)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    lo, hi = shard_bounds(n, world, rank)
+    outputs, check_rows, exc_row, exc_code = compute(lo, hi)
+    vec = torch.from_numpy(_status_vector(check_rows, exc_row, exc_code, lo))
+    if device is not None:
+        vec = vec.to(device)
+    if world > 1:
+        dist.all_reduce(vec, op=dist.ReduceOp.MIN, group=group)
+    outcome = merge_status(vec.cpu().numpy())
+    if gather and world > 1 and outcome is None:
+        full = {}
+        for name, shard in outputs.items():
+            t = shard if torch.is_tensor(shard) else torch.from_numpy(np.ascontiguousarray(shard))
+            if device is not None:
+                t = t.to(device)
+            sizes = [shard_bounds(n, world, r)[1] - shard_bounds(n, world, r)[0] for r in range(world)]
+            m = max(sizes)
+            padded = torch.zeros(m, dtype=t.dtype, device=t.device)
+            padded[:t.numel()] = t
+            parts = [torch.empty(m, dtype=t.dtype, device=t.device) for _ in sizes]
+            dist.all_gather(parts, padded, group=group)        # equal-size collective
+            full[name] = torch.cat([p[:sz] for p, sz in zip(parts, sizes)])
+        outputs = full
+    return outputs, outcome
+
+
+def batch_iv_sharded(model, method, cols, n, group=None, gather=False):
+    """Sharded ``batch_iv`` on device-resident torch columns (each rank holds
+    the full logical columns or at least its shard's rows; broadcast
+    columns are 1-element tensors).  Returns ((iv, status) or gathered
+    dict, outcome) -- outcome as in ``merge_status``."""
+    import torch
+    from . import _native
+    from .models import as_model
+    lib = _native.lib_for_compute()
+    m = as_model(model).code
+    dev = cols["strike"].device
+
+    def compute(lo, hi):
+        sl = {k: (v if v.numel() == 1 else v[lo:hi]) for k, v in cols.items()}
+        k = hi - lo
+        iv = torch.empty(k, dtype=torch.float64, device=dev)
+        st = torch.empty(k, dtype=torch.int8, device=dev)
+        err = _native.fv_error()
+        lib.fv_batch_iv(m, 1 if method == "lbr" else 0,
+                        *[_native.col(sl[c]) for c in ("flag", "underlying", "strike", "t", "r", "q", "price")],
+                        k, iv.data_ptr(), st.data_ptr(), None, err)
+        cr, er, ec = _native.last_outcome(lib)
+        return {"iv": iv, "status": st}, cr, int(er[0]), int(ec[0])
+
+    return run_sharded(compute, n, group=group, device=dev, gather=gather)

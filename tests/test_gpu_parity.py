@@ -285,3 +285,26 @@ def test_host_chunked_pipeline_matches_device(fv):
     assert a[0] == 0 and b[0] == 0
     assert_bits(a[2], b[2], "iv host vs device")
     assert_bits(a[3], b[3], "status host vs device")
+
+
+def test_device_constant_division_is_ieee(fv):
+    import ctypes
+    from paper_2604_27210_b200 import _native
+    lib = _native.lib_for_compute()
+    bad = ctypes.c_int64(-1)
+    assert lib.fv_selftest_div_const(200_000_000, 2024, ctypes.byref(bad)) == 0
+    assert bad.value == 0
+
+
+def test_sharded_single_rank_equals_batch(fv):
+    import torch
+    from paper_2604_27210_b200 import distributed as D
+    from paper_2604_27210_b200 import workloads as W
+    flag, S, K, t, r, q, sig = W.chain_draws(50_001, seed=21)
+    px = fv.batch_price("black", W.flag_chars(flag), S, K, t, r, sigma=sig)["price"]
+    ref = fv.batch_iv("black", "lbr", W.flag_chars(flag), S, K, t, r, price=px)
+    cols = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in
+            dict(flag=flag, underlying=S, strike=K, t=t, r=r, q=np.zeros(1), price=px).items()}
+    out, outcome = D.batch_iv_sharded("black", "lbr", cols, len(flag))
+    assert outcome is None
+    assert_bits(out["iv"].cpu().numpy(), ref["iv"], "sharded iv")

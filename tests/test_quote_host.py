@@ -1,0 +1,136 @@
+"""CPU pre-check of the device per-quote code (csrc/fv_quote.h compiled for
+the host): bit-identical to the live reference's golden outputs (IV + NaN
+mask, status, LBR region, prices, Greeks), to the reference's exception
+behaviour on fuzzed extreme rows, and the GPU's fused far-low solver
+identical to the reference-order one.  The kernels compile this same header;
+tests/test_gpu_parity.py re-checks everything on the B200."""
+import ctypes
+import glob
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from _helpers import assert_bits, bits_equal, load
+from conftest import GOLDEN
+
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), "native"))
+import build as native_build  # noqa: E402
+
+MID = {"black": 0, "bs": 1, "bsm": 2}
+P = ctypes.c_void_p
+
+
+@pytest.fixture(scope="module")
+def Q():
+    return ctypes.CDLL(native_build.build("quote_hostcheck"))
+
+
+def _p(a):
+    return P(a.ctypes.data)
+
+
+def _iv(Q, model, method, flag, un, k, t, r, q, px):
+    n = len(flag)
+    cols = [np.ascontiguousarray(flag, np.int8)] + [np.ascontiguousarray(c, np.float64)
+                                                    for c in (un, k, t, r, q, px)]
+    iv, st, reg = np.empty(n), np.empty(n, np.int8), np.empty(n, np.int8)
+    exc, ev, en = np.empty(n, np.int8), np.empty(n), np.empty(n, np.int8)
+    Q.qh_iv(MID[model], 1 if method == "lbr" else 0, *[_p(c) for c in cols], ctypes.c_int64(n),
+            _p(iv), _p(st), _p(reg), _p(exc), _p(ev), _p(en))
+    return iv, st, reg, exc, ev, en
+
+
+FIX = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "lbr_*.npz"))
+             + glob.glob(os.path.join(GOLDEN, "halley_c*.npz")))
+
+
+@pytest.mark.parametrize("name", FIX)
+def test_iv_golden(Q, name):
+    g = load(os.path.join(GOLDEN, name))
+    iv, st, reg, exc, _, _ = _iv(Q, str(g["model"]), str(g["method"]), g["flag"], g["underlying"],
+                                 g["strike"], g["t"], g["r"], g["q"], g["price"])
+    assert not exc.any()
+    assert_bits(st, g["status"], name + " status")
+    assert_bits(iv, g["iv"], name + " iv")
+    if "region" in g:
+        assert_bits(reg, g["region"], name + " region")
+
+
+@pytest.mark.parametrize("model", ["bsm", "bs", "black"])
+def test_price_greeks_golden(Q, model):
+    g = load(os.path.join(GOLDEN, "price_greeks.npz"))
+    n = len(g["flag"])
+    q = g["q"] if model == "bsm" else np.zeros(n)
+    cols = [np.ascontiguousarray(a) for a in (g["flag"], g["underlying"], g["strike"], g["t"], g["r"], q, g["sigma"])]
+    pr, g5, st = np.empty(n), np.empty(5 * n), np.empty(n, np.int8)
+    ep, eg = np.empty(n, np.int8), np.empty(n, np.int8)
+    Q.qh_price_greeks(MID[model], *[_p(c) for c in cols], ctypes.c_int64(n), _p(pr), _p(g5), _p(st), _p(ep), _p(eg))
+    g5 = g5.reshape(n, 5)
+    assert_bits(pr, g[f"{model}_price"], "price")
+    assert_bits(st, g[f"{model}_status"], "status")
+    for j, nm in enumerate(("delta", "gamma", "theta", "rho", "vega")):
+        assert_bits(g5[:, j], g[f"{model}_{nm}"], nm)
+    pr2, ex = np.empty(n), np.empty(n, np.int8)
+    Q.qh_price(MID[model], *[_p(c) for c in cols], ctypes.c_int64(n), _p(pr2), _p(ex))
+    assert_bits(pr2, g[f"{model}_price"], "price-only kernel")
+
+
+def test_exception_rows(Q):
+    from oracle import fvoracle as O
+    cases = json.load(open(os.path.join(GOLDEN, "exceptions.json")))
+    by = {}
+    for c in cases:
+        by.setdefault(c["in"]["model"], []).append(c)
+    checked = 0
+    for m, cs in by.items():
+        col = {k: np.array([c["in"][k] for c in cs]) for k in
+               ("flag", "underlying", "strike", "t", "r", "q", "sigma", "price")}
+        n = len(cs)
+        base = [np.ascontiguousarray(a) for a in (col["flag"].astype(np.int8), col["underlying"],
+                                                 col["strike"], col["t"], col["r"], col["q"])]
+        sg = np.ascontiguousarray(col["sigma"])
+        pr, g5, st = np.empty(n), np.empty(5 * n), np.empty(n, np.int8)
+        ep, eg = np.empty(n, np.int8), np.empty(n, np.int8)
+        Q.qh_price_greeks(MID[m], *[_p(c) for c in base], _p(sg), ctypes.c_int64(n), _p(pr), _p(g5), _p(st), _p(ep), _p(eg))
+        g5 = g5.reshape(n, 5)
+        res = {meth: _iv(Q, m, meth, *base, col["price"]) for meth in ("lbr", "halley")}
+        for i, c in enumerate(cs):
+            for key in ("price", "greeks", "lbr", "halley"):
+                if key not in c:
+                    continue
+                want = c[key]
+                if key == "price":
+                    code, val, np_ = ep[i], 0.0, 0
+                    gv = {"price": pr[i]}
+                elif key == "greeks":
+                    code, val, np_ = eg[i], 0.0, 0
+                    gv = dict(zip(("delta", "gamma", "theta", "rho", "vega"), g5[i]))
+                else:
+                    iv, st2, _, exc, ev, en = res[key]
+                    code, val, np_ = exc[i], ev[i], en[i]
+                    gv = {"iv": iv[i], "status": list(O.IV_STATUS)[st2[i]]}
+                if code:
+                    e = O.exception_for(code, val, bool(np_))
+                    name = "DomainError" if isinstance(e, O.OracleDomainError) else type(e).__name__
+                    assert want.get("exc") == name and want.get("msg") == str(e), (key, c["in"], want, str(e))
+                else:
+                    assert "exc" not in want, (key, c["in"], want, gv)
+                    for k, v in want.items():
+                        assert (v == gv[k]) if isinstance(v, str) else bits_equal(gv[k], v), (key, c["in"], want, gv)
+                checked += 1
+    assert checked > 5000
+
+
+def test_fused_far_low_matches_reference_order(Q):
+    from oracle import fvoracle as O
+    from paper_2604_27210_b200 import workloads as W
+    Q.qh_far_low_fused_check.restype = ctypes.c_int64
+    flag, S, K, t, r, q, sig = W.chain_draws(100_000, seed=3)
+    px = O.rows_price("black", flag, S, K, t, r, 0.0, sig)["price"]
+    cols = [np.ascontiguousarray(a) for a in (flag, S, K, t, r, px)]
+    nf = ctypes.c_int64(0)
+    bad = Q.qh_far_low_fused_check(*[_p(c) for c in cols], ctypes.c_int64(len(flag)), ctypes.byref(nf))
+    assert nf.value > 30_000 and bad == 0
