@@ -251,7 +251,10 @@ __device__ __forceinline__ unsigned int warp_append(unsigned int* counter, bool 
 // Householder(3) code over a dense queue, so warps are region-uniform and
 // each kernel's instruction footprint stays small.
 struct LbrQueues {
-  FvLbrState* state;     // [chunk] per local row
+  // per-local-row state, structure of arrays (each pass writes / reads whole
+  // 32-byte sectors of the fields it touches)
+  double* sx;      double* sbeta;  double* ssqrt_t; double* ss_c;
+  double* sb0;     double* sb1;    double* sE0;     double* sE1;
   int32_t* q[4];         // 0..2: local rows per region class; 3: rows pending anchors
   unsigned int* count;   // [4]
 };
@@ -260,9 +263,25 @@ __device__ __forceinline__ int region_class(int region) {
   return region == FV_FAR_LOW ? 0 : (region == FV_FAR_HIGH ? 2 : 1);
 }
 
+// Warp-aggregated append of up to two entries per lane, in lane order
+// (lane 0's two, lane 1's two, ...) so a queue segment follows row order.
+__device__ __forceinline__ unsigned int warp_append2(unsigned int* counter, bool p0, bool p1) {
+  const unsigned m0 = __ballot_sync(0xffffffffu, p0);
+  const unsigned m1 = __ballot_sync(0xffffffffu, p1);
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1;
+  const unsigned total = __popc(m0) + __popc(m1);
+  unsigned int base = 0;
+  if (total) {
+    if (lane == 0) base = atomicAdd(counter, total);
+    base = __shfl_sync(0xffffffffu, base, 0);
+  }
+  return base + __popc(m0 & lt) + __popc(m1 & lt);
+}
+
 // Pass 1: validation + normalize_quote + bounds + ATM (small code, one pass
 // over the input columns).  Finished quotes are written out; the rest get
-// (x, beta, sqrt_t) in the state block and their row in the pending queue.
+// (x, beta, sqrt_t) in the state arrays and their row in the pending queue.
 __global__ void __launch_bounds__(256) k_lbr_normalize(KArgs a, LbrQueues lq) {
   const int64_t npair = (a.n + 1) >> 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -274,9 +293,10 @@ __global__ void __launch_bounds__(256) k_lbr_normalize(KArgs a, LbrQueues lq) {
     const bool two = active && (i + 1 < a.n);
     double iv[2] = {0.0, 0.0};
     int stt[2] = {FV_IV_MAX_ITER, FV_IV_MAX_ITER};
+    bool pend[2] = {false, false};
+    double px_[2], pb_[2], pt_[2];
     Pair p;
     if (active) load_pair(a, i, two, p);
-    // uniform trip count so the queue ballot sees the full warp
 #pragma unroll 1
     for (int u = 0; u < 2; ++u) {
       const bool valid = active && (u == 0 || two);
@@ -284,6 +304,7 @@ __global__ void __launch_bounds__(256) k_lbr_normalize(KArgs a, LbrQueues lq) {
       double ivu = __builtin_nan("");
       int stu = FV_IV_MAX_ITER;
       FvLbrState st;
+      st.x = 0.0; st.beta = 0.0; st.sqrt_t = 0.0;
       if (valid) {
         const int fl = u ? p.fl[1] : p.fl[0];
         const double un = u ? p.un[1] : p.un[0], k = u ? p.k[1] : p.k[0];
@@ -314,16 +335,17 @@ __global__ void __launch_bounds__(256) k_lbr_normalize(KArgs a, LbrQueues lq) {
           }
         }
       }
-      unsigned int slot = warp_append(lq.count + 3, pending);
-      if (pending) {
-        lq.q[3][slot] = (int32_t)(i + u);
-        FvLbrState* d = lq.state + (i + u);
-        d->x = st.x; d->beta = st.beta; d->sqrt_t = st.sqrt_t;
-      }
-      if (u) { iv[1] = ivu; stt[1] = stu; }
-      else { iv[0] = ivu; stt[0] = stu; }
+      if (u) { iv[1] = ivu; stt[1] = stu; pend[1] = pending; px_[1] = st.x; pb_[1] = st.beta; pt_[1] = st.sqrt_t; }
+      else { iv[0] = ivu; stt[0] = stu; pend[0] = pending; px_[0] = st.x; pb_[0] = st.beta; pt_[0] = st.sqrt_t; }
     }
+    unsigned int slot = warp_append2(lq.count + 3, pend[0], pend[1]);
+    if (pend[0]) { lq.q[3][slot++] = (int32_t)i; }
+    if (pend[1]) { lq.q[3][slot] = (int32_t)(i + 1); }
     if (active) {
+      // state rows written for every row of the pair (coalesced, full sectors)
+      st2(lq.sx, i, two, true, px_[0], px_[1]);
+      st2(lq.sbeta, i, two, true, pb_[0], pb_[1]);
+      st2(lq.ssqrt_t, i, two, true, pt_[0], pt_[1]);
       st2(a.o0, i, two, a.out_vec, iv[0], iv[1]);
       st2i8(a.status, i, two, stt[0], stt[1]);
       st2i8(a.region, i, two, -1, -1);
@@ -331,8 +353,8 @@ __global__ void __launch_bounds__(256) k_lbr_normalize(KArgs a, LbrQueues lq) {
   }
 }
 
-// Pass 2: anchors + region over the pending queue; appends each quote to its
-// region class queue.
+// Pass 2: anchors + region over the pending queue (row order); appends each
+// quote to its region class queue.
 __global__ void __launch_bounds__(256) k_lbr_anchors(KArgs a, LbrQueues lq) {
   const unsigned int n = lq.count[3];
   const unsigned int stride = gridDim.x * blockDim.x;
@@ -344,7 +366,7 @@ __global__ void __launch_bounds__(256) k_lbr_anchors(KArgs a, LbrQueues lq) {
     FvLbrState st;
     if (j < n) {
       row = lq.q[3][j];
-      st = lq.state[row];
+      st.x = lq.sx[row]; st.beta = lq.sbeta[row]; st.sqrt_t = lq.ssqrt_t[row];
       FvExc e = {0, 0, 0.0};
       FvLbrOut o;
       o.region = -1;
@@ -355,17 +377,15 @@ __global__ void __launch_bounds__(256) k_lbr_anchors(KArgs a, LbrQueues lq) {
       } else {
         region = o.region;
         cls = region_class(region);
+        lq.ss_c[row] = st.s_c; lq.sb0[row] = st.b0; lq.sb1[row] = st.b1;
+        lq.sE0[row] = st.E0; lq.sE1[row] = st.E1;
       }
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       unsigned int slot = warp_append(lq.count + c, cls == c);
-      if (cls == c) {
-        // entry = local row * 2 + near-high bit (the near class holds both)
-        lq.q[c][slot] = (int32_t)(2 * row + (region == FV_NEAR_HIGH ? 1 : 0));
-        FvLbrState* d = lq.state + row;
-        d->s_c = st.s_c; d->b0 = st.b0; d->b1 = st.b1; d->E0 = st.E0; d->E1 = st.E1;
-      }
+      // entry = local row * 2 + near-high bit (the near class holds both)
+      if (cls == c) lq.q[c][slot] = (int32_t)(2 * row + (region == FV_NEAR_HIGH ? 1 : 0));
     }
     if (j < n && a.region && cls >= 0) a.region[row] = (int8_t)region;
   }
@@ -379,7 +399,10 @@ __global__ void __launch_bounds__(256, 4) k_lbr_solve(KArgs a, LbrQueues lq) {
   for (unsigned int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const int32_t ent = q[j];
     const int32_t row = ent >> 1;
-    const FvLbrState st = lq.state[row];
+    FvLbrState st;
+    st.x = lq.sx[row]; st.beta = lq.sbeta[row]; st.sqrt_t = lq.ssqrt_t[row]; st.s_c = lq.ss_c[row];
+    if (R == FV_NEAR_LOW) { st.b0 = lq.sb0[row]; st.b1 = lq.sb1[row]; st.E0 = lq.sE0[row]; st.E1 = lq.sE1[row]; }
+    else { st.b0 = st.b1 = st.E0 = st.E1 = 0.0; }
     const int region = (R == FV_NEAR_LOW) ? ((ent & 1) ? FV_NEAR_HIGH : FV_NEAR_LOW) : R;
     FvExc e = {0, 0, 0.0};
     FvLbrOut o = (R == FV_FAR_LOW) ? fv_lbr_far_low_fused(st, e) : fv_lbr_solve<R>(region, st, e);
@@ -564,7 +587,7 @@ struct DevWork {
   int64_t chunk_cap_rows[FV_NSLOT] = {};
   ExplainOut* explain = nullptr;
   // LBR classify -> solve workspace (per slot)
-  FvLbrState* lbr_state[FV_NSLOT] = {};
+  double* lbr_state[FV_NSLOT] = {};     // 8 SoA fields x lbr_cap
   int32_t* lbr_q[FV_NSLOT] = {};        // 4 queues of lbr_cap entries each
   unsigned int* lbr_count = nullptr;    // [FV_NSLOT][4]
   int64_t lbr_cap[FV_NSLOT] = {};
@@ -634,8 +657,8 @@ cudaError_t ensure_lbr(DevWork* w, int slot, int64_t rows) {
   w->lbr_state[slot] = nullptr;
   w->lbr_q[slot] = nullptr;
   w->lbr_cap[slot] = 0;
-  int64_t cap = rows < 4096 ? 4096 : rows;
-  CK(cudaMalloc(&w->lbr_state[slot], sizeof(FvLbrState) * cap));
+  int64_t cap = rows < 4096 ? 4096 : ((rows + 255) / 256) * 256;   // keeps every SoA field 16B-aligned
+  CK(cudaMalloc(&w->lbr_state[slot], sizeof(double) * 8 * cap));
   CK(cudaMalloc(&w->lbr_q[slot], sizeof(int32_t) * 4 * cap));
   w->lbr_cap[slot] = cap;
   return cudaSuccess;
@@ -705,7 +728,10 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
         for (int64_t off = 0; off < a.n; off += chunk) {
           KArgs b = sub_args(a, off, (a.n - off) < chunk ? (a.n - off) : chunk);
           LbrQueues lq;
-          lq.state = w->lbr_state[slot];
+          double* sb = w->lbr_state[slot];
+          const int64_t cp = w->lbr_cap[slot];
+          lq.sx = sb; lq.sbeta = sb + cp; lq.ssqrt_t = sb + 2 * cp; lq.ss_c = sb + 3 * cp;
+          lq.sb0 = sb + 4 * cp; lq.sb1 = sb + 5 * cp; lq.sE0 = sb + 6 * cp; lq.sE1 = sb + 7 * cp;
           for (int c3 = 0; c3 < 4; ++c3) lq.q[c3] = w->lbr_q[slot] + c3 * w->lbr_cap[slot];
           lq.count = w->lbr_count + 4 * slot;
           CK(cudaMemsetAsync(lq.count, 0, 4 * sizeof(unsigned int), s));

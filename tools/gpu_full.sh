@@ -1,0 +1,23 @@
+#!/bin/bash
+# Full round run on one B200: GPU tests, smoke, the C4 bench line (with e2e +
+# CPU baseline), other workloads, the reference arm, an ncu launch list and
+# an ncu --set full capture of the LBR kernels.  Outputs in gpurun_out/.
+set -u
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+TAG=${TAG:-full}
+nvidia-smi --query-gpu=name,driver_version,clocks.sm,clocks.max.sm,power.limit --format=csv > gpurun_out/gpu_${TAG}.txt 2>&1
+lscpu > gpurun_out/cpu_${TAG}.txt 2>&1
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -15 > gpurun_out/pytest_gpu_${TAG}.txt
+tail -3 gpurun_out/pytest_gpu_${TAG}.txt
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${TAG}.txt 2>&1; tail -1 gpurun_out/smoke_${TAG}.txt
+timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; tail -c 600 gpurun_out/bench_${TAG}.json
+for w in c1 c2 c3 c5; do
+  timeout 600 python bench.py --workload $w --steps 5 --warmup 3 --no-cpu > gpurun_out/bench_${TAG}_$w.json 2>> gpurun_out/bench_${TAG}.err
+done
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_${TAG}_ref.json 2>> gpurun_out/bench_${TAG}.err; cat gpurun_out/bench_${TAG}_ref.json | head -c 400; echo
+if [ "${NCU:-1}" = "1" ]; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_lbr -c 5 -o gpurun_out/prof_${TAG} python bench.py --rows 10000000 --steps 1 --warmup 0 --no-e2e --no-cpu > gpurun_out/ncu_${TAG}.log 2>&1
+  tail -1 gpurun_out/ncu_${TAG}.log
+fi
