@@ -31,21 +31,22 @@ def _stale(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale(OUT, DEPS):
-        return OUT
-    tmp = OUT + ".tmp%d" % os.getpid()
-    cmd = [NVCC] + NVCC_FLAGS + ["-o", tmp] + SOURCES
+def build(force=False, verbose=False, out=None, defines=()):
+    out = out or OUT
+    if not force and not _stale(out, DEPS):
+        return out
+    tmp = out + ".tmp%d" % os.getpid()
+    cmd = [NVCC] + NVCC_FLAGS + ["-D" + d for d in defines] + ["-o", tmp] + SOURCES
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
-    log = os.path.join(HERE, "_build_ptxas.log")
+    log = os.path.join(os.path.dirname(out), "_build_ptxas.log" if out == OUT else os.path.basename(out) + ".ptxas.log")
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
     if verbose:
         sys.stdout.write(res.stderr)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

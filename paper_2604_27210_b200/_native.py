@@ -12,7 +12,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfastvol_b200.so")
+LIB_PATH = os.environ.get("FV_LIB") or os.path.join(HERE, "libfastvol_b200.so")
 
 FV_OK, FV_ERR_BATCH, FV_ERR_PYEXC, FV_ERR_CUDA, FV_ERR_ARG = 0, 1, 2, 3, 4
 

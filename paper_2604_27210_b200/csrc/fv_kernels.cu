@@ -34,6 +34,13 @@
 #include "../../include/fastvol_b200.h"
 
 #define FV_VERSION "fastvol_b200 0.1.0 (sm_100a)"
+// tuning knobs (occupancy hints; see profiles/README.md for the sweep)
+#ifndef FV_SOLVE_MINB
+#define FV_SOLVE_MINB 4
+#endif
+#ifndef FV_ANCH_MINB
+#define FV_ANCH_MINB 1
+#endif
 #define FV_NSLOT 3
 
 // ---------------------------------------------------------------------------
@@ -355,7 +362,7 @@ __global__ void __launch_bounds__(256) k_lbr_normalize(KArgs a, LbrQueues lq) {
 
 // Pass 2: anchors + region over the pending queue (row order); appends each
 // quote to its region class queue.
-__global__ void __launch_bounds__(256) k_lbr_anchors(KArgs a, LbrQueues lq) {
+__global__ void __launch_bounds__(256, FV_ANCH_MINB) k_lbr_anchors(KArgs a, LbrQueues lq) {
   const unsigned int n = lq.count[3];
   const unsigned int stride = gridDim.x * blockDim.x;
   const unsigned int nloop = (n + stride - 1) / stride;
@@ -392,7 +399,7 @@ __global__ void __launch_bounds__(256) k_lbr_anchors(KArgs a, LbrQueues lq) {
 }
 
 template <int R>
-__global__ void __launch_bounds__(256, 4) k_lbr_solve(KArgs a, LbrQueues lq) {
+__global__ void __launch_bounds__(256, FV_SOLVE_MINB) k_lbr_solve(KArgs a, LbrQueues lq) {
   const int c = R == FV_FAR_LOW ? 0 : (R == FV_FAR_HIGH ? 2 : 1);
   const unsigned int n = lq.count[c];
   const int32_t* q = lq.q[c];
@@ -412,19 +419,17 @@ __global__ void __launch_bounds__(256, 4) k_lbr_solve(KArgs a, LbrQueues lq) {
   }
 }
 
-// Halley phase-2 queue entry
-struct HQ {
+// Halley setup pass: validation + :60-86 for every row, coalesced; quotes
+// that need the iteration get a prepared record in a dense queue.
+struct HsmRec {
   FvHalleyCtx c;
-  FvHalleyState s;
-  int64_t row;   // local row
+  double guess;
+  int64_t row;
 };
 
-
-__global__ void __launch_bounds__(256) k_halley1(KArgs a, HQ* queue, unsigned int* qlen) {
+__global__ void __launch_bounds__(256) k_halley_setup(KArgs a, HsmRec* recs, unsigned int* count) {
   const int64_t npair = (a.n + 1) >> 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  // the loop trip count is uniform per warp so warp_append's ballot sees the
-  // whole warp; lanes past the end participate with want = false.
   const int64_t nloop = (npair + stride - 1) / stride;
   for (int64_t it = 0; it < nloop; ++it) {
     const int64_t j = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -432,46 +437,43 @@ __global__ void __launch_bounds__(256) k_halley1(KArgs a, HQ* queue, unsigned in
     const int64_t i = 2 * j;
     const bool two = active && (i + 1 < a.n);
     double iv[2] = {0.0, 0.0};
-    int stt[2] = {0, 0};
+    int stt[2] = {FV_IV_MAX_ITER, FV_IV_MAX_ITER};
     bool need[2] = {false, false};
-    FvHalleyCtx cx[2];
-    FvHalleyState sx[2];
-    if (active) {
-      Pair p;
-      load_pair(a, i, two, p);
+    FvHalleySM m0, m1;
+    Pair p;
+    if (active) load_pair(a, i, two, p);
 #pragma unroll 1
-      for (int u = 0; u < (two ? 2 : 1); ++u) {
-        uint32_t bad = row_checks(a, p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u], p.q[u], p.last[u]);
-        if (bad) {
-          publish_checks(a.st, bad, a.row0 + i + u);
-          iv[u] = __builtin_nan(""); stt[u] = FV_IV_MAX_ITER;
-          continue;
-        }
-        FvExc e = {0, 0, 0.0};
-        int status;
-        double sig;
-        int done = fv_halley_phase1(a.model, (double)p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u],
-                                    p.q[u], p.last[u], cx[u], sx[u], &status, &sig, e);
-        publish_exc(&a.st->exc_first, e.code, a.row0 + i + u);
-        if (done || e.code) {
-          iv[u] = (status == FV_IV_CONVERGED || status == FV_IV_FELL_BACK) ? sig : __builtin_nan("");
-          stt[u] = status;
-        } else {
-          need[u] = true;
-        }
-      }
-    }
-#pragma unroll
     for (int u = 0; u < 2; ++u) {
-      unsigned int slot = warp_append(qlen, need[u]);
-      if (need[u]) {
-        HQ h;
-        h.c = cx[u]; h.s = sx[u]; h.row = i + u;
-        queue[slot] = h;
+      const bool valid = active && (u == 0 || two);
+      if (!valid) continue;
+      const int fl = u ? p.fl[1] : p.fl[0];
+      const double un = u ? p.un[1] : p.un[0], k = u ? p.k[1] : p.k[0];
+      const double t = u ? p.t[1] : p.t[0], r = u ? p.r[1] : p.r[0];
+      const double q = u ? p.q[1] : p.q[0], px = u ? p.last[1] : p.last[0];
+      uint32_t bad = row_checks(a, fl, un, k, t, r, q, px);
+      double ivu = __builtin_nan("");
+      int stu = FV_IV_MAX_ITER;
+      bool nd = false;
+      FvHalleySM m;
+      if (bad) {
+        publish_checks(a.st, bad, a.row0 + i + u);
+      } else {
+        FvExc e = {0, 0, 0.0};
+        if (fv_hsm_setup(a.model, (double)fl, un, k, t, r, q, px, m, e)) {
+          publish_exc(&a.st->exc_first, e.code, a.row0 + i + u);
+          ivu = (m.status == FV_IV_CONVERGED || m.status == FV_IV_FELL_BACK) ? m.out_sigma : __builtin_nan("");
+          stu = m.status;
+        } else {
+          nd = true;
+        }
       }
+      if (u) { iv[1] = ivu; stt[1] = stu; need[1] = nd; m1 = m; }
+      else { iv[0] = ivu; stt[0] = stu; need[0] = nd; m0 = m; }
     }
+    unsigned int slot = warp_append2(count, need[0], need[1]);
+    if (need[0]) { HsmRec h; h.c = m0.c; h.guess = m0.guess; h.row = i; recs[slot++] = h; }
+    if (need[1]) { HsmRec h; h.c = m1.c; h.guess = m1.guess; h.row = i + 1; recs[slot] = h; }
     if (active) {
-      // queued rows are overwritten by phase 2
       st2(a.o0, i, two, a.out_vec, iv[0], iv[1]);
       st2i8(a.status, i, two, stt[0], stt[1]);
       if (a.region) st2i8(a.region, i, two, -1, -1);
@@ -479,17 +481,69 @@ __global__ void __launch_bounds__(256) k_halley1(KArgs a, HQ* queue, unsigned in
   }
 }
 
-__global__ void __launch_bounds__(256) k_halley2(KArgs a, const HQ* queue, const unsigned int* qlen) {
-  const unsigned int n = *qlen;
-  for (unsigned int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    HQ h = queue[j];
+// Halley as a persistent per-lane state machine (fv_quote.h: fv_hsm_*) over
+// the prepared queue.  Each loop trip: idle lanes take the next records
+// (warp-aggregated), then every busy lane performs one solver step whose
+// heavy part -- one black_kernel evaluation -- is the same code for all.
+__global__ void __launch_bounds__(256) k_halley_sm(KArgs a, const HsmRec* recs,
+                                                   const unsigned int* count,
+                                                   unsigned long long* next) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long n = *count;
+  FvHalleySM m;
+  m.state = FV_HS_DONE;
+  int64_t row = -1;
+  bool busy = false;
+  bool exhausted = false;
+  for (;;) {
+    // ---- refill idle lanes -------------------------------------------------
+    {
+      const bool need = !busy && !exhausted;
+      const unsigned mask = __ballot_sync(0xffffffffu, need);
+      if (mask) {
+        unsigned long long base = 0;
+        if (lane == __ffs(mask) - 1) base = atomicAdd(next, (unsigned long long)__popc(mask));
+        base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
+        if (need) {
+          const unsigned long long jq = base + __popc(mask & ((1u << lane) - 1));
+          if (jq >= n) {
+            exhausted = true;
+          } else {
+            const HsmRec h = recs[jq];
+            m.c = h.c; m.guess = h.guess; row = h.row;
+            m.iterations = 0; m.k = 0;
+            m.lo = FV_K_1EM9; m.hi = 10.0;
+            m.state = FV_HS_LO;
+            busy = true;
+          }
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, busy)) break;
+    // ---- one solver step -------------------------------------------------
+    // Lanes leave fv_hsm_pre from different states; the explicit warp syncs
+    // make them enter the shared black_kernel evaluation together (without
+    // them the compiler reconverges only around the evaluation itself and
+    // each state's lanes run it separately: ~6 of 32 lanes active).
     FvExc e = {0, 0, 0.0};
-    int status;
-    double sig;
-    fv_halley_phase2(h.c, h.s, &status, &sig, e);
-    publish_exc(&a.st->exc_first, e.code, a.row0 + h.row);
-    a.o0[h.row] = (status == FV_IV_CONVERGED || status == FV_IV_FELL_BACK) ? sig : __builtin_nan("");
-    a.status[h.row] = (int8_t)status;
+    double x = 0.0;
+    bool eval = busy && fv_hsm_pre(m, &x, e);
+    __syncwarp();
+    double fx = 0.0;
+    if (eval) fx = fv_halley_f(m.c, x, e);                // the shared heavy code
+    __syncwarp();
+    if (busy) {
+      if (eval) fv_hsm_post(m, fx, e);
+      if (e.code) {
+        publish_exc(&a.st->exc_first, e.code, a.row0 + row);
+        fv_hsm_finish(m, FV_IV_MAX_ITER, __builtin_nan(""));
+      }
+      if (m.state == FV_HS_DONE) {
+        a.o0[row] = (m.status == FV_IV_CONVERGED || m.status == FV_IV_FELL_BACK) ? m.out_sigma : __builtin_nan("");
+        a.status[row] = (int8_t)m.status;
+        busy = false;
+      }
+    }
   }
 }
 
@@ -503,10 +557,9 @@ __global__ void k_explain(KArgs a, int method, int64_t local_row, ExplainOut* ou
   if (method == FV_METHOD_LBR) {
     fv_lbr_batch_row(a.model, (double)p.fl[0], p.un[0], p.k[0], p.t[0], p.r[0], p.q[0], p.last[0], e);
   } else {
-    FvHalleyCtx c; FvHalleyState s; int status; double sig;
-    if (!fv_halley_phase1(a.model, (double)p.fl[0], p.un[0], p.k[0], p.t[0], p.r[0], p.q[0],
-                          p.last[0], c, s, &status, &sig, e) && !e.code)
-      fv_halley_phase2(c, s, &status, &sig, e);
+    int status; double sig;
+    fv_halley_row_sm(a.model, (double)p.fl[0], p.un[0], p.k[0], p.t[0], p.r[0], p.q[0], p.last[0],
+                     &status, &sig, e);
   }
   out->code = e.code; out->np = e.np; out->val = e.val;
 }
@@ -579,9 +632,6 @@ struct DevWork {
   cudaStream_t streams[FV_NSLOT] = {};
   FvDevStatus* st = nullptr;            // device
   FvDevStatus* st_host = nullptr;       // pinned mirror
-  unsigned int* qlen = nullptr;         // [FV_NSLOT]
-  HQ* queue[FV_NSLOT] = {};
-  int64_t queue_cap[FV_NSLOT] = {};
   // chunk buffers for host-pointer calls
   char* chunk[FV_NSLOT] = {};
   int64_t chunk_cap_rows[FV_NSLOT] = {};
@@ -591,7 +641,12 @@ struct DevWork {
   int32_t* lbr_q[FV_NSLOT] = {};        // 4 queues of lbr_cap entries each
   unsigned int* lbr_count = nullptr;    // [FV_NSLOT][4]
   int64_t lbr_cap[FV_NSLOT] = {};
-  int blocks_price = 0, blocks_greeks = 0, blocks_h1 = 0, blocks_h2 = 0;
+  int blocks_price = 0, blocks_greeks = 0, blocks_hsm = 0;
+  unsigned long long* work_ctr = nullptr;   // [FV_NSLOT]
+  unsigned int* hsm_count = nullptr;        // [FV_NSLOT]
+  HsmRec* hsm_recs[FV_NSLOT] = {};
+  int64_t hsm_cap[FV_NSLOT] = {};
+  int blocks_hset = 0;
   int blocks_lbr_norm = 0, blocks_lbr_anch = 0, blocks_lbr_fl = 0, blocks_lbr_near = 0, blocks_lbr_fh = 0;
   std::mutex mu;
 };
@@ -620,7 +675,6 @@ cudaError_t get_work(DevWork** out) {
     for (int s = 0; s < FV_NSLOT; ++s) CK(cudaStreamCreateWithFlags(&w->streams[s], cudaStreamNonBlocking));
     CK(cudaMalloc(&w->st, sizeof(FvDevStatus)));
     CK(cudaMallocHost(&w->st_host, sizeof(FvDevStatus)));
-    CK(cudaMalloc(&w->qlen, sizeof(unsigned int) * FV_NSLOT));
     CK(cudaMalloc(&w->explain, sizeof(ExplainOut)));
     w->blocks_price = occupancy_blocks((const void*)k_price, w->sm_count);
     w->blocks_greeks = occupancy_blocks((const void*)k_price_greeks<true, true>, w->sm_count);
@@ -630,22 +684,16 @@ cudaError_t get_work(DevWork** out) {
     w->blocks_lbr_fl = occupancy_blocks((const void*)k_lbr_solve<FV_FAR_LOW>, w->sm_count);
     w->blocks_lbr_near = occupancy_blocks((const void*)k_lbr_solve<FV_NEAR_LOW>, w->sm_count);
     w->blocks_lbr_fh = occupancy_blocks((const void*)k_lbr_solve<FV_FAR_HIGH>, w->sm_count);
-    w->blocks_h1 = occupancy_blocks((const void*)k_halley1, w->sm_count);
-    w->blocks_h2 = occupancy_blocks((const void*)k_halley2, w->sm_count);
+    w->blocks_hsm = occupancy_blocks((const void*)k_halley_sm, w->sm_count);
+    CK(cudaMalloc(&w->work_ctr, sizeof(unsigned long long) * FV_NSLOT));
+    CK(cudaMalloc(&w->hsm_count, sizeof(unsigned int) * FV_NSLOT));
+    w->blocks_hset = occupancy_blocks((const void*)k_halley_setup, w->sm_count);
     g_work[dev] = w;
   }
   *out = g_work[dev];
   return cudaSuccess;
 }
 
-cudaError_t ensure_queue(DevWork* w, int slot, int64_t rows) {
-  if (w->queue_cap[slot] >= rows) return cudaSuccess;
-  if (w->queue[slot]) cudaFree(w->queue[slot]);
-  int64_t cap = rows < 1024 ? 1024 : rows;
-  CK(cudaMalloc(&w->queue[slot], sizeof(HQ) * cap));
-  w->queue_cap[slot] = cap;
-  return cudaSuccess;
-}
 
 // rows per LBR classify/solve round (bounds the state workspace: 64 B/row)
 const int64_t kLbrChunk = 1 << 25;
@@ -680,6 +728,17 @@ KArgs sub_args(const KArgs& a, int64_t off, int64_t len) {
   b.row0 = a.row0 + off;
   if (off & 1) b.out_vec = 0;
   return b;
+}
+
+cudaError_t ensure_hsm(DevWork* w, int slot, int64_t rows) {
+  if (w->hsm_cap[slot] >= rows) return cudaSuccess;
+  if (w->hsm_recs[slot]) cudaFree(w->hsm_recs[slot]);
+  w->hsm_recs[slot] = nullptr;
+  w->hsm_cap[slot] = 0;
+  int64_t cap = rows < 4096 ? 4096 : rows;
+  CK(cudaMalloc(&w->hsm_recs[slot], sizeof(HsmRec) * cap));
+  w->hsm_cap[slot] = cap;
+  return cudaSuccess;
 }
 
 enum Kind { KIND_PRICE, KIND_IV, KIND_GREEKS, KIND_PRICE_GREEKS };
@@ -744,10 +803,14 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
           t_launches += 5;
         }
       } else {
-        CK(ensure_queue(w, slot, a.n));
-        CK(cudaMemsetAsync(w->qlen + slot, 0, sizeof(unsigned int), s));
-        k_halley1<<<blocks_for(w->blocks_h1, a.n), 256, 0, s>>>(a, w->queue[slot], w->qlen + slot);
-        k_halley2<<<w->blocks_h2, 256, 0, s>>>(a, w->queue[slot], w->qlen + slot);
+        CK(ensure_hsm(w, slot, a.n));
+        unsigned long long* ctr = w->work_ctr + slot;
+        unsigned int* cnt = w->hsm_count + slot;
+        CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned int), s));
+        k_halley_setup<<<blocks_for(w->blocks_hset, a.n), 256, 0, s>>>(a, w->hsm_recs[slot], cnt);
+        int64_t need = (a.n + 255) / 256;
+        k_halley_sm<<<need < w->blocks_hsm ? need : w->blocks_hsm, 256, 0, s>>>(a, w->hsm_recs[slot], cnt, ctr);
         t_launches += 2;
       }
       break;

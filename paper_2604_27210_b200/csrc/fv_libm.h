@@ -302,14 +302,15 @@ FV_HD double fv_pow_pos_i(double x, double y) {
 // erfc: glibc 2.39 sysdeps/ieee754/dbl-64/s_erf.c (fdlibm-derived, Estrin-style
 // pairs), built WITHOUT fma; its two exp calls resolve to __exp_fma (fv_exp).
 // ---------------------------------------------------------------------------
-FV_HD double fv_erfc_i(double x) {
+template <bool kMergeInner, bool kMergeTail>
+FV_HD double fv_erfc_t(double x) {
   uint64_t ux = fv_asuint64(x);
   int32_t hx = (int32_t)(ux >> 32);
   int32_t ix = hx & 0x7fffffff;
   if (ix >= 0x7ff00000) {  // erfc(nan) = nan, erfc(+-inf) = 0, 2
     return (double)(((uint32_t)hx >> 31) << 1) + 1.0 / x;
   }
-  if (ix < 0x3feb0000) {   // |x| < 0.84375
+  if (!kMergeInner && ix < 0x3feb0000) {   // |x| < 0.84375
     if (ix < 0x3c700000) return 1.0 - x;
     double z = x * x;
     double r1 = z * FV_ERFC_PP1 + FV_ERFC_PP0;
@@ -322,14 +323,12 @@ FV_HD double fv_erfc_i(double x) {
     double r = (r1 + z2 * r2) + z4 * FV_ERFC_PP4;
     double s = (s1 + z2 * s2) + z4 * s3;
     double y = r / s;
-    if (hx < 0x3fd00000) {  // x < 1/4
-      return 1.0 - (x + x * y);
-    }
+    if (hx < 0x3fd00000) return 1.0 - (x + x * y);
     r = x * y;
     r = r + (x - 0.5);
     return 0.5 - r;
   }
-  if (ix < 0x3ff40000) {   // 0.84375 <= |x| < 1.25
+  if (!kMergeInner && ix < 0x3ff40000) {   // 0.84375 <= |x| < 1.25
     double s = fv_fabs(x) - 1.0;
     double P1 = s * FV_ERFC_PA1 + FV_ERFC_PA0;
     double s2 = s * s;
@@ -346,11 +345,55 @@ FV_HD double fv_erfc_i(double x) {
     double zz = FV_ERFC_ERX + P / Q;
     return 1.0 + zz;
   }
+  if (kMergeInner && ix < 0x3ff40000) {   // |x| < 1.25
+    if (ix < 0x3c700000) return 1.0 - x;
+    // |x| < 0.84375 (pp/qq in u = x^2) and 0.84375 <= |x| < 1.25 (pa/qa in
+    // u = |x| - 1) evaluate one shared rational form over a two-row table
+    // (zero coefficients add exact +0s), then take their own final formula:
+    // bit-identical to glibc's two branches without splitting the warp.
+    const bool inner = ix < 0x3feb0000;
+    const double u = inner ? x * x : fv_fabs(x) - 1.0;
+    const int row = inner ? 0 : 16;
+    double n0 = FV_TAB(fv_erfc_mid, row + 0), n1 = FV_TAB(fv_erfc_mid, row + 1);
+    double n2 = FV_TAB(fv_erfc_mid, row + 2), n3 = FV_TAB(fv_erfc_mid, row + 3);
+    double n4 = FV_TAB(fv_erfc_mid, row + 4), n5 = FV_TAB(fv_erfc_mid, row + 5);
+    double n6 = FV_TAB(fv_erfc_mid, row + 6);
+    double e1 = FV_TAB(fv_erfc_mid, row + 7), e2 = FV_TAB(fv_erfc_mid, row + 8);
+    double e3 = FV_TAB(fv_erfc_mid, row + 9), e4 = FV_TAB(fv_erfc_mid, row + 10);
+    double e5 = FV_TAB(fv_erfc_mid, row + 11), e6 = FV_TAB(fv_erfc_mid, row + 12);
+    double N1 = u * n1 + n0;
+    double u2 = u * u;
+    double D1 = u * e1 + 1.0;
+    double u4 = u2 * u2;
+    double N2 = u * n3 + n2;
+    double u6 = u4 * u2;
+    double D2 = u * e3 + e2;
+    double N3 = u * n5 + n4;
+    double D3 = u * e5 + e4;
+    double num = ((N1 + u2 * N2) + u4 * N3) + u6 * n6;
+    double den = ((D1 + u2 * D2) + u4 * D3) + u6 * e6;
+    double y = num / den;
+    if (inner) {
+      if (hx < 0x3fd00000) return 1.0 - (x + x * y);   // x < 1/4
+      double r = x * y;
+      r = r + (x - 0.5);
+      return 0.5 - r;
+    }
+    if (hx >= 0) return FV_ERFC_ONE_M_ERX - y;
+    double zz = FV_ERFC_ERX + y;
+    return 1.0 + zz;
+  }
   if (ix < 0x403c0000) {   // |x| < 28
     double ax = fv_fabs(x);
     double s = 1.0 / (x * x);
+    // The two tail ranges (|x| < 1/0.35: ra/sa; else rb/sb) share one code
+    // path over a two-row coefficient table: the rb row has explicit zeros
+    // where rb/sb have no term, which only adds exact +0s, so every result
+    // is bit-identical to glibc's two separate branches while neighbouring
+    // lanes in different ranges no longer diverge.
     double R, S;
-    if (ix < 0x4006db6d) { // |x| < 1/0.35
+    if (!kMergeTail) {
+    if (ix < 0x4006db6d) {
       double R1 = s * FV_ERFC_RA1 + FV_ERFC_RA0;
       double s2 = s * s;
       double S1 = s * FV_ERFC_SA1 + 1.0;
@@ -365,8 +408,8 @@ FV_HD double fv_erfc_i(double x) {
       double S4 = s * FV_ERFC_SA7 + FV_ERFC_SA6;
       R = ((R1 + s2 * R2) + s4 * R3) + s6 * R4;
       S = (((S1 + s2 * S2) + s4 * S3) + s6 * S4) + s8 * FV_ERFC_SA8;
-    } else {               // |x| >= 1/0.35
-      if (hx < 0 && ix >= 0x40180000) return FV_K_TWO_M_TINY;  // x < -6: two - tiny
+    } else {
+      if (hx < 0 && ix >= 0x40180000) return FV_K_TWO_M_TINY;
       double R1 = s * FV_ERFC_RB1 + FV_ERFC_RB0;
       double s2 = s * s;
       double S1 = s * FV_ERFC_SB1 + 1.0;
@@ -379,6 +422,32 @@ FV_HD double fv_erfc_i(double x) {
       double S4 = s * FV_ERFC_SB7 + FV_ERFC_SB6;
       R = ((R1 + s2 * R2) + s4 * R3) + s6 * FV_ERFC_RB6;
       S = ((S1 + s2 * S2) + s4 * S3) + s6 * S4;
+    }
+    } else {
+    if (ix >= 0x4006db6d && hx < 0 && ix >= 0x40180000) return FV_K_TWO_M_TINY;  // x < -6
+    const int row = (ix < 0x4006db6d) ? 0 : 16;
+    double c0 = FV_TAB(fv_erfc_tail, row + 0), c1 = FV_TAB(fv_erfc_tail, row + 1);
+    double c2 = FV_TAB(fv_erfc_tail, row + 2), c3 = FV_TAB(fv_erfc_tail, row + 3);
+    double c4 = FV_TAB(fv_erfc_tail, row + 4), c5 = FV_TAB(fv_erfc_tail, row + 5);
+    double c6 = FV_TAB(fv_erfc_tail, row + 6), c7 = FV_TAB(fv_erfc_tail, row + 7);
+    double d1 = FV_TAB(fv_erfc_tail, row + 8), d2 = FV_TAB(fv_erfc_tail, row + 9);
+    double d3 = FV_TAB(fv_erfc_tail, row + 10), d4 = FV_TAB(fv_erfc_tail, row + 11);
+    double d5 = FV_TAB(fv_erfc_tail, row + 12), d6 = FV_TAB(fv_erfc_tail, row + 13);
+    double d7 = FV_TAB(fv_erfc_tail, row + 14), d8 = FV_TAB(fv_erfc_tail, row + 15);
+    double R1 = s * c1 + c0;
+    double s2 = s * s;
+    double S1 = s * d1 + 1.0;
+    double s4 = s2 * s2;
+    double R2 = s * c3 + c2;
+    double s6 = s4 * s2;
+    double S2 = s * d3 + d2;
+    double s8 = s4 * s4;
+    double R3 = s * c5 + c4;
+    double S3 = s * d5 + d4;
+    double R4 = s * c7 + c6;
+    double S4 = s * d7 + d6;
+    R = ((R1 + s2 * R2) + s4 * R3) + s6 * R4;
+    S = (((S1 + s2 * S2) + s4 * S3) + s6 * S4) + s8 * d8;
     }
     double z = fv_asdouble(fv_asuint64(ax) & 0xffffffff00000000ull);
     double e1 = fv_exp(-z * z - 0.5625);
@@ -431,4 +500,10 @@ FV_HD double fv_erfcx_i(double x) {
 FV_HDN double fv_log(double x) { return fv_log_i(x); }
 FV_HDN double fv_pow_pos(double x, double y) { return fv_pow_pos_i(x, y); }
 FV_HDN double fv_erfcx(double x) { return fv_erfcx_i(x); }
-FV_HDN double fv_erfc(double x) { return fv_erfc_i(x); }
+// Two builds of erfc: separate fdlibm branches (constants in the constant
+// bank; best where neighbouring lanes share a range, e.g. the LBR anchors) and
+// the merged-table form (best where lanes' arguments scatter over the ranges:
+// pricing, Greeks, Halley).  Bit-identical; chosen per caller.
+FV_HD double fv_erfc_i(double x) { return fv_erfc_t<false, false>(x); }
+FV_HDN double fv_erfc(double x) { return fv_erfc_t<false, false>(x); }
+FV_HDN double fv_erfc_m(double x) { return fv_erfc_t<true, false>(x); }

@@ -116,6 +116,8 @@ FV_HD double py_min(double a, double b) { return (b < a) ? b : a; }   // builtin
 // ---- distributions.py ------------------------------------------------------
 FV_HD double fv_norm_cdf(double x) { return 0.5 * fv_erfc(FV_DIV_SQRT2(-x)); }
 FV_HD double fv_norm_cdf_i(double x) { return 0.5 * fv_erfc_i(FV_DIV_SQRT2(-x)); }
+// pricing / Greeks / Halley: arguments scatter over erfc's ranges across lanes
+FV_HD double fv_norm_cdf_m(double x) { return 0.5 * fv_erfc_m(FV_DIV_SQRT2(-x)); }
 FV_HD double fv_norm_pdf(double x) { return FV_INV_SQRT_TWO_PI * fv_exp(-0.5 * x * x); }
 
 FV_HD double as241_poly(double c0, double c1, double c2, double c3, double c4, double c5,
@@ -187,7 +189,7 @@ FV_HD double fv_black_kernel(double th, double Fw, double K, double disc, double
   if (fk_bad) e.raise(FV_EXC_MATH_DOMAIN);
   double d1 = (lnFK + 0.5 * s * s) / s;
   double d2 = d1 - s;
-  double raw = th * (Fw * fv_norm_cdf(th * d1) - K * fv_norm_cdf(th * d2));
+  double raw = th * (Fw * fv_norm_cdf_m(th * d1) - K * fv_norm_cdf_m(th * d2));
   return disc * py_min(py_max(raw, intrinsic), cap);
 }
 
@@ -261,8 +263,8 @@ FV_HD FvGreeks fv_price_greeks_row(int model, double th, double un, double K, do
   if (bad) { if (want_price) ep.raise(FV_EXC_MATH_DOMAIN); if (want_greeks) eg.raise(FV_EXC_MATH_DOMAIN); }
   double d1 = (lnFK + 0.5 * s * s) / s;
   double d2 = d1 - s;
-  double cdf_td1 = fv_norm_cdf(th * d1);
-  double cdf_td2 = fv_norm_cdf(th * d2);
+  double cdf_td1 = fv_norm_cdf_m(th * d1);
+  double cdf_td2 = fv_norm_cdf_m(th * d2);
   double raw = th * (Fw * cdf_td1 - K * cdf_td2);
   o.price = disc * py_min(py_max(raw, intrinsic), cap);
   if (!want_greeks) return o;
@@ -407,10 +409,198 @@ FV_HD void fv_halley_phase2(const FvHalleyCtx& c, FvHalleyState st, int* status,
   *status = FV_IV_MAX_ITER; *sigma_out = __builtin_nan("");
 }
 
+// ---- solver.py implied_vol_halley as a per-lane state machine ---------------
+// The GPU form of :49-161.  Every step of the solver is "decide sigma ->
+// evaluate f(sigma) = black_kernel(...) - target -> update"; the kernel runs
+// that step for all lanes in lockstep (the expensive black_kernel is the
+// shared code) and refills a lane as soon as its quote finishes, so neither
+// the spread of Halley iteration counts nor the 51-60-step bisection tail of
+// ~4% of quotes leaves lanes idle.  The sequence of f evaluations and every
+// value per quote are exactly the reference's.
+#define FV_HS_DONE 0
+#define FV_HS_LO 1       // f(SIGMA_LO)                      :91-96
+#define FV_HS_HI 2       // f(hi), doubling while negative    :97-102
+#define FV_HS_GUESS 3    // f(guess)                          :104-112
+#define FV_HS_ITER 4     // Halley candidate (needs vega)     :115-135
+#define FV_HS_CHECK 5    // f(cand) evaluated: accept?        :129-132
+#define FV_HS_MID 6      // rejected: f(mid)                  :133-135
+#define FV_HS_BISECT 7   // bisection tail                    :147-157
+
+struct FvHalleySM {
+  FvHalleyCtx c;
+  double lo, hi, sigma, fval, cand, guess;
+  int state, k, iterations, status;
+  double out_sigma;
+};
+
+FV_HD void fv_hsm_finish(FvHalleySM& m, int status, double sigma) {
+  m.state = FV_HS_DONE; m.status = status; m.out_sigma = sigma;
+}
+
+// :60-86 (everything before the first f evaluation).  Returns 1 when the
+// quote is already finished (bounds / t <= 0 / exception).
+FV_HD int fv_hsm_setup(int model, double th, double un, double K, double t, double r, double q,
+                       double target, FvHalleySM& m, FvExc& e) {
+  const double nan = __builtin_nan("");
+  m.iterations = 0; m.k = 0;
+  double Fw = (model == 0) ? un : un * py_exp((r - q) * t, e);
+  double discount = py_exp(-r * t, e);
+  double sqrt_t = sqrt(t);
+  if (e.code) { fv_hsm_finish(m, FV_IV_MAX_ITER, nan); return 1; }
+  double disc_intrinsic = discount * py_max(th * (Fw - K), 0.0);
+  double disc_cap = discount * ((th > 0.0) ? Fw : K);
+  double tie_tol = FV_K_1EM12 * py_max(1.0, disc_cap);
+  if (!fv_isfinite(target)) { fv_hsm_finish(m, FV_IV_BELOW_INTRINSIC, nan); return 1; }
+  if (target <= disc_intrinsic + tie_tol) { fv_hsm_finish(m, FV_IV_BELOW_INTRINSIC, nan); return 1; }
+  if (target > disc_cap + tie_tol) { fv_hsm_finish(m, FV_IV_ABOVE_UPPER, nan); return 1; }
+  double tol_price = py_min(tie_tol, FV_K_1EM10 * (target - disc_intrinsic));
+  if (t <= 0.0) { fv_hsm_finish(m, FV_IV_ABOVE_UPPER, nan); return 1; }
+  m.c.th = th; m.c.Fw = Fw; m.c.K = K; m.c.disc = discount; m.c.sqrt_t = sqrt_t;
+  m.c.lnFK = fv_log_fk(Fw / K, &m.c.fk_bad);
+  m.c.target = target; m.c.tol_price = tol_price;
+  m.guess = sqrt(FV_TWO_PI / t) * target / un;            // :105, before clamping
+  m.lo = FV_K_1EM9; m.hi = 10.0;
+  m.state = FV_HS_LO;
+  return 0;
+}
+
+// Decide where this step evaluates f.  Returns 0 if the quote finished
+// without needing an evaluation (m.state == DONE).
+FV_HD int fv_hsm_pre(FvHalleySM& m, double* x, FvExc& e) {
+  const double nan = __builtin_nan("");
+  switch (m.state) {
+    case FV_HS_LO: *x = m.lo; return 1;
+    case FV_HS_HI: *x = m.hi; return 1;
+    case FV_HS_GUESS: *x = m.sigma; return 1;
+    case FV_HS_MID: *x = m.cand; return 1;
+    case FV_HS_ITER: {
+      if (fv_fabs(m.fval) <= m.c.tol_price) { fv_hsm_finish(m, FV_IV_CONVERGED, m.sigma); return 0; }
+      // _raw_vega (:40-46) and the d1/d2 of :121-123 share s and d1
+      const double sigma = m.sigma, sqrt_t = m.c.sqrt_t;
+      double s = sigma * sqrt_t;
+      double vega = 0.0, d1 = 0.0;
+      if (!(s < FV_K_1EM12)) {
+        if (m.c.fk_bad) { e.raise(FV_EXC_MATH_DOMAIN); fv_hsm_finish(m, FV_IV_MAX_ITER, nan); return 0; }
+        d1 = (m.c.lnFK + 0.5 * s * s) / s;
+        vega = m.c.disc * m.c.Fw * fv_norm_pdf(d1) * sqrt_t;
+      }
+      double cand = nan;
+      if (vega > 0.0) {
+        double d2 = d1 - s;
+        double vomma = vega * d1 * d2 / sigma;
+        double denom = 2.0 * vega * vega - m.fval * vomma;
+        if (denom != 0.0) cand = sigma - 2.0 * m.fval * vega / denom;
+      }
+      if (fv_isfinite(cand) && m.lo < cand && cand < m.hi) { m.cand = cand; m.state = FV_HS_CHECK; }
+      else { m.cand = 0.5 * (m.lo + m.hi); m.state = FV_HS_MID; }
+      *x = m.cand;
+      return 1;
+    }
+    case FV_HS_BISECT: {
+      if (fv_fabs(m.fval) <= m.c.tol_price || (m.hi - m.lo) <= FV_K_1EM12 * py_max(1.0, m.sigma)) {
+        fv_hsm_finish(m, FV_IV_FELL_BACK, m.sigma); return 0;
+      }
+      m.sigma = 0.5 * (m.lo + m.hi);
+      *x = m.sigma;
+      return 1;
+    }
+  }
+  return 0;
+}
+
+// Consume fx = f(x) for the evaluation decided by fv_hsm_pre.
+FV_HD void fv_hsm_post(FvHalleySM& m, double fx, FvExc& e) {
+  const double nan = __builtin_nan("");
+  if (e.code) { fv_hsm_finish(m, FV_IV_MAX_ITER, nan); return; }
+  switch (m.state) {
+    case FV_HS_LO:                                         // :92-96
+      if (fx >= 0.0) {
+        if (fv_fabs(fx) <= m.c.tol_price) fv_hsm_finish(m, FV_IV_CONVERGED, m.lo);
+        else fv_hsm_finish(m, FV_IV_BELOW_INTRINSIC, nan);
+        return;
+      }
+      m.state = FV_HS_HI;
+      return;
+    case FV_HS_HI:                                         // :97-112
+      if (fx < 0.0 && m.hi < 100.0) { m.hi = py_min(2.0 * m.hi, 100.0); return; }
+      if (fx < 0.0) { fv_hsm_finish(m, FV_IV_MAX_ITER, nan); return; }
+      {
+        double sigma = py_min(py_max(m.guess, FV_K_0P05), 2.0);
+        m.sigma = py_min(py_max(sigma, m.lo), m.hi);
+      }
+      m.state = FV_HS_GUESS;
+      return;
+    case FV_HS_GUESS:                                      // :108-112
+      m.fval = fx;
+      if (fx > 0.0) m.hi = py_min(m.hi, m.sigma);
+      else if (fx < 0.0) m.lo = py_max(m.lo, m.sigma);
+      m.k = 0; m.iterations = 0;
+      m.state = FV_HS_ITER;
+      return;
+    case FV_HS_CHECK:                                      // :129-132
+      if (!(fv_fabs(fx) < fv_fabs(m.fval))) {              // rejected -> f(mid)
+        m.cand = 0.5 * (m.lo + m.hi);
+        m.state = FV_HS_MID;
+        return;
+      }
+      // fall through: accepted
+    case FV_HS_MID: {                                      // :136-144
+      const double cand = m.cand;
+      if (fx > 0.0) m.hi = cand;
+      else if (fx < 0.0) m.lo = cand;
+      double step = cand - m.sigma;
+      m.sigma = cand; m.fval = fx;
+      m.iterations += 1;
+      if (fv_fabs(step) <= FV_K_1EM12 * py_max(1.0, m.sigma)) { fv_hsm_finish(m, FV_IV_CONVERGED, m.sigma); return; }
+      m.k += 1;
+      if (m.k == 16) { m.k = 0; m.state = FV_HS_BISECT; }
+      else m.state = FV_HS_ITER;
+      return;
+    }
+    case FV_HS_BISECT:                                     // :151-161
+      m.fval = fx;
+      if (fx > 0.0) m.hi = m.sigma;
+      else m.lo = m.sigma;
+      m.iterations += 1;
+      m.k += 1;
+      if (m.k == 128) {
+        if (fv_fabs(m.fval) <= m.c.tol_price || (m.hi - m.lo) <= FV_K_1EM12 * py_max(1.0, m.sigma))
+          fv_hsm_finish(m, FV_IV_FELL_BACK, m.sigma);
+        else fv_hsm_finish(m, FV_IV_MAX_ITER, nan);
+      }
+      return;
+  }
+}
+
+// Whole solver for one row through the state machine (host checks, explain).
+FV_HD void fv_halley_row_sm(int model, double th, double un, double K, double t, double r,
+                            double q, double target, int* status, double* sigma, FvExc& e) {
+  FvHalleySM m;
+  if (!fv_hsm_setup(model, th, un, K, t, r, q, target, m, e)) {
+    for (;;) {
+      double x;
+      if (!fv_hsm_pre(m, &x, e)) break;
+      double fx = fv_halley_f(m.c, x, e);
+      fv_hsm_post(m, fx, e);
+      if (m.state == FV_HS_DONE) break;
+    }
+  }
+  *status = m.status;
+  *sigma = (m.status == FV_IV_CONVERGED || m.status == FV_IV_FELL_BACK) ? m.out_sigma : __builtin_nan("");
+}
+
 // ---- lbr.py: normalized Black --------------------------------------------
 // normalized_black (:112-129) for Python-float x (x_work) and s of numpy-ness
 // s_np.  *E (if non-null) receives exp(-(h^2+t^2)/2) -- the factor
 // normalized_vega (:152-156) shares -- computed here when the branch needs it.
+#ifndef FV_NB_INLINE_ERFCX
+#define FV_NB_INLINE_ERFCX 0
+#endif
+#if FV_NB_INLINE_ERFCX
+#define FV_NB_ERFCX(x) fv_erfcx_i(x)
+#else
+#define FV_NB_ERFCX(x) fv_erfcx(x)
+#endif
 struct NbRes { double b; double E; int code; int branch; };
 FV_HDN NbRes fv_normalized_black_impl(double x, double s, bool s_np) {
   NbRes o;
@@ -446,7 +636,7 @@ FV_HDN NbRes fv_normalized_black_impl(double x, double s, bool s_np) {
   if (t < FV_SMALL_T_THRESHOLD) {
     // _small_t_black (:74-103)
     o.branch = 1;
-    double a = 1.0 + h * FV_HALF_SQRT_TWO_PI * fv_erfcx(FV_DIV_SQRT2(-h));
+    double a = 1.0 + h * FV_HALF_SQRT_TWO_PI * FV_NB_ERFCX(FV_DIV_SQRT2(-h));
     double w = t * t;
     double h2 = h * h;
     double c1 = FV_DIV_INT(-1.0 + 3.0 * a + a * h2, 6);
@@ -476,7 +666,7 @@ FV_HDN NbRes fv_normalized_black_impl(double x, double s, bool s_np) {
   o.branch = 3;
   double Ev = fv_exp(-0.5 * (h * h + t * t));
   o.E = Ev;
-  double b = 0.5 * Ev * (fv_erfcx(FV_DIV_SQRT2(-(h + t))) - fv_erfcx(FV_DIV_SQRT2(-(h - t))));
+  double b = 0.5 * Ev * (FV_NB_ERFCX(FV_DIV_SQRT2(-(h + t))) - FV_NB_ERFCX(FV_DIV_SQRT2(-(h - t))));
   o.b = py_max(b, 0.0); o.code = e.code; return o;
 }
 

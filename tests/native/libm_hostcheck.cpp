@@ -48,3 +48,8 @@ int64_t fvh_div_const_check(const double* x, int64_t n) {
   return bad;
 }
 }
+extern "C" {
+ARR1(fvh_erfc_m, fv_erfc_m(v))
+ARR1(fvh_erfc_t11, (fv_erfc_t<true, true>(v)))
+ARR1(fvh_erfc_t01, (fv_erfc_t<false, true>(v)))
+}

@@ -42,11 +42,9 @@ void qh_iv(int model, int method, const int8_t* flag, const double* un, const do
       FvLbrOut o = fv_lbr_batch_row(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], px[i], e);
       iv[i] = o.sigma; status[i] = (int8_t)o.status; region[i] = (int8_t)o.region;
     } else {
-      FvHalleyCtx c; FvHalleyState st; int status_; double sig;
-      int done = fv_halley_phase1(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], px[i],
-                                  c, st, &status_, &sig, e);
-      if (!done) fv_halley_phase2(c, st, &status_, &sig, e);
-      iv[i] = (status_ == FV_IV_CONVERGED || status_ == FV_IV_FELL_BACK) ? sig : __builtin_nan("");
+      int status_; double sig;
+      fv_halley_row_sm(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], px[i], &status_, &sig, e);
+      iv[i] = sig;
       status[i] = (int8_t)status_; region[i] = -1;
     }
     exc[i] = (int8_t)e.code; exc_val[i] = e.val; exc_np[i] = (int8_t)e.np;

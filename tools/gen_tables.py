@@ -249,6 +249,30 @@ def main():
         lines.append("#define FV_ERFC_%s %s" % (name.upper(), hexd(v)))
     lines.append("")
 
+    # erfc tail ranges [1.25, 1/0.35) and [1/0.35, 28) as one table so the
+    # kernel evaluates one shared code path (no lane divergence between the
+    # two): row 0 = ra0..ra7, sa1..sa8 ; row 1 = rb0..rb6, 0, sb1..sb7, 0.
+    # The zero entries turn the missing terms into exact +0 additions.
+    ev = {name: sign * erf_lc[lc] for name, (lc, sign, approx) in ERFC_MAP.items()}
+    tail = ([ev["ra%d" % i] for i in range(8)] + [ev["sa%d" % i] for i in range(1, 9)]
+            + [ev["rb%d" % i] for i in range(7)] + [0.0] + [ev["sb%d" % i] for i in range(1, 8)] + [0.0])
+    lines.append("// fdlibm erfc tail coefficients, two rows of 16 (see tools/gen_tables.py)")
+    emit_array(lines, "double", "fv_erfc_tail", tail, hexd)
+    lines.append("")
+
+    # erfc inner ranges |x| < 0.84375 (pp/qq in u = x^2) and [0.84375, 1.25)
+    # (pa/qa in u = |x| - 1) as one rational form
+    # ((n0 + u n1) + u^2 (n2 + u n3) + u^4 (n4 + u n5)) + u^6 n6 over
+    # ((1 + u d1) + u^2 (d2 + u d3) + u^4 (d4 + u d5)) + u^6 d6, rows of 16:
+    # n0..n6, d1..d6, pad.  Zero entries are exact +0 additions.
+    mid = ([ev["pp%d" % i] for i in range(5)] + [0.0, 0.0] + [ev["qq%d" % i] for i in range(1, 6)] + [0.0]
+           + [0.0, 0.0, 0.0]
+           + [ev["pa%d" % i] for i in range(7)] + [ev["qa%d" % i] for i in range(1, 7)] + [0.0, 0.0, 0.0])
+    assert len(mid) == 32
+    lines.append("// fdlibm erfc inner-range coefficients, two rows of 16 (see tools/gen_tables.py)")
+    emit_array(lines, "double", "fv_erfc_mid", mid, hexd)
+    lines.append("")
+
     # ---- Faddeeva erfcx_y100 Chebyshev table -------------------------------
     cheb = erfcx_table(torch_math_h())
     lines.append("// Faddeeva erfcx_y100: 100 intervals x 7 coefficients (c0..c6),")
