@@ -41,6 +41,9 @@
 #ifndef FV_ANCH_MINB
 #define FV_ANCH_MINB 1
 #endif
+#ifndef FV_NORM_MINB
+#define FV_NORM_MINB 2
+#endif
 #define FV_NSLOT 3
 
 // ---------------------------------------------------------------------------
@@ -286,10 +289,12 @@ __device__ __forceinline__ unsigned int warp_append2(unsigned int* counter, bool
   return base + __popc(m0 & lt) + __popc(m1 & lt);
 }
 
-// Pass 1: validation + normalize_quote + bounds + ATM (small code, one pass
-// over the input columns).  Finished quotes are written out; the rest get
-// (x, beta, sqrt_t) in the state arrays and their row in the pending queue.
-__global__ void __launch_bounds__(256) k_lbr_normalize(KArgs a, LbrQueues lq) {
+// Pass 1: validation + normalize_quote + bounds + ATM + the first anchor
+// (one pass over the input columns).  Finished quotes are written out; the
+// rest get (x, beta, sqrt_t, s_c) in the state arrays, and their row in the
+// far-low queue (beta < b_lo: no further anchor is needed, see
+// fv_lbr_anchor_lo) or in the pending queue with (b_lo, E_lo) for pass 2.
+__global__ void __launch_bounds__(256, FV_NORM_MINB) k_lbr_normalize(KArgs a, LbrQueues lq) {
   const int64_t npair = (a.n + 1) >> 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t nloop = (npair + stride - 1) / stride;
@@ -298,70 +303,77 @@ __global__ void __launch_bounds__(256) k_lbr_normalize(KArgs a, LbrQueues lq) {
     const bool active = j < npair;
     const int64_t i = 2 * j;
     const bool two = active && (i + 1 < a.n);
-    double iv[2] = {0.0, 0.0};
-    int stt[2] = {FV_IV_MAX_ITER, FV_IV_MAX_ITER};
-    bool pend[2] = {false, false};
-    double px_[2], pb_[2], pt_[2];
+    bool pend[2] = {false, false}, flow[2] = {false, false};
     Pair p;
     if (active) load_pair(a, i, two, p);
+    // Each row's results are stored as soon as they exist (8-byte stores: the
+    // pair's two rows fill each sector back to back), so only the pair's
+    // inputs stay live across the row loop -- this keeps the kernel at <= 80
+    // registers with the out-of-line normalized_black call inside.
 #pragma unroll 1
     for (int u = 0; u < 2; ++u) {
       const bool valid = active && (u == 0 || two);
-      bool pending = false;
+      if (!valid) continue;
+      const int64_t row = i + u;
+      bool pending = false, far_low = false;
       double ivu = __builtin_nan("");
       int stu = FV_IV_MAX_ITER;
       FvLbrState st;
-      st.x = 0.0; st.beta = 0.0; st.sqrt_t = 0.0;
-      if (valid) {
-        const int fl = u ? p.fl[1] : p.fl[0];
-        const double un = u ? p.un[1] : p.un[0], k = u ? p.k[1] : p.k[0];
-        const double t = u ? p.t[1] : p.t[0], r = u ? p.r[1] : p.r[0];
-        const double q = u ? p.q[1] : p.q[0], px = u ? p.last[1] : p.last[0];
-        uint32_t bad = row_checks(a, fl, un, k, t, r, q, px);
-        if (bad) {
-          publish_checks(a.st, bad, a.row0 + i + u);
+      st.x = 0.0; st.beta = 0.0; st.sqrt_t = 0.0; st.s_c = 0.0; st.b0 = 0.0; st.E0 = 0.0;
+      const int fl = u ? p.fl[1] : p.fl[0];
+      const double un = u ? p.un[1] : p.un[0], k = u ? p.k[1] : p.k[0];
+      const double t = u ? p.t[1] : p.t[0], r = u ? p.r[1] : p.r[0];
+      const double q = u ? p.q[1] : p.q[0], px = u ? p.last[1] : p.last[0];
+      uint32_t bad = row_checks(a, fl, un, k, t, r, q, px);
+      if (bad) {
+        publish_checks(a.st, bad, a.row0 + row);
+      } else {
+        FvExc e = {0, 0, 0.0};
+        FvLbrOut o;
+        o.sigma = __builtin_nan(""); o.status = FV_IV_MAX_ITER; o.region = -1; o.iterations = 0;
+        double Fw = un;
+        bool done = true;
+        if (a.model != 0) Fw = un * py_exp((r - q) * t, e);     // batch.py:229
+        if (e.code) {
+        } else if (!(t > 0.0)) {
+          o.status = FV_IV_BELOW_INTRINSIC;                      // batch.py:230-236
         } else {
-          FvExc e = {0, 0, 0.0};
-          FvLbrOut o;
-          o.sigma = __builtin_nan(""); o.status = FV_IV_MAX_ITER; o.region = -1; o.iterations = 0;
-          double Fw = un;
-          bool done = true;
-          if (a.model != 0) Fw = un * py_exp((r - q) * t, e);     // batch.py:229
-          if (e.code) {
-          } else if (!(t > 0.0)) {
-            o.status = FV_IV_BELOW_INTRINSIC;                      // batch.py:230-236
-          } else {
-            done = fv_lbr_normalize((double)fl, Fw, k, t, r, px, st, o, e) != 0;
-          }
-          publish_exc(&a.st->exc_first, e.code, a.row0 + i + u);
-          if (done || e.code) {
-            ivu = (o.status == FV_IV_CONVERGED) ? o.sigma : __builtin_nan("");
-            stu = o.status;
-          } else {
-            pending = true;
-          }
+          done = fv_lbr_normalize((double)fl, Fw, k, t, r, px, st, o, e) != 0;
+        }
+        if (!(done || e.code)) {
+          const int cls = fv_lbr_anchor_lo(st, e);      // s_c, b_lo, far-low test
+          if (cls < 0) { o.sigma = __builtin_nan(""); o.status = FV_IV_MAX_ITER; }
+          else if (cls == FV_FAR_LOW) far_low = true;
+          else pending = true;
+        }
+        publish_exc(&a.st->exc_first, e.code, a.row0 + row);
+        if (!(far_low || pending)) {
+          ivu = (o.status == FV_IV_CONVERGED) ? o.sigma : __builtin_nan("");
+          stu = o.status;
         }
       }
-      if (u) { iv[1] = ivu; stt[1] = stu; pend[1] = pending; px_[1] = st.x; pb_[1] = st.beta; pt_[1] = st.sqrt_t; }
-      else { iv[0] = ivu; stt[0] = stu; pend[0] = pending; px_[0] = st.x; pb_[0] = st.beta; pt_[0] = st.sqrt_t; }
+      if (far_low || pending) {
+        lq.sx[row] = st.x; lq.sbeta[row] = st.beta; lq.ssqrt_t[row] = st.sqrt_t; lq.ss_c[row] = st.s_c;
+        if (pending) { lq.sb0[row] = st.b0; lq.sE0[row] = st.E0; }   // read by pass 2
+      }
+      a.o0[row] = ivu;
+      a.status[row] = (int8_t)stu;
+      if (a.region) a.region[row] = (int8_t)(far_low ? FV_FAR_LOW : -1);
+      if (u) { pend[1] = pending; flow[1] = far_low; } else { pend[0] = pending; flow[0] = far_low; }
     }
-    unsigned int slot = warp_append2(lq.count + 3, pend[0], pend[1]);
+    // queue appends in row order (lane 0's pair, lane 1's pair, ...); far-low
+    // entries are 2 * row (the solve's entry format), pending rows plain
+    unsigned int slot = warp_append2(lq.count + 0, flow[0], flow[1]);
+    if (flow[0]) { lq.q[0][slot++] = (int32_t)(2 * i); }
+    if (flow[1]) { lq.q[0][slot] = (int32_t)(2 * (i + 1)); }
+    slot = warp_append2(lq.count + 3, pend[0], pend[1]);
     if (pend[0]) { lq.q[3][slot++] = (int32_t)i; }
     if (pend[1]) { lq.q[3][slot] = (int32_t)(i + 1); }
-    if (active) {
-      // state rows written for every row of the pair (coalesced, full sectors)
-      st2(lq.sx, i, two, true, px_[0], px_[1]);
-      st2(lq.sbeta, i, two, true, pb_[0], pb_[1]);
-      st2(lq.ssqrt_t, i, two, true, pt_[0], pt_[1]);
-      st2(a.o0, i, two, a.out_vec, iv[0], iv[1]);
-      st2i8(a.status, i, two, stt[0], stt[1]);
-      st2i8(a.region, i, two, -1, -1);
-    }
   }
 }
 
-// Pass 2: anchors + region over the pending queue (row order); appends each
-// quote to its region class queue.
+// Pass 2: the remaining anchors + region (fv_lbr_anchor_rest) over the
+// pending queue (row order); appends each quote to its region class queue.
 __global__ void __launch_bounds__(256, FV_ANCH_MINB) k_lbr_anchors(KArgs a, LbrQueues lq) {
   const unsigned int n = lq.count[3];
   const unsigned int stride = gridDim.x * blockDim.x;
@@ -373,23 +385,24 @@ __global__ void __launch_bounds__(256, FV_ANCH_MINB) k_lbr_anchors(KArgs a, LbrQ
     FvLbrState st;
     if (j < n) {
       row = lq.q[3][j];
-      st.x = lq.sx[row]; st.beta = lq.sbeta[row]; st.sqrt_t = lq.ssqrt_t[row];
+      st.x = lq.sx[row]; st.beta = lq.sbeta[row]; st.s_c = lq.ss_c[row];
+      st.b0 = lq.sb0[row]; st.E0 = lq.sE0[row];
       FvExc e = {0, 0, 0.0};
-      FvLbrOut o;
-      o.region = -1;
-      if (fv_lbr_anchors(st, o, e)) {
+      region = fv_lbr_anchor_rest(st, e);
+      if (region < 0) {
         publish_exc(&a.st->exc_first, e.code, a.row0 + row);
         a.o0[row] = __builtin_nan("");
         a.status[row] = (int8_t)FV_IV_MAX_ITER;
       } else {
-        region = o.region;
         cls = region_class(region);
-        lq.ss_c[row] = st.s_c; lq.sb0[row] = st.b0; lq.sb1[row] = st.b1;
-        lq.sE0[row] = st.E0; lq.sE1[row] = st.E1;
+        if (region != FV_FAR_HIGH) {
+          if (region == FV_NEAR_HIGH) { lq.sb0[row] = st.b0; lq.sE0[row] = st.E0; }
+          lq.sb1[row] = st.b1; lq.sE1[row] = st.E1;
+        }
       }
     }
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
+    for (int c = 1; c < 3; ++c) {
       unsigned int slot = warp_append(lq.count + c, cls == c);
       // entry = local row * 2 + near-high bit (the near class holds both)
       if (cls == c) lq.q[c][slot] = (int32_t)(2 * row + (region == FV_NEAR_HIGH ? 1 : 0));

@@ -778,26 +778,49 @@ FV_HD int fv_lbr_normalize(double th, double Fw, double K, double t, double r, d
 }
 
 // anchors (:231-238) + _region (:241-248), computed once (initial_guess
-// recomputes them, :325).  Returns 1 if an exception was raised.
+// recomputes them, :325) and LAZILY: _region compares beta with b_lo, then
+// b_c, then b_hi, and each anchor is needed only if the comparison chain
+// reaches it.  Skipping the ones it does not reach is bit-neutral because the
+// anchors are pure: normalized_black cannot raise for x <= 0 < s (its only
+// raising sites are the x / s, t / h, h / rr divisions, none of which can
+// divide by zero there, and an exp of a non-positive argument), and nothing
+// else in _anchors can raise.  A far-low quote -- the bulk of an OTM chain --
+// therefore costs one normalized_black instead of three.
+//
+// First stage: s_c, b_lo (-> st.b0, st.E0) and the far-low test.  Returns
+// FV_FAR_LOW, FV_NEAR_LOW ("the rest of the chain is needed") or -1 if an
+// exception was raised.
+FV_HD int fv_lbr_anchor_lo(FvLbrState& st, FvExc& e) {
+  const double x = st.x;
+  st.s_c = py_sqrt(2.0 * fv_fabs(x), e);
+  double E_lo = 0.0;
+  st.b0 = fv_normalized_black(x, st.s_c * 0.5, false, e, &E_lo, nullptr);
+  st.E0 = E_lo;
+  if (e.code) return -1;
+  return st.beta < st.b0 ? FV_FAR_LOW : FV_NEAR_LOW;
+}
+// Second stage, for quotes not in the far-low region (st.b0 / st.E0 hold
+// b_lo / E_lo): b_c, then b_hi only if beta >= b_c.  Returns the region (or
+// -1 on an exception) with the anchor pair the solve needs in b0/b1/E0/E1:
+// NEAR_LOW (b_lo, b_c), NEAR_HIGH (b_c, b_hi).
+FV_HD int fv_lbr_anchor_rest(FvLbrState& st, FvExc& e) {
+  const double x = st.x, beta = st.beta, s_c = st.s_c;
+  double E_c = 0.0;
+  const double b_c = fv_normalized_black(x, s_c, false, e, &E_c, nullptr);
+  if (e.code) return -1;
+  if (beta < b_c) { st.b1 = b_c; st.E1 = E_c; return FV_NEAR_LOW; }
+  double E_hi = 0.0;
+  const double b_hi = fv_normalized_black(x, s_c / 0.5, false, e, &E_hi, nullptr);
+  if (e.code) return -1;
+  st.b0 = b_c; st.E0 = E_c; st.b1 = b_hi; st.E1 = E_hi;
+  return beta < b_hi ? FV_NEAR_HIGH : FV_FAR_HIGH;
+}
+// Both stages.  Returns 1 if an exception was raised.
 FV_HD int fv_lbr_anchors(FvLbrState& st, FvLbrOut& o, FvExc& e) {
-  const double x = st.x, beta = st.beta;
-  double s_c = py_sqrt(2.0 * fv_fabs(x), e);
-  double s_lo = s_c * 0.5;
-  double s_hi = s_c / 0.5;
-  double E_lo = 0.0, E_c = 0.0, E_hi = 0.0;
-  double b_lo = fv_normalized_black(x, s_lo, false, e, &E_lo, nullptr);
-  double b_c = fv_normalized_black(x, s_c, false, e, &E_c, nullptr);
-  double b_hi = fv_normalized_black(x, s_hi, false, e, &E_hi, nullptr);
-  if (e.code) return 1;
-  int region;
-  if (beta < b_lo) region = FV_FAR_LOW;
-  else if (beta < b_c) region = FV_NEAR_LOW;
-  else if (beta < b_hi) region = FV_NEAR_HIGH;
-  else region = FV_FAR_HIGH;
+  int region = fv_lbr_anchor_lo(st, e);
+  if (region == FV_NEAR_LOW) region = fv_lbr_anchor_rest(st, e);
+  if (region < 0) return 1;
   o.region = region;
-  st.s_c = s_c;
-  if (region == FV_NEAR_HIGH) { st.b0 = b_c; st.b1 = b_hi; st.E0 = E_c; st.E1 = E_hi; }
-  else { st.b0 = b_lo; st.b1 = b_c; st.E0 = E_lo; st.E1 = E_c; }
   return 0;
 }
 
