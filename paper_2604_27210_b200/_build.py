@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libfastvol_b200.so")
 SOURCES = [os.path.join(CSRC, "fv_kernels.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("fv_quote.h", "fv_libm.h", "fv_tables.h")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("fv_quote.h", "fv_libm.h", "fv_tables.h", "fv_fast.h", "fv_consts.h")] + [
     os.path.join(os.path.dirname(HERE), "include", "fastvol_b200.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -54,6 +54,7 @@ SIGNATURES = {
     "fv_probe_fp64_peak": ([_P, _P], ctypes.c_int),
     "fv_last_outcome": ([_P, _P, _P], ctypes.c_int),
     "fv_selftest_div_const": ([_I64, ctypes.c_uint64, _P], ctypes.c_int),
+    "fv_selftest_fast": ([_I64, ctypes.c_uint64, _P, _P], ctypes.c_int),
 }
 
 

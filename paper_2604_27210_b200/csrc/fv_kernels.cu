@@ -30,7 +30,7 @@
 #include <mutex>
 #include <vector>
 
-#include "fv_quote.h"
+#include "fv_fast.h"
 #include "../../include/fastvol_b200.h"
 
 #define FV_VERSION "fastvol_b200 0.1.0 (sm_100a)"
@@ -43,6 +43,9 @@
 #endif
 #ifndef FV_NORM_MINB
 #define FV_NORM_MINB 2
+#endif
+#ifndef FV_FAST_MINB
+#define FV_FAST_MINB 4
 #endif
 #define FV_NSLOT 3
 
@@ -265,8 +268,9 @@ struct LbrQueues {
   // 32-byte sectors of the fields it touches)
   double* sx;      double* sbeta;  double* ssqrt_t; double* ss_c;
   double* sb0;     double* sb1;    double* sE0;     double* sE1;
-  int32_t* q[4];         // 0..2: local rows per region class; 3: rows pending anchors
-  unsigned int* count;   // [4]
+  int32_t* q[5];         // 0..2: local rows per region class; 3: rows pending anchors;
+                         // 4: far-low rows the straight-line solver handed back
+  unsigned int* count;   // [5]
 };
 
 __device__ __forceinline__ int region_class(int region) {
@@ -411,9 +415,39 @@ __global__ void __launch_bounds__(256, FV_ANCH_MINB) k_lbr_anchors(KArgs a, LbrQ
   }
 }
 
+// Far-low solve on the straight-line fx_* routines (fv_fast.h) over queue 0;
+// a quote that leaves their domain is appended to queue 4 for the careful
+// solver (k_lbr_solve<FV_FAR_LOW>), which recomputes it from scratch.
+__global__ void __launch_bounds__(256, FV_FAST_MINB) k_lbr_far_low_fast(KArgs a, LbrQueues lq) {
+  const unsigned int n = lq.count[0];
+  const int32_t* q = lq.q[0];
+  const unsigned int stride = gridDim.x * blockDim.x;
+  const unsigned int nloop = (n + stride - 1) / stride;
+  for (unsigned int it = 0; it < nloop; ++it) {
+    const unsigned int j = it * stride + blockIdx.x * blockDim.x + threadIdx.x;
+    bool bad = false;
+    int32_t ent = 0;
+    if (j < n) {
+      ent = q[j];
+      const int32_t row = ent >> 1;
+      FvLbrState st;
+      st.x = lq.sx[row]; st.beta = lq.sbeta[row]; st.sqrt_t = lq.ssqrt_t[row]; st.s_c = lq.ss_c[row];
+      st.b0 = st.b1 = st.E0 = st.E1 = 0.0;
+      FvLbrOut o = fx_lbr_far_low(st, bad);
+      if (!bad) {
+        a.o0[row] = (o.status == FV_IV_CONVERGED) ? o.sigma : __builtin_nan("");
+        a.status[row] = (int8_t)o.status;
+      }
+    }
+    const unsigned int slot = warp_append(lq.count + 4, bad);
+    if (bad) lq.q[4][slot] = ent;
+  }
+}
+
 template <int R>
 __global__ void __launch_bounds__(256, FV_SOLVE_MINB) k_lbr_solve(KArgs a, LbrQueues lq) {
-  const int c = R == FV_FAR_LOW ? 0 : (R == FV_FAR_HIGH ? 2 : 1);
+  // far-low: the careful solver over the quotes the straight-line one handed back
+  const int c = R == FV_FAR_LOW ? 4 : (R == FV_FAR_HIGH ? 2 : 1);
   const unsigned int n = lq.count[c];
   const int32_t* q = lq.q[c];
   for (unsigned int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
@@ -625,6 +659,96 @@ __global__ void k_selftest_div_const(int64_t n, uint64_t seed, unsigned long lon
   if (local) atomicAdd(bad, local);
 }
 
+// fx_* (fv_fast.h) against the careful routines on random inputs; counts,
+// per routine, unflagged mismatches and flagged inputs.
+__device__ __forceinline__ double st_uniform(uint64_t u) { return (double)(u >> 11) * 0x1p-53; }
+__device__ __forceinline__ double st_bits(uint64_t u, int e_lo, int e_hi) {
+  // random sign-less mantissa, exponent uniform in [e_lo, e_hi]
+  const int span = e_hi - e_lo + 1;
+  const uint64_t e = (uint64_t)(1023 + e_lo + (int)((u >> 52) % (uint64_t)span));
+  uint64_t m = u & 0x000fffffffffffffull;
+  // every 8th input: mantissa near all-zeros / all-ones (division/rounding edges)
+  if (((u >> 40) & 7) == 0) m = (u & 1) ? (0x000fffffffffffffull - ((u >> 1) & 0xff)) : ((u >> 1) & 0xff);
+  return __longlong_as_double((long long)((e << 52) | m));
+}
+__device__ __forceinline__ bool st_same(double a, double b) {
+  return __double_as_longlong(a) == __double_as_longlong(b) || (a != a && b != b);
+}
+__global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mism, unsigned long long* flg) {
+  unsigned long long lm[7] = {0, 0, 0, 0, 0, 0, 0}, lf[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t u1 = splitmix64(seed + 7919ull * (uint64_t)i);
+    const uint64_t u2 = splitmix64(u1 ^ 0x9e3779b97f4a7c15ull);
+    const uint64_t u3 = splitmix64(u2 + 12345ull);
+    bool bad;
+    // 0: a / b, exponents spanning the whole range (incl. slow-path ones)
+    {
+      const int wide = (int)(u3 & 3) == 0;
+      double a = st_bits(u1, wide ? -1074 + 52 : -600, wide ? 1023 : 600);
+      double b = st_bits(u2, wide ? -1022 : -600, wide ? 1023 : 600);
+      if (u3 & 16) a = -a;
+      if (u3 & 32) b = -b;
+      bad = false;
+      const double f = fx_div(a, b, bad);
+      if (bad) ++lf[0]; else if (!st_same(f, __ddiv_rn(a, b))) ++lm[0];
+    }
+    // 1: exp over [-800, 800] and tiny arguments
+    {
+      double x = ((u3 >> 8) & 3) ? (st_uniform(u1) * 1600.0 - 800.0) : st_bits(u1, -70, 10);
+      if (u3 & 64) x = -x;
+      bad = false;
+      const double f = fx_exp(x, bad);
+      if (bad) ++lf[1]; else if (!st_same(f, fv_exp(x))) ++lm[1];
+    }
+    // 2: log of positives, half of them in [0.5, 2]
+    {
+      const double x = ((u3 >> 10) & 1) ? st_bits(u2, -1, 0) : st_bits(u2, -1000, 1000);
+      bad = false;
+      const double f = fx_log(x, bad);
+      if (bad) ++lf[2]; else if (!st_same(f, fv_log_i(x))) ++lm[2];
+    }
+    // 3: x ** n, n in {2, 3, 4}
+    {
+      const int nn = 2 + (int)((u3 >> 12) % 3);
+      double x = ((u3 >> 14) & 1) ? st_bits(u1 ^ u2, -2, 1) : st_bits(u1 ^ u2, -300, 300);
+      if (u3 & 128) x = -x;
+      bad = false;
+      const double f = fx_powi(x, nn, bad);
+      FvExc e = {0, 0, 0.0};
+      if (bad) ++lf[3]; else if (!st_same(f, py_powi_t<true>(x, nn, false, e)) || e.code) ++lm[3];
+    }
+    // 4: erfcx over [0, 1e8] (log-uniform) and [0, 60] (uniform)
+    {
+      const double x = ((u3 >> 16) & 1) ? st_uniform(u2) * 60.0 : exp10(st_uniform(u2) * 11.0 - 3.0);
+      bad = false;
+      const double f = fx_erfcx_pos(x, bad);
+      if (bad) ++lf[4]; else if (!st_same(f, fv_erfcx_i(x))) ++lm[4];
+    }
+    // 5: normalized_black_log(h, s) on far-low-like arguments
+    {
+      const double s = exp10(st_uniform(u1) * 8.5 - 8.0);
+      const double h = -exp10(st_uniform(u3) * 7.0 - 2.0);
+      bad = false;
+      const double f = fx_nbl_h(h, s, bad);
+      FvExc e = {0, 0, 0.0};
+      const double c = fv_nbl_h<true>(h, s, e);
+      if (bad) ++lf[5]; else if (!st_same(f, c) || e.code) ++lm[5];
+    }
+    // 6: x / sqrt(2) by the constant-division product
+    {
+      const double x = st_bits(u3, -1000, 1000);
+      bad = false;
+      const double f = FX_DIV_SQRT2(x, bad);
+      if (bad) ++lf[6]; else if (!st_same(f, __ddiv_rn(x, FV_DIV_SQRT2_C))) ++lm[6];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    if (lm[k]) atomicAdd(mism + k, lm[k]);
+    if (lf[k]) atomicAdd(flg + k, lf[k]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -651,8 +775,8 @@ struct DevWork {
   ExplainOut* explain = nullptr;
   // LBR classify -> solve workspace (per slot)
   double* lbr_state[FV_NSLOT] = {};     // 8 SoA fields x lbr_cap
-  int32_t* lbr_q[FV_NSLOT] = {};        // 4 queues of lbr_cap entries each
-  unsigned int* lbr_count = nullptr;    // [FV_NSLOT][4]
+  int32_t* lbr_q[FV_NSLOT] = {};        // 5 queues of lbr_cap entries each
+  unsigned int* lbr_count = nullptr;    // [FV_NSLOT][8]
   int64_t lbr_cap[FV_NSLOT] = {};
   int blocks_price = 0, blocks_greeks = 0, blocks_hsm = 0;
   unsigned long long* work_ctr = nullptr;   // [FV_NSLOT]
@@ -660,7 +784,7 @@ struct DevWork {
   HsmRec* hsm_recs[FV_NSLOT] = {};
   int64_t hsm_cap[FV_NSLOT] = {};
   int blocks_hset = 0;
-  int blocks_lbr_norm = 0, blocks_lbr_anch = 0, blocks_lbr_fl = 0, blocks_lbr_near = 0, blocks_lbr_fh = 0;
+  int blocks_lbr_norm = 0, blocks_lbr_anch = 0, blocks_lbr_fast = 0, blocks_lbr_fl = 0, blocks_lbr_near = 0, blocks_lbr_fh = 0;
   std::mutex mu;
 };
 
@@ -691,9 +815,10 @@ cudaError_t get_work(DevWork** out) {
     CK(cudaMalloc(&w->explain, sizeof(ExplainOut)));
     w->blocks_price = occupancy_blocks((const void*)k_price, w->sm_count);
     w->blocks_greeks = occupancy_blocks((const void*)k_price_greeks<true, true>, w->sm_count);
-    CK(cudaMalloc(&w->lbr_count, sizeof(unsigned int) * 4 * FV_NSLOT));
+    CK(cudaMalloc(&w->lbr_count, sizeof(unsigned int) * 8 * FV_NSLOT));
     w->blocks_lbr_norm = occupancy_blocks((const void*)k_lbr_normalize, w->sm_count);
     w->blocks_lbr_anch = occupancy_blocks((const void*)k_lbr_anchors, w->sm_count);
+    w->blocks_lbr_fast = occupancy_blocks((const void*)k_lbr_far_low_fast, w->sm_count);
     w->blocks_lbr_fl = occupancy_blocks((const void*)k_lbr_solve<FV_FAR_LOW>, w->sm_count);
     w->blocks_lbr_near = occupancy_blocks((const void*)k_lbr_solve<FV_NEAR_LOW>, w->sm_count);
     w->blocks_lbr_fh = occupancy_blocks((const void*)k_lbr_solve<FV_FAR_HIGH>, w->sm_count);
@@ -720,7 +845,7 @@ cudaError_t ensure_lbr(DevWork* w, int slot, int64_t rows) {
   w->lbr_cap[slot] = 0;
   int64_t cap = rows < 4096 ? 4096 : ((rows + 255) / 256) * 256;   // keeps every SoA field 16B-aligned
   CK(cudaMalloc(&w->lbr_state[slot], sizeof(double) * 8 * cap));
-  CK(cudaMalloc(&w->lbr_q[slot], sizeof(int32_t) * 4 * cap));
+  CK(cudaMalloc(&w->lbr_q[slot], sizeof(int32_t) * 5 * cap));
   w->lbr_cap[slot] = cap;
   return cudaSuccess;
 }
@@ -804,16 +929,17 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
           const int64_t cp = w->lbr_cap[slot];
           lq.sx = sb; lq.sbeta = sb + cp; lq.ssqrt_t = sb + 2 * cp; lq.ss_c = sb + 3 * cp;
           lq.sb0 = sb + 4 * cp; lq.sb1 = sb + 5 * cp; lq.sE0 = sb + 6 * cp; lq.sE1 = sb + 7 * cp;
-          for (int c3 = 0; c3 < 4; ++c3) lq.q[c3] = w->lbr_q[slot] + c3 * w->lbr_cap[slot];
-          lq.count = w->lbr_count + 4 * slot;
-          CK(cudaMemsetAsync(lq.count, 0, 4 * sizeof(unsigned int), s));
+          for (int c3 = 0; c3 < 5; ++c3) lq.q[c3] = w->lbr_q[slot] + c3 * w->lbr_cap[slot];
+          lq.count = w->lbr_count + 8 * slot;
+          CK(cudaMemsetAsync(lq.count, 0, 8 * sizeof(unsigned int), s));
           k_lbr_normalize<<<blocks_for(w->blocks_lbr_norm, b.n), 256, 0, s>>>(b, lq);
           int64_t cap1 = (b.n + 255) / 256;
           k_lbr_anchors<<<cap1 < w->blocks_lbr_anch ? cap1 : w->blocks_lbr_anch, 256, 0, s>>>(b, lq);
+          k_lbr_far_low_fast<<<cap1 < w->blocks_lbr_fast ? cap1 : w->blocks_lbr_fast, 256, 0, s>>>(b, lq);
           k_lbr_solve<FV_FAR_LOW><<<cap1 < w->blocks_lbr_fl ? cap1 : w->blocks_lbr_fl, 256, 0, s>>>(b, lq);
           k_lbr_solve<FV_NEAR_LOW><<<cap1 < w->blocks_lbr_near ? cap1 : w->blocks_lbr_near, 256, 0, s>>>(b, lq);
           k_lbr_solve<FV_FAR_HIGH><<<cap1 < w->blocks_lbr_fh ? cap1 : w->blocks_lbr_fh, 256, 0, s>>>(b, lq);
-          t_launches += 5;
+          t_launches += 6;
         }
       } else {
         CK(ensure_hsm(w, slot, a.n));
@@ -1340,6 +1466,19 @@ FV_API int fv_selftest_div_const(int64_t n, uint64_t seed, int64_t* mismatches) 
   cudaFree(d);
   if (ce != cudaSuccess) return FV_ERR_CUDA;
   *mismatches = (int64_t)h;
+  return FV_OK;
+}
+
+FV_API int fv_selftest_fast(int64_t n, uint64_t seed, int64_t* mismatches, int64_t* flagged) {
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, sizeof(*d) * 14) != cudaSuccess) return FV_ERR_CUDA;
+  cudaMemset(d, 0, sizeof(*d) * 14);
+  k_selftest_fast<<<148 * 8, 256>>>(n, seed, d, d + 7);
+  unsigned long long h[14];
+  cudaError_t ce = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (ce != cudaSuccess) return FV_ERR_CUDA;
+  for (int k = 0; k < 7; ++k) { mismatches[k] = (int64_t)h[k]; flagged[k] = (int64_t)h[7 + k]; }
   return FV_OK;
 }
 

@@ -43,7 +43,7 @@
 #include "fv_tables.h"
 #undef FV_TABLE
 #if defined(__CUDACC__)
-#define FV_TABLE(type, name, n) static __device__ const type name##_d[n]
+#define FV_TABLE(type, name, n) static __device__ const type __align__(16) name##_d[n]
 #include "fv_tables.h"
 #undef FV_TABLE
 #endif

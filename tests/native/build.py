@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 OUT = os.path.join(HERE, "_build")
 FLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
 DEPS = [os.path.join(HERE, "..", "..", "paper_2604_27210_b200", "csrc", f)
-        for f in ("fv_libm.h", "fv_quote.h", "fv_tables.h", "fv_consts.h")]
+        for f in ("fv_libm.h", "fv_quote.h", "fv_tables.h", "fv_consts.h", "fv_fast.h")]
 
 
 def build(name):

@@ -2,7 +2,7 @@
 // code) for CPU pre-checks against the oracle / golden fixtures.  Test
 // infrastructure only: the product runs the CUDA build of the same header.
 // Build: g++ -O2 -ffp-contract=off -fno-fast-math -shared -fPIC
-#include "../../paper_2604_27210_b200/csrc/fv_quote.h"
+#include "../../paper_2604_27210_b200/csrc/fv_fast.h"
 
 extern "C" {
 
@@ -80,6 +80,35 @@ int64_t qh_far_low_fused_check(const int8_t* flag, const double* F, const double
     if (!same) ++bad;
   }
   *nfar = nf;
+  return bad;
+}
+
+// The straight-line far-low solver (fv_fast.h) against the careful one on the
+// far-low quotes of a batch: returns mismatching unflagged rows; *nflag gets
+// the flagged (handed-back) ones.
+int64_t qh_far_low_fast_check(const int8_t* flag, const double* F, const double* k,
+                              const double* t, const double* r, const double* px, int64_t n,
+                              int64_t* nfar, int64_t* nflag) {
+  int64_t bad = 0, nf = 0, nb = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    FvExc e = {0, 0, 0.0};
+    FvLbrState st; FvLbrOut o;
+    if (!(t[i] > 0.0)) continue;
+    if (fv_lbr_classify((double)flag[i], F[i], k[i], t[i], r[i], px[i], st, o, e)) continue;
+    if (o.region != FV_FAR_LOW) continue;
+    ++nf;
+    FvExc e2 = {0, 0, 0.0};
+    bool flagged = false;
+    FvLbrOut a = fx_lbr_far_low(st, flagged);
+    FvLbrOut b = fv_lbr_far_low_fused(st, e2);
+    if (flagged) { ++nb; continue; }
+    uint64_t ua, ub; memcpy(&ua, &a.sigma, 8); memcpy(&ub, &b.sigma, 8);
+    bool same = (ua == ub || (a.sigma != a.sigma && b.sigma != b.sigma)) && a.status == b.status &&
+                a.iterations == b.iterations && e2.code == 0;
+    if (!same) ++bad;
+  }
+  *nfar = nf;
+  *nflag = nb;
   return bad;
 }
 }

@@ -2,6 +2,7 @@
 pointers) against the golden fixtures from the live reference and against the
 CPU oracle on larger seeded workloads.  Bit-exact everywhere: IV values and NaN
 masks, statuses, LBR regions, prices, Greeks, exception rows, BatchErrors."""
+import ctypes
 import glob
 import json
 import os
@@ -294,6 +295,22 @@ def test_device_constant_division_is_ieee(fv):
     bad = ctypes.c_int64(-1)
     assert lib.fv_selftest_div_const(200_000_000, 2024, ctypes.byref(bad)) == 0
     assert bad.value == 0
+
+
+def test_fast_routines_match_careful_forms():
+    """fv_fast.h: every unflagged result of the straight-line routines equals
+    the careful routine bit for bit (and the flagged share stays small)."""
+    from paper_2604_27210_b200 import _native
+    lib = _native.lib_for_compute()
+    mism = (ctypes.c_int64 * 7)()
+    flg = (ctypes.c_int64 * 7)()
+    n = 100_000_000
+    assert lib.fv_selftest_fast(n, 77, mism, flg) == 0
+    names = ["div", "exp", "log", "pow", "erfcx", "nbl", "div_sqrt2"]
+    print({k: (mism[i], flg[i]) for i, k in enumerate(names)})
+    assert list(mism) == [0] * 7, {k: mism[i] for i, k in enumerate(names)}
+    # the flagged share is what the test inputs put outside the main paths
+    assert flg[4] < n // 4 and flg[5] < n // 2
 
 
 def test_sharded_single_rank_equals_batch(fv):

@@ -134,3 +134,25 @@ def test_fused_far_low_matches_reference_order(Q):
     nf = ctypes.c_int64(0)
     bad = Q.qh_far_low_fused_check(*[_p(c) for c in cols], ctypes.c_int64(len(flag)), ctypes.byref(nf))
     assert nf.value > 30_000 and bad == 0
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_straight_line_far_low_matches_careful(Q, seed):
+    """fv_fast.h's far-low solver, host build: every quote it does not hand
+    back to the careful solver is bit-identical to it (sigma, status,
+    iterations), on C1-like draws and on the C4 chain."""
+    from oracle import fvoracle as O
+    from paper_2604_27210_b200 import workloads as W
+    Q.qh_far_low_fast_check.restype = ctypes.c_int64
+    if seed == 3:
+        flag, S, K, t, r, q, sig = W.chain_draws(100_000, seed=seed)
+    else:
+        import bench
+        flag, S, K, t, r, sig, _ = bench.cpu_sample_c4(100_000)
+    px = O.rows_price("black", flag, S, K, t, r, 0.0, sig)["price"]
+    cols = [np.ascontiguousarray(a) for a in (flag, S, K, t, r, px)]
+    nf, nb = ctypes.c_int64(0), ctypes.c_int64(0)
+    bad = Q.qh_far_low_fast_check(*[_p(c) for c in cols], ctypes.c_int64(len(flag)),
+                                  ctypes.byref(nf), ctypes.byref(nb))
+    assert nf.value > 30_000 and bad == 0
+    assert nb.value < nf.value // 100, (nb.value, nf.value)

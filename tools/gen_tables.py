@@ -279,6 +279,13 @@ def main():
     lines.append("// t = 2*y100 - (2k+1), value = c0 + (c1 + (... + c6*t)*t)*t")
     emit_array(lines, "double", "fv_erfcx_tab", cheb, hexd, per_line=7)
     lines.append("")
+    # the same rows padded to 8 (64-byte rows): four 16-byte loads per lookup
+    cheb8 = []
+    for k in range(100):
+        cheb8 += list(cheb[7 * k:7 * k + 7]) + [0.0]
+    lines.append("// fv_erfcx_tab padded to 8 per row (c0..c6, 0) for 16-byte loads")
+    emit_array(lines, "double", "fv_erfcx_tab8", cheb8, hexd, per_line=8)
+    lines.append("")
 
     # ---- fastvol constants --------------------------------------------------
     import math
