@@ -171,12 +171,13 @@ FV_API int fv_last_outcome(int64_t* check_rows /*[FV_NCHECK]*/, int64_t* exc_row
 FV_API int fv_selftest_div_const(int64_t n, uint64_t seed, int64_t* mismatches);
 
 /* Self-test of the straight-line routines of the far-low solver (fv_fast.h)
- * against their careful forms on n random inputs each, for 7 routines
- * (division, exp, log, pow, erfcx, normalized_black_log, constant division):
+ * against their careful forms on n random inputs each, for 9 routines
+ * (division, exp, log, pow, erfcx, normalized_black_log, constant division,
+ * sqrt, two-path log):
  * per routine, the inputs whose result differs although the routine did not
  * flag them (must be 0) and the inputs it flagged for the careful path. */
-FV_API int fv_selftest_fast(int64_t n, uint64_t seed, int64_t* mismatches /*[7]*/,
-                            int64_t* flagged /*[7]*/);
+FV_API int fv_selftest_fast(int64_t n, uint64_t seed, int64_t* mismatches /*[9]*/,
+                            int64_t* flagged /*[9]*/);
 
 /* Diagnostics: measured DFMA instruction rate of the current device (the
  * FP64-pipe roofline denominator for this path). */

@@ -42,7 +42,7 @@
 #define FV_ANCH_MINB 1
 #endif
 #ifndef FV_NORM_MINB
-#define FV_NORM_MINB 2
+#define FV_NORM_MINB 3
 #endif
 #ifndef FV_FAST_MINB
 #define FV_FAST_MINB 4
@@ -268,9 +268,10 @@ struct LbrQueues {
   // 32-byte sectors of the fields it touches)
   double* sx;      double* sbeta;  double* ssqrt_t; double* ss_c;
   double* sb0;     double* sb1;    double* sE0;     double* sE1;
-  int32_t* q[5];         // 0..2: local rows per region class; 3: rows pending anchors;
-                         // 4: far-low rows the straight-line solver handed back
-  unsigned int* count;   // [5]
+  int32_t* q[6];         // 0..2: local rows per region class; 3: rows pending anchors;
+                         // 4: far-low rows the straight-line solver handed back;
+                         // 5: rows the straight-line normalize pass handed back
+  unsigned int* count;   // [6]
 };
 
 __device__ __forceinline__ int region_class(int region) {
@@ -293,11 +294,59 @@ __device__ __forceinline__ unsigned int warp_append2(unsigned int* counter, bool
   return base + __popc(m0 & lt) + __popc(m1 & lt);
 }
 
-// Pass 1: validation + normalize_quote + bounds + ATM + the first anchor
-// (one pass over the input columns).  Finished quotes are written out; the
-// rest get (x, beta, sqrt_t, s_c) in the state arrays, and their row in the
-// far-low queue (beta < b_lo: no further anchor is needed, see
-// fv_lbr_anchor_lo) or in the pending queue with (b_lo, E_lo) for pass 2.
+// One row of pass 1 on the careful routines (fv_quote.h): normalize_quote +
+// bounds + ATM + the first anchor, outputs and state written, *far_low /
+// *pending say which queue the row belongs in.  Validation is the caller's.
+__device__ __forceinline__ void lbr_norm_row_careful(const KArgs& a, const LbrQueues& lq, int64_t row,
+                                                     int fl, double un, double k, double t, double r,
+                                                     double q, double px, bool* far_low_out,
+                                                     bool* pending_out) {
+  bool pending = false, far_low = false;
+  double ivu = __builtin_nan("");
+  int stu = FV_IV_MAX_ITER;
+  FvLbrState st;
+  st.x = 0.0; st.beta = 0.0; st.sqrt_t = 0.0; st.s_c = 0.0; st.b0 = 0.0; st.E0 = 0.0;
+  FvExc e = {0, 0, 0.0};
+  FvLbrOut o;
+  o.sigma = __builtin_nan(""); o.status = FV_IV_MAX_ITER; o.region = -1; o.iterations = 0;
+  double Fw = un;
+  bool done = true;
+  if (a.model != 0) Fw = un * py_exp((r - q) * t, e);     // batch.py:229
+  if (e.code) {
+  } else if (!(t > 0.0)) {
+    o.status = FV_IV_BELOW_INTRINSIC;                      // batch.py:230-236
+  } else {
+    done = fv_lbr_normalize((double)fl, Fw, k, t, r, px, st, o, e) != 0;
+  }
+  if (!(done || e.code)) {
+    const int cls = fv_lbr_anchor_lo(st, e);      // s_c, b_lo, far-low test
+    if (cls < 0) { o.sigma = __builtin_nan(""); o.status = FV_IV_MAX_ITER; }
+    else if (cls == FV_FAR_LOW) far_low = true;
+    else pending = true;
+  }
+  publish_exc(&a.st->exc_first, e.code, a.row0 + row);
+  if (!(far_low || pending)) {
+    ivu = (o.status == FV_IV_CONVERGED) ? o.sigma : __builtin_nan("");
+    stu = o.status;
+  }
+  if (far_low || pending) {
+    lq.sx[row] = st.x; lq.sbeta[row] = st.beta; lq.ssqrt_t[row] = st.sqrt_t; lq.ss_c[row] = st.s_c;
+    if (pending) { lq.sb0[row] = st.b0; lq.sE0[row] = st.E0; }   // read by pass 2
+  }
+  a.o0[row] = ivu;
+  a.status[row] = (int8_t)stu;
+  if (a.region) a.region[row] = (int8_t)(far_low ? FV_FAR_LOW : -1);
+  *far_low_out = far_low;
+  *pending_out = pending;
+}
+
+// Pass 1: validation + normalize_quote + bounds + the first anchor (one pass
+// over the input columns), on the straight-line routines (fv_fast.h).
+// Finished quotes are written out; the rest get (x, beta, sqrt_t, s_c) in the
+// state arrays and their row in the far-low queue (beta < b_lo: no further
+// anchor is needed, see fv_lbr_anchor_lo) or in the pending queue with (b_lo,
+// E_lo) for pass 2.  Rows the straight-line routines flag (ATM shortcut,
+// exceptions, range edges) go to queue 5 for k_lbr_normalize_replay.
 __global__ void __launch_bounds__(256, FV_NORM_MINB) k_lbr_normalize(KArgs a, LbrQueues lq) {
   const int64_t npair = (a.n + 1) >> 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -307,19 +356,15 @@ __global__ void __launch_bounds__(256, FV_NORM_MINB) k_lbr_normalize(KArgs a, Lb
     const bool active = j < npair;
     const int64_t i = 2 * j;
     const bool two = active && (i + 1 < a.n);
-    bool pend[2] = {false, false}, flow[2] = {false, false};
+    bool pend[2] = {false, false}, flow[2] = {false, false}, rep[2] = {false, false};
     Pair p;
     if (active) load_pair(a, i, two, p);
-    // Each row's results are stored as soon as they exist (8-byte stores: the
-    // pair's two rows fill each sector back to back), so only the pair's
-    // inputs stay live across the row loop -- this keeps the kernel at <= 80
-    // registers with the out-of-line normalized_black call inside.
 #pragma unroll 1
     for (int u = 0; u < 2; ++u) {
       const bool valid = active && (u == 0 || two);
       if (!valid) continue;
       const int64_t row = i + u;
-      bool pending = false, far_low = false;
+      bool pending = false, far_low = false, flagged = false;
       double ivu = __builtin_nan("");
       int stu = FV_IV_MAX_ITER;
       FvLbrState st;
@@ -328,51 +373,71 @@ __global__ void __launch_bounds__(256, FV_NORM_MINB) k_lbr_normalize(KArgs a, Lb
       const double un = u ? p.un[1] : p.un[0], k = u ? p.k[1] : p.k[0];
       const double t = u ? p.t[1] : p.t[0], r = u ? p.r[1] : p.r[0];
       const double q = u ? p.q[1] : p.q[0], px = u ? p.last[1] : p.last[0];
-      uint32_t bad = row_checks(a, fl, un, k, t, r, q, px);
-      if (bad) {
-        publish_checks(a.st, bad, a.row0 + row);
+      uint32_t badc = row_checks(a, fl, un, k, t, r, q, px);
+      if (badc) {
+        publish_checks(a.st, badc, a.row0 + row);
       } else {
-        FvExc e = {0, 0, 0.0};
         FvLbrOut o;
-        o.sigma = __builtin_nan(""); o.status = FV_IV_MAX_ITER; o.region = -1; o.iterations = 0;
-        double Fw = un;
-        bool done = true;
-        if (a.model != 0) Fw = un * py_exp((r - q) * t, e);     // batch.py:229
-        if (e.code) {
-        } else if (!(t > 0.0)) {
-          o.status = FV_IV_BELOW_INTRINSIC;                      // batch.py:230-236
-        } else {
-          done = fv_lbr_normalize((double)fl, Fw, k, t, r, px, st, o, e) != 0;
-        }
-        if (!(done || e.code)) {
-          const int cls = fv_lbr_anchor_lo(st, e);      // s_c, b_lo, far-low test
-          if (cls < 0) { o.sigma = __builtin_nan(""); o.status = FV_IV_MAX_ITER; }
-          else if (cls == FV_FAR_LOW) far_low = true;
-          else pending = true;
-        }
-        publish_exc(&a.st->exc_first, e.code, a.row0 + row);
-        if (!(far_low || pending)) {
-          ivu = (o.status == FV_IV_CONVERGED) ? o.sigma : __builtin_nan("");
-          stu = o.status;
+        const int cls = fx_lbr_classify_lo(a.model, (double)fl, un, k, t, r, q, px, st, o, flagged);
+        if (!flagged) {
+          if (cls == FV_FAR_LOW) far_low = true;
+          else if (cls == FV_NEAR_LOW) pending = true;
+          else { ivu = (o.status == FV_IV_CONVERGED) ? o.sigma : __builtin_nan(""); stu = o.status; }
         }
       }
       if (far_low || pending) {
         lq.sx[row] = st.x; lq.sbeta[row] = st.beta; lq.ssqrt_t[row] = st.sqrt_t; lq.ss_c[row] = st.s_c;
         if (pending) { lq.sb0[row] = st.b0; lq.sE0[row] = st.E0; }   // read by pass 2
       }
-      a.o0[row] = ivu;
-      a.status[row] = (int8_t)stu;
-      if (a.region) a.region[row] = (int8_t)(far_low ? FV_FAR_LOW : -1);
-      if (u) { pend[1] = pending; flow[1] = far_low; } else { pend[0] = pending; flow[0] = far_low; }
+      if (!flagged) {
+        a.o0[row] = ivu;
+        a.status[row] = (int8_t)stu;
+        if (a.region) a.region[row] = (int8_t)(far_low ? FV_FAR_LOW : -1);
+      }
+      if (u) { pend[1] = pending; flow[1] = far_low; rep[1] = flagged; }
+      else { pend[0] = pending; flow[0] = far_low; rep[0] = flagged; }
     }
     // queue appends in row order (lane 0's pair, lane 1's pair, ...); far-low
-    // entries are 2 * row (the solve's entry format), pending rows plain
+    // entries are 2 * row (the solve's entry format), the others plain rows
     unsigned int slot = warp_append2(lq.count + 0, flow[0], flow[1]);
     if (flow[0]) { lq.q[0][slot++] = (int32_t)(2 * i); }
     if (flow[1]) { lq.q[0][slot] = (int32_t)(2 * (i + 1)); }
     slot = warp_append2(lq.count + 3, pend[0], pend[1]);
     if (pend[0]) { lq.q[3][slot++] = (int32_t)i; }
     if (pend[1]) { lq.q[3][slot] = (int32_t)(i + 1); }
+    if (__any_sync(0xffffffffu, rep[0] || rep[1])) {
+      slot = warp_append2(lq.count + 5, rep[0], rep[1]);
+      if (rep[0]) { lq.q[5][slot++] = (int32_t)i; }
+      if (rep[1]) { lq.q[5][slot] = (int32_t)(i + 1); }
+    }
+  }
+}
+
+__device__ __forceinline__ double ld1(const DCol& c, int64_t i) {
+  return c.mode == 0 ? __ldg(c.p) : __ldg(c.p + i * c.stride);
+}
+__device__ __forceinline__ int ldf1(const DFlag& c, int64_t i) {
+  return c.mode == 0 ? c.p[0] : c.p[i * c.stride];
+}
+
+// Pass 1b: the rows pass 1 flagged, on the careful routines.
+__global__ void __launch_bounds__(256) k_lbr_normalize_replay(KArgs a, LbrQueues lq) {
+  const unsigned int n = lq.count[5];
+  const unsigned int stride = gridDim.x * blockDim.x;
+  const unsigned int nloop = (n + stride - 1) / stride;
+  for (unsigned int it = 0; it < nloop; ++it) {
+    const unsigned int j = it * stride + blockIdx.x * blockDim.x + threadIdx.x;
+    bool far_low = false, pending = false;
+    int32_t row = 0;
+    if (j < n) {
+      row = lq.q[5][j];
+      lbr_norm_row_careful(a, lq, row, ldf1(a.flag, row), ld1(a.un, row), ld1(a.k, row), ld1(a.t, row),
+                           ld1(a.r, row), ld1(a.q, row), ld1(a.last, row), &far_low, &pending);
+    }
+    unsigned int slot = warp_append(lq.count + 0, far_low);
+    if (far_low) lq.q[0][slot] = 2 * row;
+    slot = warp_append(lq.count + 3, pending);
+    if (pending) lq.q[3][slot] = row;
   }
 }
 
@@ -674,8 +739,9 @@ __device__ __forceinline__ double st_bits(uint64_t u, int e_lo, int e_hi) {
 __device__ __forceinline__ bool st_same(double a, double b) {
   return __double_as_longlong(a) == __double_as_longlong(b) || (a != a && b != b);
 }
+#define FX_NTEST 9
 __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mism, unsigned long long* flg) {
-  unsigned long long lm[7] = {0, 0, 0, 0, 0, 0, 0}, lf[7] = {0, 0, 0, 0, 0, 0, 0};
+  unsigned long long lm[FX_NTEST] = {}, lf[FX_NTEST] = {};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t u1 = splitmix64(seed + 7919ull * (uint64_t)i);
     const uint64_t u2 = splitmix64(u1 ^ 0x9e3779b97f4a7c15ull);
@@ -741,9 +807,24 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
       const double f = FX_DIV_SQRT2(x, bad);
       if (bad) ++lf[6]; else if (!st_same(f, __ddiv_rn(x, FV_DIV_SQRT2_C))) ++lm[6];
     }
+    // 7: sqrt over the whole positive range (and some negatives)
+    {
+      double x = st_bits(u1 ^ u3, -1074 + 52, 1023);
+      if ((u2 & 63) == 0) x = -x;
+      bad = false;
+      const double f = fx_sqrt(x, bad);
+      if (bad) ++lf[7]; else if (!st_same(f, __dsqrt_rn(x))) ++lm[7];
+    }
+    // 8: log, both paths (half of the inputs within 2^-4 of 1)
+    {
+      const double x = ((u3 >> 20) & 1) ? 1.0 + (st_uniform(u2) - 0.5) * 0.13 : st_bits(u2 ^ u3, -1000, 1000);
+      bad = false;
+      const double f = fx_log_any(x, bad);
+      if (bad) ++lf[8]; else if (!st_same(f, fv_log_i(x))) ++lm[8];
+    }
   }
 #pragma unroll
-  for (int k = 0; k < 7; ++k) {
+  for (int k = 0; k < FX_NTEST; ++k) {
     if (lm[k]) atomicAdd(mism + k, lm[k]);
     if (lf[k]) atomicAdd(flg + k, lf[k]);
   }
@@ -775,7 +856,7 @@ struct DevWork {
   ExplainOut* explain = nullptr;
   // LBR classify -> solve workspace (per slot)
   double* lbr_state[FV_NSLOT] = {};     // 8 SoA fields x lbr_cap
-  int32_t* lbr_q[FV_NSLOT] = {};        // 5 queues of lbr_cap entries each
+  int32_t* lbr_q[FV_NSLOT] = {};        // 6 queues of lbr_cap entries each
   unsigned int* lbr_count = nullptr;    // [FV_NSLOT][8]
   int64_t lbr_cap[FV_NSLOT] = {};
   int blocks_price = 0, blocks_greeks = 0, blocks_hsm = 0;
@@ -784,7 +865,7 @@ struct DevWork {
   HsmRec* hsm_recs[FV_NSLOT] = {};
   int64_t hsm_cap[FV_NSLOT] = {};
   int blocks_hset = 0;
-  int blocks_lbr_norm = 0, blocks_lbr_anch = 0, blocks_lbr_fast = 0, blocks_lbr_fl = 0, blocks_lbr_near = 0, blocks_lbr_fh = 0;
+  int blocks_lbr_norm = 0, blocks_lbr_nrep = 0, blocks_lbr_anch = 0, blocks_lbr_fast = 0, blocks_lbr_fl = 0, blocks_lbr_near = 0, blocks_lbr_fh = 0;
   std::mutex mu;
 };
 
@@ -817,6 +898,7 @@ cudaError_t get_work(DevWork** out) {
     w->blocks_greeks = occupancy_blocks((const void*)k_price_greeks<true, true>, w->sm_count);
     CK(cudaMalloc(&w->lbr_count, sizeof(unsigned int) * 8 * FV_NSLOT));
     w->blocks_lbr_norm = occupancy_blocks((const void*)k_lbr_normalize, w->sm_count);
+    w->blocks_lbr_nrep = occupancy_blocks((const void*)k_lbr_normalize_replay, w->sm_count);
     w->blocks_lbr_anch = occupancy_blocks((const void*)k_lbr_anchors, w->sm_count);
     w->blocks_lbr_fast = occupancy_blocks((const void*)k_lbr_far_low_fast, w->sm_count);
     w->blocks_lbr_fl = occupancy_blocks((const void*)k_lbr_solve<FV_FAR_LOW>, w->sm_count);
@@ -845,7 +927,7 @@ cudaError_t ensure_lbr(DevWork* w, int slot, int64_t rows) {
   w->lbr_cap[slot] = 0;
   int64_t cap = rows < 4096 ? 4096 : ((rows + 255) / 256) * 256;   // keeps every SoA field 16B-aligned
   CK(cudaMalloc(&w->lbr_state[slot], sizeof(double) * 8 * cap));
-  CK(cudaMalloc(&w->lbr_q[slot], sizeof(int32_t) * 5 * cap));
+  CK(cudaMalloc(&w->lbr_q[slot], sizeof(int32_t) * 6 * cap));
   w->lbr_cap[slot] = cap;
   return cudaSuccess;
 }
@@ -929,17 +1011,18 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
           const int64_t cp = w->lbr_cap[slot];
           lq.sx = sb; lq.sbeta = sb + cp; lq.ssqrt_t = sb + 2 * cp; lq.ss_c = sb + 3 * cp;
           lq.sb0 = sb + 4 * cp; lq.sb1 = sb + 5 * cp; lq.sE0 = sb + 6 * cp; lq.sE1 = sb + 7 * cp;
-          for (int c3 = 0; c3 < 5; ++c3) lq.q[c3] = w->lbr_q[slot] + c3 * w->lbr_cap[slot];
+          for (int c3 = 0; c3 < 6; ++c3) lq.q[c3] = w->lbr_q[slot] + c3 * w->lbr_cap[slot];
           lq.count = w->lbr_count + 8 * slot;
           CK(cudaMemsetAsync(lq.count, 0, 8 * sizeof(unsigned int), s));
           k_lbr_normalize<<<blocks_for(w->blocks_lbr_norm, b.n), 256, 0, s>>>(b, lq);
           int64_t cap1 = (b.n + 255) / 256;
+          k_lbr_normalize_replay<<<cap1 < w->blocks_lbr_nrep ? cap1 : w->blocks_lbr_nrep, 256, 0, s>>>(b, lq);
           k_lbr_anchors<<<cap1 < w->blocks_lbr_anch ? cap1 : w->blocks_lbr_anch, 256, 0, s>>>(b, lq);
           k_lbr_far_low_fast<<<cap1 < w->blocks_lbr_fast ? cap1 : w->blocks_lbr_fast, 256, 0, s>>>(b, lq);
           k_lbr_solve<FV_FAR_LOW><<<cap1 < w->blocks_lbr_fl ? cap1 : w->blocks_lbr_fl, 256, 0, s>>>(b, lq);
           k_lbr_solve<FV_NEAR_LOW><<<cap1 < w->blocks_lbr_near ? cap1 : w->blocks_lbr_near, 256, 0, s>>>(b, lq);
           k_lbr_solve<FV_FAR_HIGH><<<cap1 < w->blocks_lbr_fh ? cap1 : w->blocks_lbr_fh, 256, 0, s>>>(b, lq);
-          t_launches += 6;
+          t_launches += 7;
         }
       } else {
         CK(ensure_hsm(w, slot, a.n));
@@ -1471,14 +1554,14 @@ FV_API int fv_selftest_div_const(int64_t n, uint64_t seed, int64_t* mismatches) 
 
 FV_API int fv_selftest_fast(int64_t n, uint64_t seed, int64_t* mismatches, int64_t* flagged) {
   unsigned long long* d = nullptr;
-  if (cudaMalloc(&d, sizeof(*d) * 14) != cudaSuccess) return FV_ERR_CUDA;
-  cudaMemset(d, 0, sizeof(*d) * 14);
-  k_selftest_fast<<<148 * 8, 256>>>(n, seed, d, d + 7);
-  unsigned long long h[14];
+  if (cudaMalloc(&d, sizeof(*d) * 2 * FX_NTEST) != cudaSuccess) return FV_ERR_CUDA;
+  cudaMemset(d, 0, sizeof(*d) * 2 * FX_NTEST);
+  k_selftest_fast<<<148 * 8, 256>>>(n, seed, d, d + FX_NTEST);
+  unsigned long long h[2 * FX_NTEST];
   cudaError_t ce = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   cudaFree(d);
   if (ce != cudaSuccess) return FV_ERR_CUDA;
-  for (int k = 0; k < 7; ++k) { mismatches[k] = (int64_t)h[k]; flagged[k] = (int64_t)h[7 + k]; }
+  for (int k = 0; k < FX_NTEST; ++k) { mismatches[k] = (int64_t)h[k]; flagged[k] = (int64_t)h[FX_NTEST + k]; }
   return FV_OK;
 }
 
@@ -1519,3 +1602,4 @@ FV_API int fv_probe_fp64_peak(double* dfma_per_s, double* seconds) {
 }
 
 }  // extern "C"
+

@@ -83,6 +83,51 @@ int64_t qh_far_low_fused_check(const int8_t* flag, const double* F, const double
   return bad;
 }
 
+// The straight-line first pass (fx_lbr_classify_lo) against the careful one
+// (batch.py fill's forward + fv_lbr_normalize + fv_lbr_anchor_lo): returns
+// mismatching unflagged rows; *nflag gets the flagged ones.
+int64_t qh_classify_fast_check(int model, const int8_t* flag, const double* un, const double* k,
+                               const double* t, const double* r, const double* q, const double* px,
+                               int64_t n, int64_t* nflag) {
+  int64_t bad = 0, nb = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    bool flagged = false;
+    FvLbrState sf; FvLbrOut of;
+    sf.x = sf.beta = sf.sqrt_t = sf.s_c = sf.b0 = sf.E0 = 0.0;
+    const int cf = fx_lbr_classify_lo(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], px[i], sf, of, flagged);
+    if (flagged) { ++nb; continue; }
+    // careful
+    FvExc e = {0, 0, 0.0};
+    FvLbrState sc; FvLbrOut oc;
+    sc.x = sc.beta = sc.sqrt_t = sc.s_c = sc.b0 = sc.E0 = 0.0;
+    oc.sigma = __builtin_nan(""); oc.status = FV_IV_MAX_ITER;
+    double Fw = un[i];
+    bool done = true;
+    if (model != 0) Fw = un[i] * py_exp((r[i] - q[i]) * t[i], e);
+    if (e.code) {
+    } else if (!(t[i] > 0.0)) {
+      oc.status = FV_IV_BELOW_INTRINSIC;
+    } else {
+      done = fv_lbr_normalize((double)flag[i], Fw, k[i], t[i], r[i], px[i], sc, oc, e) != 0;
+    }
+    int cc = FV_REGION_NONE;
+    if (!(done || e.code)) cc = fv_lbr_anchor_lo(sc, e);
+    if (e.code) { ++bad; continue; }                 // unflagged but the careful path raises
+    bool same = cf == cc;
+    if (same && cc == FV_REGION_NONE) {
+      uint64_t ua, ub; memcpy(&ua, &of.sigma, 8); memcpy(&ub, &oc.sigma, 8);
+      same = of.status == oc.status && (oc.status != FV_IV_CONVERGED || ua == ub);
+    } else if (same) {
+      const double fa[6] = {sf.x, sf.beta, sf.sqrt_t, sf.s_c, sf.b0, sf.E0};
+      const double ca[6] = {sc.x, sc.beta, sc.sqrt_t, sc.s_c, sc.b0, sc.E0};
+      same = memcmp(fa, ca, sizeof(fa)) == 0;
+    }
+    if (!same) ++bad;
+  }
+  *nflag = nb;
+  return bad;
+}
+
 // The straight-line far-low solver (fv_fast.h) against the careful one on the
 // far-low quotes of a batch: returns mismatching unflagged rows; *nflag gets
 // the flagged (handed-back) ones.

@@ -302,13 +302,13 @@ def test_fast_routines_match_careful_forms():
     the careful routine bit for bit (and the flagged share stays small)."""
     from paper_2604_27210_b200 import _native
     lib = _native.lib_for_compute()
-    mism = (ctypes.c_int64 * 7)()
-    flg = (ctypes.c_int64 * 7)()
+    names = ["div", "exp", "log", "pow", "erfcx", "nbl", "div_sqrt2", "sqrt", "log2"]
+    mism = (ctypes.c_int64 * len(names))()
+    flg = (ctypes.c_int64 * len(names))()
     n = 100_000_000
     assert lib.fv_selftest_fast(n, 77, mism, flg) == 0
-    names = ["div", "exp", "log", "pow", "erfcx", "nbl", "div_sqrt2"]
     print({k: (mism[i], flg[i]) for i, k in enumerate(names)})
-    assert list(mism) == [0] * 7, {k: mism[i] for i, k in enumerate(names)}
+    assert list(mism) == [0] * len(names), {k: mism[i] for i, k in enumerate(names)}
     # the flagged share is what the test inputs put outside the main paths
     assert flg[4] < n // 4 and flg[5] < n // 2
 

@@ -156,3 +156,38 @@ def test_straight_line_far_low_matches_careful(Q, seed):
                                   ctypes.byref(nf), ctypes.byref(nb))
     assert nf.value > 30_000 and bad == 0
     assert nb.value < nf.value // 100, (nb.value, nf.value)
+
+
+@pytest.mark.parametrize("case", ["c1", "c4", "c5", "bsm"])
+def test_straight_line_classify_matches_careful(Q, case):
+    """fv_fast.h's first pass (normalize_quote, bounds, first anchor, far-low
+    test): every row it does not flag reproduces the careful pass exactly
+    (classification, outputs of finished rows, the state handed on)."""
+    from paper_2604_27210_b200 import workloads as W
+    from oracle import fvoracle as O
+    Q.qh_classify_fast_check.restype = ctypes.c_int64
+    model, q = 0, None
+    if case == "c1":
+        flag, S, K, t, r, q, sig = W.chain_draws(100_000, seed=11)
+        q = np.zeros_like(S)
+        px = O.rows_price("black", flag, S, K, t, r, 0.0, sig)["price"]
+    elif case == "bsm":
+        flag, S, K, t, r, q, sig = W.chain_draws(100_000, seed=12)
+        model = 2
+        px = O.rows_price("bsm", flag, S, K, t, r, q, sig)["price"]
+    elif case == "c4":
+        import bench
+        flag, S, K, t, r, sig, _ = bench.cpu_sample_c4(100_000)
+        q = np.zeros_like(S)
+        px = O.rows_price("black", flag, S, K, t, r, 0.0, sig)["price"]
+    else:
+        flag, S, K, t, r, sig, kind, side = W.c5_params(100_000, seed=5)
+        q = np.zeros_like(S)
+        px0 = O.rows_price("black", flag, S, K, t, r, 0.0, sig)["price"]
+        px = W.c5_prices(flag, S, K, t, r, kind, side, px0)
+    cols = [np.ascontiguousarray(a) for a in (flag, S, K, t, r, q, px)]
+    nb = ctypes.c_int64(0)
+    bad = Q.qh_classify_fast_check(ctypes.c_int(model), *[_p(c) for c in cols], ctypes.c_int64(len(flag)),
+                                   ctypes.byref(nb))
+    assert bad == 0
+    assert nb.value < len(flag) // 20, nb.value
