@@ -755,7 +755,9 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
       if (u3 & 16) a = -a;
       if (u3 & 32) b = -b;
       bad = false;
-      const double f = fx_div(a, b, bad);
+      const bool z = (u3 & 0xf00) == 0;             // 1/16: zero numerators through fx_div0
+      if (z) a = (u3 & 16) ? -0.0 : 0.0;
+      const double f = z ? fx_div0(a, b, bad) : fx_div(a, b, bad);
       if (bad) ++lf[0]; else if (!st_same(f, __ddiv_rn(a, b))) ++lm[0];
     }
     // 1: exp over [-800, 800] and tiny arguments
