@@ -373,6 +373,24 @@ def run_ours(args):
     ms_step = total_ms / args.steps
     value = world * n / (ms_step * 1e-3)
 
+    # ---- per-kernel split of a step (CUDA events around each launch, on the
+    # launching stream; a separate pass so the headline timing has no events)
+    kernels = None
+    try:
+        lib.fv_set_kernel_timing(1)
+        _native.kernel_times(lib)
+        nk = max(1, min(args.steps, 3))
+        for _ in range(nk):
+            step()
+        torch.cuda.synchronize(dev)
+        kt = _native.kernel_times(lib)
+        lib.fv_set_kernel_timing(0)
+        tot = sum(v[0] for v in kt.values()) or 1.0
+        kernels = {k: {"ms_per_step": v[0] / nk, "launches_per_step": v[1] / nk, "share": v[0] / tot}
+                   for k, v in sorted(kt.items(), key=lambda kv: -kv[1][0])}
+    except Exception as exc:  # noqa: BLE001
+        kernels = {"error": repr(exc)}
+
     # ---- status mix of the solved chain (for the record) --------------------
     st = torch.bincount(out_st.to(torch.int64) + 0, minlength=5).cpu().tolist()
 
@@ -436,11 +454,15 @@ def run_ours(args):
     except (OSError, ValueError):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    # DRAM bytes (read + write) per launch of the call, from the committed
+    # `ncu --set full` capture (profiles/roofline_traffic.json: bytes per
+    # quote summed over the call's kernels) scaled to this launch's rows
     traffic = None
     try:
         prof = json.load(open(os.path.join(REPO, "profiles", "roofline_traffic.json")))
-        traffic = prof.get(args.workload)
-    except (OSError, ValueError):
+        bpq = prof.get(args.workload, {}).get("dram_bytes_per_quote")
+        traffic = bpq * n if bpq else None
+    except (OSError, ValueError, AttributeError):
         pass
 
     if rank == 0:
@@ -467,8 +489,12 @@ def run_ours(args):
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_tops,
                          "unit": "T weighted-fp64-ops/s", "frac": achieved / peak_tops if peak_tops else None,
                          "traffic": traffic,
-                         "note": "achieved = W=%.0f weighted distinct fp64 ops/quote (SURVEY 8(d)) x quotes/s per GPU; "
-                                 "peak = measured DFMA issue rate (fv_probe_fp64_peak, this run)" % W_OPS[args.workload]},
+                         "note": "kernel = one fv_batch_iv/fv_price_greeks call (its kernels in sequence on one "
+                                 "stream); achieved = W=%.0f weighted distinct fp64 ops/quote (SURVEY 8(d)) x rows per "
+                                 "call / mean call duration (CUDA events on the launching stream); peak = measured "
+                                 "DFMA issue rate (fv_probe_fp64_peak, this run); traffic = ncu DRAM read+write bytes "
+                                 "per call (profiles/roofline_traffic.json)" % W_OPS[args.workload]},
+            "kernels": kernels,
             "roofline_hbm": {"bound": "hbm", "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": hbm_gbs / hbm_peak, "bytes_per_quote": (in_bytes + out_bytes) / n,
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs"},

@@ -171,13 +171,34 @@ FV_API int fv_last_outcome(int64_t* check_rows /*[FV_NCHECK]*/, int64_t* exc_row
 FV_API int fv_selftest_div_const(int64_t n, uint64_t seed, int64_t* mismatches);
 
 /* Self-test of the straight-line routines of the far-low solver (fv_fast.h)
- * against their careful forms on n random inputs each, for 9 routines
+ * against their careful forms on n random inputs each, for 10 routines
  * (division, exp, log, pow, erfcx, normalized_black_log, constant division,
- * sqrt, two-path log):
+ * sqrt, two-path log, erfc):
  * per routine, the inputs whose result differs although the routine did not
  * flag them (must be 0) and the inputs it flagged for the careful path. */
-FV_API int fv_selftest_fast(int64_t n, uint64_t seed, int64_t* mismatches /*[9]*/,
-                            int64_t* flagged /*[9]*/);
+FV_API int fv_selftest_fast(int64_t n, uint64_t seed, int64_t* mismatches /*[10]*/,
+                            int64_t* flagged /*[10]*/);
+
+/* Per-kernel timing (diagnostics; off by default).  While on, every kernel
+ * the calling thread launches is bracketed by CUDA events on its stream;
+ * fv_kernel_times sums the elapsed milliseconds and launch counts per kernel
+ * (FV_KID_* order, names from fv_kernel_name) since the previous call and
+ * resets them. */
+#define FV_KID_PRICE 0
+#define FV_KID_PRICE_GREEKS 1
+#define FV_KID_LBR_NORM 2
+#define FV_KID_LBR_NREP 3
+#define FV_KID_LBR_ANCH 4
+#define FV_KID_LBR_FAST 5
+#define FV_KID_LBR_FL 6
+#define FV_KID_LBR_NEAR 7
+#define FV_KID_LBR_FH 8
+#define FV_KID_HALLEY_SETUP 9
+#define FV_KID_HALLEY_SM 10
+#define FV_NKERNEL 11
+FV_API int fv_set_kernel_timing(int on);
+FV_API int fv_kernel_times(double* ms /*[FV_NKERNEL]*/, int64_t* launches /*[FV_NKERNEL]*/);
+FV_API const char* fv_kernel_name(int id);
 
 /* Diagnostics: measured DFMA instruction rate of the current device (the
  * FP64-pipe roofline denominator for this path). */

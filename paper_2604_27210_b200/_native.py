@@ -55,6 +55,9 @@ SIGNATURES = {
     "fv_last_outcome": ([_P, _P, _P], ctypes.c_int),
     "fv_selftest_div_const": ([_I64, ctypes.c_uint64, _P], ctypes.c_int),
     "fv_selftest_fast": ([_I64, ctypes.c_uint64, _P, _P], ctypes.c_int),
+    "fv_set_kernel_timing": ([ctypes.c_int], ctypes.c_int),
+    "fv_kernel_times": ([_P, _P], ctypes.c_int),
+    "fv_kernel_name": ([ctypes.c_int], ctypes.c_char_p),
 }
 
 
@@ -111,3 +114,16 @@ def last_outcome(lib):
     ec = np.empty(2, np.int32)
     lib.fv_last_outcome(cr.ctypes.data, er.ctypes.data, ec.ctypes.data)
     return cr, er, ec
+
+
+NKERNEL = 11
+
+
+def kernel_times(lib):
+    """{kernel name: (ms, launches)} accumulated since the last call
+    (fv_set_kernel_timing must have been on)."""
+    ms = (ctypes.c_double * NKERNEL)()
+    ln = (ctypes.c_int64 * NKERNEL)()
+    if lib.fv_kernel_times(ms, ln) != 0:
+        raise RuntimeError("fv_kernel_times failed")
+    return {lib.fv_kernel_name(k).decode(): (ms[k], ln[k]) for k in range(NKERNEL) if ln[k]}

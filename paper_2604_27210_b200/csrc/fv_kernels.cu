@@ -44,6 +44,9 @@
 #ifndef FV_NORM_MINB
 #define FV_NORM_MINB 3
 #endif
+#ifndef FV_PG_MINB
+#define FV_PG_MINB 2
+#endif
 #ifndef FV_FAST_MINB
 #define FV_FAST_MINB 4
 #endif
@@ -185,7 +188,29 @@ __device__ __forceinline__ void load_pair(const KArgs& a, int64_t i, bool two, P
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_price(KArgs a) {
+// Careful rows (fv_quote.h) for the rows the straight-line forms flag; out of
+// line so the kernels keep the fast path's small footprint.
+__device__ __noinline__ double price_row_careful(const KArgs& a, int64_t row, int fl, double un, double k,
+                                                 double t, double r, double q, double sig) {
+  FvExc e = {0, 0, 0.0};
+  const double v = fv_price_row(a.model, (double)fl, un, k, t, r, q, sig, e);
+  publish_exc(&a.st->exc_first, e.code, a.row0 + row);
+  return v;
+}
+template <bool kPrice, bool kGreeks>
+__device__ __noinline__ FvGreeks price_greeks_row_careful(const KArgs& a, int64_t row, int fl, double un,
+                                                          double k, double t, double r, double q, double sig) {
+  FvExc ep = {0, 0, 0.0}, eg = {0, 0, 0.0};
+  FvGreeks g = fv_price_greeks_row(a.model, (double)fl, un, k, t, r, q, sig, kPrice, kGreeks, ep, eg);
+  if (kPrice) publish_exc(&a.st->exc_first, ep.code, a.row0 + row);
+  if (kGreeks) publish_exc(&a.st->exc2_first, eg.code, a.row0 + row);
+  return g;
+}
+
+// Pricing (batch_price): straight-line row (fx_price_row), careful row where
+// it flags.  Inputs of a pair are picked with selects (no local-memory
+// arrays); 16-byte loads and stores of the pair.
+__global__ void __launch_bounds__(256, FV_PG_MINB) k_price(KArgs a) {
   const int64_t npair = (a.n + 1) >> 1;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair;
        j += (int64_t)gridDim.x * blockDim.x) {
@@ -193,22 +218,33 @@ __global__ void __launch_bounds__(256) k_price(KArgs a) {
     const bool two = i + 1 < a.n;
     Pair p;
     load_pair(a, i, two, p);
-    double out[2] = {0.0, 0.0};
+    double out0 = 0.0, out1 = 0.0;
 #pragma unroll 1
     for (int u = 0; u < (two ? 2 : 1); ++u) {
-      uint32_t bad = row_checks(a, p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u], p.q[u], p.last[u]);
-      if (bad) { publish_checks(a.st, bad, a.row0 + i + u); out[u] = __builtin_nan(""); continue; }
-      FvExc e = {0, 0, 0.0};
-      out[u] = fv_price_row(a.model, (double)p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u], p.q[u],
-                            p.last[u], e);
-      publish_exc(&a.st->exc_first, e.code, a.row0 + i + u);
+      const int fl = u ? p.fl[1] : p.fl[0];
+      const double un = u ? p.un[1] : p.un[0], k = u ? p.k[1] : p.k[0];
+      const double t = u ? p.t[1] : p.t[0], r = u ? p.r[1] : p.r[0];
+      const double q = u ? p.q[1] : p.q[0], sg = u ? p.last[1] : p.last[0];
+      double v;
+      uint32_t bad = row_checks(a, fl, un, k, t, r, q, sg);
+      if (bad) {
+        publish_checks(a.st, bad, a.row0 + i + u);
+        v = __builtin_nan("");
+      } else {
+        bool flagged = false;
+        v = fx_price_row(a.model, (double)fl, un, k, t, r, q, sg, flagged);
+        if (flagged) v = price_row_careful(a, i + u, fl, un, k, t, r, q, sg);
+      }
+      if (u) out1 = v; else out0 = v;
     }
-    st2(a.o0, i, two, a.out_vec, out[0], out[1]);
+    st2(a.o0, i, two, a.out_vec, out0, out1);
   }
 }
 
+// Fused price + Greeks (batch_price and/or batch_greeks in one pass):
+// straight-line row (fx_price_greeks_row), careful row where it flags.
 template <bool kPrice, bool kGreeks>
-__global__ void __launch_bounds__(256) k_price_greeks(KArgs a) {
+__global__ void __launch_bounds__(256, FV_PG_MINB) k_price_greeks(KArgs a) {
   const int64_t npair = (a.n + 1) >> 1;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair;
        j += (int64_t)gridDim.x * blockDim.x) {
@@ -216,31 +252,35 @@ __global__ void __launch_bounds__(256) k_price_greeks(KArgs a) {
     const bool two = i + 1 < a.n;
     Pair p;
     load_pair(a, i, two, p);
-    FvGreeks g[2];
+    FvGreeks g0, g1;
 #pragma unroll 1
     for (int u = 0; u < (two ? 2 : 1); ++u) {
-      uint32_t bad = row_checks(a, p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u], p.q[u], p.last[u]);
+      const int fl = u ? p.fl[1] : p.fl[0];
+      const double un = u ? p.un[1] : p.un[0], k = u ? p.k[1] : p.k[0];
+      const double t = u ? p.t[1] : p.t[0], r = u ? p.r[1] : p.r[0];
+      const double q = u ? p.q[1] : p.q[0], sg = u ? p.last[1] : p.last[0];
+      FvGreeks g;
+      uint32_t bad = row_checks(a, fl, un, k, t, r, q, sg);
       if (bad) {
         publish_checks(a.st, bad, a.row0 + i + u);
-        g[u].price = g[u].delta = g[u].gamma = g[u].theta = g[u].rho = g[u].vega = __builtin_nan("");
-        g[u].status = 0;
-        continue;
+        g.price = g.delta = g.gamma = g.theta = g.rho = g.vega = __builtin_nan("");
+        g.status = 0;
+      } else {
+        bool flagged = false;
+        g = fx_price_greeks_row(a.model, (double)fl, un, k, t, r, q, sg, kGreeks, flagged);
+        if (flagged) g = price_greeks_row_careful<kPrice, kGreeks>(a, i + u, fl, un, k, t, r, q, sg);
       }
-      FvExc ep = {0, 0, 0.0}, eg = {0, 0, 0.0};
-      g[u] = fv_price_greeks_row(a.model, (double)p.fl[u], p.un[u], p.k[u], p.t[u], p.r[u],
-                                 p.q[u], p.last[u], kPrice, kGreeks, ep, eg);
-      if (kPrice) publish_exc(&a.st->exc_first, ep.code, a.row0 + i + u);
-      if (kGreeks) publish_exc(&a.st->exc2_first, eg.code, a.row0 + i + u);
+      if (u) g1 = g; else g0 = g;
     }
-    if (!two) g[1] = g[0];
-    if (kPrice) st2(a.o0, i, two, a.out_vec, g[0].price, g[1].price);
+    if (!two) g1 = g0;
+    if (kPrice) st2(a.o0, i, two, a.out_vec, g0.price, g1.price);
     if (kGreeks) {
-      st2(a.o1, i, two, a.out_vec, g[0].delta, g[1].delta);
-      st2(a.o2, i, two, a.out_vec, g[0].gamma, g[1].gamma);
-      st2(a.o3, i, two, a.out_vec, g[0].theta, g[1].theta);
-      st2(a.o4, i, two, a.out_vec, g[0].rho, g[1].rho);
-      st2(a.o5, i, two, a.out_vec, g[0].vega, g[1].vega);
-      st2i8(a.status, i, two, g[0].status, g[1].status);
+      st2(a.o1, i, two, a.out_vec, g0.delta, g1.delta);
+      st2(a.o2, i, two, a.out_vec, g0.gamma, g1.gamma);
+      st2(a.o3, i, two, a.out_vec, g0.theta, g1.theta);
+      st2(a.o4, i, two, a.out_vec, g0.rho, g1.rho);
+      st2(a.o5, i, two, a.out_vec, g0.vega, g1.vega);
+      st2i8(a.status, i, two, g0.status, g1.status);
     }
   }
 }
@@ -739,7 +779,7 @@ __device__ __forceinline__ double st_bits(uint64_t u, int e_lo, int e_hi) {
 __device__ __forceinline__ bool st_same(double a, double b) {
   return __double_as_longlong(a) == __double_as_longlong(b) || (a != a && b != b);
 }
-#define FX_NTEST 9
+#define FX_NTEST 10
 __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mism, unsigned long long* flg) {
   unsigned long long lm[FX_NTEST] = {}, lf[FX_NTEST] = {};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -817,6 +857,14 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
       const double f = fx_sqrt(x, bad);
       if (bad) ++lf[7]; else if (!st_same(f, __dsqrt_rn(x))) ++lm[7];
     }
+    // 9: erfc over [-30, 30] (and a few wider)
+    {
+      double x = st_uniform(u1 ^ (u3 << 7)) * 60.0 - 30.0;
+      if ((u2 & 15) == 0) x = st_bits(u2, -60, 8) * ((u2 & 16) ? -1.0 : 1.0);
+      bad = false;
+      const double f = fx_erfc(x, bad);
+      if (bad) ++lf[9]; else if (!st_same(f, fv_erfc(x))) ++lm[9];
+    }
     // 8: log, both paths (half of the inputs within 2^-4 of 1)
     {
       const double x = ((u3 >> 20) & 1) ? 1.0 + (st_uniform(u2) - 0.5) * 0.13 : st_bits(u2 ^ u3, -1000, 1000);
@@ -839,6 +887,30 @@ namespace {
 
 thread_local cudaStream_t t_user_stream = nullptr;
 thread_local int64_t t_launches = 0;
+
+// Optional per-kernel timing (fv_set_kernel_timing): CUDA events around every
+// launch on the launching stream, summed per kernel by fv_kernel_times.
+const char* const kKernelNames[FV_NKERNEL] = {
+    "k_price", "k_price_greeks", "k_lbr_normalize", "k_lbr_normalize_replay", "k_lbr_anchors",
+    "k_lbr_far_low_fast", "k_lbr_solve<FAR_LOW>", "k_lbr_solve<NEAR>", "k_lbr_solve<FAR_HIGH>",
+    "k_halley_setup", "k_halley_sm"};
+struct TimedLaunch { int id; cudaEvent_t a, b; };
+thread_local bool t_timing = false;
+thread_local std::vector<TimedLaunch> t_timed;
+inline void time_begin(int id, cudaStream_t s) {
+  if (!t_timing) return;
+  TimedLaunch tl;
+  tl.id = id;
+  cudaEventCreate(&tl.a);
+  cudaEventCreate(&tl.b);
+  cudaEventRecord(tl.a, s);
+  t_timed.push_back(tl);
+}
+inline void time_end(cudaStream_t s) {
+  if (!t_timing || t_timed.empty()) return;
+  cudaEventRecord(t_timed.back().b, s);
+}
+#define FV_LAUNCH(id, s, ...) do { time_begin((id), (s)); __VA_ARGS__; time_end(s); ++t_launches; } while (0)
 // raw outcome of this thread's last call (for sharded callers that merge
 // the first-failure rows of several shards)
 thread_local int64_t t_check_rows[FV_NCHECK];
@@ -986,21 +1058,18 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
   if (a.n <= 0) return cudaSuccess;
   switch (c.kind) {
     case KIND_PRICE:
-      k_price<<<blocks_for(w->blocks_price, a.n), 256, 0, s>>>(a);
-      ++t_launches;
+      FV_LAUNCH(FV_KID_PRICE, s, k_price<<<blocks_for(w->blocks_price, a.n), 256, 0, s>>>(a));
       break;
     case KIND_GREEKS:
-      k_price_greeks<false, true><<<blocks_for(w->blocks_greeks, a.n), 256, 0, s>>>(a);
-      ++t_launches;
+      FV_LAUNCH(FV_KID_PRICE_GREEKS, s, k_price_greeks<false, true><<<blocks_for(w->blocks_greeks, a.n), 256, 0, s>>>(a));
       break;
     case KIND_PRICE_GREEKS:
       if (c.want_price && c.want_greeks)
-        k_price_greeks<true, true><<<blocks_for(w->blocks_greeks, a.n), 256, 0, s>>>(a);
+        FV_LAUNCH(FV_KID_PRICE_GREEKS, s, k_price_greeks<true, true><<<blocks_for(w->blocks_greeks, a.n), 256, 0, s>>>(a));
       else if (c.want_greeks)
-        k_price_greeks<false, true><<<blocks_for(w->blocks_greeks, a.n), 256, 0, s>>>(a);
+        FV_LAUNCH(FV_KID_PRICE_GREEKS, s, k_price_greeks<false, true><<<blocks_for(w->blocks_greeks, a.n), 256, 0, s>>>(a));
       else
-        k_price_greeks<true, false><<<blocks_for(w->blocks_greeks, a.n), 256, 0, s>>>(a);
-      ++t_launches;
+        FV_LAUNCH(FV_KID_PRICE_GREEKS, s, k_price_greeks<true, false><<<blocks_for(w->blocks_greeks, a.n), 256, 0, s>>>(a));
       break;
     case KIND_IV:
       if (c.method == FV_METHOD_LBR) {
@@ -1016,15 +1085,15 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
           for (int c3 = 0; c3 < 6; ++c3) lq.q[c3] = w->lbr_q[slot] + c3 * w->lbr_cap[slot];
           lq.count = w->lbr_count + 8 * slot;
           CK(cudaMemsetAsync(lq.count, 0, 8 * sizeof(unsigned int), s));
-          k_lbr_normalize<<<blocks_for(w->blocks_lbr_norm, b.n), 256, 0, s>>>(b, lq);
-          int64_t cap1 = (b.n + 255) / 256;
-          k_lbr_normalize_replay<<<cap1 < w->blocks_lbr_nrep ? cap1 : w->blocks_lbr_nrep, 256, 0, s>>>(b, lq);
-          k_lbr_anchors<<<cap1 < w->blocks_lbr_anch ? cap1 : w->blocks_lbr_anch, 256, 0, s>>>(b, lq);
-          k_lbr_far_low_fast<<<cap1 < w->blocks_lbr_fast ? cap1 : w->blocks_lbr_fast, 256, 0, s>>>(b, lq);
-          k_lbr_solve<FV_FAR_LOW><<<cap1 < w->blocks_lbr_fl ? cap1 : w->blocks_lbr_fl, 256, 0, s>>>(b, lq);
-          k_lbr_solve<FV_NEAR_LOW><<<cap1 < w->blocks_lbr_near ? cap1 : w->blocks_lbr_near, 256, 0, s>>>(b, lq);
-          k_lbr_solve<FV_FAR_HIGH><<<cap1 < w->blocks_lbr_fh ? cap1 : w->blocks_lbr_fh, 256, 0, s>>>(b, lq);
-          t_launches += 7;
+          const int64_t cap1 = (b.n + 255) / 256;
+          auto g = [cap1](int blocks) { return (int)(cap1 < blocks ? cap1 : blocks); };
+          FV_LAUNCH(FV_KID_LBR_NORM, s, k_lbr_normalize<<<blocks_for(w->blocks_lbr_norm, b.n), 256, 0, s>>>(b, lq));
+          FV_LAUNCH(FV_KID_LBR_NREP, s, k_lbr_normalize_replay<<<g(w->blocks_lbr_nrep), 256, 0, s>>>(b, lq));
+          FV_LAUNCH(FV_KID_LBR_ANCH, s, k_lbr_anchors<<<g(w->blocks_lbr_anch), 256, 0, s>>>(b, lq));
+          FV_LAUNCH(FV_KID_LBR_FAST, s, k_lbr_far_low_fast<<<g(w->blocks_lbr_fast), 256, 0, s>>>(b, lq));
+          FV_LAUNCH(FV_KID_LBR_FL, s, k_lbr_solve<FV_FAR_LOW><<<g(w->blocks_lbr_fl), 256, 0, s>>>(b, lq));
+          FV_LAUNCH(FV_KID_LBR_NEAR, s, k_lbr_solve<FV_NEAR_LOW><<<g(w->blocks_lbr_near), 256, 0, s>>>(b, lq));
+          FV_LAUNCH(FV_KID_LBR_FH, s, k_lbr_solve<FV_FAR_HIGH><<<g(w->blocks_lbr_fh), 256, 0, s>>>(b, lq));
         }
       } else {
         CK(ensure_hsm(w, slot, a.n));
@@ -1032,10 +1101,9 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
         unsigned int* cnt = w->hsm_count + slot;
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s));
         CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned int), s));
-        k_halley_setup<<<blocks_for(w->blocks_hset, a.n), 256, 0, s>>>(a, w->hsm_recs[slot], cnt);
+        FV_LAUNCH(FV_KID_HALLEY_SETUP, s, k_halley_setup<<<blocks_for(w->blocks_hset, a.n), 256, 0, s>>>(a, w->hsm_recs[slot], cnt));
         int64_t need = (a.n + 255) / 256;
-        k_halley_sm<<<need < w->blocks_hsm ? need : w->blocks_hsm, 256, 0, s>>>(a, w->hsm_recs[slot], cnt, ctr);
-        t_launches += 2;
+        FV_LAUNCH(FV_KID_HALLEY_SM, s, k_halley_sm<<<need < w->blocks_hsm ? need : w->blocks_hsm, 256, 0, s>>>(a, w->hsm_recs[slot], cnt, ctr));
       }
       break;
   }
@@ -1540,6 +1608,31 @@ FV_API int fv_set_chunk_rows(int64_t rows) {
 }
 
 FV_API int64_t fv_last_launch_count(void) { return t_launches; }
+
+FV_API int fv_set_kernel_timing(int on) {
+  t_timing = on != 0;
+  return FV_OK;
+}
+
+FV_API int fv_kernel_times(double* ms, int64_t* launches) {
+  for (int k = 0; k < FV_NKERNEL; ++k) { ms[k] = 0.0; launches[k] = 0; }
+  int rc = FV_OK;
+  for (TimedLaunch& tl : t_timed) {
+    float e = 0.0f;
+    if (cudaEventSynchronize(tl.b) != cudaSuccess || cudaEventElapsedTime(&e, tl.a, tl.b) != cudaSuccess)
+      rc = FV_ERR_CUDA;
+    ms[tl.id] += e;
+    launches[tl.id] += 1;
+    cudaEventDestroy(tl.a);
+    cudaEventDestroy(tl.b);
+  }
+  t_timed.clear();
+  return rc;
+}
+
+FV_API const char* fv_kernel_name(int id) {
+  return (id >= 0 && id < FV_NKERNEL) ? kKernelNames[id] : "";
+}
 
 FV_API int fv_selftest_div_const(int64_t n, uint64_t seed, int64_t* mismatches) {
   unsigned long long* d = nullptr;

@@ -128,6 +128,33 @@ int64_t qh_classify_fast_check(int model, const int8_t* flag, const double* un, 
   return bad;
 }
 
+// Straight-line price / fused price+Greeks rows against the careful rows:
+// mismatching unflagged rows (any output bit, status, or a careful-path
+// exception); *nflag gets the flagged ones.
+int64_t qh_price_greeks_fast_check(int model, const int8_t* flag, const double* un, const double* k,
+                                   const double* t, const double* r, const double* q, const double* sg,
+                                   int64_t n, int64_t* nflag) {
+  int64_t bad = 0, nb = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    bool f1 = false, f2 = false;
+    const double pf = fx_price_row(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], sg[i], f1);
+    const FvGreeks gf = fx_price_greeks_row(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], sg[i], true, f2);
+    if (f1 || f2) { ++nb; }
+    FvExc e = {0, 0, 0.0}, ep = {0, 0, 0.0}, eg = {0, 0, 0.0};
+    const double pc = fv_price_row(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], sg[i], e);
+    const FvGreeks gc = fv_price_greeks_row(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], sg[i],
+                                            true, true, ep, eg);
+    if (!f1 && (memcmp(&pf, &pc, 8) != 0 || e.code)) ++bad;
+    if (!f2) {
+      const double a[6] = {gf.price, gf.delta, gf.gamma, gf.theta, gf.rho, gf.vega};
+      const double b[6] = {gc.price, gc.delta, gc.gamma, gc.theta, gc.rho, gc.vega};
+      if (memcmp(a, b, sizeof(a)) != 0 || gf.status != gc.status || ep.code || eg.code) ++bad;
+    }
+  }
+  *nflag = nb;
+  return bad;
+}
+
 // The straight-line far-low solver (fv_fast.h) against the careful one on the
 // far-low quotes of a batch: returns mismatching unflagged rows; *nflag gets
 // the flagged (handed-back) ones.

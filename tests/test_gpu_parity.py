@@ -254,6 +254,42 @@ def test_c5_wings_vs_oracle(fv, oracle_mod):
         assert_bits(iv, want["iv"], f"C5 {method} iv")
 
 
+@pytest.mark.parametrize("model", ["black", "bs", "bsm"])
+def test_c3_price_greeks_vs_oracle(fv, oracle_mod, model):
+    """C3-like rows plus wings (deep ITM/OTM, tiny/long maturities, tiny vols),
+    fused price + Greeks on the device vs the oracle, bit for bit."""
+    import torch
+    from paper_2604_27210_b200 import _native
+    from paper_2604_27210_b200 import workloads as W
+    flag, S, K, t, r, q, sig = W.chain_draws(300_000, seed=13)
+    if model != "bsm":
+        q = np.zeros_like(q)
+    m = len(flag) // 10
+    K[:m] = S[:m] * np.exp(np.linspace(-8, 8, m))
+    t[m:2 * m] = 10.0 ** np.linspace(-8, 1.5, m)
+    sig[2 * m:3 * m] = 10.0 ** np.linspace(-7, 0.7, m)
+    p = oracle_mod.rows_price(model, flag, S, K, t, r, q, sig)
+    g = oracle_mod.rows_greeks(model, flag, S, K, t, r, q, sig)
+    lib = _native.lib_for_compute()
+    n = len(flag)
+    cols = [torch.from_numpy(np.ascontiguousarray(c)).cuda() for c in (flag, S, K, t, r, q, sig)]
+    outs = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(6)]
+    st = torch.empty(n, dtype=torch.int8, device="cuda")
+    ep, eg = _native.fv_error(), _native.fv_error()
+    code = {"black": 0, "bs": 1, "bsm": 2}[model]
+    rc = lib.fv_price_greeks(code, *[_native.col(c) for c in cols], n, *[o.data_ptr() for o in outs],
+                             st.data_ptr(), ep, eg)
+    assert rc == 0, (ep.message, eg.message)
+    assert_bits(outs[0].cpu().numpy(), p["price"], f"C3 {model} price")
+    for j, name in enumerate(("delta", "gamma", "theta", "rho", "vega")):
+        assert_bits(outs[j + 1].cpu().numpy(), g[name], f"C3 {model} {name}")
+    assert_bits(st.cpu().numpy(), g["status_code"], f"C3 {model} status")
+    px = torch.empty(n, dtype=torch.float64, device="cuda")
+    e1 = _native.fv_error()
+    assert lib.fv_batch_price(code, *[_native.col(c) for c in cols], n, px.data_ptr(), e1) == 0
+    assert_bits(px.cpu().numpy(), p["price"], f"C3 {model} price-only kernel")
+
+
 def test_c4_chain_sample_vs_oracle(fv, oracle_mod):
     from paper_2604_27210_b200 import workloads as W
     rng = np.random.default_rng(4)
@@ -302,7 +338,7 @@ def test_fast_routines_match_careful_forms():
     the careful routine bit for bit (and the flagged share stays small)."""
     from paper_2604_27210_b200 import _native
     lib = _native.lib_for_compute()
-    names = ["div", "exp", "log", "pow", "erfcx", "nbl", "div_sqrt2", "sqrt", "log2"]
+    names = ["div", "exp", "log", "pow", "erfcx", "nbl", "div_sqrt2", "sqrt", "log2", "erfc"]
     mism = (ctypes.c_int64 * len(names))()
     flg = (ctypes.c_int64 * len(names))()
     n = 100_000_000

@@ -191,3 +191,32 @@ def test_straight_line_classify_matches_careful(Q, case):
                                    ctypes.byref(nb))
     assert bad == 0
     assert nb.value < len(flag) // 20, nb.value
+
+
+@pytest.mark.parametrize("model", [0, 1, 2])
+def test_straight_line_price_greeks_match_careful(Q, model):
+    """fv_fast.h's price and fused price+Greeks rows: every row they do not
+    flag is bit-identical to the careful rows (all six outputs + status)."""
+    from paper_2604_27210_b200 import workloads as W
+    Q.qh_price_greeks_fast_check.restype = ctypes.c_int64
+    flag, S, K, t, r, q, sig = W.chain_draws(100_000, seed=30 + model)
+    if model != 2:
+        q = np.zeros_like(q)
+
+    def check(cols):
+        cols = [np.ascontiguousarray(a) for a in cols]
+        nb = ctypes.c_int64(0)
+        bad = Q.qh_price_greeks_fast_check(ctypes.c_int(model), *[_p(c) for c in cols],
+                                           ctypes.c_int64(len(cols[0])), ctypes.byref(nb))
+        return bad, nb.value
+
+    bad, nb = check((flag, S, K, t, r, q, sig))
+    assert bad == 0 and nb < len(flag) // 100, (bad, nb)
+    # wings: deep ITM/OTM, tiny and long maturities, tiny vols (many of these
+    # leave the straight-line domains and go to the careful rows)
+    m = len(flag) // 3
+    K[:m] = S[:m] * np.exp(np.linspace(-8, 8, m))
+    t[m:2 * m] = 10.0 ** np.linspace(-8, 1.5, m)
+    sig[2 * m:3 * m] = 10.0 ** np.linspace(-7, 0.7, m)
+    bad, nb = check((flag, S, K, t, r, q, sig))
+    assert bad == 0, bad
