@@ -116,7 +116,7 @@ def last_outcome(lib):
     return cr, er, ec
 
 
-NKERNEL = 11
+NKERNEL = 12
 
 
 def kernel_times(lib):

@@ -637,14 +637,24 @@ __global__ void __launch_bounds__(256) k_halley_setup(KArgs a, HsmRec* recs, uns
 // the prepared queue.  Each loop trip: idle lanes take the next records
 // (warp-aggregated), then every busy lane performs one solver step whose
 // heavy part -- one black_kernel evaluation -- is the same code for all.
-__global__ void __launch_bounds__(256) k_halley_sm(KArgs a, const HsmRec* recs,
+// kFast: the step runs on the straight-line routines (fx_hsm_pre,
+// fx_halley_f); a quote they flag is dropped and its record index appended
+// to `ridx` for the careful pass (kFast = false), which walks `ridx` and
+// recomputes those quotes from scratch on the careful routines.
+#ifndef FV_HSM_MINB
+#define FV_HSM_MINB 3
+#endif
+template <bool kFast>
+__global__ void __launch_bounds__(256, kFast ? FV_HSM_MINB : 1) k_halley_sm(KArgs a, const HsmRec* recs,
                                                    const unsigned int* count,
-                                                   unsigned long long* next) {
+                                                   unsigned long long* next, int32_t* ridx,
+                                                   unsigned int* rcount) {
   const int lane = threadIdx.x & 31;
   const unsigned long long n = *count;
   FvHalleySM m;
   m.state = FV_HS_DONE;
   int64_t row = -1;
+  int32_t rec = -1;
   bool busy = false;
   bool exhausted = false;
   for (;;) {
@@ -661,7 +671,8 @@ __global__ void __launch_bounds__(256) k_halley_sm(KArgs a, const HsmRec* recs,
           if (jq >= n) {
             exhausted = true;
           } else {
-            const HsmRec h = recs[jq];
+            rec = kFast ? (int32_t)jq : ridx[jq];
+            const HsmRec h = recs[rec];
             m.c = h.c; m.guess = h.guess; row = h.row;
             m.iterations = 0; m.k = 0;
             m.lo = FV_K_1EM9; m.hi = 10.0;
@@ -678,12 +689,17 @@ __global__ void __launch_bounds__(256) k_halley_sm(KArgs a, const HsmRec* recs,
     // them the compiler reconverges only around the evaluation itself and
     // each state's lanes run it separately: ~6 of 32 lanes active).
     FvExc e = {0, 0, 0.0};
+    bool flagged = false;
     double x = 0.0;
-    bool eval = busy && fv_hsm_pre(m, &x, e);
+    bool eval = busy && (kFast ? fx_hsm_pre(m, &x, flagged) : fv_hsm_pre(m, &x, e));
     __syncwarp();
     double fx = 0.0;
-    if (eval) fx = fv_halley_f(m.c, x, e);                // the shared heavy code
+    if (eval) fx = kFast ? fx_halley_f(m.c, x, flagged) : fv_halley_f(m.c, x, e);   // the shared heavy code
     __syncwarp();
+    if (kFast) {
+      const unsigned int slot = warp_append(rcount, busy && flagged);
+      if (busy && flagged) { ridx[slot] = rec; busy = false; }
+    }
     if (busy) {
       if (eval) fv_hsm_post(m, fx, e);
       if (e.code) {
@@ -893,7 +909,7 @@ thread_local int64_t t_launches = 0;
 const char* const kKernelNames[FV_NKERNEL] = {
     "k_price", "k_price_greeks", "k_lbr_normalize", "k_lbr_normalize_replay", "k_lbr_anchors",
     "k_lbr_far_low_fast", "k_lbr_solve<FAR_LOW>", "k_lbr_solve<NEAR>", "k_lbr_solve<FAR_HIGH>",
-    "k_halley_setup", "k_halley_sm"};
+    "k_halley_setup", "k_halley_sm", "k_halley_sm<careful>"};
 struct TimedLaunch { int id; cudaEvent_t a, b; };
 thread_local bool t_timing = false;
 thread_local std::vector<TimedLaunch> t_timed;
@@ -933,10 +949,11 @@ struct DevWork {
   int32_t* lbr_q[FV_NSLOT] = {};        // 6 queues of lbr_cap entries each
   unsigned int* lbr_count = nullptr;    // [FV_NSLOT][8]
   int64_t lbr_cap[FV_NSLOT] = {};
-  int blocks_price = 0, blocks_greeks = 0, blocks_hsm = 0;
+  int blocks_price = 0, blocks_greeks = 0, blocks_hsm = 0, blocks_hsm2 = 0;
   unsigned long long* work_ctr = nullptr;   // [FV_NSLOT]
-  unsigned int* hsm_count = nullptr;        // [FV_NSLOT]
+  unsigned int* hsm_count = nullptr;        // [FV_NSLOT][2]: records, records handed back
   HsmRec* hsm_recs[FV_NSLOT] = {};
+  int32_t* hsm_ridx[FV_NSLOT] = {};         // records handed back by the fast pass
   int64_t hsm_cap[FV_NSLOT] = {};
   int blocks_hset = 0;
   int blocks_lbr_norm = 0, blocks_lbr_nrep = 0, blocks_lbr_anch = 0, blocks_lbr_fast = 0, blocks_lbr_fl = 0, blocks_lbr_near = 0, blocks_lbr_fh = 0;
@@ -978,9 +995,10 @@ cudaError_t get_work(DevWork** out) {
     w->blocks_lbr_fl = occupancy_blocks((const void*)k_lbr_solve<FV_FAR_LOW>, w->sm_count);
     w->blocks_lbr_near = occupancy_blocks((const void*)k_lbr_solve<FV_NEAR_LOW>, w->sm_count);
     w->blocks_lbr_fh = occupancy_blocks((const void*)k_lbr_solve<FV_FAR_HIGH>, w->sm_count);
-    w->blocks_hsm = occupancy_blocks((const void*)k_halley_sm, w->sm_count);
-    CK(cudaMalloc(&w->work_ctr, sizeof(unsigned long long) * FV_NSLOT));
-    CK(cudaMalloc(&w->hsm_count, sizeof(unsigned int) * FV_NSLOT));
+    w->blocks_hsm = occupancy_blocks((const void*)k_halley_sm<true>, w->sm_count);
+    w->blocks_hsm2 = occupancy_blocks((const void*)k_halley_sm<false>, w->sm_count);
+    CK(cudaMalloc(&w->work_ctr, sizeof(unsigned long long) * 2 * FV_NSLOT));
+    CK(cudaMalloc(&w->hsm_count, sizeof(unsigned int) * 2 * FV_NSLOT));
     w->blocks_hset = occupancy_blocks((const void*)k_halley_setup, w->sm_count);
     g_work[dev] = w;
   }
@@ -1027,10 +1045,13 @@ KArgs sub_args(const KArgs& a, int64_t off, int64_t len) {
 cudaError_t ensure_hsm(DevWork* w, int slot, int64_t rows) {
   if (w->hsm_cap[slot] >= rows) return cudaSuccess;
   if (w->hsm_recs[slot]) cudaFree(w->hsm_recs[slot]);
+  if (w->hsm_ridx[slot]) cudaFree(w->hsm_ridx[slot]);
   w->hsm_recs[slot] = nullptr;
+  w->hsm_ridx[slot] = nullptr;
   w->hsm_cap[slot] = 0;
   int64_t cap = rows < 4096 ? 4096 : rows;
   CK(cudaMalloc(&w->hsm_recs[slot], sizeof(HsmRec) * cap));
+  CK(cudaMalloc(&w->hsm_ridx[slot], sizeof(int32_t) * cap));
   w->hsm_cap[slot] = cap;
   return cudaSuccess;
 }
@@ -1097,13 +1118,16 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
         }
       } else {
         CK(ensure_hsm(w, slot, a.n));
-        unsigned long long* ctr = w->work_ctr + slot;
-        unsigned int* cnt = w->hsm_count + slot;
-        CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s));
-        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned int), s));
+        unsigned long long* ctr = w->work_ctr + 2 * slot;   // [0] fast pass, [1] careful pass
+        unsigned int* cnt = w->hsm_count + 2 * slot;         // [0] records, [1] handed back
+        CK(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned int), s));
         FV_LAUNCH(FV_KID_HALLEY_SETUP, s, k_halley_setup<<<blocks_for(w->blocks_hset, a.n), 256, 0, s>>>(a, w->hsm_recs[slot], cnt));
-        int64_t need = (a.n + 255) / 256;
-        FV_LAUNCH(FV_KID_HALLEY_SM, s, k_halley_sm<<<need < w->blocks_hsm ? need : w->blocks_hsm, 256, 0, s>>>(a, w->hsm_recs[slot], cnt, ctr));
+        const int64_t need = (a.n + 255) / 256;
+        FV_LAUNCH(FV_KID_HALLEY_SM, s, k_halley_sm<true><<<need < w->blocks_hsm ? need : w->blocks_hsm, 256, 0, s>>>(
+            a, w->hsm_recs[slot], cnt, ctr, w->hsm_ridx[slot], cnt + 1));
+        FV_LAUNCH(FV_KID_HALLEY_SM2, s, k_halley_sm<false><<<need < w->blocks_hsm2 ? need : w->blocks_hsm2, 256, 0, s>>>(
+            a, w->hsm_recs[slot], cnt + 1, ctr + 1, w->hsm_ridx[slot], nullptr));
       }
       break;
   }

@@ -155,6 +155,39 @@ int64_t qh_price_greeks_fast_check(int model, const int8_t* flag, const double* 
   return bad;
 }
 
+// The straight-line Halley state machine (fx_hsm_pre / fx_halley_f) against
+// the careful solver (fv_halley_row_sm): mismatching unflagged rows; *nflag
+// gets the flagged ones.
+int64_t qh_halley_fast_check(int model, const int8_t* flag, const double* un, const double* k,
+                             const double* t, const double* r, const double* q, const double* px,
+                             int64_t n, int64_t* nflag) {
+  int64_t bad = 0, nb = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    FvExc e0 = {0, 0, 0.0};
+    FvHalleySM m;
+    int st_c; double sg_c;
+    FvExc ec = {0, 0, 0.0};
+    fv_halley_row_sm(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], px[i], &st_c, &sg_c, ec);
+    if (fv_hsm_setup(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], px[i], m, e0)) continue;
+    bool flagged = false;
+    for (;;) {
+      double x;
+      if (!fx_hsm_pre(m, &x, flagged)) break;
+      const double fx = fx_halley_f(m.c, x, flagged);
+      if (flagged) break;
+      FvExc e = {0, 0, 0.0};
+      fv_hsm_post(m, fx, e);
+      if (m.state == FV_HS_DONE) break;
+    }
+    if (flagged) { ++nb; continue; }
+    const double sg = (m.status == FV_IV_CONVERGED || m.status == FV_IV_FELL_BACK) ? m.out_sigma : __builtin_nan("");
+    uint64_t ua, ub; memcpy(&ua, &sg, 8); memcpy(&ub, &sg_c, 8);
+    if (m.status != st_c || !(ua == ub || (sg != sg && sg_c != sg_c)) || ec.code) ++bad;
+  }
+  *nflag = nb;
+  return bad;
+}
+
 // The straight-line far-low solver (fv_fast.h) against the careful one on the
 // far-low quotes of a batch: returns mismatching unflagged rows; *nflag gets
 // the flagged (handed-back) ones.

@@ -220,3 +220,30 @@ def test_straight_line_price_greeks_match_careful(Q, model):
     sig[2 * m:3 * m] = 10.0 ** np.linspace(-7, 0.7, m)
     bad, nb = check((flag, S, K, t, r, q, sig))
     assert bad == 0, bad
+
+
+@pytest.mark.parametrize("case", ["c2", "black", "c5"])
+def test_straight_line_halley_matches_careful(Q, case):
+    """fv_fast.h's Halley step (fx_hsm_pre / fx_halley_f): every quote it does
+    not flag ends with the careful solver's status and sigma bits."""
+    from oracle import fvoracle as O
+    from paper_2604_27210_b200 import workloads as W
+    Q.qh_halley_fast_check.restype = ctypes.c_int64
+    if case == "c5":
+        flag, S, K, t, r, sig, kind, side = W.c5_params(20_000, seed=5)
+        q = np.zeros_like(S)
+        model = 0
+        px = W.c5_prices(flag, S, K, t, r, kind, side, O.rows_price("black", flag, S, K, t, r, 0.0, sig)["price"])
+    else:
+        flag, S, K, t, r, q, sig = W.chain_draws(20_000, seed=40)
+        model = 2 if case == "c2" else 0
+        if model == 0:
+            q = np.zeros_like(q)
+        px = O.rows_price("bsm" if model else "black", flag, S, K, t, r, q, sig)["price"]
+    cols = [np.ascontiguousarray(a) for a in (flag, S, K, t, r, q, px)]
+    nb = ctypes.c_int64(0)
+    bad = Q.qh_halley_fast_check(ctypes.c_int(model), *[_p(c) for c in cols], ctypes.c_int64(len(flag)),
+                                 ctypes.byref(nb))
+    assert bad == 0
+    if case != "c5":
+        assert nb.value < len(flag) // 100, nb.value
