@@ -211,33 +211,42 @@ __device__ __noinline__ FvGreeks price_greeks_row_careful(const KArgs& a, int64_
 // it flags.  Inputs of a pair are picked with selects (no local-memory
 // arrays); 16-byte loads and stores of the pair.
 __global__ void __launch_bounds__(256, FV_PG_MINB) k_price(KArgs a) {
+  __shared__ double sm_x[8][64], sm_r[8][64];      // range-bucketed erfc staging
+  __shared__ unsigned char sm_f[8][64];
+  const int wib = threadIdx.x >> 5;
   const int64_t npair = (a.n + 1) >> 1;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = 2 * j;
-    const bool two = i + 1 < a.n;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nloop = (npair + stride - 1) / stride;
+  for (int64_t it = 0; it < nloop; ++it) {          // warp-uniform trip count
+    const int64_t j = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool active = j < npair;
+    const int64_t i = active ? 2 * j : 0;
+    const bool two = active && i + 1 < a.n;
     Pair p;
     load_pair(a, i, two, p);
     double out0 = 0.0, out1 = 0.0;
 #pragma unroll 1
-    for (int u = 0; u < (two ? 2 : 1); ++u) {
+    for (int u = 0; u < 2; ++u) {           // warp-uniform trip count (bucketed erfc)
+      const bool valid = active && (u == 0 || two);
       const int fl = u ? p.fl[1] : p.fl[0];
       const double un = u ? p.un[1] : p.un[0], k = u ? p.k[1] : p.k[0];
       const double t = u ? p.t[1] : p.t[0], r = u ? p.r[1] : p.r[0];
       const double q = u ? p.q[1] : p.q[0], sg = u ? p.last[1] : p.last[0];
-      double v;
-      uint32_t bad = row_checks(a, fl, un, k, t, r, q, sg);
-      if (bad) {
-        publish_checks(a.st, bad, a.row0 + i + u);
-        v = __builtin_nan("");
-      } else {
-        bool flagged = false;
-        v = fx_price_row(a.model, (double)fl, un, k, t, r, q, sg, flagged);
-        if (flagged) v = price_row_careful(a, i + u, fl, un, k, t, r, q, sg);
+      const uint32_t bad = valid ? row_checks(a, fl, un, k, t, r, q, sg) : 0u;
+      bool flagged = false;
+      double v = fx_price_row(a.model, (double)fl, un, k, t, r, q, sg, flagged, valid && !bad,
+                              sm_x[wib], sm_r[wib], sm_f[wib]);
+      if (valid) {
+        if (bad) {
+          publish_checks(a.st, bad, a.row0 + i + u);
+          v = __builtin_nan("");
+        } else if (flagged) {
+          v = price_row_careful(a, i + u, fl, un, k, t, r, q, sg);
+        }
       }
       if (u) out1 = v; else out0 = v;
     }
-    st2(a.o0, i, two, a.out_vec, out0, out1);
+    if (active) st2(a.o0, i, two, a.out_vec, out0, out1);
   }
 }
 
@@ -245,33 +254,43 @@ __global__ void __launch_bounds__(256, FV_PG_MINB) k_price(KArgs a) {
 // straight-line row (fx_price_greeks_row), careful row where it flags.
 template <bool kPrice, bool kGreeks>
 __global__ void __launch_bounds__(256, FV_PG_MINB) k_price_greeks(KArgs a) {
+  __shared__ double sm_x[8][64], sm_r[8][64];      // range-bucketed erfc staging
+  __shared__ unsigned char sm_f[8][64];
+  const int wib = threadIdx.x >> 5;
   const int64_t npair = (a.n + 1) >> 1;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npair;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = 2 * j;
-    const bool two = i + 1 < a.n;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nloop = (npair + stride - 1) / stride;
+  for (int64_t it = 0; it < nloop; ++it) {          // warp-uniform trip count
+    const int64_t j = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool active = j < npair;
+    const int64_t i = active ? 2 * j : 0;
+    const bool two = active && i + 1 < a.n;
     Pair p;
     load_pair(a, i, two, p);
     FvGreeks g0, g1;
 #pragma unroll 1
-    for (int u = 0; u < (two ? 2 : 1); ++u) {
+    for (int u = 0; u < 2; ++u) {           // warp-uniform trip count (bucketed erfc)
+      const bool valid = active && (u == 0 || two);
       const int fl = u ? p.fl[1] : p.fl[0];
       const double un = u ? p.un[1] : p.un[0], k = u ? p.k[1] : p.k[0];
       const double t = u ? p.t[1] : p.t[0], r = u ? p.r[1] : p.r[0];
       const double q = u ? p.q[1] : p.q[0], sg = u ? p.last[1] : p.last[0];
-      FvGreeks g;
-      uint32_t bad = row_checks(a, fl, un, k, t, r, q, sg);
-      if (bad) {
-        publish_checks(a.st, bad, a.row0 + i + u);
-        g.price = g.delta = g.gamma = g.theta = g.rho = g.vega = __builtin_nan("");
-        g.status = 0;
-      } else {
-        bool flagged = false;
-        g = fx_price_greeks_row(a.model, (double)fl, un, k, t, r, q, sg, kGreeks, flagged);
-        if (flagged) g = price_greeks_row_careful<kPrice, kGreeks>(a, i + u, fl, un, k, t, r, q, sg);
+      const uint32_t bad = valid ? row_checks(a, fl, un, k, t, r, q, sg) : 0u;
+      bool flagged = false;
+      FvGreeks g = fx_price_greeks_row(a.model, (double)fl, un, k, t, r, q, sg, kGreeks, flagged,
+                                       valid && !bad, sm_x[wib], sm_r[wib], sm_f[wib]);
+      if (valid) {
+        if (bad) {
+          publish_checks(a.st, bad, a.row0 + i + u);
+          g.price = g.delta = g.gamma = g.theta = g.rho = g.vega = __builtin_nan("");
+          g.status = 0;
+        } else if (flagged) {
+          g = price_greeks_row_careful<kPrice, kGreeks>(a, i + u, fl, un, k, t, r, q, sg);
+        }
       }
       if (u) g1 = g; else g0 = g;
     }
+    if (!active) continue;
     if (!two) g1 = g0;
     if (kPrice) st2(a.o0, i, two, a.out_vec, g0.price, g1.price);
     if (kGreeks) {
@@ -651,6 +670,9 @@ __global__ void __launch_bounds__(256, kFast ? FV_HSM_MINB : 1) k_halley_sm(KArg
                                                    unsigned int* rcount) {
   const int lane = threadIdx.x & 31;
   const unsigned long long n = *count;
+  __shared__ double sm_x[8][64], sm_r[8][64];      // range-bucketed erfc staging (fast pass)
+  __shared__ unsigned char sm_f[8][64];
+  const int wib = threadIdx.x >> 5;
   FvHalleySM m;
   m.state = FV_HS_DONE;
   int64_t row = -1;
@@ -694,7 +716,8 @@ __global__ void __launch_bounds__(256, kFast ? FV_HSM_MINB : 1) k_halley_sm(KArg
     bool eval = busy && (kFast ? fx_hsm_pre(m, &x, flagged) : fv_hsm_pre(m, &x, e));
     __syncwarp();
     double fx = 0.0;
-    if (eval) fx = kFast ? fx_halley_f(m.c, x, flagged) : fv_halley_f(m.c, x, e);   // the shared heavy code
+    if (kFast) fx = fx_halley_f_warp(eval, m.c, x, flagged, sm_x[wib], sm_r[wib], sm_f[wib]);
+    else if (eval) fx = fv_halley_f(m.c, x, e);          // the shared heavy code
     __syncwarp();
     if (kFast) {
       const unsigned int slot = warp_append(rcount, busy && flagged);
