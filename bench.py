@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-kernel-timing", action="store_true",
+                    help="skip the per-kernel event-timing pass (ncu traffic captures)")
     return ap.parse_args()
 
 
@@ -377,6 +379,8 @@ def run_ours(args):
     # launching stream; a separate pass so the headline timing has no events)
     kernels = None
     try:
+        if args.no_kernel_timing:
+            raise RuntimeError("skipped (--no-kernel-timing)")
         lib.fv_set_kernel_timing(1)
         _native.kernel_times(lib)
         nk = max(1, min(args.steps, 3))

@@ -1,7 +1,8 @@
 #!/bin/bash
 # Full round run on one B200: GPU tests, smoke, the C4 bench line (with e2e +
-# CPU baseline), other workloads, the reference arm, an ncu launch list and
-# an ncu --set full capture of the LBR kernels.  Outputs in gpurun_out/.
+# CPU baseline), the other workloads, the reference arm, an ncu launch list of
+# the bench command, ncu DRAM traffic per workload, and an ncu --set full
+# capture of the LBR kernels.  Outputs in gpurun_out/.
 set -u
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
@@ -18,6 +19,11 @@ done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_${TAG}_ref.json 2>> gpurun_out/bench_${TAG}.err; cat gpurun_out/bench_${TAG}_ref.json | head -c 400; echo
 if [ "${NCU:-1}" = "1" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_lbr -c 5 -o gpurun_out/prof_${TAG} python bench.py --rows 10000000 --steps 1 --warmup 0 --no-e2e --no-cpu > gpurun_out/ncu_${TAG}.log 2>&1
+  M=dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum
+  for spec in c4:k_lbr c1:k_lbr c5:k_lbr c2:k_halley c3:k_price_greeks; do
+    w=${spec%%:*}; k=${spec#*:}
+    timeout 900 ncu --metrics $M --clock-control none -k regex:$k --csv --log-file gpurun_out/traffic_${TAG}_$w.csv python bench.py --workload $w --steps 1 --warmup 0 --no-e2e --no-cpu --no-kernel-timing > /dev/null 2>&1
+  done
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_lbr -c 7 -o gpurun_out/prof_${TAG} python bench.py --rows 10000000 --steps 1 --warmup 0 --no-e2e --no-cpu --no-kernel-timing > gpurun_out/ncu_${TAG}.log 2>&1
   tail -1 gpurun_out/ncu_${TAG}.log
 fi
