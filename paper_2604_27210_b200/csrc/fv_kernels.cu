@@ -330,7 +330,7 @@ struct LbrQueues {
   int32_t* q[6];         // 0..2: local rows per region class; 3: rows pending anchors;
                          // 4: far-low rows the straight-line solver handed back;
                          // 5: rows the straight-line normalize pass handed back
-  unsigned int* count;   // [6]
+  unsigned int* count;   // [8]: queue lengths [0..5], far-low work counter [6]
 };
 
 __device__ __forceinline__ int region_class(int region) {
@@ -545,10 +545,17 @@ __global__ void __launch_bounds__(256, FV_ANCH_MINB) k_lbr_anchors(KArgs a, LbrQ
 __global__ void __launch_bounds__(256, FV_FAST_MINB) k_lbr_far_low_fast(KArgs a, LbrQueues lq) {
   const unsigned int n = lq.count[0];
   const int32_t* q = lq.q[0];
-  const unsigned int stride = gridDim.x * blockDim.x;
-  const unsigned int nloop = (n + stride - 1) / stride;
-  for (unsigned int it = 0; it < nloop; ++it) {
-    const unsigned int j = it * stride + blockIdx.x * blockDim.x + threadIdx.x;
+  // dynamic distribution: each warp takes the next 32 queue entries (one
+  // atomic per warp per 32 quotes).  A static grid stride hands each block a
+  // fixed strike band of every stride window, and per-quote cost depends on
+  // the strike, so blocks finished unevenly (ncu: 25 of 32 warps/SM active).
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned int base = 0;
+    if (lane == 0) base = atomicAdd(lq.count + 6, 32u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= n) break;
+    const unsigned int j = base + lane;
     bool bad = false;
     int32_t ent = 0;
     if (j < n) {
