@@ -330,7 +330,8 @@ struct LbrQueues {
   int32_t* q[6];         // 0..2: local rows per region class; 3: rows pending anchors;
                          // 4: far-low rows the straight-line solver handed back;
                          // 5: rows the straight-line normalize pass handed back
-  unsigned int* count;   // [8]: queue lengths [0..5], far-low work counter [6]
+  unsigned int* count;   // [8]: queue lengths [0..5], work counters of the far-low
+                         // solve [6] and the normalize pass [7]
 };
 
 __device__ __forceinline__ int region_class(int region) {
@@ -408,10 +409,15 @@ __device__ __forceinline__ void lbr_norm_row_careful(const KArgs& a, const LbrQu
 // exceptions, range edges) go to queue 5 for k_lbr_normalize_replay.
 __global__ void __launch_bounds__(256, FV_NORM_MINB) k_lbr_normalize(KArgs a, LbrQueues lq) {
   const int64_t npair = (a.n + 1) >> 1;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t nloop = (npair + stride - 1) / stride;
-  for (int64_t it = 0; it < nloop; ++it) {
-    const int64_t j = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  // dynamic distribution: each warp takes the next 32 pairs (see
+  // k_lbr_far_low_fast: per-row cost depends on the strike band)
+  for (;;) {
+    unsigned int base = 0;
+    if (lane == 0) base = atomicAdd(lq.count + 7, 32u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if ((int64_t)base >= npair) break;
+    const int64_t j = (int64_t)base + lane;
     const bool active = j < npair;
     const int64_t i = 2 * j;
     const bool two = active && (i + 1 < a.n);
