@@ -170,6 +170,13 @@ __device__ __forceinline__ void publish_exc(unsigned long long* slot, int code, 
   if (code) atomicMin(slot, ((unsigned long long)row << 8) | (unsigned long long)code);
 }
 
+__device__ __forceinline__ double ld1(const DCol& c, int64_t i) {
+  return c.mode == 0 ? __ldg(c.p) : __ldg(c.p + i * c.stride);
+}
+__device__ __forceinline__ int ldf1(const DFlag& c, int64_t i) {
+  return c.mode == 0 ? c.p[0] : c.p[i * c.stride];
+}
+
 // Loads the pair (i, i+1) of every input column.
 struct Pair {
   int fl[2];
@@ -478,12 +485,6 @@ __global__ void __launch_bounds__(256, FV_NORM_MINB) k_lbr_normalize(KArgs a, Lb
   }
 }
 
-__device__ __forceinline__ double ld1(const DCol& c, int64_t i) {
-  return c.mode == 0 ? __ldg(c.p) : __ldg(c.p + i * c.stride);
-}
-__device__ __forceinline__ int ldf1(const DFlag& c, int64_t i) {
-  return c.mode == 0 ? c.p[0] : c.p[i * c.stride];
-}
 
 // Pass 1b: the rows pass 1 flagged, on the careful routines.
 __global__ void __launch_bounds__(256) k_lbr_normalize_replay(KArgs a, LbrQueues lq) {
@@ -611,57 +612,44 @@ struct HsmRec {
   int64_t row;
 };
 
-__global__ void __launch_bounds__(256) k_halley_setup(KArgs a, HsmRec* recs, unsigned int* count) {
-  const int64_t npair = (a.n + 1) >> 1;
+// One row per thread (8-byte coalesced column loads): with a pair per
+// thread the two rows' solver state stayed live (126 registers, 25 % of warps)
+// and the pass was latency-bound at 0.9 ms per 10M rows.
+__global__ void __launch_bounds__(256, 4) k_halley_setup(KArgs a, HsmRec* recs, unsigned int* count) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t nloop = (npair + stride - 1) / stride;
+  const int64_t nloop = (a.n + stride - 1) / stride;
   for (int64_t it = 0; it < nloop; ++it) {
-    const int64_t j = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool active = j < npair;
-    const int64_t i = 2 * j;
-    const bool two = active && (i + 1 < a.n);
-    double iv[2] = {0.0, 0.0};
-    int stt[2] = {FV_IV_MAX_ITER, FV_IV_MAX_ITER};
-    bool need[2] = {false, false};
-    FvHalleySM m0, m1;
-    Pair p;
-    if (active) load_pair(a, i, two, p);
-#pragma unroll 1
-    for (int u = 0; u < 2; ++u) {
-      const bool valid = active && (u == 0 || two);
-      if (!valid) continue;
-      const int fl = u ? p.fl[1] : p.fl[0];
-      const double un = u ? p.un[1] : p.un[0], k = u ? p.k[1] : p.k[0];
-      const double t = u ? p.t[1] : p.t[0], r = u ? p.r[1] : p.r[0];
-      const double q = u ? p.q[1] : p.q[0], px = u ? p.last[1] : p.last[0];
-      uint32_t bad = row_checks(a, fl, un, k, t, r, q, px);
+    const int64_t row = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool active = row < a.n;
+    bool nd = false;
+    FvHalleySM m;
+    if (active) {
+      const int fl = ldf1(a.flag, row);
+      const double un = ld1(a.un, row), k = ld1(a.k, row), t = ld1(a.t, row), r = ld1(a.r, row);
+      const double q = ld1(a.q, row), px = ld1(a.last, row);
+      const uint32_t bad = row_checks(a, fl, un, k, t, r, q, px);
       double ivu = __builtin_nan("");
       int stu = FV_IV_MAX_ITER;
-      bool nd = false;
-      FvHalleySM m;
       if (bad) {
-        publish_checks(a.st, bad, a.row0 + i + u);
+        publish_checks(a.st, bad, a.row0 + row);
       } else {
         FvExc e = {0, 0, 0.0};
         if (fv_hsm_setup(a.model, (double)fl, un, k, t, r, q, px, m, e)) {
-          publish_exc(&a.st->exc_first, e.code, a.row0 + i + u);
+          publish_exc(&a.st->exc_first, e.code, a.row0 + row);
           ivu = (m.status == FV_IV_CONVERGED || m.status == FV_IV_FELL_BACK) ? m.out_sigma : __builtin_nan("");
           stu = m.status;
         } else {
           nd = true;
         }
       }
-      if (u) { iv[1] = ivu; stt[1] = stu; need[1] = nd; m1 = m; }
-      else { iv[0] = ivu; stt[0] = stu; need[0] = nd; m0 = m; }
+      if (!nd) {
+        a.o0[row] = ivu;
+        a.status[row] = (int8_t)stu;
+      }
+      if (a.region) a.region[row] = -1;
     }
-    unsigned int slot = warp_append2(count, need[0], need[1]);
-    if (need[0]) { HsmRec h; h.c = m0.c; h.guess = m0.guess; h.row = i; recs[slot++] = h; }
-    if (need[1]) { HsmRec h; h.c = m1.c; h.guess = m1.guess; h.row = i + 1; recs[slot] = h; }
-    if (active) {
-      st2(a.o0, i, two, a.out_vec, iv[0], iv[1]);
-      st2i8(a.status, i, two, stt[0], stt[1]);
-      if (a.region) st2i8(a.region, i, two, -1, -1);
-    }
+    const unsigned int slot = warp_append(count, nd);
+    if (nd) { HsmRec h; h.c = m.c; h.guess = m.guess; h.row = row; recs[slot] = h; }
   }
 }
 
