@@ -435,10 +435,27 @@ def run_ours(args):
             e_ms = float(tt.item())
         # bit-identical to the device-resident result
         same = bool(torch.equal(h_iv.to(dev).view(torch.int64), out_iv.view(torch.int64)))
+        # the link's own ceiling: a plain pinned 1 GB host->device copy
+        h2d_gbs = None
+        try:
+            hb = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
+            db = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+            db.copy_(hb, non_blocking=True)
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            for _ in range(3):
+                db.copy_(hb, non_blocking=True)
+            torch.cuda.synchronize(dev)
+            h2d_gbs = 3 * (1 << 30) / (time.perf_counter() - t0) / 1e9
+            del hb, db
+        except Exception:  # noqa: BLE001
+            pass
         e2e = {"value": world * n / (e_ms * 1e-3), "unit": "quotes/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms,
                "timing": "wall clock around the synchronous C-ABI call (host buffers pinned)",
-               "bit_identical_to_device_resident": same}
+               "bit_identical_to_device_resident": same,
+               "pcie_h2d_gbs": h2d_gbs,
+               "h2d_ceiling_quotes_s": (world * n * h2d_gbs * 1e9 / h2d) if h2d_gbs and h2d else None}
 
     # ---- roofline ------------------------------------------------------------
     peak = ctypes_double()
