@@ -1031,8 +1031,14 @@ cudaError_t get_work(DevWork** out) {
 }
 
 
-// rows per LBR classify/solve round (bounds the state workspace: 64 B/row)
-const int64_t kLbrChunk = 1 << 25;
+// rows per LBR classify/solve round.  The workspace is 64 B of state + 24 B
+// of queues per row: 2^27 rows = 11.8 GB, a small slice of the B200's 180 GB,
+// so a 100M-quote chain is one round (fewer kernel boundaries and tails than
+// 2^25-row rounds, and one dynamic work pool per kernel).
+#ifndef FV_LBR_ROUND_LOG2
+#define FV_LBR_ROUND_LOG2 27
+#endif
+const int64_t kLbrChunk = 1ll << FV_LBR_ROUND_LOG2;
 
 cudaError_t ensure_lbr(DevWork* w, int slot, int64_t rows) {
   if (w->lbr_cap[slot] >= rows) return cudaSuccess;
