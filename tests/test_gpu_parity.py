@@ -428,3 +428,37 @@ def test_c4_full_chain_100m(fv, oracle_mod):
                            None, err) == 0, err.message
     assert torch.equal(hiv.view(torch.int64), iv.cpu().view(torch.int64))
     assert torch.equal(hst, st.cpu())
+
+
+def test_fast_vollib_facade_device(fv, oracle_mod):
+    """The paper-name façade on the GPU, host arrays and CUDA tensors (the
+    device-resident path), bit-identical to the oracle."""
+    import torch
+    from paper_2604_27210_b200 import fast_vollib as FV
+    from paper_2604_27210_b200 import workloads as W
+    flag, S, K, t, r, q, sig = W.chain_draws(50_000, seed=31)
+    chars = W.flag_chars(flag)
+    # pricing
+    p = FV.fast_black_scholes_merton(chars, S, K, t, r, sig, q, return_as="numpy")
+    assert_bits(p, oracle_mod.rows_price("bsm", flag, S, K, t, r, q, sig)["price"], "facade bsm price")
+    # Halley IV (BSM), host and device
+    want = oracle_mod.rows_iv("bsm", "halley", flag, S, K, t, r, q, p)["iv"]
+    iv = FV.fast_implied_volatility(p, S, K, t, r, chars, q, return_as="numpy", on_error="ignore")
+    assert_bits(iv, want, "facade bsm iv")
+    dev = [torch.from_numpy(np.ascontiguousarray(c)).cuda() for c in (p, S, K, t, r, q)]
+    ivd = FV.fast_implied_volatility(*dev[:5], torch.from_numpy(flag).cuda(), dev[5], return_native=True)
+    assert ivd.is_cuda
+    assert_bits(ivd.cpu().numpy(), want, "facade bsm iv (device)")
+    # LBR (jackel) on Black-76, host and device
+    pb = FV.fast_black(chars, S, K, t, r, sig, return_as="numpy")
+    want = oracle_mod.rows_iv("black", "lbr", flag, S, K, t, r, 0.0, pb)
+    assert_bits(FV.jackel.jackel_iv_black(pb, S, K, t, r, chars), want["iv"], "jackel iv")
+    dv = [torch.from_numpy(np.ascontiguousarray(c)).cuda() for c in (pb, S, K, t, r)]
+    ivj, stj = FV.jackel.jackel_iv_black_torch(*dv, torch.from_numpy(flag).cuda(), return_status=True)
+    assert_bits(ivj.cpu().numpy(), want["iv"], "jackel iv (device)")
+    assert_bits(stj.cpu().numpy(), want["status_code"], "jackel status (device)")
+    # Greeks
+    g = FV.get_all_greeks(chars, S, K, t, r, sig, q, model="black_scholes_merton", return_as="dict")
+    gw = oracle_mod.rows_greeks("bsm", flag, S, K, t, r, q, sig)
+    for k in ("delta", "gamma", "theta", "rho", "vega"):
+        assert_bits(g[k], gw[k], f"facade {k}")
