@@ -6,7 +6,8 @@ for the batch path: batch_price / batch_iv / batch_greeks return the same
 ChainTable, statuses and errors, computed by hand-written CUDA kernels
 (csrc/) behind the C ABI in include/fastvol_b200.h.  The paper's names
 (fast_black_scholes_merton, fast_implied_volatility, jackel_iv_black,
-get_all_greeks, ...) live in ``paper_2604_27210_b200.fast_vollib``.
+get_all_greeks, jackel.jackel_iv_black, set_backend, patch_py_vollib, ...,
+with return_as containers) live in ``paper_2604_27210_b200.fast_vollib``.
 """
 
 from .batch import (BatchError, ChainTable, batch_greeks, batch_iv, batch_price, broadcast,

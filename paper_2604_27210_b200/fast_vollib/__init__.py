@@ -129,17 +129,19 @@ def _model(model, q):
     if key not in _MODELS:
         raise ValueError(f"unknown model {model!r}")
     m = _MODELS[key]
-    if m is Model.BLACK_SCHOLES and q is not None and np.any(np.asarray(q) != 0.0):
+    if m is Model.BLACK_SCHOLES and q is not None and _any_nonzero(q):
         m = Model.BLACK_SCHOLES_MERTON         # py_vollib_vectorized: q given -> BSM
     return m
 
 
+def _any_nonzero(x):
+    if hasattr(x, "is_cuda"):                  # torch tensor: reduce where it lives
+        return bool((x != 0).any())
+    return bool(np.any(np.asarray(x) != 0.0))
+
+
 def _qcol(q):
     return 0.0 if q is None else q
-
-
-def _native_out(x, return_native):
-    return x if return_native else x.cpu().numpy()
 
 
 def _iv_errors(iv, status, on_error):
