@@ -865,9 +865,12 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
       FvExc e = {0, 0, 0.0};
       if (bad) ++lf[3]; else if (!st_same(f, py_powi_t<true>(x, nn, false, e)) || e.code) ++lm[3];
     }
-    // 4: erfcx over [0, 1e8] (log-uniform) and [0, 60] (uniform)
+    // 4: erfcx over [0, 1e8] (log-uniform), [0, 60] (uniform) and tiny x
+    //    (where 4 + x rounds to 4: erfcx's y100 == 100 branch)
     {
-      const double x = ((u3 >> 16) & 1) ? st_uniform(u2) * 60.0 : exp10(st_uniform(u2) * 11.0 - 3.0);
+      const int sel = (int)((u3 >> 16) & 3);
+      const double x = sel == 0 ? st_uniform(u2) * 60.0
+                     : (sel == 1 ? st_bits(u2, -64, -30) : exp10(st_uniform(u2) * 11.0 - 3.0));
       bad = false;
       const double f = fx_erfcx_pos(x, bad);
       if (bad) ++lf[4]; else if (!st_same(f, fv_erfcx_i(x))) ++lm[4];
