@@ -28,6 +28,7 @@
 #include <string.h>
 
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "fv_fast.h"
@@ -970,6 +971,8 @@ struct DevWork {
   // chunk buffers for host-pointer calls
   char* chunk[FV_NSLOT] = {};
   int64_t chunk_cap_rows[FV_NSLOT] = {};
+  char* stage[FV_NSLOT] = {};              // pinned host staging (pageable callers)
+  int64_t stage_cap[FV_NSLOT] = {};
   ExplainOut* explain = nullptr;
   // LBR classify -> solve workspace (per slot)
   double* lbr_state[FV_NSLOT] = {};     // 8 SoA fields x lbr_cap
@@ -1392,6 +1395,34 @@ int run_device(DevWork* w, const Call& c, cudaStream_t s, uint32_t bcast_bits, f
 }
 
 // Host-pointer path: chunked H2D -> kernel -> D2H, FV_NSLOT streams.
+// Host memcpy split over threads: pageable caller buffers are moved through
+// pinned staging slots, and one thread's memcpy (~11 GB/s) would otherwise
+// cap the pipeline far below the link (~50 GB/s pinned).
+void par_memcpy(char* dst, const char* src, size_t bytes) {
+  const size_t kMin = (size_t)8 << 20;
+  unsigned nt = std::thread::hardware_concurrency();
+  if (nt > 8) nt = 8;
+  if (nt < 2 || bytes < 2 * kMin) { memcpy(dst, src, bytes); return; }
+  size_t parts = bytes / kMin;
+  if (parts > nt) parts = nt;
+  const size_t per = ((bytes / parts) + 4095) & ~(size_t)4095;
+  std::vector<std::thread> th;
+  for (size_t k = 1; k < parts; ++k) {
+    const size_t o = k * per;
+    if (o >= bytes) break;
+    const size_t len = (o + per <= bytes) ? per : bytes - o;
+    th.emplace_back([=] { memcpy(dst + o, src + o, len); });
+  }
+  memcpy(dst, src, per < bytes ? per : bytes);
+  for (auto& t : th) t.join();
+}
+
+bool is_pageable(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return true; }
+  return at.type == cudaMemoryTypeUnregistered;
+}
+
 int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_error* e2) {
   cudaError_t ce;
   const int64_t chunk = g_chunk_rows;
@@ -1419,6 +1450,44 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
       w->chunk_cap_rows[s] = (int64_t)slot_bytes;
     }
   }
+  // pageable caller buffers go through pinned staging (parallel host copies)
+  bool stage_in[7] = {}, stage_out[6] = {}, stage_status = false, stage_region = false, any_stage = false;
+  for (int col = 0; col < 7; ++col)
+    if (c.cols[col].stride != 0) any_stage |= (stage_in[col] = is_pageable(c.cols[col].data));
+  for (int i = 0; i < 6; ++i) if (c.outs[i]) any_stage |= (stage_out[i] = is_pageable(c.outs[i]));
+  if (has_status) any_stage |= (stage_status = is_pageable(c.status));
+  if (has_region) any_stage |= (stage_region = is_pageable(c.region));
+  if (any_stage) {
+    for (int s = 0; s < FV_NSLOT; ++s) {
+      if (w->stage_cap[s] < (int64_t)slot_bytes) {
+        if (w->stage[s]) cudaFreeHost(w->stage[s]);
+        w->stage[s] = nullptr;
+        if ((ce = cudaMallocHost(&w->stage[s], slot_bytes)) != cudaSuccess) return set_cuda_err(e1, ce);
+        w->stage_cap[s] = (int64_t)slot_bytes;
+      }
+    }
+  }
+  struct SlotEvents {
+    cudaEvent_t ev[FV_NSLOT];
+    SlotEvents() { for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming); }
+    ~SlotEvents() { for (auto& e : ev) cudaEventDestroy(e); }
+  } sev;
+  cudaEvent_t* slot_done = sev.ev;
+  int64_t slot_chunk[FV_NSLOT];
+  for (int s = 0; s < FV_NSLOT; ++s) slot_chunk[s] = -1;
+  // results of chunk `ci` (in slot s) from pinned staging to the caller
+  auto drain = [&](int s) {
+    const int64_t ci = slot_chunk[s];
+    if (ci < 0) return;
+    cudaEventSynchronize(slot_done[s]);
+    const int64_t r0 = ci * chunk, rn = (r0 + chunk < n ? chunk : n - r0);
+    char* st = w->stage[s];
+    for (int i = 0; i < 6; ++i)
+      if (stage_out[i]) par_memcpy((char*)(c.outs[i] + r0), st + off_out[i], 8 * rn);
+    if (stage_status) par_memcpy((char*)(c.status + r0), st + off_status, rn);
+    if (stage_region) par_memcpy((char*)(c.region + r0), st + off_region, rn);
+    slot_chunk[s] = -1;
+  };
   if ((ce = cudaMemsetAsync(w->st, 0xff, sizeof(FvDevStatus), w->streams[0])) != cudaSuccess)
     return set_cuda_err(e1, ce);
   cudaEvent_t ready;
@@ -1433,11 +1502,17 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
     cudaStream_t s = w->streams[slot];
     int64_t r0 = ci * chunk, rn = (r0 + chunk < n ? chunk : n - r0);
     char* base = w->chunk[slot];
+    char* stg = w->stage[slot];
+    if (any_stage) drain(slot);               // the slot's previous chunk is done with staging
     void* dev_in[7];
     for (int col = 0; col < 7; ++col) {
       if (c.cols[col].stride == 0) { dev_in[col] = nullptr; continue; }
       dev_in[col] = base + off_in[col];
       const char* src = (const char*)c.cols[col].data + r0 * in_sz[col];
+      if (stage_in[col]) {
+        par_memcpy(stg + off_in[col], src, rn * in_sz[col]);
+        src = stg + off_in[col];
+      }
       if ((ce = cudaMemcpyAsync(dev_in[col], src, rn * in_sz[col], cudaMemcpyHostToDevice, s)) != cudaSuccess) {
         cudaEventDestroy(ready);
         return set_cuda_err(e1, ce);
@@ -1462,10 +1537,18 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
     if (ci == 0) a_first = a;
     if ((ce = launch(w, c, a, slot, s)) != cudaSuccess) { cudaEventDestroy(ready); return set_cuda_err(e1, ce); }
     for (int i = 0; i < 6; ++i)
-      if (c.outs[i]) cudaMemcpyAsync(c.outs[i] + r0, douts[i], 8 * rn, cudaMemcpyDeviceToHost, s);
-    if (has_status) cudaMemcpyAsync(c.status + r0, a.status, rn, cudaMemcpyDeviceToHost, s);
-    if (has_region) cudaMemcpyAsync(c.region + r0, a.region, rn, cudaMemcpyDeviceToHost, s);
+      if (c.outs[i])
+        cudaMemcpyAsync(stage_out[i] ? (void*)(stg + off_out[i]) : (void*)(c.outs[i] + r0), douts[i], 8 * rn,
+                        cudaMemcpyDeviceToHost, s);
+    if (has_status)
+      cudaMemcpyAsync(stage_status ? (void*)(stg + off_status) : (void*)(c.status + r0), a.status, rn,
+                      cudaMemcpyDeviceToHost, s);
+    if (has_region)
+      cudaMemcpyAsync(stage_region ? (void*)(stg + off_region) : (void*)(c.region + r0), a.region, rn,
+                      cudaMemcpyDeviceToHost, s);
+    if (any_stage) { cudaEventRecord(slot_done[slot], s); slot_chunk[slot] = ci; }
   }
+  if (any_stage) for (int s = 0; s < FV_NSLOT; ++s) drain(s);
   for (int s = 1; s < FV_NSLOT; ++s) {
     cudaEventRecord(ready, w->streams[s]);
     cudaStreamWaitEvent(w->streams[0], ready, 0);

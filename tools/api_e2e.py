@@ -1,0 +1,55 @@
+#!/usr/bin/env python3
+"""Time the drop-in Python API end to end (numpy in, ChainTable out) on a
+C4-shaped batch, split into its stages: flag parsing, assembly, the C-ABI
+call (H2D + kernels + D2H), status-string materialisation.
+
+    python tools/api_e2e.py [rows]
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_27210_b200 as fv                      # noqa: E402
+from paper_2604_27210_b200 import batch as B            # noqa: E402
+from paper_2604_27210_b200 import workloads as W        # noqa: E402
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 10_000_000
+    flag, F, K, t, r, sig = W.c4_params(0, n)
+    chars = W.flag_chars(flag)
+    tb = fv.batch_price("black", chars, F[:1], K, t, r[:1], sigma=sig)
+    px = tb["price"]
+    fv.batch_iv("black", "lbr", chars[:1000], F[:1], K[:1000], t[:1000], r[:1], price=px[:1000])  # warm-up
+    out = {"rows": n}
+    t0 = time.perf_counter()
+    theta = B.parse_flags(chars)
+    out["parse_flags_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    res = fv.batch_iv("black", "lbr", chars, F[:1], K, t, r[:1], price=px)
+    out["batch_iv_total_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _ = np.array(["converged", "fell_back_to_bisection", "below_intrinsic", "above_upper_bound",
+                  "max_iterations"], dtype=object)[np.zeros(n, np.int8)]
+    out["status_strings_s"] = time.perf_counter() - t0
+    lib = fv._native.lib_for_compute()
+    keep, cols = B._columns({"flag": theta, "underlying": F[:1], "strike": K, "t": t, "r": r[:1],
+                             "q": np.zeros(1), "price": px}, "price")
+    iv = np.empty(n)
+    st = np.empty(n, np.int8)
+    err = fv._native.fv_error()
+    t0 = time.perf_counter()
+    lib.fv_batch_iv(0, 1, *cols, n, iv.ctypes.data, st.ctypes.data, None, err)
+    out["c_abi_pageable_s"] = time.perf_counter() - t0
+    out["quotes_per_s_python_api"] = n / out["batch_iv_total_s"]
+    out["quotes_per_s_c_abi_pageable"] = n / out["c_abi_pageable_s"]
+    assert np.array_equal(iv.view(np.int64), res["iv"].view(np.int64))
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
