@@ -333,7 +333,10 @@ __device__ __forceinline__ unsigned int warp_append(unsigned int* counter, bool 
 struct LbrQueues {
   // per-local-row state, structure of arrays (each pass writes / reads whole
   // 32-byte sectors of the fields it touches)
-  double* sx;      double* sbeta;  double* ssqrt_t; double* ss_c;
+  // sqrt(t) and s_c = sqrt(2|x|) are not stored: the solves recompute them
+  // (one sqrt each, the same IEEE expression) instead of a 16-byte write +
+  // read per quote
+  double* sx;      double* sbeta;
   double* sb0;     double* sb1;    double* sE0;     double* sE1;
   int32_t* q[6];         // 0..2: local rows per region class; 3: rows pending anchors;
                          // 4: far-low rows the straight-line solver handed back;
@@ -398,11 +401,12 @@ __device__ __forceinline__ void lbr_norm_row_careful(const KArgs& a, const LbrQu
     stu = o.status;
   }
   if (far_low || pending) {
-    lq.sx[row] = st.x; lq.sbeta[row] = st.beta; lq.ssqrt_t[row] = st.sqrt_t; lq.ss_c[row] = st.s_c;
+    lq.sx[row] = st.x; lq.sbeta[row] = st.beta;
     if (pending) { lq.sb0[row] = st.b0; lq.sE0[row] = st.E0; }   // read by pass 2
+  } else {
+    a.o0[row] = ivu;
+    a.status[row] = (int8_t)stu;
   }
-  a.o0[row] = ivu;
-  a.status[row] = (int8_t)stu;
   if (a.region) a.region[row] = (int8_t)(far_low ? FV_FAR_LOW : -1);
   *far_low_out = far_low;
   *pending_out = pending;
@@ -459,14 +463,17 @@ __global__ void __launch_bounds__(256, FV_NORM_MINB) k_lbr_normalize(KArgs a, Lb
         }
       }
       if (far_low || pending) {
-        lq.sx[row] = st.x; lq.sbeta[row] = st.beta; lq.ssqrt_t[row] = st.sqrt_t; lq.ss_c[row] = st.s_c;
+        lq.sx[row] = st.x; lq.sbeta[row] = st.beta;
         if (pending) { lq.sb0[row] = st.b0; lq.sE0[row] = st.E0; }   // read by pass 2
       }
-      if (!flagged) {
+      // outputs of finished rows only: far-low / pending rows get theirs from
+      // the solve that finishes them (one writer per row, no placeholder
+      // write of 9 B per quote), flagged rows from the replay pass
+      if (!(flagged || far_low || pending)) {
         a.o0[row] = ivu;
         a.status[row] = (int8_t)stu;
-        if (a.region) a.region[row] = (int8_t)(far_low ? FV_FAR_LOW : -1);
       }
+      if (a.region && !flagged) a.region[row] = (int8_t)(far_low ? FV_FAR_LOW : -1);
       if (u) { pend[1] = pending; flow[1] = far_low; rep[1] = flagged; }
       else { pend[0] = pending; flow[0] = far_low; rep[0] = flagged; }
     }
@@ -521,7 +528,8 @@ __global__ void __launch_bounds__(256, FV_ANCH_MINB) k_lbr_anchors(KArgs a, LbrQ
     FvLbrState st;
     if (j < n) {
       row = lq.q[3][j];
-      st.x = lq.sx[row]; st.beta = lq.sbeta[row]; st.s_c = lq.ss_c[row];
+      st.x = lq.sx[row]; st.beta = lq.sbeta[row];
+      { FvExc e0 = {0, 0, 0.0}; st.s_c = py_sqrt(2.0 * fv_fabs(st.x), e0); }
       st.b0 = lq.sb0[row]; st.E0 = lq.sE0[row];
       FvExc e = {0, 0, 0.0};
       region = fv_lbr_anchor_rest(st, e);
@@ -570,7 +578,9 @@ __global__ void __launch_bounds__(256, FV_FAST_MINB) k_lbr_far_low_fast(KArgs a,
       ent = q[j];
       const int32_t row = ent >> 1;
       FvLbrState st;
-      st.x = lq.sx[row]; st.beta = lq.sbeta[row]; st.sqrt_t = lq.ssqrt_t[row]; st.s_c = lq.ss_c[row];
+      st.x = lq.sx[row]; st.beta = lq.sbeta[row];
+      st.sqrt_t = fx_sqrt(ld1(a.t, row), bad);
+      st.s_c = fx_sqrt(2.0 * fv_fabs(st.x), bad);
       st.b0 = st.b1 = st.E0 = st.E1 = 0.0;
       FvLbrOut o = fx_lbr_far_low(st, bad);
       if (!bad) {
@@ -593,7 +603,9 @@ __global__ void __launch_bounds__(256, FV_SOLVE_MINB) k_lbr_solve(KArgs a, LbrQu
     const int32_t ent = q[j];
     const int32_t row = ent >> 1;
     FvLbrState st;
-    st.x = lq.sx[row]; st.beta = lq.sbeta[row]; st.sqrt_t = lq.ssqrt_t[row]; st.s_c = lq.ss_c[row];
+    st.x = lq.sx[row]; st.beta = lq.sbeta[row];
+    st.sqrt_t = sqrt(ld1(a.t, row));
+    { FvExc e0 = {0, 0, 0.0}; st.s_c = py_sqrt(2.0 * fv_fabs(st.x), e0); }
     if (R == FV_NEAR_LOW) { st.b0 = lq.sb0[row]; st.b1 = lq.sb1[row]; st.E0 = lq.sE0[row]; st.E1 = lq.sE1[row]; }
     else { st.b0 = st.b1 = st.E0 = st.E1 = 0.0; }
     const int region = (R == FV_NEAR_LOW) ? ((ent & 1) ? FV_NEAR_HIGH : FV_NEAR_LOW) : R;
@@ -1054,7 +1066,7 @@ cudaError_t ensure_lbr(DevWork* w, int slot, int64_t rows) {
   w->lbr_q[slot] = nullptr;
   w->lbr_cap[slot] = 0;
   int64_t cap = rows < 4096 ? 4096 : ((rows + 255) / 256) * 256;   // keeps every SoA field 16B-aligned
-  CK(cudaMalloc(&w->lbr_state[slot], sizeof(double) * 8 * cap));
+  CK(cudaMalloc(&w->lbr_state[slot], sizeof(double) * 6 * cap));
   CK(cudaMalloc(&w->lbr_q[slot], sizeof(int32_t) * 6 * cap));
   w->lbr_cap[slot] = cap;
   return cudaSuccess;
@@ -1137,8 +1149,8 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
           LbrQueues lq;
           double* sb = w->lbr_state[slot];
           const int64_t cp = w->lbr_cap[slot];
-          lq.sx = sb; lq.sbeta = sb + cp; lq.ssqrt_t = sb + 2 * cp; lq.ss_c = sb + 3 * cp;
-          lq.sb0 = sb + 4 * cp; lq.sb1 = sb + 5 * cp; lq.sE0 = sb + 6 * cp; lq.sE1 = sb + 7 * cp;
+          lq.sx = sb; lq.sbeta = sb + cp;
+          lq.sb0 = sb + 2 * cp; lq.sb1 = sb + 3 * cp; lq.sE0 = sb + 4 * cp; lq.sE1 = sb + 5 * cp;
           for (int c3 = 0; c3 < 6; ++c3) lq.q[c3] = w->lbr_q[slot] + c3 * w->lbr_cap[slot];
           lq.count = w->lbr_count + 8 * slot;
           CK(cudaMemsetAsync(lq.count, 0, 8 * sizeof(unsigned int), s));

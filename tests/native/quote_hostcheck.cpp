@@ -118,8 +118,9 @@ int64_t qh_classify_fast_check(int model, const int8_t* flag, const double* un, 
       uint64_t ua, ub; memcpy(&ua, &of.sigma, 8); memcpy(&ub, &oc.sigma, 8);
       same = of.status == oc.status && (oc.status != FV_IV_CONVERGED || ua == ub);
     } else if (same) {
-      const double fa[6] = {sf.x, sf.beta, sf.sqrt_t, sf.s_c, sf.b0, sf.E0};
-      const double ca[6] = {sc.x, sc.beta, sc.sqrt_t, sc.s_c, sc.b0, sc.E0};
+      // (sqrt_t is recomputed by the solves, not handed on by this pass)
+      const double fa[5] = {sf.x, sf.beta, sf.s_c, sf.b0, sf.E0};
+      const double ca[5] = {sc.x, sc.beta, sc.s_c, sc.b0, sc.E0};
       same = memcmp(fa, ca, sizeof(fa)) == 0;
     }
     if (!same) ++bad;
