@@ -116,7 +116,7 @@ def last_outcome(lib):
     return cr, er, ec
 
 
-NKERNEL = 12
+NKERNEL = 13
 
 
 def kernel_times(lib):

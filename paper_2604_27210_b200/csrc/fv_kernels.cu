@@ -338,11 +338,12 @@ struct LbrQueues {
   // read per quote
   double* sx;      double* sbeta;
   double* sb0;     double* sb1;    double* sE0;     double* sE1;
-  int32_t* q[6];         // 0..2: local rows per region class; 3: rows pending anchors;
+  int32_t* q[7];         // 0..2: local rows per region class; 3: rows pending anchors;
                          // 4: far-low rows the straight-line solver handed back;
-                         // 5: rows the straight-line normalize pass handed back
-  unsigned int* count;   // [8]: queue lengths [0..5], work counters of the far-low
-                         // solve [6] and the normalize pass [7]
+                         // 5: rows the straight-line normalize pass handed back;
+                         // 6: near rows the straight-line near solver handed back
+  unsigned int* count;   // [16]: queue lengths [0..6], work counters of the far-low
+                         // solve [7], the normalize pass [8] and the near solve [9]
 };
 
 __device__ __forceinline__ int region_class(int region) {
@@ -426,7 +427,7 @@ __global__ void __launch_bounds__(256, FV_NORM_MINB) k_lbr_normalize(KArgs a, Lb
   // k_lbr_far_low_fast: per-row cost depends on the strike band)
   for (;;) {
     unsigned int base = 0;
-    if (lane == 0) base = atomicAdd(lq.count + 7, 32u);
+    if (lane == 0) base = atomicAdd(lq.count + 8, 32u);
     base = __shfl_sync(0xffffffffu, base, 0);
     if ((int64_t)base >= npair) break;
     const int64_t j = (int64_t)base + lane;
@@ -568,7 +569,7 @@ __global__ void __launch_bounds__(256, FV_FAST_MINB) k_lbr_far_low_fast(KArgs a,
   const int lane = threadIdx.x & 31;
   for (;;) {
     unsigned int base = 0;
-    if (lane == 0) base = atomicAdd(lq.count + 6, 32u);
+    if (lane == 0) base = atomicAdd(lq.count + 7, 32u);
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base >= n) break;
     const unsigned int j = base + lane;
@@ -593,10 +594,44 @@ __global__ void __launch_bounds__(256, FV_FAST_MINB) k_lbr_far_low_fast(KArgs a,
   }
 }
 
+// Near-region solve on the straight-line routines (fx_lbr_near) over queue
+// 1; a quote that leaves their domain goes to queue 6 for the careful solver.
+__global__ void __launch_bounds__(256, FV_FAST_MINB) k_lbr_near_fast(KArgs a, LbrQueues lq) {
+  const unsigned int n = lq.count[1];
+  const int32_t* q = lq.q[1];
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned int base = 0;
+    if (lane == 0) base = atomicAdd(lq.count + 9, 32u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= n) break;
+    const unsigned int j = base + lane;
+    bool bad = false;
+    int32_t ent = 0;
+    if (j < n) {
+      ent = q[j];
+      const int32_t row = ent >> 1;
+      FvLbrState st;
+      st.x = lq.sx[row]; st.beta = lq.sbeta[row];
+      st.sqrt_t = fx_sqrt(ld1(a.t, row), bad);
+      st.s_c = fx_sqrt(2.0 * fv_fabs(st.x), bad);
+      st.b0 = lq.sb0[row]; st.b1 = lq.sb1[row]; st.E0 = lq.sE0[row]; st.E1 = lq.sE1[row];
+      FvLbrOut o = fx_lbr_near((ent & 1) ? FV_NEAR_HIGH : FV_NEAR_LOW, st, bad);
+      if (!bad) {
+        a.o0[row] = (o.status == FV_IV_CONVERGED) ? o.sigma : __builtin_nan("");
+        a.status[row] = (int8_t)o.status;
+      }
+    }
+    const unsigned int slot = warp_append(lq.count + 6, bad);
+    if (bad) lq.q[6][slot] = ent;
+  }
+}
+
 template <int R>
 __global__ void __launch_bounds__(256, FV_SOLVE_MINB) k_lbr_solve(KArgs a, LbrQueues lq) {
   // far-low: the careful solver over the quotes the straight-line one handed back
-  const int c = R == FV_FAR_LOW ? 4 : (R == FV_FAR_HIGH ? 2 : 1);
+  // near: the careful solver over the quotes the straight-line one handed back
+  const int c = R == FV_FAR_LOW ? 4 : (R == FV_FAR_HIGH ? 2 : 6);
   const unsigned int n = lq.count[c];
   const int32_t* q = lq.q[c];
   for (unsigned int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
@@ -949,7 +984,7 @@ thread_local int64_t t_launches = 0;
 const char* const kKernelNames[FV_NKERNEL] = {
     "k_price", "k_price_greeks", "k_lbr_normalize", "k_lbr_normalize_replay", "k_lbr_anchors",
     "k_lbr_far_low_fast", "k_lbr_solve<FAR_LOW>", "k_lbr_solve<NEAR>", "k_lbr_solve<FAR_HIGH>",
-    "k_halley_setup", "k_halley_sm", "k_halley_sm<careful>"};
+    "k_halley_setup", "k_halley_sm", "k_halley_sm<careful>", "k_lbr_near_fast"};
 struct TimedLaunch { int id; cudaEvent_t a, b; };
 thread_local bool t_timing = false;
 thread_local std::vector<TimedLaunch> t_timed;
@@ -998,6 +1033,7 @@ struct DevWork {
   int32_t* hsm_ridx[FV_NSLOT] = {};         // records handed back by the fast pass
   int64_t hsm_cap[FV_NSLOT] = {};
   int blocks_hset = 0;
+  int blocks_lbr_nfast = 0;
   int blocks_lbr_norm = 0, blocks_lbr_nrep = 0, blocks_lbr_anch = 0, blocks_lbr_fast = 0, blocks_lbr_fl = 0, blocks_lbr_near = 0, blocks_lbr_fh = 0;
   std::mutex mu;
 };
@@ -1029,13 +1065,14 @@ cudaError_t get_work(DevWork** out) {
     CK(cudaMalloc(&w->explain, sizeof(ExplainOut)));
     w->blocks_price = occupancy_blocks((const void*)k_price, w->sm_count);
     w->blocks_greeks = occupancy_blocks((const void*)k_price_greeks<true, true>, w->sm_count);
-    CK(cudaMalloc(&w->lbr_count, sizeof(unsigned int) * 8 * FV_NSLOT));
+    CK(cudaMalloc(&w->lbr_count, sizeof(unsigned int) * 16 * FV_NSLOT));
     w->blocks_lbr_norm = occupancy_blocks((const void*)k_lbr_normalize, w->sm_count);
     w->blocks_lbr_nrep = occupancy_blocks((const void*)k_lbr_normalize_replay, w->sm_count);
     w->blocks_lbr_anch = occupancy_blocks((const void*)k_lbr_anchors, w->sm_count);
     w->blocks_lbr_fast = occupancy_blocks((const void*)k_lbr_far_low_fast, w->sm_count);
     w->blocks_lbr_fl = occupancy_blocks((const void*)k_lbr_solve<FV_FAR_LOW>, w->sm_count);
     w->blocks_lbr_near = occupancy_blocks((const void*)k_lbr_solve<FV_NEAR_LOW>, w->sm_count);
+    w->blocks_lbr_nfast = occupancy_blocks((const void*)k_lbr_near_fast, w->sm_count);
     w->blocks_lbr_fh = occupancy_blocks((const void*)k_lbr_solve<FV_FAR_HIGH>, w->sm_count);
     w->blocks_hsm = occupancy_blocks((const void*)k_halley_sm<true>, w->sm_count);
     w->blocks_hsm2 = occupancy_blocks((const void*)k_halley_sm<false>, w->sm_count);
@@ -1067,7 +1104,7 @@ cudaError_t ensure_lbr(DevWork* w, int slot, int64_t rows) {
   w->lbr_cap[slot] = 0;
   int64_t cap = rows < 4096 ? 4096 : ((rows + 255) / 256) * 256;   // keeps every SoA field 16B-aligned
   CK(cudaMalloc(&w->lbr_state[slot], sizeof(double) * 6 * cap));
-  CK(cudaMalloc(&w->lbr_q[slot], sizeof(int32_t) * 6 * cap));
+  CK(cudaMalloc(&w->lbr_q[slot], sizeof(int32_t) * 7 * cap));
   w->lbr_cap[slot] = cap;
   return cudaSuccess;
 }
@@ -1151,9 +1188,9 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
           const int64_t cp = w->lbr_cap[slot];
           lq.sx = sb; lq.sbeta = sb + cp;
           lq.sb0 = sb + 2 * cp; lq.sb1 = sb + 3 * cp; lq.sE0 = sb + 4 * cp; lq.sE1 = sb + 5 * cp;
-          for (int c3 = 0; c3 < 6; ++c3) lq.q[c3] = w->lbr_q[slot] + c3 * w->lbr_cap[slot];
-          lq.count = w->lbr_count + 8 * slot;
-          CK(cudaMemsetAsync(lq.count, 0, 8 * sizeof(unsigned int), s));
+          for (int c3 = 0; c3 < 7; ++c3) lq.q[c3] = w->lbr_q[slot] + c3 * w->lbr_cap[slot];
+          lq.count = w->lbr_count + 16 * slot;
+          CK(cudaMemsetAsync(lq.count, 0, 16 * sizeof(unsigned int), s));
           const int64_t cap1 = (b.n + 255) / 256;
           auto g = [cap1](int blocks) { return (int)(cap1 < blocks ? cap1 : blocks); };
           FV_LAUNCH(FV_KID_LBR_NORM, s, k_lbr_normalize<<<blocks_for(w->blocks_lbr_norm, b.n), 256, 0, s>>>(b, lq));
@@ -1161,6 +1198,7 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
           FV_LAUNCH(FV_KID_LBR_ANCH, s, k_lbr_anchors<<<g(w->blocks_lbr_anch), 256, 0, s>>>(b, lq));
           FV_LAUNCH(FV_KID_LBR_FAST, s, k_lbr_far_low_fast<<<g(w->blocks_lbr_fast), 256, 0, s>>>(b, lq));
           FV_LAUNCH(FV_KID_LBR_FL, s, k_lbr_solve<FV_FAR_LOW><<<g(w->blocks_lbr_fl), 256, 0, s>>>(b, lq));
+          FV_LAUNCH(FV_KID_LBR_NEAR_FAST, s, k_lbr_near_fast<<<g(w->blocks_lbr_nfast), 256, 0, s>>>(b, lq));
           FV_LAUNCH(FV_KID_LBR_NEAR, s, k_lbr_solve<FV_NEAR_LOW><<<g(w->blocks_lbr_near), 256, 0, s>>>(b, lq));
           FV_LAUNCH(FV_KID_LBR_FH, s, k_lbr_solve<FV_FAR_HIGH><<<g(w->blocks_lbr_fh), 256, 0, s>>>(b, lq));
         }

@@ -189,6 +189,34 @@ int64_t qh_halley_fast_check(int model, const int8_t* flag, const double* un, co
   return bad;
 }
 
+// The straight-line near-region solver (fx_lbr_near) against the careful one
+// on the near-region quotes of a batch: mismatching unflagged rows; *nflag
+// gets the flagged ones, *nnear the near quotes seen.
+int64_t qh_near_fast_check(const int8_t* flag, const double* F, const double* k, const double* t,
+                           const double* r, const double* px, int64_t n, int64_t* nnear, int64_t* nflag) {
+  int64_t bad = 0, nn = 0, nb = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    FvExc e = {0, 0, 0.0};
+    FvLbrState st; FvLbrOut o;
+    if (!(t[i] > 0.0)) continue;
+    if (fv_lbr_classify((double)flag[i], F[i], k[i], t[i], r[i], px[i], st, o, e)) continue;
+    if (o.region != FV_NEAR_LOW && o.region != FV_NEAR_HIGH) continue;
+    ++nn;
+    FvExc e2 = {0, 0, 0.0};
+    bool flagged = false;
+    FvLbrOut a = fx_lbr_near(o.region, st, flagged);
+    FvLbrOut c = fv_lbr_solve<FV_NEAR_LOW>(o.region, st, e2);
+    if (flagged) { ++nb; continue; }
+    uint64_t ua, uc; memcpy(&ua, &a.sigma, 8); memcpy(&uc, &c.sigma, 8);
+    bool same = (ua == uc || (a.sigma != a.sigma && c.sigma != c.sigma)) && a.status == c.status &&
+                a.iterations == c.iterations && e2.code == 0;
+    if (!same) ++bad;
+  }
+  *nnear = nn;
+  *nflag = nb;
+  return bad;
+}
+
 // The straight-line far-low solver (fv_fast.h) against the careful one on the
 // far-low quotes of a batch: returns mismatching unflagged rows; *nflag gets
 // the flagged (handed-back) ones.

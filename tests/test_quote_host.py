@@ -247,3 +247,26 @@ def test_straight_line_halley_matches_careful(Q, case):
     assert bad == 0
     if case != "c5":
         assert nb.value < len(flag) // 100, nb.value
+
+
+@pytest.mark.parametrize("case", ["c1", "wide"])
+def test_straight_line_near_matches_careful(Q, case):
+    """fv_fast.h's near-region solver (Hermite guess + Householder(3) on the
+    middle objective, all three normalized_black branches): every quote it
+    does not flag is bit-identical to the careful solver."""
+    from oracle import fvoracle as O
+    from paper_2604_27210_b200 import workloads as W
+    Q.qh_near_fast_check.restype = ctypes.c_int64
+    flag, S, K, t, r, q, sig = W.chain_draws(100_000, seed=50)
+    if case == "wide":                     # deep strikes, long/short maturities, high vols
+        rng = np.random.default_rng(51)
+        K = S * np.exp(rng.uniform(-4, 4, len(S)))
+        t = 10.0 ** rng.uniform(-3, 1.3, len(S))
+        sig = rng.uniform(0.05, 3.0, len(S))
+    px = O.rows_price("black", flag, S, K, t, r, 0.0, sig)["price"]
+    cols = [np.ascontiguousarray(a) for a in (flag, S, K, t, r, px)]
+    nn, nb = ctypes.c_int64(0), ctypes.c_int64(0)
+    bad = Q.qh_near_fast_check(*[_p(c) for c in cols], ctypes.c_int64(len(flag)), ctypes.byref(nn),
+                               ctypes.byref(nb))
+    assert nn.value > 10_000 and bad == 0, (nn.value, bad)
+    assert nb.value < nn.value // 20, (nb.value, nn.value)
