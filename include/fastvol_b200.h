@@ -171,13 +171,13 @@ FV_API int fv_last_outcome(int64_t* check_rows /*[FV_NCHECK]*/, int64_t* exc_row
 FV_API int fv_selftest_div_const(int64_t n, uint64_t seed, int64_t* mismatches);
 
 /* Self-test of the straight-line routines of the far-low solver (fv_fast.h)
- * against their careful forms on n random inputs each, for 10 routines
+ * against their careful forms on n random inputs each, for 11 routines
  * (division, exp, log, pow, erfcx, normalized_black_log, constant division,
- * sqrt, two-path log, erfc):
+ * sqrt, two-path log, erfc, erfcx incl. negative / zero arguments):
  * per routine, the inputs whose result differs although the routine did not
  * flag them (must be 0) and the inputs it flagged for the careful path. */
-FV_API int fv_selftest_fast(int64_t n, uint64_t seed, int64_t* mismatches /*[10]*/,
-                            int64_t* flagged /*[10]*/);
+FV_API int fv_selftest_fast(int64_t n, uint64_t seed, int64_t* mismatches /*[11]*/,
+                            int64_t* flagged /*[11]*/);
 
 /* Per-kernel timing (diagnostics; off by default).  While on, every kernel
  * the calling thread launches is bracketed by CUDA events on its stream;

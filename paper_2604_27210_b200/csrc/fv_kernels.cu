@@ -40,7 +40,7 @@
 #define FV_SOLVE_MINB 4
 #endif
 #ifndef FV_ANCH_MINB
-#define FV_ANCH_MINB 1
+#define FV_ANCH_MINB 3
 #endif
 #ifndef FV_NORM_MINB
 #define FV_NORM_MINB 3
@@ -518,6 +518,8 @@ __global__ void __launch_bounds__(256) k_lbr_normalize_replay(KArgs a, LbrQueues
 
 // Pass 2: the remaining anchors + region (fv_lbr_anchor_rest) over the
 // pending queue (row order); appends each quote to its region class queue.
+__device__ __noinline__ int anchor_rest_careful(FvLbrState& st, FvExc& e) { return fv_lbr_anchor_rest(st, e); }
+
 __global__ void __launch_bounds__(256, FV_ANCH_MINB) k_lbr_anchors(KArgs a, LbrQueues lq) {
   const unsigned int n = lq.count[3];
   const unsigned int stride = gridDim.x * blockDim.x;
@@ -533,7 +535,11 @@ __global__ void __launch_bounds__(256, FV_ANCH_MINB) k_lbr_anchors(KArgs a, LbrQ
       { FvExc e0 = {0, 0, 0.0}; st.s_c = py_sqrt(2.0 * fv_fabs(st.x), e0); }
       st.b0 = lq.sb0[row]; st.E0 = lq.sE0[row];
       FvExc e = {0, 0, 0.0};
-      region = fv_lbr_anchor_rest(st, e);
+      bool flagged = false;
+      FvLbrState sf = st;
+      region = fx_lbr_anchor_rest(sf, flagged);            // straight-line form
+      if (flagged) region = anchor_rest_careful(st, e);   // range edge: careful form
+      else st = sf;
       if (region < 0) {
         publish_exc(&a.st->exc_first, e.code, a.row0 + row);
         a.o0[row] = __builtin_nan("");
@@ -867,7 +873,7 @@ __device__ __forceinline__ double st_bits(uint64_t u, int e_lo, int e_hi) {
 __device__ __forceinline__ bool st_same(double a, double b) {
   return __double_as_longlong(a) == __double_as_longlong(b) || (a != a && b != b);
 }
-#define FX_NTEST 10
+#define FX_NTEST 11
 __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mism, unsigned long long* flg) {
   unsigned long long lm[FX_NTEST] = {}, lf[FX_NTEST] = {};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -955,6 +961,16 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
       bad = false;
       const double f = fx_erfc(x, bad);
       if (bad) ++lf[9]; else if (!st_same(f, fv_erfc(x))) ++lm[9];
+    }
+    // 10: erfcx over [-6.2, 60], tiny |x| (incl. +-0: y100 == 100) and wide x
+    {
+      const int sel = (int)((u3 >> 24) & 3);
+      double x = sel == 0 ? st_uniform(u1) * 66.2 - 6.2
+               : (sel == 1 ? st_bits(u1, -70, -30) : (sel == 2 ? 0.0 : exp10(st_uniform(u1) * 11.0 - 3.0)));
+      if ((u3 >> 26) & 1) x = -x;
+      bad = false;
+      const double f = fx_erfcx_any(x, bad);
+      if (bad) ++lf[10]; else if (!st_same(f, fv_erfcx_i(x))) ++lm[10];
     }
     // 8: log, both paths (half of the inputs within 2^-4 of 1)
     {

@@ -189,6 +189,36 @@ int64_t qh_halley_fast_check(int model, const int8_t* flag, const double* un, co
   return bad;
 }
 
+// The straight-line second anchor stage (fx_lbr_anchor_rest) against the
+// careful one on the non-far-low quotes of a batch.
+int64_t qh_anchor_rest_fast_check(const int8_t* flag, const double* F, const double* k, const double* t,
+                                  const double* r, const double* px, int64_t n, int64_t* nseen, int64_t* nflag) {
+  int64_t bad = 0, ns = 0, nb = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    FvExc e = {0, 0, 0.0};
+    FvLbrState st; FvLbrOut o;
+    if (!(t[i] > 0.0)) continue;
+    if (fv_lbr_normalize((double)flag[i], F[i], k[i], t[i], r[i], px[i], st, o, e)) continue;
+    if (fv_lbr_anchor_lo(st, e) != FV_NEAR_LOW) continue;
+    ++ns;
+    FvLbrState sf = st, sc = st;
+    bool flagged = false;
+    FvExc e2 = {0, 0, 0.0};
+    const int rf = fx_lbr_anchor_rest(sf, flagged);
+    const int rc = fv_lbr_anchor_rest(sc, e2);
+    if (flagged) { ++nb; continue; }
+    bool same = rf == rc && e2.code == 0;
+    if (same && rc != FV_FAR_HIGH) {
+      const double fa[4] = {sf.b0, sf.b1, sf.E0, sf.E1}, ca[4] = {sc.b0, sc.b1, sc.E0, sc.E1};
+      same = memcmp(fa, ca, sizeof(fa)) == 0;
+    }
+    if (!same) ++bad;
+  }
+  *nseen = ns;
+  *nflag = nb;
+  return bad;
+}
+
 // The straight-line near-region solver (fx_lbr_near) against the careful one
 // on the near-region quotes of a batch: mismatching unflagged rows; *nflag
 // gets the flagged ones, *nnear the near quotes seen.

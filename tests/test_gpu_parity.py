@@ -338,7 +338,7 @@ def test_fast_routines_match_careful_forms():
     the careful routine bit for bit (and the flagged share stays small)."""
     from paper_2604_27210_b200 import _native
     lib = _native.lib_for_compute()
-    names = ["div", "exp", "log", "pow", "erfcx", "nbl", "div_sqrt2", "sqrt", "log2", "erfc"]
+    names = ["div", "exp", "log", "pow", "erfcx", "nbl", "div_sqrt2", "sqrt", "log2", "erfc", "erfcx_any"]
     mism = (ctypes.c_int64 * len(names))()
     flg = (ctypes.c_int64 * len(names))()
     n = 100_000_000

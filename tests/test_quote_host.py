@@ -270,3 +270,26 @@ def test_straight_line_near_matches_careful(Q, case):
                                ctypes.byref(nb))
     assert nn.value > 10_000 and bad == 0, (nn.value, bad)
     assert nb.value < nn.value // 20, (nb.value, nn.value)
+
+
+@pytest.mark.parametrize("case", ["c1", "wide"])
+def test_straight_line_anchor_rest_matches_careful(Q, case):
+    """fv_fast.h's second anchor stage (b_c, then b_hi): same region and
+    anchor values as the careful stage on every unflagged quote (the central
+    anchor's erfcx argument is 0 up to rounding: erfcx's y100 == 100 case)."""
+    from oracle import fvoracle as O
+    from paper_2604_27210_b200 import workloads as W
+    Q.qh_anchor_rest_fast_check.restype = ctypes.c_int64
+    flag, S, K, t, r, q, sig = W.chain_draws(100_000, seed=60)
+    if case == "wide":
+        rng = np.random.default_rng(61)
+        K = S * np.exp(rng.uniform(-4, 4, len(S)))
+        t = 10.0 ** rng.uniform(-3, 1.3, len(S))
+        sig = rng.uniform(0.05, 3.0, len(S))
+    px = O.rows_price("black", flag, S, K, t, r, 0.0, sig)["price"]
+    cols = [np.ascontiguousarray(a) for a in (flag, S, K, t, r, px)]
+    ns, nb = ctypes.c_int64(0), ctypes.c_int64(0)
+    bad = Q.qh_anchor_rest_fast_check(*[_p(c) for c in cols], ctypes.c_int64(len(flag)), ctypes.byref(ns),
+                                      ctypes.byref(nb))
+    assert ns.value > 10_000 and bad == 0, (ns.value, bad)
+    assert nb.value < ns.value // 20, (nb.value, ns.value)
