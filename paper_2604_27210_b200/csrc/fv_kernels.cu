@@ -42,6 +42,9 @@
 #ifndef FV_ANCH_MINB
 #define FV_ANCH_MINB 3
 #endif
+#ifndef FV_NORM_CLAIM
+#define FV_NORM_CLAIM 128
+#endif
 #ifndef FV_NORM_MINB
 #define FV_NORM_MINB 3
 #endif
@@ -425,10 +428,15 @@ __global__ void __launch_bounds__(256, FV_NORM_MINB) k_lbr_normalize(KArgs a, Lb
   const int lane = threadIdx.x & 31;
   // dynamic distribution: each warp takes the next 32 pairs (see
   // k_lbr_far_low_fast: per-row cost depends on the strike band)
+  // (FV_NORM_CLAIM pairs per atomic, processed 32 at a time)
   for (;;) {
-    unsigned int base = 0;
-    if (lane == 0) base = atomicAdd(lq.count + 8, 32u);
-    base = __shfl_sync(0xffffffffu, base, 0);
+    unsigned int claim = 0;
+    if (lane == 0) claim = atomicAdd(lq.count + 8, (unsigned)FV_NORM_CLAIM);
+    claim = __shfl_sync(0xffffffffu, claim, 0);
+    if ((int64_t)claim >= npair) break;
+#pragma unroll 1
+  for (int sub = 0; sub < FV_NORM_CLAIM / 32; ++sub) {
+    const unsigned int base = claim + 32u * sub;
     if ((int64_t)base >= npair) break;
     const int64_t j = (int64_t)base + lane;
     const bool active = j < npair;
@@ -491,6 +499,7 @@ __global__ void __launch_bounds__(256, FV_NORM_MINB) k_lbr_normalize(KArgs a, Lb
       if (rep[0]) { lq.q[5][slot++] = (int32_t)i; }
       if (rep[1]) { lq.q[5][slot] = (int32_t)(i + 1); }
     }
+  }
   }
 }
 
