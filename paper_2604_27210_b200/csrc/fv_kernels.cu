@@ -1,27 +1,34 @@
 // fv_kernels.cu -- sm_100a kernels + the C ABI (include/fastvol_b200.h) for
 // the batched pricing / Greeks / implied-vol path.
 //
-// Execution model (one quote = one unit of independent fp64 work):
-//   * persistent grid-stride kernels, grid = SMs x resident CTAs, each thread
-//     owns a PAIR of adjacent quotes so structure-of-arrays columns are read
-//     with 128-bit (double2 / char2) coalesced loads and written back the same
-//     way; broadcast (stride-0) columns are a single cached load;
+// Execution model (one quote = one unit of independent fp64 work, one quote
+// per thread, no tensor cores -- the path is scalar fp64 transcendentals):
+//   * every hot pass runs the straight-line routines of fv_fast.h (main paths
+//     of the glibc / scipy restatements, branch-free, with range flags); a
+//     quote they flag is recomputed from scratch by the careful routines of
+//     fv_quote.h -- through a replay queue (LBR passes, Halley) or an
+//     out-of-line careful row (pricing, anchors) -- so results never depend
+//     on which path ran;
+//   * LBR: normalize + first anchor (k_lbr_normalize: a 16-byte pair of rows
+//     per thread), remaining anchors only for non-far-low quotes
+//     (k_lbr_anchors), then region-uniform solves over dense row queues
+//     (k_lbr_far_low_fast, k_lbr_near_fast, k_lbr_solve<FAR_HIGH>); work is
+//     handed out per warp by atomic counters (dynamic load balance);
+//   * Halley: a setup pass, then a persistent per-lane state machine with
+//     refill whose shared step is one black_kernel evaluation (its two CDFs
+//     through a warp's range-bucketed erfc);
+//   * pricing / Greeks: one row per thread, 8-byte coalesced column access;
 //   * the reference's batch validation (batch.py:104-124, :144-147) is fused
-//     into the compute pass: each row's failed checks go to a per-check
+//     into the first pass: each row's failed checks go to a per-check
 //     atomicMin, so the first failing row per check comes out of the same HBM
-//     read that feeds the solver;
-//   * rows whose reference execution would raise a Python exception publish
-//     (row << 8 | code) through one atomicMin -- the lowest raising row wins,
-//     exactly as _run_chunked surfaces it (batch.py:166-178);
-//   * Halley IV (solver.py:49-161) runs in two phases: phase 1 (setup + <= 16
-//     Halley steps) finishes ~96% of quotes and appends the rest, with their
-//     bracket state, to a compact queue (warp-aggregated atomics); phase 2
-//     runs the <= 128-step bisection tail on that dense queue, so lanes that
-//     finished early do not idle behind the tail;
-//   * host-pointer calls stream through chunked pinned/pageable H2D ->
-//     kernel -> D2H on NSLOT streams so copies overlap compute.
-// All arithmetic is fv_quote.h / fv_libm.h (bit-faithful to the reference);
-// compile with -fmad=false.
+//     read that feeds the solver; rows whose reference execution would raise
+//     a Python exception publish (row << 8 | code) through one atomicMin --
+//     the lowest raising row wins, exactly as _run_chunked surfaces it
+//     (batch.py:166-178);
+//   * host-pointer calls stream through chunked H2D -> kernels -> D2H on
+//     NSLOT streams (pageable buffers via pinned staging with threaded host
+//     copies) so copies overlap compute.
+// All arithmetic is bit-faithful to the reference; compile with -fmad=false.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -49,7 +56,7 @@
 #define FV_NORM_MINB 3
 #endif
 #ifndef FV_PG_MINB
-#define FV_PG_MINB 2
+#define FV_PG_MINB 3
 #endif
 #ifndef FV_FAST_MINB
 #define FV_FAST_MINB 4
@@ -96,25 +103,6 @@ __device__ __forceinline__ void ldf2(const DFlag& c, int64_t i, bool two, int& a
     b = two ? c.p[(i + 1) * c.stride] : 0;
   }
 }
-__device__ __forceinline__ void st2(double* p, int64_t i, bool two, bool vec, double a, double b) {
-  if (!p) return;
-  if (two && vec) {
-    *reinterpret_cast<double2*>(p + i) = make_double2(a, b);
-  } else {
-    p[i] = a;
-    if (two) p[i + 1] = b;
-  }
-}
-__device__ __forceinline__ void st2i8(int8_t* p, int64_t i, bool two, int a, int b) {
-  if (!p) return;
-  if (two && (((uintptr_t)(p + i)) & 1) == 0) {
-    *reinterpret_cast<char2*>(p + i) = make_char2((signed char)a, (signed char)b);
-  } else {
-    p[i] = (int8_t)a;
-    if (two) p[i + 1] = (int8_t)b;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // status block shared by all kernels of one call
 // ---------------------------------------------------------------------------
@@ -133,7 +121,6 @@ struct KArgs {
   DCol un, k, t, r, q, last;
   int64_t n;           // rows in this launch
   int64_t row0;        // global index of local row 0
-  int out_vec;         // all double outputs 16B aligned
   double* o0;          // price | iv
   double* o1;          // delta
   double* o2;          // gamma
@@ -219,98 +206,71 @@ __device__ __noinline__ FvGreeks price_greeks_row_careful(const KArgs& a, int64_
 }
 
 // Pricing (batch_price): straight-line row (fx_price_row), careful row where
-// it flags.  Inputs of a pair are picked with selects (no local-memory
-// arrays); 16-byte loads and stores of the pair.
+// it flags.  One row per thread: 8-byte loads and stores, 256 B per warp per
+// column, fully coalesced.  (A 16-byte pair per thread held both rows' state
+// across the row loop -- 128 registers, 16 warps/SM; one row per thread fits
+// 80 registers and runs 19 % faster on C3, profiles/README.md.)
 __global__ void __launch_bounds__(256, FV_PG_MINB) k_price(KArgs a) {
   __shared__ double sm_x[8][64], sm_r[8][64];      // range-bucketed erfc staging
   __shared__ unsigned char sm_f[8][64];
   const int wib = threadIdx.x >> 5;
-  const int64_t npair = (a.n + 1) >> 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t nloop = (npair + stride - 1) / stride;
-  for (int64_t it = 0; it < nloop; ++it) {          // warp-uniform trip count
-    const int64_t j = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool active = j < npair;
-    const int64_t i = active ? 2 * j : 0;
-    const bool two = active && i + 1 < a.n;
-    Pair p;
-    load_pair(a, i, two, p);
-    double out0 = 0.0, out1 = 0.0;
-#pragma unroll 1
-    for (int u = 0; u < 2; ++u) {           // warp-uniform trip count (bucketed erfc)
-      const bool valid = active && (u == 0 || two);
-      const int fl = u ? p.fl[1] : p.fl[0];
-      const double un = u ? p.un[1] : p.un[0], k = u ? p.k[1] : p.k[0];
-      const double t = u ? p.t[1] : p.t[0], r = u ? p.r[1] : p.r[0];
-      const double q = u ? p.q[1] : p.q[0], sg = u ? p.last[1] : p.last[0];
-      const uint32_t bad = valid ? row_checks(a, fl, un, k, t, r, q, sg) : 0u;
-      bool flagged = false;
-      double v = fx_price_row(a.model, (double)fl, un, k, t, r, q, sg, flagged, valid && !bad,
-                              sm_x[wib], sm_r[wib], sm_f[wib]);
-      if (valid) {
-        if (bad) {
-          publish_checks(a.st, bad, a.row0 + i + u);
-          v = __builtin_nan("");
-        } else if (flagged) {
-          v = price_row_careful(a, i + u, fl, un, k, t, r, q, sg);
-        }
-      }
-      if (u) out1 = v; else out0 = v;
+  const int64_t nloop = (a.n + stride - 1) / stride;
+  for (int64_t it = 0; it < nloop; ++it) {          // warp-uniform trip count (bucketed erfc)
+    const int64_t r0 = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool valid = r0 < a.n;
+    const int64_t row = valid ? r0 : 0;
+    const int fl = ldf1(a.flag, row);
+    const double un = ld1(a.un, row), k = ld1(a.k, row), t = ld1(a.t, row), r = ld1(a.r, row);
+    const double q = ld1(a.q, row), sg = ld1(a.last, row);
+    const uint32_t bad = valid ? row_checks(a, fl, un, k, t, r, q, sg) : 0u;
+    bool flagged = false;
+    double v = fx_price_row(a.model, (double)fl, un, k, t, r, q, sg, flagged, valid && !bad,
+                            sm_x[wib], sm_r[wib], sm_f[wib]);
+    if (!valid) continue;
+    if (bad) {
+      publish_checks(a.st, bad, a.row0 + row);
+      v = __builtin_nan("");
+    } else if (flagged) {
+      v = price_row_careful(a, row, fl, un, k, t, r, q, sg);
     }
-    if (active) st2(a.o0, i, two, a.out_vec, out0, out1);
+    a.o0[row] = v;
   }
 }
 
 // Fused price + Greeks (batch_price and/or batch_greeks in one pass):
 // straight-line row (fx_price_greeks_row), careful row where it flags.
+// One row per thread (see k_price).
 template <bool kPrice, bool kGreeks>
 __global__ void __launch_bounds__(256, FV_PG_MINB) k_price_greeks(KArgs a) {
   __shared__ double sm_x[8][64], sm_r[8][64];      // range-bucketed erfc staging
   __shared__ unsigned char sm_f[8][64];
   const int wib = threadIdx.x >> 5;
-  const int64_t npair = (a.n + 1) >> 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t nloop = (npair + stride - 1) / stride;
+  const int64_t nloop = (a.n + stride - 1) / stride;
   for (int64_t it = 0; it < nloop; ++it) {          // warp-uniform trip count
-    const int64_t j = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool active = j < npair;
-    const int64_t i = active ? 2 * j : 0;
-    const bool two = active && i + 1 < a.n;
-    Pair p;
-    load_pair(a, i, two, p);
-    FvGreeks g0, g1;
-#pragma unroll 1
-    for (int u = 0; u < 2; ++u) {           // warp-uniform trip count (bucketed erfc)
-      const bool valid = active && (u == 0 || two);
-      const int fl = u ? p.fl[1] : p.fl[0];
-      const double un = u ? p.un[1] : p.un[0], k = u ? p.k[1] : p.k[0];
-      const double t = u ? p.t[1] : p.t[0], r = u ? p.r[1] : p.r[0];
-      const double q = u ? p.q[1] : p.q[0], sg = u ? p.last[1] : p.last[0];
-      const uint32_t bad = valid ? row_checks(a, fl, un, k, t, r, q, sg) : 0u;
-      bool flagged = false;
-      FvGreeks g = fx_price_greeks_row(a.model, (double)fl, un, k, t, r, q, sg, kGreeks, flagged,
-                                       valid && !bad, sm_x[wib], sm_r[wib], sm_f[wib]);
-      if (valid) {
-        if (bad) {
-          publish_checks(a.st, bad, a.row0 + i + u);
-          g.price = g.delta = g.gamma = g.theta = g.rho = g.vega = __builtin_nan("");
-          g.status = 0;
-        } else if (flagged) {
-          g = price_greeks_row_careful<kPrice, kGreeks>(a, i + u, fl, un, k, t, r, q, sg);
-        }
-      }
-      if (u) g1 = g; else g0 = g;
+    const int64_t r0 = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool valid = r0 < a.n;
+    const int64_t row = valid ? r0 : 0;
+    const int fl = ldf1(a.flag, row);
+    const double un = ld1(a.un, row), k = ld1(a.k, row), t = ld1(a.t, row), r = ld1(a.r, row);
+    const double q = ld1(a.q, row), sg = ld1(a.last, row);
+    const uint32_t bad = valid ? row_checks(a, fl, un, k, t, r, q, sg) : 0u;
+    bool flagged = false;
+    FvGreeks g = fx_price_greeks_row(a.model, (double)fl, un, k, t, r, q, sg, kGreeks, flagged,
+                                     valid && !bad, sm_x[wib], sm_r[wib], sm_f[wib]);
+    if (!valid) continue;
+    if (bad) {
+      publish_checks(a.st, bad, a.row0 + row);
+      g.price = g.delta = g.gamma = g.theta = g.rho = g.vega = __builtin_nan("");
+      g.status = 0;
+    } else if (flagged) {
+      g = price_greeks_row_careful<kPrice, kGreeks>(a, row, fl, un, k, t, r, q, sg);
     }
-    if (!active) continue;
-    if (!two) g1 = g0;
-    if (kPrice) st2(a.o0, i, two, a.out_vec, g0.price, g1.price);
+    if (kPrice) a.o0[row] = g.price;
     if (kGreeks) {
-      st2(a.o1, i, two, a.out_vec, g0.delta, g1.delta);
-      st2(a.o2, i, two, a.out_vec, g0.gamma, g1.gamma);
-      st2(a.o3, i, two, a.out_vec, g0.theta, g1.theta);
-      st2(a.o4, i, two, a.out_vec, g0.rho, g1.rho);
-      st2(a.o5, i, two, a.out_vec, g0.vega, g1.vega);
-      st2i8(a.status, i, two, g0.status, g1.status);
+      a.o1[row] = g.delta; a.o2[row] = g.gamma; a.o3[row] = g.theta; a.o4[row] = g.rho; a.o5[row] = g.vega;
+      if (a.status) a.status[row] = (int8_t)g.status;
     }
   }
 }
@@ -1148,7 +1108,6 @@ KArgs sub_args(const KArgs& a, int64_t off, int64_t len) {
   if (b.region) b.region += off;
   b.n = len;
   b.row0 = a.row0 + off;
-  if (off & 1) b.out_vec = 0;
   return b;
 }
 
@@ -1438,12 +1397,6 @@ KArgs base_args(const Call& c, DevWork* w) {
   return a;
 }
 
-bool outs_aligned(const Call& c, double* const* outs) {
-  for (int i = 0; i < 6; ++i)
-    if (outs[i] && (((uintptr_t)outs[i]) & 15)) return false;
-  (void)c;
-  return true;
-}
 
 int run_device(DevWork* w, const Call& c, cudaStream_t s, uint32_t bcast_bits, fv_error* e1,
                fv_error* e2) {
@@ -1460,7 +1413,6 @@ int run_device(DevWork* w, const Call& c, cudaStream_t s, uint32_t bcast_bits, f
   a.row0 = 0;
   a.o0 = c.outs[0]; a.o1 = c.outs[1]; a.o2 = c.outs[2];
   a.o3 = c.outs[3]; a.o4 = c.outs[4]; a.o5 = c.outs[5];
-  a.out_vec = outs_aligned(c, c.outs);
   if ((ce = cudaMemsetAsync(w->st, 0xff, sizeof(FvDevStatus), s)) != cudaSuccess) return set_cuda_err(e1, ce);
   if ((ce = launch(w, c, a, 0, s)) != cudaSuccess) return set_cuda_err(e1, ce);
   if ((ce = cudaMemcpyAsync(w->st_host, w->st, sizeof(FvDevStatus), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
@@ -1606,7 +1558,6 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
     double* douts[6];
     for (int i = 0; i < 6; ++i) douts[i] = c.outs[i] ? (double*)(base + off_out[i]) : nullptr;
     a.o0 = douts[0]; a.o1 = douts[1]; a.o2 = douts[2]; a.o3 = douts[3]; a.o4 = douts[4]; a.o5 = douts[5];
-    a.out_vec = 1;
     a.status = has_status ? (int8_t*)(base + off_status) : nullptr;
     a.region = has_region ? (int8_t*)(base + off_region) : nullptr;
     if (ci == 0) a_first = a;
