@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(256, FV_PG_MINB) k_price(KArgs a) {
     const double un = ld1(a.un, row), k = ld1(a.k, row), t = ld1(a.t, row), r = ld1(a.r, row);
     const double q = ld1(a.q, row), sg = ld1(a.last, row);
     const uint32_t bad = valid ? row_checks(a, fl, un, k, t, r, q, sg) : 0u;
-    bool flagged = false;
+    FxBad flagged;
     double v = fx_price_row(a.model, (double)fl, un, k, t, r, q, sg, flagged, valid && !bad,
                             sm_x[wib], sm_r[wib], sm_f[wib]);
     if (!valid) continue;
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(256, FV_PG_MINB) k_price_greeks(KArgs a) {
     const double un = ld1(a.un, row), k = ld1(a.k, row), t = ld1(a.t, row), r = ld1(a.r, row);
     const double q = ld1(a.q, row), sg = ld1(a.last, row);
     const uint32_t bad = valid ? row_checks(a, fl, un, k, t, r, q, sg) : 0u;
-    bool flagged = false;
+    FxBad flagged;
     FvGreeks g = fx_price_greeks_row(a.model, (double)fl, un, k, t, r, q, sg, kGreeks, flagged,
                                      valid && !bad, sm_x[wib], sm_r[wib], sm_f[wib]);
     if (!valid) continue;
@@ -410,7 +410,8 @@ __global__ void __launch_bounds__(256, FV_NORM_MINB) k_lbr_normalize(KArgs a, Lb
       const bool valid = active && (u == 0 || two);
       if (!valid) continue;
       const int64_t row = i + u;
-      bool pending = false, far_low = false, flagged = false;
+      bool pending = false, far_low = false;
+      FxBad flagged;
       double ivu = __builtin_nan("");
       int stu = FV_IV_MAX_ITER;
       FvLbrState st;
@@ -443,8 +444,8 @@ __global__ void __launch_bounds__(256, FV_NORM_MINB) k_lbr_normalize(KArgs a, Lb
         a.status[row] = (int8_t)stu;
       }
       if (a.region && !flagged) a.region[row] = (int8_t)(far_low ? FV_FAR_LOW : -1);
-      if (u) { pend[1] = pending; flow[1] = far_low; rep[1] = flagged; }
-      else { pend[0] = pending; flow[0] = far_low; rep[0] = flagged; }
+      if (u) { pend[1] = pending; flow[1] = far_low; rep[1] = (bool)flagged; }
+      else { pend[0] = pending; flow[0] = far_low; rep[0] = (bool)flagged; }
     }
     // queue appends in row order (lane 0's pair, lane 1's pair, ...); far-low
     // entries are 2 * row (the solve's entry format), the others plain rows
@@ -504,7 +505,7 @@ __global__ void __launch_bounds__(256, FV_ANCH_MINB) k_lbr_anchors(KArgs a, LbrQ
       { FvExc e0 = {0, 0, 0.0}; st.s_c = py_sqrt(2.0 * fv_fabs(st.x), e0); }
       st.b0 = lq.sb0[row]; st.E0 = lq.sE0[row];
       FvExc e = {0, 0, 0.0};
-      bool flagged = false;
+      FxBad flagged;
       FvLbrState sf = st;
       region = fx_lbr_anchor_rest(sf, flagged);            // straight-line form
       if (flagged) region = anchor_rest_careful(st, e);   // range edge: careful form
@@ -548,7 +549,7 @@ __global__ void __launch_bounds__(256, FV_FAST_MINB) k_lbr_far_low_fast(KArgs a,
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base >= n) break;
     const unsigned int j = base + lane;
-    bool bad = false;
+    FxBad bad;
     int32_t ent = 0;
     if (j < n) {
       ent = q[j];
@@ -564,7 +565,7 @@ __global__ void __launch_bounds__(256, FV_FAST_MINB) k_lbr_far_low_fast(KArgs a,
         a.status[row] = (int8_t)o.status;
       }
     }
-    const unsigned int slot = warp_append(lq.count + 4, bad);
+    const unsigned int slot = warp_append(lq.count + 4, (bool)bad);
     if (bad) lq.q[4][slot] = ent;
   }
 }
@@ -581,7 +582,7 @@ __global__ void __launch_bounds__(256, FV_FAST_MINB) k_lbr_near_fast(KArgs a, Lb
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base >= n) break;
     const unsigned int j = base + lane;
-    bool bad = false;
+    FxBad bad;
     int32_t ent = 0;
     if (j < n) {
       ent = q[j];
@@ -597,7 +598,7 @@ __global__ void __launch_bounds__(256, FV_FAST_MINB) k_lbr_near_fast(KArgs a, Lb
         a.status[row] = (int8_t)o.status;
       }
     }
-    const unsigned int slot = warp_append(lq.count + 6, bad);
+    const unsigned int slot = warp_append(lq.count + 6, (bool)bad);
     if (bad) lq.q[6][slot] = ent;
   }
 }
@@ -735,7 +736,7 @@ __global__ void __launch_bounds__(256, kFast ? FV_HSM_MINB : 1) k_halley_sm(KArg
     // them the compiler reconverges only around the evaluation itself and
     // each state's lanes run it separately: ~6 of 32 lanes active).
     FvExc e = {0, 0, 0.0};
-    bool flagged = false;
+    FxBad flagged;
     double x = 0.0;
     bool eval = busy && (kFast ? fx_hsm_pre(m, &x, flagged) : fv_hsm_pre(m, &x, e));
     __syncwarp();
@@ -849,7 +850,7 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
     const uint64_t u1 = splitmix64(seed + 7919ull * (uint64_t)i);
     const uint64_t u2 = splitmix64(u1 ^ 0x9e3779b97f4a7c15ull);
     const uint64_t u3 = splitmix64(u2 + 12345ull);
-    bool bad;
+    FxBad bad;
     // 0: a / b, exponents spanning the whole range (incl. slow-path ones)
     {
       const int wide = (int)(u3 & 3) == 0;
@@ -857,7 +858,7 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
       double b = st_bits(u2, wide ? -1022 : -600, wide ? 1023 : 600);
       if (u3 & 16) a = -a;
       if (u3 & 32) b = -b;
-      bad = false;
+      bad = FxBad();
       const bool z = (u3 & 0xf00) == 0;             // 1/16: zero numerators through fx_div0
       if (z) a = (u3 & 16) ? -0.0 : 0.0;
       const double f = z ? fx_div0(a, b, bad) : fx_div(a, b, bad);
@@ -867,14 +868,14 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
     {
       double x = ((u3 >> 8) & 3) ? (st_uniform(u1) * 1600.0 - 800.0) : st_bits(u1, -70, 10);
       if (u3 & 64) x = -x;
-      bad = false;
+      bad = FxBad();
       const double f = fx_exp(x, bad);
       if (bad) ++lf[1]; else if (!st_same(f, fv_exp(x))) ++lm[1];
     }
     // 2: log of positives, half of them in [0.5, 2]
     {
       const double x = ((u3 >> 10) & 1) ? st_bits(u2, -1, 0) : st_bits(u2, -1000, 1000);
-      bad = false;
+      bad = FxBad();
       const double f = fx_log(x, bad);
       if (bad) ++lf[2]; else if (!st_same(f, fv_log_i(x))) ++lm[2];
     }
@@ -883,7 +884,7 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
       const int nn = 2 + (int)((u3 >> 12) % 3);
       double x = ((u3 >> 14) & 1) ? st_bits(u1 ^ u2, -2, 1) : st_bits(u1 ^ u2, -300, 300);
       if (u3 & 128) x = -x;
-      bad = false;
+      bad = FxBad();
       const double f = fx_powi(x, nn, bad);
       FvExc e = {0, 0, 0.0};
       if (bad) ++lf[3]; else if (!st_same(f, py_powi_t<true>(x, nn, false, e)) || e.code) ++lm[3];
@@ -894,7 +895,7 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
       const int sel = (int)((u3 >> 16) & 3);
       const double x = sel == 0 ? st_uniform(u2) * 60.0
                      : (sel == 1 ? st_bits(u2, -64, -30) : exp10(st_uniform(u2) * 11.0 - 3.0));
-      bad = false;
+      bad = FxBad();
       const double f = fx_erfcx_pos(x, bad);
       if (bad) ++lf[4]; else if (!st_same(f, fv_erfcx_i(x))) ++lm[4];
     }
@@ -902,7 +903,7 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
     {
       const double s = exp10(st_uniform(u1) * 8.5 - 8.0);
       const double h = -exp10(st_uniform(u3) * 7.0 - 2.0);
-      bad = false;
+      bad = FxBad();
       const double f = fx_nbl_h(h, s, bad);
       FvExc e = {0, 0, 0.0};
       const double c = fv_nbl_h<true>(h, s, e);
@@ -911,7 +912,7 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
     // 6: x / sqrt(2) by the constant-division product
     {
       const double x = st_bits(u3, -1000, 1000);
-      bad = false;
+      bad = FxBad();
       const double f = FX_DIV_SQRT2(x, bad);
       if (bad) ++lf[6]; else if (!st_same(f, __ddiv_rn(x, FV_DIV_SQRT2_C))) ++lm[6];
     }
@@ -919,7 +920,7 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
     {
       double x = st_bits(u1 ^ u3, -1074 + 52, 1023);
       if ((u2 & 63) == 0) x = -x;
-      bad = false;
+      bad = FxBad();
       const double f = fx_sqrt(x, bad);
       if (bad) ++lf[7]; else if (!st_same(f, __dsqrt_rn(x))) ++lm[7];
     }
@@ -927,7 +928,7 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
     {
       double x = st_uniform(u1 ^ (u3 << 7)) * 60.0 - 30.0;
       if ((u2 & 15) == 0) x = st_bits(u2, -60, 8) * ((u2 & 16) ? -1.0 : 1.0);
-      bad = false;
+      bad = FxBad();
       const double f = fx_erfc(x, bad);
       if (bad) ++lf[9]; else if (!st_same(f, fv_erfc(x))) ++lm[9];
     }
@@ -937,14 +938,14 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
       double x = sel == 0 ? st_uniform(u1) * 66.2 - 6.2
                : (sel == 1 ? st_bits(u1, -70, -30) : (sel == 2 ? 0.0 : exp10(st_uniform(u1) * 11.0 - 3.0)));
       if ((u3 >> 26) & 1) x = -x;
-      bad = false;
+      bad = FxBad();
       const double f = fx_erfcx_any(x, bad);
       if (bad) ++lf[10]; else if (!st_same(f, fv_erfcx_i(x))) ++lm[10];
     }
     // 8: log, both paths (half of the inputs within 2^-4 of 1)
     {
       const double x = ((u3 >> 20) & 1) ? 1.0 + (st_uniform(u2) - 0.5) * 0.13 : st_bits(u2 ^ u3, -1000, 1000);
-      bad = false;
+      bad = FxBad();
       const double f = fx_log_any(x, bad);
       if (bad) ++lf[8]; else if (!st_same(f, fv_log_i(x))) ++lm[8];
     }

@@ -91,7 +91,7 @@ int64_t qh_classify_fast_check(int model, const int8_t* flag, const double* un, 
                                int64_t n, int64_t* nflag) {
   int64_t bad = 0, nb = 0;
   for (int64_t i = 0; i < n; ++i) {
-    bool flagged = false;
+    FxBad flagged;
     FvLbrState sf; FvLbrOut of;
     sf.x = sf.beta = sf.sqrt_t = sf.s_c = sf.b0 = sf.E0 = 0.0;
     const int cf = fx_lbr_classify_lo(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], px[i], sf, of, flagged);
@@ -137,7 +137,7 @@ int64_t qh_price_greeks_fast_check(int model, const int8_t* flag, const double* 
                                    int64_t n, int64_t* nflag) {
   int64_t bad = 0, nb = 0;
   for (int64_t i = 0; i < n; ++i) {
-    bool f1 = false, f2 = false;
+    FxBad f1, f2;
     const double pf = fx_price_row(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], sg[i], f1);
     const FvGreeks gf = fx_price_greeks_row(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], sg[i], true, f2);
     if (f1 || f2) { ++nb; }
@@ -170,7 +170,7 @@ int64_t qh_halley_fast_check(int model, const int8_t* flag, const double* un, co
     FvExc ec = {0, 0, 0.0};
     fv_halley_row_sm(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], px[i], &st_c, &sg_c, ec);
     if (fv_hsm_setup(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], px[i], m, e0)) continue;
-    bool flagged = false;
+    FxBad flagged;
     for (;;) {
       double x;
       if (!fx_hsm_pre(m, &x, flagged)) break;
@@ -202,7 +202,7 @@ int64_t qh_anchor_rest_fast_check(const int8_t* flag, const double* F, const dou
     if (fv_lbr_anchor_lo(st, e) != FV_NEAR_LOW) continue;
     ++ns;
     FvLbrState sf = st, sc = st;
-    bool flagged = false;
+    FxBad flagged;
     FvExc e2 = {0, 0, 0.0};
     const int rf = fx_lbr_anchor_rest(sf, flagged);
     const int rc = fv_lbr_anchor_rest(sc, e2);
@@ -233,7 +233,7 @@ int64_t qh_near_fast_check(const int8_t* flag, const double* F, const double* k,
     if (o.region != FV_NEAR_LOW && o.region != FV_NEAR_HIGH) continue;
     ++nn;
     FvExc e2 = {0, 0, 0.0};
-    bool flagged = false;
+    FxBad flagged;
     FvLbrOut a = fx_lbr_near(o.region, st, flagged);
     FvLbrOut c = fv_lbr_solve<FV_NEAR_LOW>(o.region, st, e2);
     if (flagged) { ++nb; continue; }
@@ -262,7 +262,7 @@ int64_t qh_far_low_fast_check(const int8_t* flag, const double* F, const double*
     if (o.region != FV_FAR_LOW) continue;
     ++nf;
     FvExc e2 = {0, 0, 0.0};
-    bool flagged = false;
+    FxBad flagged;
     FvLbrOut a = fx_lbr_far_low(st, flagged);
     FvLbrOut b = fv_lbr_far_low_fused(st, e2);
     if (flagged) { ++nb; continue; }
