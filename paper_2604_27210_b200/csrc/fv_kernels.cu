@@ -1179,12 +1179,14 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
           const int64_t cap1 = (b.n + 255) / 256;
           auto g = [cap1](int blocks) { return (int)(cap1 < blocks ? cap1 : blocks); };
           FV_LAUNCH(FV_KID_LBR_NORM, s, k_lbr_normalize<<<blocks_for(w->blocks_lbr_norm, b.n), 256, 0, s>>>(b, lq));
-          FV_LAUNCH(FV_KID_LBR_NREP, s, k_lbr_normalize_replay<<<g(w->blocks_lbr_nrep), 256, 0, s>>>(b, lq));
+          // the three replay passes usually find an empty queue: one CTA per SM
+          // keeps their launch + drain short (a full occupancy grid costs ~7 us)
+          FV_LAUNCH(FV_KID_LBR_NREP, s, k_lbr_normalize_replay<<<g(w->sm_count), 256, 0, s>>>(b, lq));
           FV_LAUNCH(FV_KID_LBR_ANCH, s, k_lbr_anchors<<<g(w->blocks_lbr_anch), 256, 0, s>>>(b, lq));
           FV_LAUNCH(FV_KID_LBR_FAST, s, k_lbr_far_low_fast<<<g(w->blocks_lbr_fast), 256, 0, s>>>(b, lq));
-          FV_LAUNCH(FV_KID_LBR_FL, s, k_lbr_solve<FV_FAR_LOW><<<g(w->blocks_lbr_fl), 256, 0, s>>>(b, lq));
+          FV_LAUNCH(FV_KID_LBR_FL, s, k_lbr_solve<FV_FAR_LOW><<<g(w->sm_count), 256, 0, s>>>(b, lq));
           FV_LAUNCH(FV_KID_LBR_NEAR_FAST, s, k_lbr_near_fast<<<g(w->blocks_lbr_nfast), 256, 0, s>>>(b, lq));
-          FV_LAUNCH(FV_KID_LBR_NEAR, s, k_lbr_solve<FV_NEAR_LOW><<<g(w->blocks_lbr_near), 256, 0, s>>>(b, lq));
+          FV_LAUNCH(FV_KID_LBR_NEAR, s, k_lbr_solve<FV_NEAR_LOW><<<g(w->sm_count), 256, 0, s>>>(b, lq));
           FV_LAUNCH(FV_KID_LBR_FH, s, k_lbr_solve<FV_FAR_HIGH><<<g(w->blocks_lbr_fh), 256, 0, s>>>(b, lq));
         }
       } else {
