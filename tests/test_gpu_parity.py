@@ -462,3 +462,43 @@ def test_fast_vollib_facade_device(fv, oracle_mod):
     gw = oracle_mod.rows_greeks("bsm", flag, S, K, t, r, q, sig)
     for k in ("delta", "gamma", "theta", "rho", "vega"):
         assert_bits(g[k], gw[k], f"facade {k}")
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 32, 33, 63, 64, 65, 255, 257, 4097])
+def test_odd_sizes_and_strided_device_columns(fv, oracle_mod, n):
+    """Batch sizes around the warp / pair / work-claim granularities, and
+    device columns that are strided views (every other element of a larger
+    tensor): LBR, Halley, price and Greeks, bit for bit against the oracle."""
+    import torch
+    from paper_2604_27210_b200 import _native
+    from paper_2604_27210_b200 import workloads as W
+    lib = _native.lib_for_compute()
+    flag, S, K, t, r, q, sig = W.chain_draws(n, seed=1000 + n)
+    px = oracle_mod.rows_price("bsm", flag, S, K, t, r, q, sig)["price"]
+
+    def strided(a):
+        big = np.zeros(2 * len(a), dtype=a.dtype)
+        big[::2] = a
+        return torch.from_numpy(big).cuda()[::2]
+
+    cols = [strided(np.ascontiguousarray(c)) for c in (flag, S, K, t, r, q, px)]
+    assert cols[2].stride(0) == 2
+    for method, mcode in (("lbr", 1), ("halley", 0)):
+        want = oracle_mod.rows_iv("bsm", method, flag, S, K, t, r, q, px)
+        iv = torch.empty(n, dtype=torch.float64, device="cuda")
+        st = torch.empty(n, dtype=torch.int8, device="cuda")
+        err = _native.fv_error()
+        assert lib.fv_batch_iv(2, mcode, *[_native.col(c) for c in cols], n, iv.data_ptr(), st.data_ptr(),
+                               None, err) == 0, err.message
+        assert_bits(iv.cpu().numpy(), want["iv"], f"n={n} {method} iv")
+        assert_bits(st.cpu().numpy(), want["status_code"], f"n={n} {method} status")
+    scols = cols[:6] + [strided(np.ascontiguousarray(sig))]
+    outs = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(6)]
+    st = torch.empty(n, dtype=torch.int8, device="cuda")
+    ep, eg = _native.fv_error(), _native.fv_error()
+    assert lib.fv_price_greeks(2, *[_native.col(c) for c in scols], n, *[o.data_ptr() for o in outs],
+                               st.data_ptr(), ep, eg) == 0
+    g = oracle_mod.rows_greeks("bsm", flag, S, K, t, r, q, sig)
+    assert_bits(outs[0].cpu().numpy(), px, f"n={n} price")
+    for j, name in enumerate(("delta", "gamma", "theta", "rho", "vega")):
+        assert_bits(outs[j + 1].cpu().numpy(), g[name], f"n={n} {name}")
