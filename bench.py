@@ -378,15 +378,26 @@ def run_ours(args):
     # ---- per-kernel split of a step (CUDA events around each launch, on the
     # launching stream; a separate pass so the headline timing has no events)
     kernels = None
+    n_far_low = None
     try:
         if args.no_kernel_timing:
             raise RuntimeError("skipped (--no-kernel-timing)")
         lib.fv_set_kernel_timing(1)
         _native.kernel_times(lib)
         nk = max(1, min(args.steps, 3))
+        region = torch.empty(n, dtype=torch.int8, device=dev) if method == 1 else None
         for _ in range(nk):
-            step()
+            if region is not None:     # LBR: also record each quote's region (far-low count)
+                err = _native.fv_error()
+                rc = lib.fv_batch_iv(model, method, *ncols, n, out_iv.data_ptr(), out_st.data_ptr(),
+                                     region.data_ptr(), err)
+                if rc:
+                    raise RuntimeError(err.message)
+            else:
+                step()
         torch.cuda.synchronize(dev)
+        if region is not None:
+            n_far_low = int((region == 0).sum().item())
         kt = _native.kernel_times(lib)
         lib.fv_set_kernel_timing(0)
         tot = sum(v[0] for v in kt.values()) or 1.0
@@ -394,6 +405,24 @@ def run_ours(args):
                    for k, v in sorted(kt.items(), key=lambda kv: -kv[1][0])}
     except Exception as exc:  # noqa: BLE001
         kernels = {"error": repr(exc)}
+
+    # ---- the dominant kernel's own roofline (C4: k_lbr_far_low_fast) --------
+    # algorithmic work per launch = the reference's weighted distinct fp64 ops
+    # of the far-low solve phase per far-low quote (profiles/w_phases_c4.json,
+    # tools/w_count.py) x the far-low quotes of the call; time = its mean
+    # launch duration from the CUDA-event pass above
+    dominant = None
+    try:
+        wp = json.load(open(os.path.join(REPO, "profiles", "w_phases_%s.json" % args.workload)))
+        kname = "k_lbr_far_low_fast"
+        if n_far_low and kernels and kname in kernels:
+            w_solve = wp["by_region"]["FAR_LOW"]["W_solve"]
+            t_k = kernels[kname]["ms_per_step"] * 1e-3
+            dominant = {"kernel": kname, "share_of_call": kernels[kname]["share"], "units": n_far_low,
+                        "W_per_unit": w_solve, "ms_per_launch": t_k * 1e3,
+                        "achieved": w_solve * n_far_low / t_k / 1e12}
+    except (OSError, ValueError, KeyError):
+        pass
 
     # ---- status mix of the solved chain (for the record) --------------------
     st = torch.bincount(out_st.to(torch.int64) + 0, minlength=5).cpu().tolist()
@@ -516,6 +545,9 @@ def run_ours(args):
                                  "DFMA issue rate (fv_probe_fp64_peak, this run); traffic = ncu DRAM read+write bytes "
                                  "per call (profiles/roofline_traffic.json)" % W_OPS[args.workload]},
             "kernels": kernels,
+            "dominant_kernel": (dict(dominant, peak=peak_tops, unit="T weighted-fp64-ops/s",
+                                     frac=dominant["achieved"] / peak_tops if peak_tops else None)
+                                if dominant else None),
             "roofline_hbm": {"bound": "hbm", "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": hbm_gbs / hbm_peak, "bytes_per_quote": (in_bytes + out_bytes) / n,
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
