@@ -763,6 +763,163 @@ __global__ void __launch_bounds__(256, kFast ? FV_HSM_MINB : 1) k_halley_sm(KArg
   }
 }
 
+// The fast pass as a lean per-lane loop (FV_HSM_LEAN): the same sequence of
+// f evaluations as fv_hsm_* (fv_quote.h) -- f(SIGMA_LO), f(hi) doubling,
+// f(guess), Halley candidate / midpoint steps, the bisection tail -- with the
+// state update of one step and the decision of the next evaluation point
+// fused into one pass over a few registers, and the Halley candidate (the
+// only heavy part besides f) computed at one site for every lane that needs
+// it.  A quote the straight-line routines flag is handed back (record index
+// into `ridx`) and recomputed from scratch by k_halley_sm<false>.
+#ifndef FV_HSM_LEAN
+#define FV_HSM_LEAN 1
+#endif
+__global__ void __launch_bounds__(256, FV_HSM_MINB) k_halley_lean(KArgs a, const HsmRec* recs,
+                                                              const unsigned int* count,
+                                                              unsigned long long* next, int32_t* ridx,
+                                                              unsigned int* rcount) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long n = *count;
+  __shared__ double sm_x[8][64], sm_r[8][64];
+  __shared__ unsigned char sm_f[8][64];
+  const int wib = threadIdx.x >> 5;
+  FvHalleyCtx c;
+  double lo = 0.0, hi = 0.0, sigma = 0.0, fval = 0.0, cand = 0.0, x = 0.0;
+  int st = FV_HS_DONE, k = 0;
+  int64_t row = -1;
+  int32_t rec = -1;
+  bool busy = false, exhausted = false;
+  for (;;) {
+    {
+      const bool need = !busy && !exhausted;
+      const unsigned mask = __ballot_sync(0xffffffffu, need);
+      if (mask) {
+        unsigned long long base = 0;
+        if (lane == __ffs(mask) - 1) base = atomicAdd(next, (unsigned long long)__popc(mask));
+        base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
+        if (need) {
+          const unsigned long long jq = base + __popc(mask & ((1u << lane) - 1));
+          if (jq >= n) {
+            exhausted = true;
+          } else {
+            rec = (int32_t)jq;
+            const HsmRec h = recs[rec];
+            c = h.c; cand = h.guess; row = h.row;      // cand holds the guess until f(hi)
+            lo = FV_K_1EM9; hi = 10.0; x = lo;
+            st = FV_HS_LO;
+            busy = true;
+          }
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, busy)) break;
+    __syncwarp();
+    FxBad flagged;
+    const double fx = fx_halley_f_warp(busy, c, x, flagged, sm_x[wib], sm_r[wib], sm_f[wib]);
+    __syncwarp();
+    bool handback = busy && flagged;
+    if (handback) busy = false;
+    int fin = -1;                   // status when the quote finishes this step
+    double fin_sigma = 0.0;
+    bool need_iter = false, need_bis = false;
+    if (busy) {
+      switch (st) {
+        case FV_HS_LO:                                       // solver.py:92-96
+          if (fx >= 0.0) {
+            fin = fv_fabs(fx) <= c.tol_price ? FV_IV_CONVERGED : FV_IV_BELOW_INTRINSIC;
+            fin_sigma = lo;
+          } else {
+            st = FV_HS_HI; x = hi;
+          }
+          break;
+        case FV_HS_HI:                                       // :97-106
+          if (fx < 0.0) {
+            if (hi < 100.0) { hi = py_min(2.0 * hi, 100.0); x = hi; }
+            else fin = FV_IV_MAX_ITER;
+          } else {
+            sigma = py_min(py_max(py_min(py_max(cand, FV_K_0P05), 2.0), lo), hi);
+            st = FV_HS_GUESS; x = sigma;
+          }
+          break;
+        case FV_HS_GUESS:                                    // :108-112
+          fval = fx;
+          if (fx > 0.0) hi = py_min(hi, sigma);
+          else if (fx < 0.0) lo = py_max(lo, sigma);
+          k = 0;
+          need_iter = true;
+          break;
+        case FV_HS_CHECK:                                    // :129-135
+          if (!(fv_fabs(fx) < fv_fabs(fval))) {
+            cand = 0.5 * (lo + hi); st = FV_HS_MID; x = cand;
+            break;
+          }
+          // fall through: accepted
+        case FV_HS_MID: {                                    // :136-144
+          if (fx > 0.0) hi = cand;
+          else if (fx < 0.0) lo = cand;
+          const double step = cand - sigma;
+          sigma = cand; fval = fx;
+          if (fv_fabs(step) <= FV_K_1EM12 * py_max(1.0, sigma)) { fin = FV_IV_CONVERGED; fin_sigma = sigma; break; }
+          if (++k == 16) { k = 0; need_bis = true; }
+          else need_iter = true;
+          break;
+        }
+        default:                                             // FV_HS_BISECT, :151-161
+          fval = fx;
+          if (fx > 0.0) hi = sigma;
+          else lo = sigma;
+          if (++k == 128) {
+            const bool ok = fv_fabs(fval) <= c.tol_price || (hi - lo) <= FV_K_1EM12 * py_max(1.0, sigma);
+            fin = ok ? FV_IV_FELL_BACK : FV_IV_MAX_ITER;
+            fin_sigma = sigma;
+          } else {
+            need_bis = true;
+          }
+          break;
+      }
+    }
+    if (need_bis) {                                          // :147-150
+      if (fv_fabs(fval) <= c.tol_price || (hi - lo) <= FV_K_1EM12 * py_max(1.0, sigma)) {
+        fin = FV_IV_FELL_BACK; fin_sigma = sigma;
+      } else {
+        sigma = 0.5 * (lo + hi); x = sigma; st = FV_HS_BISECT;
+      }
+    }
+    if (need_iter) {                                         // :115-128
+      if (fv_fabs(fval) <= c.tol_price) {
+        fin = FV_IV_CONVERGED; fin_sigma = sigma;
+      } else {
+        FxBad vb;
+        const double s = sigma * c.sqrt_t;
+        double vega = 0.0, d1 = 0.0;
+        if (!(s < FV_K_1EM12)) {
+          vb |= c.fk_bad;                                    // ValueError site (:45)
+          d1 = fx_div0(c.lnFK + 0.5 * s * s, s, vb);
+          vega = c.disc * c.Fw * fx_norm_pdf(d1, vb) * c.sqrt_t;
+        }
+        double cn = __builtin_nan("");
+        if (vega > 0.0) {
+          const double d2 = d1 - s;
+          const double vomma = fx_div0(vega * d1 * d2, sigma, vb);
+          const double denom = 2.0 * vega * vega - fval * vomma;
+          if (denom != 0.0) cn = sigma - fx_div0(2.0 * fval * vega, denom, vb);
+        }
+        if (fv_isfinite(cn) && lo < cn && cn < hi) { cand = cn; st = FV_HS_CHECK; }
+        else { cand = 0.5 * (lo + hi); st = FV_HS_MID; }
+        x = cand;
+        if (vb) { handback = true; busy = false; }
+      }
+    }
+    const unsigned int slot = warp_append(rcount, handback);
+    if (handback) ridx[slot] = rec;
+    if (fin >= 0) {
+      a.o0[row] = (fin == FV_IV_CONVERGED || fin == FV_IV_FELL_BACK) ? fin_sigma : __builtin_nan("");
+      a.status[row] = (int8_t)fin;
+      busy = false;
+    }
+  }
+}
+
 // One-row re-run that records the full exception (value + numpy-ness) for
 // DomainError messages that quote a value.
 struct ExplainOut { int code; int np; double val; };
@@ -1060,7 +1217,11 @@ cudaError_t get_work(DevWork** out) {
     w->blocks_lbr_near = occupancy_blocks((const void*)k_lbr_solve<FV_NEAR_LOW>, w->sm_count);
     w->blocks_lbr_nfast = occupancy_blocks((const void*)k_lbr_near_fast, w->sm_count);
     w->blocks_lbr_fh = occupancy_blocks((const void*)k_lbr_solve<FV_FAR_HIGH>, w->sm_count);
+#if FV_HSM_LEAN
+    w->blocks_hsm = occupancy_blocks((const void*)k_halley_lean, w->sm_count);
+#else
     w->blocks_hsm = occupancy_blocks((const void*)k_halley_sm<true>, w->sm_count);
+#endif
     w->blocks_hsm2 = occupancy_blocks((const void*)k_halley_sm<false>, w->sm_count);
     CK(cudaMalloc(&w->work_ctr, sizeof(unsigned long long) * 2 * FV_NSLOT));
     CK(cudaMalloc(&w->hsm_count, sizeof(unsigned int) * 2 * FV_NSLOT));
@@ -1197,8 +1358,13 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
         CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned int), s));
         FV_LAUNCH(FV_KID_HALLEY_SETUP, s, k_halley_setup<<<blocks_for(w->blocks_hset, a.n), 256, 0, s>>>(a, w->hsm_recs[slot], cnt));
         const int64_t need = (a.n + 255) / 256;
+#if FV_HSM_LEAN
+        FV_LAUNCH(FV_KID_HALLEY_SM, s, k_halley_lean<<<need < w->blocks_hsm ? need : w->blocks_hsm, 256, 0, s>>>(
+            a, w->hsm_recs[slot], cnt, ctr, w->hsm_ridx[slot], cnt + 1));
+#else
         FV_LAUNCH(FV_KID_HALLEY_SM, s, k_halley_sm<true><<<need < w->blocks_hsm ? need : w->blocks_hsm, 256, 0, s>>>(
             a, w->hsm_recs[slot], cnt, ctr, w->hsm_ridx[slot], cnt + 1));
+#endif
         FV_LAUNCH(FV_KID_HALLEY_SM2, s, k_halley_sm<false><<<need < w->blocks_hsm2 ? need : w->blocks_hsm2, 256, 0, s>>>(
             a, w->hsm_recs[slot], cnt + 1, ctr + 1, w->hsm_ridx[slot], nullptr));
       }

@@ -276,3 +276,32 @@ int64_t qh_far_low_fast_check(const int8_t* flag, const double* F, const double*
   return bad;
 }
 }
+
+extern "C" {
+// fx_erfc_u2 (all ranges through one rational form) on pairs (x[i],
+// x[n-1-i]): every unflagged value must carry fv_erfc_i's bits, and the
+// flags must be fx_erfc's.  Returns mismatches; *nflag = flagged values.
+int64_t qh_erfc_u_check(const double* x, int64_t n, int64_t* nflag) {
+  int64_t bad = 0, nb = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double xa = x[i], xb = x[n - 1 - i];
+    for (int mode = 0; mode < 3; ++mode) {           // both wanted, only a, only b
+      const bool va = mode != 2, vb = mode != 1;
+      double ra, rb;
+      FxBad f;
+      fx_erfc_u2(xa, xb, va, vb, ra, rb, f);
+      FxBad fa, fb;
+      const double ca = fx_erfc(xa, fa), cb = fx_erfc(xb, fb);
+      const bool want_flag = (va && fa) || (vb && fb);
+      if ((bool)f != want_flag) { ++bad; continue; }
+      if (f) { ++nb; continue; }
+      const double ea = fv_erfc_i(xa), eb = fv_erfc_i(xb);
+      uint64_t u0, u1;
+      if (va) { memcpy(&u0, &ra, 8); memcpy(&u1, &ea, 8); if (u0 != u1) ++bad; memcpy(&u1, &ca, 8); if (u0 != u1) ++bad; }
+      if (vb) { memcpy(&u0, &rb, 8); memcpy(&u1, &eb, 8); if (u0 != u1) ++bad; memcpy(&u1, &cb, 8); if (u0 != u1) ++bad; }
+    }
+  }
+  *nflag = nb;
+  return bad;
+}
+}

@@ -293,3 +293,24 @@ def test_straight_line_anchor_rest_matches_careful(Q, case):
                                       ctypes.byref(nb))
     assert ns.value > 10_000 and bad == 0, (ns.value, bad)
     assert nb.value < ns.value // 20, (nb.value, ns.value)
+
+
+def test_unified_erfc_matches_glibc(Q):
+    """fx_erfc_u2: the four fdlibm erfc ranges through one rational form give
+    glibc's bits (fv_erfc_i) and fx_erfc's range flags, for every argument
+    class: each range and its edges, |x| < 2^-56, x < -6, |x| >= 28, inf, nan."""
+    Q.qh_erfc_u_check.restype = ctypes.c_int64
+    rng = np.random.default_rng(11)
+    edges = np.array([0.0, -0.0, 2.0**-60, 2.0**-56, 0.25, 0.84375, 1.25, 1 / 0.35, 6.0, 28.0,
+                      np.inf, np.nan, 1e-300, 5e-324])
+    edges = np.concatenate([edges, np.nextafter(edges, np.inf), np.nextafter(edges, -np.inf)])
+    x = np.concatenate([edges, -edges,
+                        rng.uniform(-30, 30, 200_000),
+                        rng.uniform(-1.5, 1.5, 200_000),
+                        rng.standard_normal(200_000) * 4,
+                        np.exp(rng.uniform(-40, 4, 100_000)) * rng.choice([-1, 1], 100_000)])
+    x = np.ascontiguousarray(x[rng.permutation(len(x))])
+    nb = ctypes.c_int64(0)
+    assert Q.qh_erfc_u_check(_p(x), ctypes.c_int64(len(x)), ctypes.byref(nb)) == 0
+    # flags are fx_erfc's (checked above): |x| beyond ~26.5 (exp underflow) and nan / inf
+    assert nb.value < 3 * len(x) // 8

@@ -273,6 +273,18 @@ def main():
     emit_array(lines, "double", "fv_erfc_mid", mid, hexd)
     lines.append("")
 
+    # all four erfc rational ranges in the tail's form, rows of 16:
+    # P = ((c0 + s c1) + s^2 (c2 + s c3) + s^4 (c4 + s c5)) + s^6 (c6 + s c7),
+    # Q = (((1 + s d1) + s^2 (d2 + s d3) + s^4 (d4 + s d5)) + s^6 (d6 + s d7)) + s^8 d8;
+    # rows: |x| < 0.84375, [0.84375, 1.25), [1.25, 1/0.35), [1/0.35, 28).  The
+    # inner rows' c7 = d7 = d8 = 0 add exact zeros (fx_erfc_u, fv_fast.h).
+    uni = (mid[0:7] + [0.0] + mid[7:13] + [0.0, 0.0]
+           + mid[16:23] + [0.0] + mid[23:29] + [0.0, 0.0] + tail)
+    assert len(uni) == 64
+    lines.append("// fdlibm erfc rationals of all four ranges in one form, rows of 16 (see tools/gen_tables.py)")
+    emit_array(lines, "double", "fv_erfc_uni", uni, hexd)
+    lines.append("")
+
     # ---- Faddeeva erfcx_y100 Chebyshev table -------------------------------
     cheb = erfcx_table(torch_math_h())
     lines.append("// Faddeeva erfcx_y100: 100 intervals x 7 coefficients (c0..c6),")
