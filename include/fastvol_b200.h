@@ -197,7 +197,8 @@ FV_API int fv_selftest_fast(int64_t n, uint64_t seed, int64_t* mismatches /*[11]
 #define FV_KID_HALLEY_SM 10
 #define FV_KID_HALLEY_SM2 11
 #define FV_KID_LBR_NEAR_FAST 12
-#define FV_NKERNEL 13
+#define FV_KID_HALLEY_BISECT 13
+#define FV_NKERNEL 14
 FV_API int fv_set_kernel_timing(int on);
 FV_API int fv_kernel_times(double* ms /*[FV_NKERNEL]*/, int64_t* launches /*[FV_NKERNEL]*/);
 FV_API const char* fv_kernel_name(int id);

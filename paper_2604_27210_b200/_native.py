@@ -116,7 +116,7 @@ def last_outcome(lib):
     return cr, er, ec
 
 
-NKERNEL = 13
+NKERNEL = 14
 
 
 def kernel_times(lib):

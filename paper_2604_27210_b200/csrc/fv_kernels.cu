@@ -628,295 +628,321 @@ __global__ void __launch_bounds__(256, FV_SOLVE_MINB) k_lbr_solve(KArgs a, LbrQu
   }
 }
 
-// Halley setup pass: validation + :60-86 for every row, coalesced; quotes
-// that need the iteration get a prepared record in a dense queue.
-struct HsmRec {
-  FvHalleyCtx c;
-  double guess;
-  int64_t row;
+// ---- Halley + bisection (solver.py:49-161) in three passes ------------------
+// The reference's sequence of f evaluations per quote is f(SIGMA_LO), f(hi)
+// (doubling while negative), f(guess), up to 16 Halley steps (candidate, or
+// the midpoint when the candidate leaves the bracket / does not improve), and
+// for ~4 % of quotes a bisection tail of up to 128 steps.  The passes follow
+// that shape so each one runs a short, nearly branch-free loop:
+//   k_halley_bracket  one row per thread: validation + :60-86, then the three
+//                     fixed evaluations f(SIGMA_LO), f(10), f(guess) (:91-112);
+//                     quotes still open get a HalRec in a dense queue;
+//   k_halley_iter     per-lane loop with refill over that queue: the Halley
+//                     steps (:115-144); quotes reaching 16 steps are re-queued;
+//   k_halley_bisect   per-lane loop with refill over the re-queued ones (:146-161);
+//   k_halley_careful  a row per thread over the quotes any pass handed back:
+//                     the whole careful solver from the inputs (fv_halley_row_sm).
+// The fast passes evaluate f on the straight-line routines (range-bucketed
+// erfc); anything they flag -- range edges, F/K <= 0, exceptions, the rare
+// f(10) < 0 doubling -- is handed back, so every value is the careful
+// solver's.
+struct HalRec {            // 96 bytes, 16-byte aligned: a quote between passes
+  double Fw, K, disc, sqrt_t, lnFK, target, tol, pad;
+  double lo, hi, sigma, fval;
 };
+struct HalRecRow { int64_t rowbits; };   // row | (call << 62), parallel array
 
-// One row per thread (8-byte coalesced column loads): with a pair per
-// thread the two rows' solver state stayed live (126 registers, 25 % of warps)
-// and the pass was latency-bound at 0.9 ms per 10M rows.
-__global__ void __launch_bounds__(256, 4) k_halley_setup(KArgs a, HsmRec* recs, unsigned int* count) {
+#define FV_HAL_CALL (1ll << 62)
+
+__device__ __forceinline__ void hal_store(HalRec* r, const FvHalleyCtx& c, double lo, double hi,
+                                          double sigma, double fval) {
+  double2* p = reinterpret_cast<double2*>(r);
+  p[0] = make_double2(c.Fw, c.K);
+  p[1] = make_double2(c.disc, c.sqrt_t);
+  p[2] = make_double2(c.lnFK, c.target);
+  p[3] = make_double2(c.tol_price, 0.0);
+  p[4] = make_double2(lo, hi);
+  p[5] = make_double2(sigma, fval);
+}
+__device__ __forceinline__ void hal_load(const HalRec* r, int64_t rowbits, FvHalleyCtx& c, double& lo,
+                                         double& hi, double& sigma, double& fval) {
+  const double2* p = reinterpret_cast<const double2*>(r);
+  const double2 v0 = p[0], v1 = p[1], v2 = p[2], v3 = p[3], v4 = p[4], v5 = p[5];
+  c.Fw = v0.x; c.K = v0.y; c.disc = v1.x; c.sqrt_t = v1.y; c.lnFK = v2.x; c.target = v2.y;
+  c.tol_price = v3.x;
+  c.th = (rowbits & FV_HAL_CALL) ? 1.0 : -1.0;
+  c.fk_bad = false;                        // such quotes never enter the queues
+  lo = v4.x; hi = v4.y; sigma = v5.x; fval = v5.y;
+}
+
+#ifndef FV_HSET_MINB
+#define FV_HSET_MINB 3
+#endif
+__global__ void __launch_bounds__(256, FV_HSET_MINB) k_halley_bracket(KArgs a, HalRec* recs, int64_t* rrow,
+                                                                  unsigned int* count, int32_t* hrow) {
+  __shared__ double sm_x[8][64], sm_r[8][64];
+  __shared__ unsigned char sm_f[8][64];
+  const int wib = threadIdx.x >> 5;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t nloop = (a.n + stride - 1) / stride;
   for (int64_t it = 0; it < nloop; ++it) {
     const int64_t row = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool active = row < a.n;
-    bool nd = false;
+    bool open = false, hb = false;
     FvHalleySM m;
+    m.c.th = 1.0; m.c.Fw = m.c.K = m.c.disc = m.c.sqrt_t = m.c.lnFK = m.c.target = m.c.tol_price = 0.0;
+    m.c.fk_bad = false; m.guess = 0.0;
     if (active) {
       const int fl = ldf1(a.flag, row);
       const double un = ld1(a.un, row), k = ld1(a.k, row), t = ld1(a.t, row), r = ld1(a.r, row);
       const double q = ld1(a.q, row), px = ld1(a.last, row);
       const uint32_t bad = row_checks(a, fl, un, k, t, r, q, px);
-      double ivu = __builtin_nan("");
-      int stu = FV_IV_MAX_ITER;
       if (bad) {
         publish_checks(a.st, bad, a.row0 + row);
+        a.o0[row] = __builtin_nan("");
+        a.status[row] = (int8_t)FV_IV_MAX_ITER;
       } else {
         FvExc e = {0, 0, 0.0};
         if (fv_hsm_setup(a.model, (double)fl, un, k, t, r, q, px, m, e)) {
           publish_exc(&a.st->exc_first, e.code, a.row0 + row);
-          ivu = (m.status == FV_IV_CONVERGED || m.status == FV_IV_FELL_BACK) ? m.out_sigma : __builtin_nan("");
-          stu = m.status;
+          a.o0[row] = (m.status == FV_IV_CONVERGED || m.status == FV_IV_FELL_BACK) ? m.out_sigma : __builtin_nan("");
+          a.status[row] = (int8_t)m.status;
+        } else if (m.c.fk_bad) {
+          hb = true;                                         // log(F/K) raises: careful pass
         } else {
-          nd = true;
+          open = true;
         }
-      }
-      if (!nd) {
-        a.o0[row] = ivu;
-        a.status[row] = (int8_t)stu;
       }
       if (a.region) a.region[row] = -1;
     }
-    const unsigned int slot = warp_append(count, nd);
-    if (nd) { HsmRec h; h.c = m.c; h.guess = m.guess; h.row = row; recs[slot] = h; }
+    // f(SIGMA_LO) (:91-96)
+    __syncwarp();
+    FxBad f1;
+    const double flo = fx_halley_f_warp(open, m.c, FV_K_1EM9, f1, sm_x[wib], sm_r[wib], sm_f[wib]);
+    __syncwarp();
+    if (open && f1) { open = false; hb = true; }
+    if (open && flo >= 0.0) {
+      const bool conv = fv_fabs(flo) <= m.c.tol_price;
+      a.o0[row] = conv ? FV_K_1EM9 : __builtin_nan("");
+      a.status[row] = (int8_t)(conv ? FV_IV_CONVERGED : FV_IV_BELOW_INTRINSIC);
+      open = false;
+    }
+    // f(10) (:97-102); f(10) < 0 (doubling) is left to the careful pass
+    FxBad f2;
+    const double fhi = fx_halley_f_warp(open, m.c, 10.0, f2, sm_x[wib], sm_r[wib], sm_f[wib]);
+    __syncwarp();
+    if (open && (f2 || fhi < 0.0)) { open = false; hb = true; }
+    // f(guess) (:104-112)
+    const double sigma = py_min(py_max(py_min(py_max(m.guess, FV_K_0P05), 2.0), FV_K_1EM9), 10.0);
+    FxBad f3;
+    const double fval = fx_halley_f_warp(open, m.c, sigma, f3, sm_x[wib], sm_r[wib], sm_f[wib]);
+    __syncwarp();
+    if (open && f3) { open = false; hb = true; }
+    double lo = FV_K_1EM9, hi = 10.0;
+    if (fval > 0.0) hi = py_min(hi, sigma);
+    else if (fval < 0.0) lo = py_max(lo, sigma);
+    if (open && fv_fabs(fval) <= m.c.tol_price) {            // :116-117 of the first step
+      a.o0[row] = sigma;
+      a.status[row] = (int8_t)FV_IV_CONVERGED;
+      open = false;
+    }
+    const unsigned int slot = warp_append(count, open);
+    if (open) {
+      hal_store(recs + slot, m.c, lo, hi, sigma, fval);
+      rrow[slot] = row | (m.c.th > 0.0 ? FV_HAL_CALL : 0);
+    }
+    const unsigned int hs = warp_append(count + 1, hb);
+    if (hb) hrow[hs] = (int32_t)row;
   }
 }
 
-// Halley as a persistent per-lane state machine (fv_quote.h: fv_hsm_*) over
-// the prepared queue.  Each loop trip: idle lanes take the next records
-// (warp-aggregated), then every busy lane performs one solver step whose
-// heavy part -- one black_kernel evaluation -- is the same code for all.
-// kFast: the step runs on the straight-line routines (fx_hsm_pre,
-// fx_halley_f); a quote they flag is dropped and its record index appended
-// to `ridx` for the careful pass (kFast = false), which walks `ridx` and
-// recomputes those quotes from scratch on the careful routines.
+// Warp-aggregated claim of queue entries for the lanes in `need`: returns the
+// lane's entry index (>= n: queue exhausted).
+__device__ __forceinline__ unsigned long long claim(bool need, unsigned long long* next, int lane) {
+  const unsigned mask = __ballot_sync(0xffffffffu, need);
+  unsigned long long base = 0;
+  if (mask) {
+    if (lane == __ffs(mask) - 1) base = atomicAdd(next, (unsigned long long)__popc(mask));
+    base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
+  }
+  return base + __popc(mask & ((1u << lane) - 1));
+}
+
 #ifndef FV_HSM_MINB
 #define FV_HSM_MINB 3
 #endif
-template <bool kFast>
-__global__ void __launch_bounds__(256, kFast ? FV_HSM_MINB : 1) k_halley_sm(KArgs a, const HsmRec* recs,
-                                                   const unsigned int* count,
-                                                   unsigned long long* next, int32_t* ridx,
-                                                   unsigned int* rcount) {
-  const int lane = threadIdx.x & 31;
-  const unsigned long long n = *count;
-  __shared__ double sm_x[8][64], sm_r[8][64];      // range-bucketed erfc staging (fast pass)
-  __shared__ unsigned char sm_f[8][64];
-  const int wib = threadIdx.x >> 5;
-  FvHalleySM m;
-  m.state = FV_HS_DONE;
-  int64_t row = -1;
-  int32_t rec = -1;
-  bool busy = false;
-  bool exhausted = false;
-  for (;;) {
-    // ---- refill idle lanes -------------------------------------------------
-    {
-      const bool need = !busy && !exhausted;
-      const unsigned mask = __ballot_sync(0xffffffffu, need);
-      if (mask) {
-        unsigned long long base = 0;
-        if (lane == __ffs(mask) - 1) base = atomicAdd(next, (unsigned long long)__popc(mask));
-        base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
-        if (need) {
-          const unsigned long long jq = base + __popc(mask & ((1u << lane) - 1));
-          if (jq >= n) {
-            exhausted = true;
-          } else {
-            rec = kFast ? (int32_t)jq : ridx[jq];
-            const HsmRec h = recs[rec];
-            m.c = h.c; m.guess = h.guess; row = h.row;
-            m.iterations = 0; m.k = 0;
-            m.lo = FV_K_1EM9; m.hi = 10.0;
-            m.state = FV_HS_LO;
-            busy = true;
-          }
-        }
-      }
-    }
-    if (!__any_sync(0xffffffffu, busy)) break;
-    // ---- one solver step -------------------------------------------------
-    // Lanes leave fv_hsm_pre from different states; the explicit warp syncs
-    // make them enter the shared black_kernel evaluation together (without
-    // them the compiler reconverges only around the evaluation itself and
-    // each state's lanes run it separately: ~6 of 32 lanes active).
-    FvExc e = {0, 0, 0.0};
-    FxBad flagged;
-    double x = 0.0;
-    bool eval = busy && (kFast ? fx_hsm_pre(m, &x, flagged) : fv_hsm_pre(m, &x, e));
-    __syncwarp();
-    double fx = 0.0;
-    if (kFast) fx = fx_halley_f_warp(eval, m.c, x, flagged, sm_x[wib], sm_r[wib], sm_f[wib]);
-    else if (eval) fx = fv_halley_f(m.c, x, e);          // the shared heavy code
-    __syncwarp();
-    if (kFast) {
-      const unsigned int slot = warp_append(rcount, busy && flagged);
-      if (busy && flagged) { ridx[slot] = rec; busy = false; }
-    }
-    if (busy) {
-      if (eval) fv_hsm_post(m, fx, e);
-      if (e.code) {
-        publish_exc(&a.st->exc_first, e.code, a.row0 + row);
-        fv_hsm_finish(m, FV_IV_MAX_ITER, __builtin_nan(""));
-      }
-      if (m.state == FV_HS_DONE) {
-        a.o0[row] = (m.status == FV_IV_CONVERGED || m.status == FV_IV_FELL_BACK) ? m.out_sigma : __builtin_nan("");
-        a.status[row] = (int8_t)m.status;
-        busy = false;
-      }
-    }
-  }
-}
-
-// The fast pass as a lean per-lane loop (FV_HSM_LEAN): the same sequence of
-// f evaluations as fv_hsm_* (fv_quote.h) -- f(SIGMA_LO), f(hi) doubling,
-// f(guess), Halley candidate / midpoint steps, the bisection tail -- with the
-// state update of one step and the decision of the next evaluation point
-// fused into one pass over a few registers, and the Halley candidate (the
-// only heavy part besides f) computed at one site for every lane that needs
-// it.  A quote the straight-line routines flag is handed back (record index
-// into `ridx`) and recomputed from scratch by k_halley_sm<false>.
-#ifndef FV_HSM_LEAN
-#define FV_HSM_LEAN 1
-#endif
-__global__ void __launch_bounds__(256, FV_HSM_MINB) k_halley_lean(KArgs a, const HsmRec* recs,
+// Halley steps (:115-144) over the bracket pass's queue.  One f evaluation
+// per loop trip: at the Halley candidate when it lies inside the bracket,
+// else (and after a candidate that did not improve |f|) at the midpoint.
+__global__ void __launch_bounds__(256, FV_HSM_MINB) k_halley_iter(KArgs a, HalRec* recs, const int64_t* rrow,
                                                               const unsigned int* count,
-                                                              unsigned long long* next, int32_t* ridx,
-                                                              unsigned int* rcount) {
+                                                              unsigned long long* next, int32_t* bis,
+                                                              unsigned int* nbis, int32_t* hrow,
+                                                              unsigned int* nhb) {
   const int lane = threadIdx.x & 31;
   const unsigned long long n = *count;
   __shared__ double sm_x[8][64], sm_r[8][64];
   __shared__ unsigned char sm_f[8][64];
   const int wib = threadIdx.x >> 5;
   FvHalleyCtx c;
-  double lo = 0.0, hi = 0.0, sigma = 0.0, fval = 0.0, cand = 0.0, x = 0.0;
-  int st = FV_HS_DONE, k = 0;
-  int64_t row = -1;
-  int32_t rec = -1;
-  bool busy = false, exhausted = false;
+  c.th = 1.0; c.Fw = c.K = c.disc = c.sqrt_t = c.lnFK = c.target = c.tol_price = 0.0; c.fk_bad = false;
+  double lo = 0.0, hi = 0.0, sigma = 0.0, fval = 0.0;
+  int k = 0;
+  int64_t row = 0;
+  int32_t rec = 0;
+  bool busy = false, exhausted = false, midp = false;
   for (;;) {
-    {
-      const bool need = !busy && !exhausted;
-      const unsigned mask = __ballot_sync(0xffffffffu, need);
-      if (mask) {
-        unsigned long long base = 0;
-        if (lane == __ffs(mask) - 1) base = atomicAdd(next, (unsigned long long)__popc(mask));
-        base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
-        if (need) {
-          const unsigned long long jq = base + __popc(mask & ((1u << lane) - 1));
-          if (jq >= n) {
-            exhausted = true;
-          } else {
-            rec = (int32_t)jq;
-            const HsmRec h = recs[rec];
-            c = h.c; cand = h.guess; row = h.row;      // cand holds the guess until f(hi)
-            lo = FV_K_1EM9; hi = 10.0; x = lo;
-            st = FV_HS_LO;
-            busy = true;
-          }
-        }
+    const bool need = !busy && !exhausted;
+    const unsigned long long jq = claim(need, next, lane);
+    if (need) {
+      if (jq >= n) {
+        exhausted = true;
+      } else {
+        rec = (int32_t)jq;
+        const int64_t rb = rrow[rec];
+        row = rb & (FV_HAL_CALL - 1);
+        hal_load(recs + rec, rb, c, lo, hi, sigma, fval);
+        k = 0; midp = false; busy = true;
       }
     }
     if (!__any_sync(0xffffffffu, busy)) break;
+    // next evaluation point (:118-128)
+    double x = 0.5 * (lo + hi);
+    bool chk = false;
+    bool hb = false;
+    if (busy && !midp) {
+      FxBad vb;
+      const double s = sigma * c.sqrt_t;
+      double vega = 0.0, d1 = 0.0;
+      if (!(s < FV_K_1EM12)) {
+        d1 = fx_div0(c.lnFK + 0.5 * s * s, s, vb);
+        vega = c.disc * c.Fw * fx_norm_pdf(d1, vb) * c.sqrt_t;
+      }
+      double cn = __builtin_nan("");
+      if (vega > 0.0) {
+        const double d2 = d1 - s;
+        const double vomma = fx_div0(vega * d1 * d2, sigma, vb);
+        const double denom = 2.0 * vega * vega - fval * vomma;
+        if (denom != 0.0) cn = sigma - fx_div0(2.0 * fval * vega, denom, vb);
+      }
+      if (fv_isfinite(cn) && lo < cn && cn < hi) { x = cn; chk = true; }
+      if (vb) hb = true;
+    }
+    if (hb) busy = false;
     __syncwarp();
-    FxBad flagged;
-    const double fx = fx_halley_f_warp(busy, c, x, flagged, sm_x[wib], sm_r[wib], sm_f[wib]);
+    FxBad fb;
+    const double fx = fx_halley_f_warp(busy, c, x, fb, sm_x[wib], sm_r[wib], sm_f[wib]);
     __syncwarp();
-    bool handback = busy && flagged;
-    if (handback) busy = false;
-    int fin = -1;                   // status when the quote finishes this step
-    double fin_sigma = 0.0;
-    bool need_iter = false, need_bis = false;
+    if (busy && fb) { hb = true; busy = false; }
+    int fin = -1;
+    bool to_bis = false;
     if (busy) {
-      switch (st) {
-        case FV_HS_LO:                                       // solver.py:92-96
-          if (fx >= 0.0) {
-            fin = fv_fabs(fx) <= c.tol_price ? FV_IV_CONVERGED : FV_IV_BELOW_INTRINSIC;
-            fin_sigma = lo;
-          } else {
-            st = FV_HS_HI; x = hi;
-          }
-          break;
-        case FV_HS_HI:                                       // :97-106
-          if (fx < 0.0) {
-            if (hi < 100.0) { hi = py_min(2.0 * hi, 100.0); x = hi; }
-            else fin = FV_IV_MAX_ITER;
-          } else {
-            sigma = py_min(py_max(py_min(py_max(cand, FV_K_0P05), 2.0), lo), hi);
-            st = FV_HS_GUESS; x = sigma;
-          }
-          break;
-        case FV_HS_GUESS:                                    // :108-112
-          fval = fx;
-          if (fx > 0.0) hi = py_min(hi, sigma);
-          else if (fx < 0.0) lo = py_max(lo, sigma);
-          k = 0;
-          need_iter = true;
-          break;
-        case FV_HS_CHECK:                                    // :129-135
-          if (!(fv_fabs(fx) < fv_fabs(fval))) {
-            cand = 0.5 * (lo + hi); st = FV_HS_MID; x = cand;
-            break;
-          }
-          // fall through: accepted
-        case FV_HS_MID: {                                    // :136-144
-          if (fx > 0.0) hi = cand;
-          else if (fx < 0.0) lo = cand;
-          const double step = cand - sigma;
-          sigma = cand; fval = fx;
-          if (fv_fabs(step) <= FV_K_1EM12 * py_max(1.0, sigma)) { fin = FV_IV_CONVERGED; fin_sigma = sigma; break; }
-          if (++k == 16) { k = 0; need_bis = true; }
-          else need_iter = true;
-          break;
-        }
-        default:                                             // FV_HS_BISECT, :151-161
-          fval = fx;
-          if (fx > 0.0) hi = sigma;
-          else lo = sigma;
-          if (++k == 128) {
-            const bool ok = fv_fabs(fval) <= c.tol_price || (hi - lo) <= FV_K_1EM12 * py_max(1.0, sigma);
-            fin = ok ? FV_IV_FELL_BACK : FV_IV_MAX_ITER;
-            fin_sigma = sigma;
-          } else {
-            need_bis = true;
-          }
-          break;
+      if (chk && !(fv_fabs(fx) < fv_fabs(fval))) {          // :129-135: rejected -> f(mid) next
+        midp = true;
+      } else {                                               // :136-144
+        midp = false;
+        if (fx > 0.0) hi = x;
+        else if (fx < 0.0) lo = x;
+        const double step = x - sigma;
+        sigma = x; fval = fx;
+        if (fv_fabs(step) <= FV_K_1EM12 * py_max(1.0, sigma)) fin = FV_IV_CONVERGED;
+        else if (++k == 16) to_bis = true;
+        else if (fv_fabs(fval) <= c.tol_price) fin = FV_IV_CONVERGED;   // :116-117 of the next step
       }
     }
-    if (need_bis) {                                          // :147-150
-      if (fv_fabs(fval) <= c.tol_price || (hi - lo) <= FV_K_1EM12 * py_max(1.0, sigma)) {
-        fin = FV_IV_FELL_BACK; fin_sigma = sigma;
-      } else {
-        sigma = 0.5 * (lo + hi); x = sigma; st = FV_HS_BISECT;
-      }
-    }
-    if (need_iter) {                                         // :115-128
-      if (fv_fabs(fval) <= c.tol_price) {
-        fin = FV_IV_CONVERGED; fin_sigma = sigma;
-      } else {
-        FxBad vb;
-        const double s = sigma * c.sqrt_t;
-        double vega = 0.0, d1 = 0.0;
-        if (!(s < FV_K_1EM12)) {
-          vb |= c.fk_bad;                                    // ValueError site (:45)
-          d1 = fx_div0(c.lnFK + 0.5 * s * s, s, vb);
-          vega = c.disc * c.Fw * fx_norm_pdf(d1, vb) * c.sqrt_t;
-        }
-        double cn = __builtin_nan("");
-        if (vega > 0.0) {
-          const double d2 = d1 - s;
-          const double vomma = fx_div0(vega * d1 * d2, sigma, vb);
-          const double denom = 2.0 * vega * vega - fval * vomma;
-          if (denom != 0.0) cn = sigma - fx_div0(2.0 * fval * vega, denom, vb);
-        }
-        if (fv_isfinite(cn) && lo < cn && cn < hi) { cand = cn; st = FV_HS_CHECK; }
-        else { cand = 0.5 * (lo + hi); st = FV_HS_MID; }
-        x = cand;
-        if (vb) { handback = true; busy = false; }
-      }
-    }
-    const unsigned int slot = warp_append(rcount, handback);
-    if (handback) ridx[slot] = rec;
     if (fin >= 0) {
-      a.o0[row] = (fin == FV_IV_CONVERGED || fin == FV_IV_FELL_BACK) ? fin_sigma : __builtin_nan("");
+      a.o0[row] = sigma;
       a.status[row] = (int8_t)fin;
       busy = false;
     }
+    if (to_bis) {
+      double2* p = reinterpret_cast<double2*>(recs + rec);
+      p[4] = make_double2(lo, hi);
+      p[5] = make_double2(sigma, fval);
+      busy = false;
+    }
+    const unsigned int bs = warp_append(nbis, to_bis);
+    if (to_bis) bis[bs] = rec;
+    const unsigned int hs = warp_append(nhb, hb);
+    if (hb) hrow[hs] = (int32_t)row;
+  }
+}
+
+// Bisection tail (:146-161) over the quotes the Halley pass re-queued.
+__global__ void __launch_bounds__(256, FV_HSM_MINB) k_halley_bisect(KArgs a, const HalRec* recs,
+                                                                const int64_t* rrow, const int32_t* bis,
+                                                                const unsigned int* nbis,
+                                                                unsigned long long* next, int32_t* hrow,
+                                                                unsigned int* nhb) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long n = *nbis;
+  __shared__ double sm_x[8][64], sm_r[8][64];
+  __shared__ unsigned char sm_f[8][64];
+  const int wib = threadIdx.x >> 5;
+  FvHalleyCtx c;
+  c.th = 1.0; c.Fw = c.K = c.disc = c.sqrt_t = c.lnFK = c.target = c.tol_price = 0.0; c.fk_bad = false;
+  double lo = 0.0, hi = 0.0, sigma = 0.0, fval = 0.0;
+  int k = 0;
+  int64_t row = 0;
+  bool busy = false, exhausted = false;
+  for (;;) {
+    const bool need = !busy && !exhausted;
+    const unsigned long long jq = claim(need, next, lane);
+    if (need) {
+      if (jq >= n) {
+        exhausted = true;
+      } else {
+        const int32_t rec = bis[jq];
+        const int64_t rb = rrow[rec];
+        row = rb & (FV_HAL_CALL - 1);
+        hal_load(recs + rec, rb, c, lo, hi, sigma, fval);
+        k = 0; busy = true;
+      }
+    }
+    if (!__any_sync(0xffffffffu, busy)) break;
+    if (busy && (fv_fabs(fval) <= c.tol_price || (hi - lo) <= FV_K_1EM12 * py_max(1.0, sigma))) {
+      a.o0[row] = sigma;                                     // :147-149
+      a.status[row] = (int8_t)FV_IV_FELL_BACK;
+      busy = false;
+    }
+    const double x = 0.5 * (lo + hi);
+    __syncwarp();
+    FxBad fb;
+    const double fx = fx_halley_f_warp(busy, c, x, fb, sm_x[wib], sm_r[wib], sm_f[wib]);
+    __syncwarp();
+    const bool hb = busy && fb;
+    if (hb) busy = false;
+    if (busy) {                                              // :150-157
+      sigma = x; fval = fx;
+      if (fx > 0.0) hi = x;
+      else lo = x;
+      if (++k == 128) {                                      // :158-161
+        const bool ok = fv_fabs(fval) <= c.tol_price || (hi - lo) <= FV_K_1EM12 * py_max(1.0, sigma);
+        a.o0[row] = ok ? sigma : __builtin_nan("");
+        a.status[row] = (int8_t)(ok ? FV_IV_FELL_BACK : FV_IV_MAX_ITER);
+        busy = false;
+      }
+    }
+    const unsigned int hs = warp_append(nhb, hb);
+    if (hb) hrow[hs] = (int32_t)row;
+  }
+}
+
+// Handed-back quotes: the careful solver from the row's inputs.
+__global__ void __launch_bounds__(256) k_halley_careful(KArgs a, const int32_t* hrow, const unsigned int* nhb) {
+  const int64_t n = *nhb;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = hrow[j];
+    const int fl = ldf1(a.flag, row);
+    const double un = ld1(a.un, row), k = ld1(a.k, row), t = ld1(a.t, row), r = ld1(a.r, row);
+    const double q = ld1(a.q, row), px = ld1(a.last, row);
+    FvExc e = {0, 0, 0.0};
+    int status;
+    double sig;
+    fv_halley_row_sm(a.model, (double)fl, un, k, t, r, q, px, &status, &sig, e);
+    if (e.code) publish_exc(&a.st->exc_first, e.code, a.row0 + row);
+    a.o0[row] = (status == FV_IV_CONVERGED || status == FV_IV_FELL_BACK) ? sig : __builtin_nan("");
+    a.status[row] = (int8_t)status;
   }
 }
 
@@ -1127,7 +1153,7 @@ thread_local int64_t t_launches = 0;
 const char* const kKernelNames[FV_NKERNEL] = {
     "k_price", "k_price_greeks", "k_lbr_normalize", "k_lbr_normalize_replay", "k_lbr_anchors",
     "k_lbr_far_low_fast", "k_lbr_solve<FAR_LOW>", "k_lbr_solve<NEAR>", "k_lbr_solve<FAR_HIGH>",
-    "k_halley_setup", "k_halley_sm", "k_halley_sm<careful>", "k_lbr_near_fast"};
+    "k_halley_bracket", "k_halley_iter", "k_halley_careful", "k_lbr_near_fast", "k_halley_bisect"};
 struct TimedLaunch { int id; cudaEvent_t a, b; };
 thread_local bool t_timing = false;
 thread_local std::vector<TimedLaunch> t_timed;
@@ -1169,11 +1195,12 @@ struct DevWork {
   int32_t* lbr_q[FV_NSLOT] = {};        // 6 queues of lbr_cap entries each
   unsigned int* lbr_count = nullptr;    // [FV_NSLOT][8]
   int64_t lbr_cap[FV_NSLOT] = {};
-  int blocks_price = 0, blocks_greeks = 0, blocks_hsm = 0, blocks_hsm2 = 0;
-  unsigned long long* work_ctr = nullptr;   // [FV_NSLOT]
-  unsigned int* hsm_count = nullptr;        // [FV_NSLOT][2]: records, records handed back
-  HsmRec* hsm_recs[FV_NSLOT] = {};
-  int32_t* hsm_ridx[FV_NSLOT] = {};         // records handed back by the fast pass
+  int blocks_price = 0, blocks_greeks = 0, blocks_hiter = 0, blocks_hbis = 0, blocks_hcare = 0;
+  unsigned long long* work_ctr = nullptr;   // [FV_NSLOT][2]: Halley / bisection claims
+  unsigned int* hsm_count = nullptr;        // [FV_NSLOT][4]: records, handed back, bisection queue
+  HalRec* hsm_recs[FV_NSLOT] = {};
+  int64_t* hsm_rrow[FV_NSLOT] = {};         // row | call bit per record
+  int32_t* hsm_ridx[FV_NSLOT] = {};         // [cap] handed-back rows, [cap] bisection queue
   int64_t hsm_cap[FV_NSLOT] = {};
   int blocks_hset = 0;
   int blocks_lbr_nfast = 0;
@@ -1217,15 +1244,12 @@ cudaError_t get_work(DevWork** out) {
     w->blocks_lbr_near = occupancy_blocks((const void*)k_lbr_solve<FV_NEAR_LOW>, w->sm_count);
     w->blocks_lbr_nfast = occupancy_blocks((const void*)k_lbr_near_fast, w->sm_count);
     w->blocks_lbr_fh = occupancy_blocks((const void*)k_lbr_solve<FV_FAR_HIGH>, w->sm_count);
-#if FV_HSM_LEAN
-    w->blocks_hsm = occupancy_blocks((const void*)k_halley_lean, w->sm_count);
-#else
-    w->blocks_hsm = occupancy_blocks((const void*)k_halley_sm<true>, w->sm_count);
-#endif
-    w->blocks_hsm2 = occupancy_blocks((const void*)k_halley_sm<false>, w->sm_count);
+    w->blocks_hiter = occupancy_blocks((const void*)k_halley_iter, w->sm_count);
+    w->blocks_hbis = occupancy_blocks((const void*)k_halley_bisect, w->sm_count);
+    w->blocks_hcare = occupancy_blocks((const void*)k_halley_careful, w->sm_count);
     CK(cudaMalloc(&w->work_ctr, sizeof(unsigned long long) * 2 * FV_NSLOT));
-    CK(cudaMalloc(&w->hsm_count, sizeof(unsigned int) * 2 * FV_NSLOT));
-    w->blocks_hset = occupancy_blocks((const void*)k_halley_setup, w->sm_count);
+    CK(cudaMalloc(&w->hsm_count, sizeof(unsigned int) * 4 * FV_NSLOT));
+    w->blocks_hset = occupancy_blocks((const void*)k_halley_bracket, w->sm_count);
     g_work[dev] = w;
   }
   *out = g_work[dev];
@@ -1241,6 +1265,7 @@ cudaError_t get_work(DevWork** out) {
 #define FV_LBR_ROUND_LOG2 27
 #endif
 const int64_t kLbrChunk = 1ll << FV_LBR_ROUND_LOG2;
+const int64_t kHalleyChunk = 1ll << 26;
 
 cudaError_t ensure_lbr(DevWork* w, int slot, int64_t rows) {
   if (w->lbr_cap[slot] >= rows) return cudaSuccess;
@@ -1276,13 +1301,16 @@ KArgs sub_args(const KArgs& a, int64_t off, int64_t len) {
 cudaError_t ensure_hsm(DevWork* w, int slot, int64_t rows) {
   if (w->hsm_cap[slot] >= rows) return cudaSuccess;
   if (w->hsm_recs[slot]) cudaFree(w->hsm_recs[slot]);
+  if (w->hsm_rrow[slot]) cudaFree(w->hsm_rrow[slot]);
   if (w->hsm_ridx[slot]) cudaFree(w->hsm_ridx[slot]);
   w->hsm_recs[slot] = nullptr;
+  w->hsm_rrow[slot] = nullptr;
   w->hsm_ridx[slot] = nullptr;
   w->hsm_cap[slot] = 0;
   int64_t cap = rows < 4096 ? 4096 : rows;
-  CK(cudaMalloc(&w->hsm_recs[slot], sizeof(HsmRec) * cap));
-  CK(cudaMalloc(&w->hsm_ridx[slot], sizeof(int32_t) * cap));
+  CK(cudaMalloc(&w->hsm_recs[slot], sizeof(HalRec) * cap));
+  CK(cudaMalloc(&w->hsm_rrow[slot], sizeof(int64_t) * cap));
+  CK(cudaMalloc(&w->hsm_ridx[slot], sizeof(int32_t) * 2 * cap));
   w->hsm_cap[slot] = cap;
   return cudaSuccess;
 }
@@ -1351,22 +1379,27 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
           FV_LAUNCH(FV_KID_LBR_FH, s, k_lbr_solve<FV_FAR_HIGH><<<g(w->blocks_lbr_fh), 256, 0, s>>>(b, lq));
         }
       } else {
-        CK(ensure_hsm(w, slot, a.n));
-        unsigned long long* ctr = w->work_ctr + 2 * slot;   // [0] fast pass, [1] careful pass
-        unsigned int* cnt = w->hsm_count + 2 * slot;         // [0] records, [1] handed back
-        CK(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s));
-        CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned int), s));
-        FV_LAUNCH(FV_KID_HALLEY_SETUP, s, k_halley_setup<<<blocks_for(w->blocks_hset, a.n), 256, 0, s>>>(a, w->hsm_recs[slot], cnt));
-        const int64_t need = (a.n + 255) / 256;
-#if FV_HSM_LEAN
-        FV_LAUNCH(FV_KID_HALLEY_SM, s, k_halley_lean<<<need < w->blocks_hsm ? need : w->blocks_hsm, 256, 0, s>>>(
-            a, w->hsm_recs[slot], cnt, ctr, w->hsm_ridx[slot], cnt + 1));
-#else
-        FV_LAUNCH(FV_KID_HALLEY_SM, s, k_halley_sm<true><<<need < w->blocks_hsm ? need : w->blocks_hsm, 256, 0, s>>>(
-            a, w->hsm_recs[slot], cnt, ctr, w->hsm_ridx[slot], cnt + 1));
-#endif
-        FV_LAUNCH(FV_KID_HALLEY_SM2, s, k_halley_sm<false><<<need < w->blocks_hsm2 ? need : w->blocks_hsm2, 256, 0, s>>>(
-            a, w->hsm_recs[slot], cnt + 1, ctr + 1, w->hsm_ridx[slot], nullptr));
+        // chunks of <= 2^26 rows: int32 row indices in the queues, bounded buffers
+        const int64_t chunk = a.n < kHalleyChunk ? a.n : kHalleyChunk;
+        CK(ensure_hsm(w, slot, chunk));
+        for (int64_t off = 0; off < a.n; off += chunk) {
+          KArgs b = sub_args(a, off, (a.n - off) < chunk ? (a.n - off) : chunk);
+          unsigned long long* ctr = w->work_ctr + 2 * slot;   // [0] Halley, [1] bisection claims
+          unsigned int* cnt = w->hsm_count + 4 * slot;         // [0] records, [1] handed back, [2] bisection
+          int32_t* hrow = w->hsm_ridx[slot];
+          int32_t* bis = w->hsm_ridx[slot] + w->hsm_cap[slot];
+          CK(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s));
+          CK(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned int), s));
+          const int64_t need = (b.n + 255) / 256;
+          auto g = [need](int blocks) { return (int)(need < blocks ? need : blocks); };
+          FV_LAUNCH(FV_KID_HALLEY_SETUP, s, k_halley_bracket<<<blocks_for(w->blocks_hset, b.n), 256, 0, s>>>(
+              b, w->hsm_recs[slot], w->hsm_rrow[slot], cnt, hrow));
+          FV_LAUNCH(FV_KID_HALLEY_SM, s, k_halley_iter<<<g(w->blocks_hiter), 256, 0, s>>>(
+              b, w->hsm_recs[slot], w->hsm_rrow[slot], cnt, ctr, bis, cnt + 2, hrow, cnt + 1));
+          FV_LAUNCH(FV_KID_HALLEY_BISECT, s, k_halley_bisect<<<g(w->blocks_hbis), 256, 0, s>>>(
+              b, w->hsm_recs[slot], w->hsm_rrow[slot], bis, cnt + 2, ctr + 1, hrow, cnt + 1));
+          FV_LAUNCH(FV_KID_HALLEY_SM2, s, k_halley_careful<<<g(w->sm_count), 256, 0, s>>>(b, hrow, cnt + 1));
+        }
       }
       break;
   }
