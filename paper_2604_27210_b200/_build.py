@@ -49,5 +49,32 @@ def build(force=False, verbose=False, out=None, defines=()):
     return out
 
 
+HOST_SRC = os.path.join(CSRC, "fv_host.cpp")
+
+
+def host_ext_path():
+    import sysconfig
+    return os.path.join(HERE, "_fvhost" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_host(force=False):
+    """The CPython extension with the batch front end's host loops
+    (csrc/fv_host.cpp: flag parsing, status object columns)."""
+    import sysconfig
+    import numpy
+    out = host_ext_path()
+    if not force and not _stale(out, [HOST_SRC]):
+        return out
+    tmp = out + ".tmp%d" % os.getpid()
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-pthread", "-fvisibility=hidden",
+           "-I" + sysconfig.get_paths()["include"], "-I" + numpy.get_include(), "-o", tmp, HOST_SRC]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("g++ failed:\n" + res.stdout + res.stderr)
+    os.replace(tmp, out)
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    print(build_host(force="--force" in sys.argv))

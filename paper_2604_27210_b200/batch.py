@@ -29,6 +29,19 @@ GREEK_COLUMNS = ("delta", "gamma", "theta", "rho", "vega")
 
 _IV_STATUS = np.array(IV_STATUS_NAMES, dtype=object)
 _GREEK_STATUS = np.array(GREEK_STATUS_NAMES, dtype=object)
+
+try:                        # csrc/fv_host.cpp: threaded flag parsing / status columns
+    from . import _fvhost
+except ImportError:         # not built: the numpy forms below (same results)
+    _fvhost = None
+_HOST_MIN_ROWS = 1 << 16
+
+
+def _status_column(table: np.ndarray, codes: np.ndarray) -> np.ndarray:
+    """``table[codes]`` as a fresh object array (batch.py:217, :259)."""
+    if _fvhost is not None and codes.shape[0] >= _HOST_MIN_ROWS:
+        return _fvhost.status_objects(tuple(table), codes)
+    return table[codes]
 _CHECK_KIND = ["BadFlag"] + ["NonFiniteInput"] * 6 + ["DomainError"] * 5
 _CHECK_COLUMN = ["flag", "underlying", "strike", "t", "r", "q", None,
                  "underlying", "strike", "t", "sigma", "q"]
@@ -107,6 +120,11 @@ def parse_flags(flags: Union[str, Sequence[str]]) -> np.ndarray:
         n = arr.shape[0]
         if n == 0:
             return np.empty(0, dtype=np.int8)
+        if _fvhost is not None and n >= _HOST_MIN_ROWS:
+            out, bad = _fvhost.parse_flags_u(np.ascontiguousarray(arr))
+            if bad >= 0:
+                raise _flag_error(bad, flags[bad])
+            return out
         cp = np.ascontiguousarray(arr).view(np.uint32).reshape(n, arr.dtype.itemsize // 4)
         low = cp[:, 0] | np.uint32(0x20)
         is_c = low == 0x63
@@ -323,7 +341,7 @@ def batch_iv(model, method: str, flag, underlying, strike, t, r, price=None, q=0
         _ok_or_raise(rc, err, table, model, "price")
     cols_out = dict(table)
     cols_out["iv"] = iv
-    cols_out["status"] = _IV_STATUS[codes]
+    cols_out["status"] = _status_column(_IV_STATUS, codes)
     return ChainTable(cols_out)
 
 
@@ -346,7 +364,7 @@ def batch_greeks(model, flag, underlying, strike, t, r, q=0.0, sigma=None) -> Ch
         _ok_or_raise(rc, err, table, model, "sigma")
     cols_out = dict(table)
     cols_out.update(outs)
-    cols_out["status"] = _GREEK_STATUS[codes]
+    cols_out["status"] = _status_column(_GREEK_STATUS, codes)
     return ChainTable(cols_out)
 
 
