@@ -30,12 +30,20 @@ def main():
     theta = B.parse_flags(chars)
     out["parse_flags_s"] = time.perf_counter() - t0
     t0 = time.perf_counter()
+    _fvh, B._fvhost = B._fvhost, None
+    B.parse_flags(chars)
+    B._fvhost = _fvh
+    out["parse_flags_numpy_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
     res = fv.batch_iv("black", "lbr", chars, F[:1], K, t, r[:1], price=px)
     out["batch_iv_total_s"] = time.perf_counter() - t0
     t0 = time.perf_counter()
-    _ = np.array(["converged", "fell_back_to_bisection", "below_intrinsic", "above_upper_bound",
-                  "max_iterations"], dtype=object)[np.zeros(n, np.int8)]
+    _ = B._status_column(B._IV_STATUS, np.zeros(n, np.int8))
     out["status_strings_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _ = B._IV_STATUS[np.zeros(n, np.int8)]
+    out["status_strings_numpy_take_s"] = time.perf_counter() - t0
+    out["host_frontend_ext"] = B._fvhost is not None
     lib = fv._native.lib_for_compute()
     keep, cols = B._columns({"flag": theta, "underlying": F[:1], "strike": K, "t": t, "r": r[:1],
                              "q": np.zeros(1), "price": px}, "price")
