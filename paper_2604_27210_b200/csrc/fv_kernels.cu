@@ -307,6 +307,7 @@ struct LbrQueues {
                          // 6: near rows the straight-line near solver handed back
   unsigned int* count;   // [16]: queue lengths [0..6], work counters of the far-low
                          // solve [7], the normalize pass [8] and the near solve [9]
+  unsigned int norm_claim;  // pairs per work claim of the normalize pass (32 | 64 | 128)
 };
 
 __device__ __forceinline__ int region_class(int region) {
@@ -391,11 +392,11 @@ __global__ void __launch_bounds__(256, FV_NORM_MINB) k_lbr_normalize(KArgs a, Lb
   // (FV_NORM_CLAIM pairs per atomic, processed 32 at a time)
   for (;;) {
     unsigned int claim = 0;
-    if (lane == 0) claim = atomicAdd(lq.count + 8, (unsigned)FV_NORM_CLAIM);
+    if (lane == 0) claim = atomicAdd(lq.count + 8, lq.norm_claim);
     claim = __shfl_sync(0xffffffffu, claim, 0);
     if ((int64_t)claim >= npair) break;
 #pragma unroll 1
-  for (int sub = 0; sub < FV_NORM_CLAIM / 32; ++sub) {
+  for (int sub = 0; sub < (int)(lq.norm_claim / 32); ++sub) {
     const unsigned int base = claim + 32u * sub;
     if ((int64_t)base >= npair) break;
     const int64_t j = (int64_t)base + lane;
@@ -1364,6 +1365,16 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
           lq.sb0 = sb + 2 * cp; lq.sb1 = sb + 3 * cp; lq.sE0 = sb + 4 * cp; lq.sE1 = sb + 5 * cp;
           for (int c3 = 0; c3 < 7; ++c3) lq.q[c3] = w->lbr_q[slot] + c3 * w->lbr_cap[slot];
           lq.count = w->lbr_count + 16 * slot;
+          // claims as large as FV_NORM_CLAIM pairs while every warp still gets
+          // >= 4 of them: a small batch (C1: 1M rows = 141 pairs per warp) with
+          // 128-pair claims leaves a tenth of the warps a second claim to run
+          // alone after the rest are done
+          {
+            const int64_t npair = (b.n + 1) / 2, warps = (int64_t)w->blocks_lbr_norm * 8;
+            unsigned cl = FV_NORM_CLAIM;
+            while (cl > 32 && npair < warps * (int64_t)cl * 4) cl /= 2;
+            lq.norm_claim = cl;
+          }
           CK(cudaMemsetAsync(lq.count, 0, 16 * sizeof(unsigned int), s));
           const int64_t cap1 = (b.n + 255) / 256;
           auto g = [cap1](int blocks) { return (int)(cap1 < blocks ? cap1 : blocks); };
