@@ -35,6 +35,7 @@ try:                        # csrc/fv_host.cpp: threaded flag parsing / status c
 except ImportError:         # not built: the numpy forms below (same results)
     _fvhost = None
 _HOST_MIN_ROWS = 1 << 16
+_CSV_MIN_ROWS = 1024
 
 
 def _status_column(table: np.ndarray, codes: np.ndarray) -> np.ndarray:
@@ -397,31 +398,43 @@ def _plain_text(value) -> str:
     return str(value)
 
 
+def _csv(table: ChainTable, names) -> str:
+    if _fvhost is not None and table.length >= _CSV_MIN_ROWS:
+        # threaded shortest-round-trip formatting (csrc/fv_host.cpp); None when
+        # a column is outside its float64 / integer / str-object cases
+        text = _fvhost.format_csv(tuple(names), tuple(np.asarray(table[c]) for c in names))
+        if text is not None:
+            return text
+    cols = [table[c] for c in names]
+    rows = (",".join(_cell_text(col[i]) for col in cols) for i in range(table.length))
+    return "\n".join([",".join(names), *rows]) + "\n"
+
+
+def _json(table: ChainTable, names) -> str:
+    obj = {}
+    for name in names:
+        col = table[name]
+        if col.dtype.kind == "f":
+            obj[name] = [float(v) if math.isfinite(v) else None for v in col]
+        elif name == "flag":
+            obj[name] = ["p" if v <= 0 else "c" for v in col]
+        else:
+            obj[name] = [str(v) for v in col]
+    return json.dumps(obj)
+
+
+def _plain(table: ChainTable, names) -> str:
+    grid = [list(names)] + [[_plain_text(table[c][i]) for c in names] for i in range(table.length)]
+    widths = [max(len(row[j]) for row in grid) for j in range(len(names))]
+    return "".join("  ".join(cell.ljust(w) for cell, w in zip(row, widths)) + "\n" for row in grid)
+
+
+_FORMATS = {"csv": _csv, "json": _json, "plain": _plain}
+
+
 def format_output(table: ChainTable, fmt: str = "csv") -> str:
-    """Serialize a table to csv, json, or a plain aligned listing."""
-    names = list(table.columns)
-    n = table.length
-    if fmt == "csv":
-        lines = [",".join(names)]
-        for i in range(n):
-            lines.append(",".join(_cell_text(table[c][i]) for c in names))
-        return "\n".join(lines) + "\n"
-    if fmt == "json":
-        obj = {}
-        for name in names:
-            col = table[name]
-            if col.dtype.kind == "f":
-                obj[name] = [None if not math.isfinite(v) else float(v) for v in col]
-            elif name == "flag":
-                obj[name] = ["c" if v > 0 else "p" for v in col]
-            else:
-                obj[name] = [str(v) for v in col]
-        return json.dumps(obj)
-    if fmt == "plain":
-        cells = [[_plain_text(table[c][i]) for c in names] for i in range(n)]
-        widths = [max([len(name)] + [len(row[j]) for row in cells]) for j, name in enumerate(names)]
-        lines = ["  ".join(name.ljust(widths[j]) for j, name in enumerate(names))]
-        for row in cells:
-            lines.append("  ".join(cell.ljust(widths[j]) for j, cell in enumerate(row)))
-        return "\n".join(lines) + "\n"
-    raise BatchError("DomainError", 0, f"unknown output format {fmt!r}")
+    """Serialize a table to csv, json, or a plain aligned listing
+    (batch.py:294-326)."""
+    if fmt not in _FORMATS:
+        raise BatchError("DomainError", 0, f"unknown output format {fmt!r}")
+    return _FORMATS[fmt](table, list(table.columns))

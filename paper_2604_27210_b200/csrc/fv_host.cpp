@@ -27,6 +27,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <charconv>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -138,7 +140,206 @@ PyObject* status_objects(PyObject*, PyObject* args) {
   return (PyObject*)out;
 }
 
+// ---- CSV serialisation (batch.py:287-306 format_output(table, "csv")) -------
+// Cell text: float columns -> repr(float(v)) (shortest round trip), integer
+// columns -> 'c' if v > 0 else 'p', str objects -> the string itself.  The
+// shortest digits come from std::to_chars (C++17: the shortest string that
+// round-trips, nearest to the value on ties -- the digits of CPython's
+// repr); the layout is CPython's float_repr_style 'short' rule: positional
+// when -4 < decpt <= 16, else d[.ddd]e+XX with at least two exponent digits.
+int repr_double(double v, char* out) {
+  if (v != v) { memcpy(out, "nan", 3); return 3; }
+  char buf[40];
+  auto res = std::to_chars(buf, buf + sizeof(buf), v, std::chars_format::scientific);
+  const char* p = buf;
+  const char* end = res.ptr;
+  int o = 0;
+  if (*p == '-') { out[o++] = '-'; ++p; }
+  if (*p == 'i') { memcpy(out + o, "inf", 3); return o + 3; }
+  char dig[24];
+  int nd = 0;
+  while (p < end && *p != 'e') { if (*p != '.') dig[nd++] = *p; ++p; }
+  int e10 = 0;
+  if (p < end) {                                   // 'e' [+-] digits
+    ++p;
+    const bool neg = *p == '-';
+    ++p;
+    while (p < end) e10 = e10 * 10 + (*p++ - '0');
+    if (neg) e10 = -e10;
+  }
+  const int decpt = e10 + 1;                       // value = 0.d1d2... x 10^decpt
+  if (decpt > -4 && decpt <= 16) {
+    if (decpt <= 0) {
+      out[o++] = '0'; out[o++] = '.';
+      for (int i = 0; i < -decpt; ++i) out[o++] = '0';
+      memcpy(out + o, dig, nd); o += nd;
+    } else if (decpt < nd) {
+      memcpy(out + o, dig, decpt); o += decpt;
+      out[o++] = '.';
+      memcpy(out + o, dig + decpt, nd - decpt); o += nd - decpt;
+    } else {
+      memcpy(out + o, dig, nd); o += nd;
+      for (int i = nd; i < decpt; ++i) out[o++] = '0';
+      out[o++] = '.'; out[o++] = '0';
+    }
+    return o;
+  }
+  out[o++] = dig[0];
+  if (nd > 1) { out[o++] = '.'; memcpy(out + o, dig + 1, nd - 1); o += nd - 1; }
+  out[o++] = 'e';
+  int x = decpt - 1;
+  out[o++] = x < 0 ? '-' : '+';
+  if (x < 0) x = -x;
+  char xe[8];
+  int nx = 0;
+  do { xe[nx++] = (char)('0' + x % 10); x /= 10; } while (x);
+  if (nx < 2) xe[nx++] = '0';
+  while (nx) out[o++] = xe[--nx];
+  return o;
+}
+
+PyObject* repr_doubles(PyObject*, PyObject* args) {       // test hook: list of repr strings
+  PyArrayObject* arr;
+  if (!PyArg_ParseTuple(args, "O!", &PyArray_Type, &arr)) return nullptr;
+  if (PyArray_NDIM(arr) != 1 || PyArray_TYPE(arr) != NPY_FLOAT64) {
+    PyErr_SetString(PyExc_TypeError, "repr_doubles: 1-d float64 array expected");
+    return nullptr;
+  }
+  const int64_t n = PyArray_DIM(arr, 0);
+  PyObject* lst = PyList_New(n);
+  if (!lst) return nullptr;
+  char buf[48];
+  for (int64_t i = 0; i < n; ++i) {
+    const double v = *(const double*)PyArray_GETPTR1(arr, i);
+    const int k = repr_double(v, buf);
+    PyList_SET_ITEM(lst, i, PyUnicode_FromStringAndSize(buf, k));
+  }
+  return lst;
+}
+
+enum ColKind { COL_F64, COL_INT, COL_STR };
+struct CsvCol {
+  ColKind kind;
+  const char* base;
+  int64_t stride;          // bytes
+  int isize;               // integer item size
+  bool is_signed;
+  std::vector<PyObject*> objs;          // COL_STR: distinct objects ...
+  std::vector<std::string> text;        // ... and their UTF-8
+};
+
+// format_csv(names, columns) -> str, or None when a column is outside the
+// fast path (the caller then runs the Python loop).
+PyObject* format_csv(PyObject*, PyObject* args) {
+  PyObject* names;
+  PyObject* cols;
+  if (!PyArg_ParseTuple(args, "O!O!", &PyTuple_Type, &names, &PyTuple_Type, &cols)) return nullptr;
+  const Py_ssize_t m = PyTuple_GET_SIZE(names);
+  if (m != PyTuple_GET_SIZE(cols) || m == 0) Py_RETURN_NONE;
+  std::string header;
+  for (Py_ssize_t j = 0; j < m; ++j) {
+    PyObject* nm = PyTuple_GET_ITEM(names, j);
+    if (!PyUnicode_CheckExact(nm)) Py_RETURN_NONE;
+    Py_ssize_t len;
+    const char* u = PyUnicode_AsUTF8AndSize(nm, &len);
+    if (!u) return nullptr;
+    if (j) header += ',';
+    header.append(u, len);
+  }
+  header += '\n';
+  int64_t n = -1;
+  std::vector<CsvCol> cc(m);
+  for (Py_ssize_t j = 0; j < m; ++j) {
+    PyObject* o = PyTuple_GET_ITEM(cols, j);
+    if (!PyArray_Check(o)) Py_RETURN_NONE;
+    PyArrayObject* a = (PyArrayObject*)o;
+    if (PyArray_NDIM(a) != 1) Py_RETURN_NONE;
+    if (n < 0) n = PyArray_DIM(a, 0);
+    if (PyArray_DIM(a, 0) != n) Py_RETURN_NONE;
+    CsvCol& c = cc[j];
+    c.base = (const char*)PyArray_DATA(a);
+    c.stride = PyArray_STRIDE(a, 0);
+    const int t = PyArray_TYPE(a);
+    if (t == NPY_FLOAT64 && PyArray_ISNOTSWAPPED(a)) {
+      c.kind = COL_F64;
+    } else if (PyArray_ISINTEGER(a) && PyArray_ISNOTSWAPPED(a) && PyArray_ITEMSIZE(a) <= 8) {
+      c.kind = COL_INT;
+      c.isize = (int)PyArray_ITEMSIZE(a);
+      c.is_signed = PyArray_ISSIGNED(a);
+    } else if (t == NPY_OBJECT) {
+      c.kind = COL_STR;
+      for (int64_t i = 0; i < n; ++i) {                 // distinct objects (a status column has <= 5)
+        PyObject* v = *(PyObject* const*)(c.base + i * c.stride);
+        bool seen = false;
+        for (PyObject* w : c.objs) if (w == v) { seen = true; break; }
+        if (seen) continue;
+        if (c.objs.size() >= 16 || !v || !PyUnicode_CheckExact(v)) Py_RETURN_NONE;
+        Py_ssize_t len;
+        const char* u = PyUnicode_AsUTF8AndSize(v, &len);
+        if (!u) return nullptr;
+        c.objs.push_back(v);
+        c.text.emplace_back(u, len);
+      }
+    } else {
+      Py_RETURN_NONE;
+    }
+  }
+  unsigned nt = std::thread::hardware_concurrency();
+  if (nt > 16) nt = 16;
+  int64_t parts = n / 65536;
+  if (parts > (int64_t)nt) parts = nt;
+  if (parts < 1) parts = 1;
+  std::vector<std::string> chunk(parts);
+  Py_BEGIN_ALLOW_THREADS
+  auto work = [&](int64_t k) {
+    const int64_t a = n * k / parts, b = n * (k + 1) / parts;
+    std::string& s = chunk[k];
+    s.reserve((size_t)(b - a) * (size_t)m * 20);
+    char buf[48];
+    for (int64_t i = a; i < b; ++i) {
+      for (Py_ssize_t j = 0; j < m; ++j) {
+        const CsvCol& c = cc[j];
+        const char* p = c.base + i * c.stride;
+        if (c.kind == COL_F64) {
+          double v;
+          memcpy(&v, p, 8);
+          s.append(buf, repr_double(v, buf));
+        } else if (c.kind == COL_INT) {
+          bool pos;
+          switch (c.isize) {
+            case 1: pos = c.is_signed ? *(const int8_t*)p > 0 : *(const uint8_t*)p > 0; break;
+            case 2: pos = c.is_signed ? *(const int16_t*)p > 0 : *(const uint16_t*)p > 0; break;
+            case 4: pos = c.is_signed ? *(const int32_t*)p > 0 : *(const uint32_t*)p > 0; break;
+            default: pos = c.is_signed ? *(const int64_t*)p > 0 : *(const uint64_t*)p > 0; break;
+          }
+          s += pos ? 'c' : 'p';
+        } else {
+          PyObject* v = *(PyObject* const*)p;
+          size_t w = 0;
+          while (c.objs[w] != v) ++w;
+          s += c.text[w];
+        }
+        s += (j + 1 < m) ? ',' : '\n';
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (int64_t k = 1; k < parts; ++k) th.emplace_back(work, k);
+  work(0);
+  for (auto& t : th) t.join();
+  Py_END_ALLOW_THREADS
+  size_t total = header.size();
+  for (auto& s : chunk) total += s.size();
+  std::string all;
+  all.reserve(total);
+  all += header;
+  for (auto& s : chunk) { all += s; std::string().swap(s); }
+  return PyUnicode_DecodeUTF8(all.data(), (Py_ssize_t)all.size(), "strict");
+}
+
 PyMethodDef kMethods[] = {
+    {"format_csv", format_csv, METH_VARARGS, "format_output(table, 'csv') for float / integer-flag / str columns, or None"},
+    {"repr_doubles", repr_doubles, METH_VARARGS, "repr(float(v)) for each element (test hook)"},
     {"parse_flags_u", parse_flags_u, METH_VARARGS, "case-insensitive c/p -> int8 +1/-1; (flags, first_bad)"},
     {"status_objects", status_objects, METH_VARARGS, "object array names[codes]"},
     {nullptr, nullptr, 0, nullptr}};

@@ -88,3 +88,89 @@ def test_status_objects_rejects_bad_codes(H):
     with pytest.raises(ValueError, match="row 2000000"):
         H.status_objects(names, codes)
     assert [sys.getrefcount(x) for x in names] == before
+
+
+def test_repr_doubles_is_python_repr(H):
+    """Shortest round-trip digits + CPython's 'r' layout, on random bit
+    patterns (every exponent, subnormals, nan/inf) and typical values."""
+    rng = np.random.default_rng(5)
+    x = np.concatenate([
+        rng.integers(0, 2**64, 300_000, dtype=np.uint64).view(np.float64),
+        rng.standard_normal(100_000) * 10.0 ** rng.integers(-30, 30, 100_000),
+        np.round(rng.uniform(0, 500, 50_000), 4),
+        np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e16, 1e15, 9999999999999998.0, 1e-4, 1e-5,
+                  5e-324, 1.7976931348623157e308, 2.2250738585072014e-308, 1e22, 1e23, 0.1, 100.0]),
+    ])
+    assert H.repr_doubles(x) == [repr(float(v)) for v in x]
+
+
+def _python_csv(table):
+    from paper_2604_27210_b200 import batch as B
+    saved, B._fvhost = B._fvhost, None
+    try:
+        return B.format_output(table, "csv")
+    finally:
+        B._fvhost = saved
+
+
+def test_format_csv_matches_python_rules(H):
+    from paper_2604_27210_b200 import batch as B
+    from paper_2604_27210_b200.solver import IV_STATUS_NAMES
+    rng = np.random.default_rng(9)
+    n = 50_000
+    iv = rng.uniform(0.05, 2.0, n)
+    iv[rng.integers(0, n, 500)] = np.nan
+    cols = {
+        "flag": np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8),
+        "underlying": np.broadcast_to(np.float64(100.0), (n,)),       # stride-0 broadcast column
+        "strike": 100 * np.exp(rng.uniform(-0.6, 0.6, n)),
+        "t": rng.uniform(1e-9, 30, n),
+        "r": np.full(n, -0.0),
+        "price": rng.integers(0, 2**64, n, dtype=np.uint64).view(np.float64),
+        "iv": iv,
+        "status": np.array(IV_STATUS_NAMES, dtype=object)[rng.integers(0, 5, n)],
+    }
+    t = B.ChainTable(cols)
+    fast = B.format_output(t, "csv")
+    assert fast == _python_csv(t)
+    assert fast.startswith("flag,underlying,strike,t,r,price,iv,status\n")
+
+
+def test_format_csv_falls_back_outside_fast_path(H):
+    from paper_2604_27210_b200 import batch as B
+    n = 2000
+    odd = np.empty(n, dtype=object)
+    odd[:] = [1.5, "x", 3] * (n // 3) + [2.0] * (n % 3)   # mixed objects: Python rules per cell
+    t = B.ChainTable({"a": np.arange(n, dtype=np.float32), "b": odd, "c": np.zeros(n, dtype=bool)})
+    assert H.format_csv(("a", "b", "c"), (t["a"], t["b"], t["c"])) is None
+    assert B.format_output(t, "csv") == _python_csv(t)
+
+
+@pytest.mark.parametrize("fmt", ["csv", "json", "plain"])
+@pytest.mark.parametrize("fast", [True, False])
+def test_format_output_reference_golden(fmt, fast):
+    """format_output against the reference's own text (tests/golden/gen_format.py)."""
+    import json
+    import os
+    from paper_2604_27210_b200 import batch as B
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "format_output.json")))
+    cols = {}
+    for k, v in g["columns"].items():
+        if k == "flag":
+            cols[k] = np.array(v, dtype=np.int8)
+        elif k == "status":
+            cols[k] = np.array(v, dtype=object)
+        else:
+            cols[k] = np.array([float.fromhex(x) for x in v])
+    saved = B._fvhost
+    if not fast:
+        B._fvhost = None
+    else:
+        B._CSV_MIN_ROWS, saved_min = 1, B._CSV_MIN_ROWS
+    try:
+        text = B.format_output(B.ChainTable(cols), fmt)
+    finally:
+        B._fvhost = saved
+        if fast:
+            B._CSV_MIN_ROWS = saved_min
+    assert text == g[fmt]
