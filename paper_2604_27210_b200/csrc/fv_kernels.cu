@@ -676,6 +676,9 @@ __device__ __forceinline__ void hal_load(const HalRec* r, int64_t rowbits, FvHal
   lo = v4.x; hi = v4.y; sigma = v5.x; fval = v5.y;
 }
 
+#ifndef FV_HAL_SIGN32
+#define FV_HAL_SIGN32 1
+#endif
 #ifndef FV_HSET_MINB
 #define FV_HSET_MINB 3
 #endif
@@ -728,11 +731,17 @@ __global__ void __launch_bounds__(256, FV_HSET_MINB) k_halley_bracket(KArgs a, H
       a.status[row] = (int8_t)(conv ? FV_IV_CONVERGED : FV_IV_BELOW_INTRINSIC);
       open = false;
     }
-    // f(10) (:97-102); f(10) < 0 (doubling) is left to the careful pass
+    // f(10) (:97-102): only its sign is consumed -- fp32 with a rigorous margin
+    // (fx_halley_sign); f(10) < 0 (doubling) and undecided signs are left to
+    // the careful pass
+#if FV_HAL_SIGN32
+    if (open && fx_halley_sign(m.c, 10.0) <= 0) { open = false; hb = true; }
+#else
     FxBad f2;
     const double fhi = fx_halley_f_warp(open, m.c, 10.0, f2, sm_x[wib], sm_r[wib], sm_f[wib]);
     __syncwarp();
     if (open && (f2 || fhi < 0.0)) { open = false; hb = true; }
+#endif
     // f(guess) (:104-112)
     const double sigma = py_min(py_max(py_min(py_max(m.guess, FV_K_0P05), 2.0), FV_K_1EM9), 10.0);
     FxBad f3;

@@ -305,3 +305,29 @@ int64_t qh_erfc_u_check(const double* x, int64_t n, int64_t* nflag) {
   return bad;
 }
 }
+
+extern "C" {
+// fx_halley_sign (fp32 with a margin) against the sign of the careful f(sigma)
+// at the bracket's sigma values: returns rows where a decided sign differs;
+// *undecided = rows it left to the exact evaluation.
+int64_t qh_halley_sign_check(int model, const int8_t* flag, const double* un, const double* k,
+                             const double* t, const double* r, const double* q, const double* px,
+                             int64_t n, const double* sigmas, int nsig, int64_t* undecided) {
+  int64_t bad = 0, und = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    FvExc e = {0, 0, 0.0};
+    FvHalleySM m;
+    if (fv_hsm_setup(model, (double)flag[i], un[i], k[i], t[i], r[i], q[i], px[i], m, e)) continue;
+    if (m.c.fk_bad) continue;
+    for (int j = 0; j < nsig; ++j) {
+      FvExc e2 = {0, 0, 0.0};
+      const double f = fv_halley_f(m.c, sigmas[j], e2);
+      const int sg = fx_halley_sign(m.c, sigmas[j]);
+      if (sg == 0) { ++und; continue; }
+      if (e2.code || (sg > 0 && !(f > 0.0)) || (sg < 0 && !(f < 0.0))) ++bad;
+    }
+  }
+  *undecided = und;
+  return bad;
+}
+}

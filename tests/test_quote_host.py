@@ -314,3 +314,34 @@ def test_unified_erfc_matches_glibc(Q):
     assert Q.qh_erfc_u_check(_p(x), ctypes.c_int64(len(x)), ctypes.byref(nb)) == 0
     # flags are fx_erfc's (checked above): |x| beyond ~26.5 (exp underflow) and nan / inf
     assert nb.value < 3 * len(x) // 8
+
+
+@pytest.mark.parametrize("case", ["c2", "wide", "c5"])
+def test_halley_fp32_sign_matches_careful(Q, case):
+    """fx_halley_sign (the bracket pass's fp32 sign of f(10), margin 1e-4 disc
+    (F + K)) never decides a sign the careful f disagrees with; checked at
+    sigma = 10 and at values where f is small (near the solution)."""
+    from oracle import fvoracle as O
+    from paper_2604_27210_b200 import workloads as W
+    Q.qh_halley_sign_check.restype = ctypes.c_int64
+    rng = np.random.default_rng(21)
+    if case == "c5":
+        flag, S, K, t, r, sig, kind, side = W.c5_params(30_000, seed=5)
+        q = np.zeros_like(S)
+        model = 0
+        px = W.c5_prices(flag, S, K, t, r, kind, side, O.rows_price("black", flag, S, K, t, r, 0.0, sig)["price"])
+    else:
+        flag, S, K, t, r, q, sig = W.chain_draws(30_000, seed=41)
+        model = 2
+        if case == "wide":
+            t = 10.0 ** rng.uniform(-6, 2.5, len(t))
+            K = S * np.exp(rng.uniform(-8, 8, len(K)))
+            sig = 10.0 ** rng.uniform(-3, 0.9, len(sig))
+        px = O.rows_price("bsm", flag, S, K, t, r, q, sig)["price"]
+    sigmas = np.array([10.0, 20.0, 40.0, 80.0, 100.0, 5.0, 2.0, 1.0, 0.5, 0.2, 0.1, 0.05])
+    cols = [np.ascontiguousarray(a) for a in (flag.astype(np.int8), S, K, t, r, q, px)]
+    und = ctypes.c_int64(0)
+    bad = Q.qh_halley_sign_check(ctypes.c_int(model), *[_p(c) for c in cols], ctypes.c_int64(len(flag)),
+                                 _p(sigmas), ctypes.c_int(len(sigmas)), ctypes.byref(und))
+    assert bad == 0
+    assert und.value < len(flag) * len(sigmas) // 4
