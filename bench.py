@@ -543,7 +543,9 @@ def run_ours(args):
                                  "stream); achieved = W=%.0f weighted distinct fp64 ops/quote (SURVEY 8(d)) x rows per "
                                  "call / mean call duration (CUDA events on the launching stream); peak = measured "
                                  "DFMA issue rate (fv_probe_fp64_peak, this run); traffic = ncu DRAM read+write bytes "
-                                 "per call (profiles/roofline_traffic.json)" % W_OPS[args.workload]},
+                                 "per call (profiles/roofline_traffic.json)" % W_OPS[args.workload]
+                                 + ("; C2: the bracket pass decides f(10)'s sign in fp32 instead of evaluating "
+                                    "it (~8 % of W counted but not executed)" if args.workload == "c2" else "")},
             "kernels": kernels,
             "dominant_kernel": (dict(dominant, peak=peak_tops, unit="T weighted-fp64-ops/s",
                                      frac=dominant["achieved"] / peak_tops if peak_tops else None)
