@@ -337,7 +337,149 @@ PyObject* format_csv(PyObject*, PyObject* args) {
   return PyUnicode_DecodeUTF8(all.data(), (Py_ssize_t)all.size(), "strict");
 }
 
+// ---- CSV chain input (cli.py:140-173 _read_chain + _numeric) ---------------
+// parse_chain_csv(data) -> None when the text is outside the fast path (any
+// '"' or '\r', a ragged row, a non-ASCII byte, a non-flag text column), else
+// (header, columns, bad) with columns[j] a float64 array (numeric columns:
+// every cell that is a plain decimal -- [-]digits[.digits][(e|E)[+-]digits] --
+// parsed by std::from_chars, correctly rounded like float()) or, for the
+// 'flag' column, a numpy 'U1' array; bad = list of (row, column) cells the
+// strict form did not take (the caller applies float() to them, which either
+// parses them or raises the reference's error).  csv.reader semantics for
+// this subset: lines end at '\n', a final '\n' ends the last row, an empty
+// line is a row of 0 cells.
+bool plain_decimal(const char* p, const char* e) {
+  if (p < e && *p == '-') ++p;
+  const char* d0 = p;
+  while (p < e && *p >= '0' && *p <= '9') ++p;
+  bool digits = p > d0;
+  if (p < e && *p == '.') {
+    ++p;
+    const char* f0 = p;
+    while (p < e && *p >= '0' && *p <= '9') ++p;
+    digits = digits || p > f0;
+  }
+  if (!digits) return false;
+  if (p < e && (*p == 'e' || *p == 'E')) {
+    ++p;
+    if (p < e && (*p == '+' || *p == '-')) ++p;
+    const char* x0 = p;
+    while (p < e && *p >= '0' && *p <= '9') ++p;
+    if (p == x0) return false;
+  }
+  return p == e;
+}
+
+PyObject* parse_chain_csv(PyObject*, PyObject* args) {
+  Py_buffer buf;
+  if (!PyArg_ParseTuple(args, "y*", &buf)) return nullptr;
+  struct Release { Py_buffer* b; ~Release() { PyBuffer_Release(b); } } rel{&buf};
+  const char* d = (const char*)buf.buf;
+  const int64_t len = buf.len;
+  for (int64_t i = 0; i < len; ++i) {
+    const unsigned char ch = (unsigned char)d[i];
+    if (ch == '"' || ch == '\r' || ch >= 0x80) Py_RETURN_NONE;
+  }
+  // line starts
+  std::vector<int64_t> ls;
+  ls.push_back(0);
+  for (int64_t i = 0; i < len; ++i)
+    if (d[i] == '\n' && i + 1 < len) ls.push_back(i + 1);
+  if (len == 0) Py_RETURN_NONE;
+  auto line_end = [&](size_t k) {
+    int64_t e = (k + 1 < ls.size()) ? ls[k + 1] - 1 : len;
+    if (e > ls[k] && d[e - 1] == '\n') --e;         // the final line's '\n'
+    return e;
+  };
+  // header
+  std::vector<std::pair<int64_t, int64_t>> hcells;
+  {
+    int64_t a = ls[0], e = line_end(0);
+    if (a == e) Py_RETURN_NONE;                         // csv gives [] for an empty header line
+    int64_t c0 = a;
+    for (int64_t i = a; i <= e; ++i)
+      if (i == e || d[i] == ',') { hcells.emplace_back(c0, i); c0 = i + 1; }
+  }
+  const int64_t m = (int64_t)hcells.size();
+  const int64_t n = (int64_t)ls.size() - 1;
+  int flag_col = -1;
+  for (int64_t j = 0; j < m; ++j)
+    if (hcells[j].second - hcells[j].first == 4 && memcmp(d + hcells[j].first, "flag", 4) == 0) flag_col = (int)j;
+  std::vector<double*> out(m, nullptr);
+  std::vector<PyObject*> arrays(m, nullptr);
+  npy_intp dims[1] = {(npy_intp)n};
+  for (int64_t j = 0; j < m; ++j) {
+    arrays[j] = (j == flag_col) ? PyArray_New(&PyArray_Type, 1, dims, NPY_UNICODE, nullptr, nullptr, 4, 0, nullptr)
+                                : PyArray_SimpleNew(1, dims, NPY_FLOAT64);
+    if (!arrays[j]) { for (auto* o : arrays) Py_XDECREF(o); return nullptr; }
+  }
+  uint32_t* flag_out = flag_col >= 0 ? (uint32_t*)PyArray_DATA((PyArrayObject*)arrays[flag_col]) : nullptr;
+  for (int64_t j = 0; j < m; ++j)
+    if (j != flag_col) out[j] = (double*)PyArray_DATA((PyArrayObject*)arrays[j]);
+  unsigned nt = std::thread::hardware_concurrency();
+  if (nt > 16) nt = 16;
+  int64_t parts = n / 65536;
+  if (parts > (int64_t)nt) parts = nt;
+  if (parts < 1) parts = 1;
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> bad(parts);
+  std::vector<char> fallback(parts, 0);
+  Py_BEGIN_ALLOW_THREADS
+  auto work = [&](int64_t k) {
+    const int64_t r0 = n * k / parts, r1 = n * (k + 1) / parts;
+    for (int64_t r = r0; r < r1 && !fallback[k]; ++r) {
+      const int64_t a = ls[r + 1], e = line_end(r + 1);
+      if (a == e) { fallback[k] = 1; break; }            // empty line: csv gives a 0-cell row
+      int64_t j = 0, c0 = a;
+      for (int64_t i = a; i <= e; ++i) {
+        if (i != e && d[i] != ',') continue;
+        if (j >= m) { fallback[k] = 1; break; }          // ragged row: the Python path reports it
+        if (j == flag_col) {
+          if (i - c0 != 1) { fallback[k] = 1; break; }   // flag cells other than one character
+          flag_out[r] = (unsigned char)d[c0];
+        } else if (plain_decimal(d + c0, d + i)) {
+          double v;
+          auto res = std::from_chars(d + c0, d + i, v);
+          if (res.ec == std::errc::result_out_of_range) {
+            bad[k].emplace_back(r, j);                   // float() gives inf / 0 here: let it
+            v = 0.0;
+          }
+          out[j][r] = v;
+        } else {
+          out[j][r] = 0.0;
+          bad[k].emplace_back(r, j);
+        }
+        ++j;
+        c0 = i + 1;
+      }
+      if (j != m) fallback[k] = 1;
+    }
+  };
+  std::vector<std::thread> th;
+  for (int64_t k = 1; k < parts; ++k) th.emplace_back(work, k);
+  work(0);
+  for (auto& t : th) t.join();
+  Py_END_ALLOW_THREADS
+  bool fb = false;
+  for (char f : fallback) fb = fb || f;
+  if (fb) { for (auto* o : arrays) Py_XDECREF(o); Py_RETURN_NONE; }
+  PyObject* hdr = PyTuple_New(m);
+  PyObject* cols = PyTuple_New(m);
+  PyObject* badl = PyList_New(0);
+  for (int64_t j = 0; j < m; ++j) {
+    PyTuple_SET_ITEM(hdr, j, PyUnicode_DecodeASCII(d + hcells[j].first, hcells[j].second - hcells[j].first, "strict"));
+    PyTuple_SET_ITEM(cols, j, arrays[j]);
+  }
+  for (auto& v : bad)
+    for (auto& rc : v) {
+      PyObject* t = Py_BuildValue("(LL)", (long long)rc.first, (long long)rc.second);
+      PyList_Append(badl, t);
+      Py_DECREF(t);
+    }
+  return Py_BuildValue("(NNN)", hdr, cols, badl);
+}
+
 PyMethodDef kMethods[] = {
+    {"parse_chain_csv", parse_chain_csv, METH_VARARGS, "fast path of the chain CSV reader, or None"},
     {"format_csv", format_csv, METH_VARARGS, "format_output(table, 'csv') for float / integer-flag / str columns, or None"},
     {"repr_doubles", repr_doubles, METH_VARARGS, "repr(float(v)) for each element (test hook)"},
     {"parse_flags_u", parse_flags_u, METH_VARARGS, "case-insensitive c/p -> int8 +1/-1; (flags, first_bad)"},
