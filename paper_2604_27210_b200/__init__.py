@@ -7,9 +7,11 @@ ChainTable, statuses and errors, computed by hand-written CUDA kernels
 (csrc/) behind the C ABI in include/fastvol_b200.h.  The paper's names
 (fast_black_scholes_merton, fast_implied_volatility, jackel_iv_black,
 get_all_greeks, jackel.jackel_iv_black, set_backend, patch_py_vollib, ...,
-with return_as containers) live in ``paper_2604_27210_b200.fast_vollib``.
+with return_as containers) live in ``paper_2604_27210_b200.fast_vollib``; the
+chain CSV reader of the reference's CLI (cli.py:140-173) in ``chain_csv``.
 """
 
+from . import chain_csv
 from .batch import (BatchError, ChainTable, batch_greeks, batch_iv, batch_price, broadcast,
                     format_output, parse_flags, validate)
 from .errors import AboveUpperBoundError, BelowIntrinsicError, DomainError, StepFunctionEdge
@@ -22,5 +24,5 @@ __all__ = [
     "BatchError", "ChainTable", "batch_greeks", "batch_iv", "batch_price", "broadcast",
     "format_output", "parse_flags", "validate",
     "AboveUpperBoundError", "BelowIntrinsicError", "DomainError", "StepFunctionEdge",
-    "Model", "PricingInputs", "parse_flag", "SolverResult", "SolverStatus",
+    "Model", "PricingInputs", "parse_flag", "SolverResult", "SolverStatus", "chain_csv",
 ]
