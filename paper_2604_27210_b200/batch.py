@@ -411,6 +411,12 @@ def _csv(table: ChainTable, names) -> str:
 
 
 def _json(table: ChainTable, names) -> str:
+    if _fvhost is not None and table.length >= _CSV_MIN_ROWS:
+        text = _fvhost.format_json(tuple(json.dumps(n) for n in names),
+                                   tuple(np.asarray(table[c]) for c in names),
+                                   names.index("flag") if "flag" in names else -1)
+        if text is not None:
+            return text
     obj = {}
     for name in names:
         col = table[name]

@@ -478,7 +478,135 @@ PyObject* parse_chain_csv(PyObject*, PyObject* args) {
   return Py_BuildValue("(NNN)", hdr, cols, badl);
 }
 
+// format_json(keys, columns, flag_index) -> str or None: batch.py:307-317
+// json.dumps({name: [...]}) with float64 columns as repr / null (non-finite),
+// the integer 'flag' column as "c" / "p", str-object columns as their text;
+// keys arrive JSON-encoded from the caller.  Strings that would need JSON
+// escapes (quote, backslash, control or non-ASCII characters) -> None.
+bool json_plain(const std::string& s) {
+  for (unsigned char ch : s)
+    if (ch < 0x20 || ch >= 0x7f || ch == '"' || ch == '\\') return false;
+  return true;
+}
+
+PyObject* format_json(PyObject*, PyObject* args) {
+  PyObject* keys;
+  PyObject* cols;
+  int flag_index;
+  if (!PyArg_ParseTuple(args, "O!O!i", &PyTuple_Type, &keys, &PyTuple_Type, &cols, &flag_index)) return nullptr;
+  const Py_ssize_t m = PyTuple_GET_SIZE(keys);
+  if (m != PyTuple_GET_SIZE(cols)) Py_RETURN_NONE;
+  std::vector<std::string> kenc(m);
+  for (Py_ssize_t j = 0; j < m; ++j) {
+    PyObject* k = PyTuple_GET_ITEM(keys, j);
+    if (!PyUnicode_CheckExact(k)) Py_RETURN_NONE;
+    Py_ssize_t len;
+    const char* u = PyUnicode_AsUTF8AndSize(k, &len);
+    if (!u) return nullptr;
+    kenc[j].assign(u, len);
+  }
+  int64_t n = -1;
+  std::vector<CsvCol> cc(m);
+  for (Py_ssize_t j = 0; j < m; ++j) {
+    PyObject* o = PyTuple_GET_ITEM(cols, j);
+    if (!PyArray_Check(o)) Py_RETURN_NONE;
+    PyArrayObject* a = (PyArrayObject*)o;
+    if (PyArray_NDIM(a) != 1) Py_RETURN_NONE;
+    if (n < 0) n = PyArray_DIM(a, 0);
+    if (PyArray_DIM(a, 0) != n) Py_RETURN_NONE;
+    CsvCol& c = cc[j];
+    c.base = (const char*)PyArray_DATA(a);
+    c.stride = PyArray_STRIDE(a, 0);
+    const int t = PyArray_TYPE(a);
+    if (t == NPY_FLOAT64 && PyArray_ISNOTSWAPPED(a)) {
+      c.kind = COL_F64;
+    } else if (PyArray_ISFLOAT(a)) {
+      Py_RETURN_NONE;                                  // other float widths: Python path
+    } else if (j == flag_index && PyArray_ISINTEGER(a) && PyArray_ISNOTSWAPPED(a) && PyArray_ITEMSIZE(a) <= 8) {
+      c.kind = COL_INT;
+      c.isize = (int)PyArray_ITEMSIZE(a);
+      c.is_signed = PyArray_ISSIGNED(a);
+    } else if (t == NPY_OBJECT && j != flag_index) {
+      c.kind = COL_STR;
+      for (int64_t i = 0; i < n; ++i) {
+        PyObject* v = *(PyObject* const*)(c.base + i * c.stride);
+        bool seen = false;
+        for (PyObject* w : c.objs) if (w == v) { seen = true; break; }
+        if (seen) continue;
+        if (c.objs.size() >= 16 || !v || !PyUnicode_CheckExact(v)) Py_RETURN_NONE;
+        Py_ssize_t len;
+        const char* u = PyUnicode_AsUTF8AndSize(v, &len);
+        if (!u) return nullptr;
+        std::string q = "\"";
+        q.append(u, len);
+        if (!json_plain(q.substr(1))) Py_RETURN_NONE;
+        q += '"';
+        c.objs.push_back(v);
+        c.text.push_back(q);
+      }
+    } else {
+      Py_RETURN_NONE;
+    }
+  }
+  unsigned nt = std::thread::hardware_concurrency();
+  if (nt > 16) nt = 16;
+  int64_t parts = n / 65536;
+  if (parts > (int64_t)nt) parts = nt;
+  if (parts < 1) parts = 1;
+  std::vector<std::string> chunk((size_t)m * parts);
+  Py_BEGIN_ALLOW_THREADS
+  auto work = [&](int64_t k) {
+    const int64_t a = n * k / parts, b = n * (k + 1) / parts;
+    char buf[48];
+    for (Py_ssize_t j = 0; j < m; ++j) {
+      const CsvCol& c = cc[j];
+      std::string& s = chunk[(size_t)j * parts + k];
+      s.reserve((size_t)(b - a) * 22);
+      for (int64_t i = a; i < b; ++i) {
+        if (i) { s += ','; s += ' '; }
+        const char* p = c.base + i * c.stride;
+        if (c.kind == COL_F64) {
+          double v;
+          memcpy(&v, p, 8);
+          if (v - v != 0.0) s.append("null", 4);         // nan, inf
+          else s.append(buf, repr_double(v, buf));
+        } else if (c.kind == COL_INT) {
+          bool pos;
+          switch (c.isize) {
+            case 1: pos = c.is_signed ? *(const int8_t*)p > 0 : *(const uint8_t*)p > 0; break;
+            case 2: pos = c.is_signed ? *(const int16_t*)p > 0 : *(const uint16_t*)p > 0; break;
+            case 4: pos = c.is_signed ? *(const int32_t*)p > 0 : *(const uint32_t*)p > 0; break;
+            default: pos = c.is_signed ? *(const int64_t*)p > 0 : *(const uint64_t*)p > 0; break;
+          }
+          s.append(pos ? "\"c\"" : "\"p\"", 3);
+        } else {
+          PyObject* v = *(PyObject* const*)p;
+          size_t w = 0;
+          while (c.objs[w] != v) ++w;
+          s += c.text[w];
+        }
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (int64_t k = 1; k < parts; ++k) th.emplace_back(work, k);
+  work(0);
+  for (auto& t : th) t.join();
+  Py_END_ALLOW_THREADS
+  std::string all = "{";
+  for (Py_ssize_t j = 0; j < m; ++j) {
+    if (j) all += ", ";
+    all += kenc[j];
+    all += ": [";
+    for (int64_t k = 0; k < parts; ++k) { all += chunk[(size_t)j * parts + k]; std::string().swap(chunk[(size_t)j * parts + k]); }
+    all += ']';
+  }
+  all += '}';
+  return PyUnicode_DecodeUTF8(all.data(), (Py_ssize_t)all.size(), "strict");
+}
+
 PyMethodDef kMethods[] = {
+    {"format_json", format_json, METH_VARARGS, "format_output(table, 'json') for float / flag / str columns, or None"},
     {"parse_chain_csv", parse_chain_csv, METH_VARARGS, "fast path of the chain CSV reader, or None"},
     {"format_csv", format_csv, METH_VARARGS, "format_output(table, 'csv') for float / integer-flag / str columns, or None"},
     {"repr_doubles", repr_doubles, METH_VARARGS, "repr(float(v)) for each element (test hook)"},

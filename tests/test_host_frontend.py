@@ -174,3 +174,27 @@ def test_format_output_reference_golden(fmt, fast):
         if fast:
             B._CSV_MIN_ROWS = saved_min
     assert text == g[fmt]
+
+
+def test_format_json_matches_python_rules(H):
+    from paper_2604_27210_b200 import batch as B
+    from paper_2604_27210_b200.solver import GREEK_STATUS_NAMES
+    rng = np.random.default_rng(19)
+    n = 120_000
+    v = rng.integers(0, 2**64, n, dtype=np.uint64).view(np.float64)
+    cols = {"flag": np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8),
+            "strike": 100 * np.exp(rng.uniform(-0.6, 0.6, n)), "vega": v,
+            "status": np.array(GREEK_STATUS_NAMES, dtype=object)[rng.integers(0, 2, n)]}
+    t = B.ChainTable(cols)
+    fast = B.format_output(t, "json")
+    saved, B._fvhost = B._fvhost, None
+    try:
+        slow = B.format_output(t, "json")
+    finally:
+        B._fvhost = saved
+    assert fast == slow
+    # outside the fast path: float32, a non-flag integer column, strings needing escapes
+    for extra in ({"x": np.ones(n, np.float32)}, {"x": np.arange(n)},
+                  {"x": np.array(['a"b', "ok"] * (n // 2), dtype=object)}):
+        c2 = dict(cols, **extra)
+        assert H.format_json(tuple('"%s"' % k for k in c2), tuple(c2.values()), 0) is None
