@@ -429,7 +429,7 @@ def run_ours(args):
 
     # ---- e2e: same call with pinned host buffers ---------------------------
     e2e = None
-    if not args.no_e2e and method >= 0:
+    if not args.no_e2e:
         hcols = {}
         for k, v in cols.items():
             if not torch.is_tensor(v):
@@ -437,15 +437,21 @@ def run_ours(args):
             hcols[k] = v.cpu().pin_memory() if v.numel() > 1 else v.cpu()
         h_iv = torch.empty(n, dtype=torch.float64).pin_memory()
         h_st = torch.empty(n, dtype=torch.int8).pin_memory()
+        h_g = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(6)] if method < 0 else []
         hn = native_cols(hcols, last)
         h2d = sum(hcols[k].numel() * hcols[k].element_size()
                   for k in ("flag", "underlying", "strike", "t", "r", "q", last)
                   if hcols[k].numel() > 1)
-        d2h = n * 9
+        d2h = n * 9 if method >= 0 else n * 49        # iv + status | price + 5 Greeks + status
 
         def estep():
             err = _native.fv_error()
-            rc = lib.fv_batch_iv(model, method, *hn, n, h_iv.data_ptr(), h_st.data_ptr(), None, err)
+            if method >= 0:
+                rc = lib.fv_batch_iv(model, method, *hn, n, h_iv.data_ptr(), h_st.data_ptr(), None, err)
+            else:
+                err2 = _native.fv_error()
+                rc = lib.fv_price_greeks(model, *hn, n, *[g.data_ptr() for g in h_g], h_st.data_ptr(),
+                                         err, err2)
             if rc:
                 raise RuntimeError(err.message)
         estep()
@@ -463,7 +469,11 @@ def run_ours(args):
             pg.all_reduce(tt, op=pg.ReduceOp.MAX)
             e_ms = float(tt.item())
         # bit-identical to the device-resident result
-        same = bool(torch.equal(h_iv.to(dev).view(torch.int64), out_iv.view(torch.int64)))
+        if method >= 0:
+            same = bool(torch.equal(h_iv.to(dev).view(torch.int64), out_iv.view(torch.int64)))
+        else:
+            same = all(bool(torch.equal(h.to(dev).view(torch.int64), g.view(torch.int64)))
+                       for h, g in zip(h_g, greeks))
         # the link's own ceiling: a plain pinned 1 GB host->device copy
         h2d_gbs = None
         try:
