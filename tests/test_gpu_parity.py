@@ -502,3 +502,43 @@ def test_odd_sizes_and_strided_device_columns(fv, oracle_mod, n):
     assert_bits(outs[0].cpu().numpy(), px, f"n={n} price")
     for j, name in enumerate(("delta", "gamma", "theta", "rho", "vega")):
         assert_bits(outs[j + 1].cpu().numpy(), g[name], f"n={n} {name}")
+
+
+@pytest.mark.gpu
+def test_c2_full_10m_halley(fv, oracle_mod):
+    """BASELINE size for the Halley path: the whole 10M-quote C2 batch (BSM
+    with dividend yield) in one device-resident call through the three Halley
+    passes.  The status mix is the reference's (95.4 %
+    converged / 4.0 % fell back / 0.67 % below intrinsic); a strided 1-in-50
+    sample and every 10th quote that fell back to bisection (the bisection
+    pass's work) are bit-compared with the oracle; the host-pointer path
+    is bit-identical to the device-resident one."""
+    import bench
+    import torch
+    from paper_2604_27210_b200 import _native
+    lib = _native.lib_for_compute()
+    dev = torch.device("cuda", 0)
+    n = 10_000_000
+    cols = bench.draws_device("c2", n, 0, dev)
+    cols["price"] = bench.price_on_device(lib, 2, cols, n)
+    iv = torch.empty(n, dtype=torch.float64, device=dev)
+    st = torch.empty(n, dtype=torch.int8, device=dev)
+    err = _native.fv_error()
+    ncols = bench.native_cols(cols, "price")
+    assert lib.fv_batch_iv(2, 0, *ncols, n, iv.data_ptr(), st.data_ptr(), None, err) == 0, err.message
+    torch.cuda.synchronize()
+    counts = torch.bincount(st.to(torch.int64), minlength=5).cpu().tolist()
+    assert counts == [9558752, 376255, 64993, 0, 0], counts
+    idx = torch.cat([torch.arange(0, n, 50, device=dev), torch.nonzero(st == 1).flatten()[::10]])
+    samp = {k: cols[k][idx].cpu().numpy() for k in ("flag", "underlying", "strike", "t", "r", "q", "price")}
+    want = oracle_mod.rows_iv("bsm", "halley", samp["flag"], samp["underlying"], samp["strike"], samp["t"],
+                              samp["r"], samp["q"], samp["price"])
+    assert_bits(st[idx].cpu().numpy(), want["status_code"], "C2-10M sample status")
+    assert_bits(iv[idx].cpu().numpy(), want["iv"], "C2-10M sample iv")
+    hcols = {k: (v.cpu().pin_memory() if v.numel() > 1 else v.cpu()) for k, v in cols.items() if torch.is_tensor(v)}
+    hiv = torch.empty(n, dtype=torch.float64).pin_memory()
+    hst = torch.empty(n, dtype=torch.int8).pin_memory()
+    assert lib.fv_batch_iv(2, 0, *bench.native_cols(hcols, "price"), n, hiv.data_ptr(), hst.data_ptr(),
+                           None, err) == 0, err.message
+    assert torch.equal(hiv.view(torch.int64), iv.cpu().view(torch.int64))
+    assert torch.equal(hst, st.cpu())
