@@ -149,6 +149,14 @@ FV_API int fv_set_stream(void* stream);
 
 /* Number of CUDA devices visible; library version string. */
 FV_API int fv_device_count(void);
+/* Devices for host-pointer calls: with n >= 2, a host call of
+ * at least n * 2^20 rows is split into n contiguous row shards, one host
+ * thread and one device each (ids may repeat), results written straight into
+ * the caller's buffers; errors and fv_last_outcome are the single-device
+ * ones.  n = 0 restores the default (the calling thread's current device).
+ * Device-pointer calls always run on the current device. */
+FV_API int fv_set_devices(const int* ids, int n);
+FV_API int fv_get_devices(int* ids, int cap);
 FV_API const char* fv_version(void);
 
 /* Host-pointer calls: rows per pipelined chunk (default 1<<22). */

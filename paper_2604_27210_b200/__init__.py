@@ -17,6 +17,7 @@ from .batch import (BatchError, ChainTable, batch_greeks, batch_iv, batch_price,
 from .errors import AboveUpperBoundError, BelowIntrinsicError, DomainError, StepFunctionEdge
 from .models import Model, PricingInputs, parse_flag
 from .solver import SolverResult, SolverStatus
+from ._native import get_devices, set_devices
 
 __version__ = "0.1.0"
 
@@ -25,4 +26,5 @@ __all__ = [
     "format_output", "parse_flags", "validate",
     "AboveUpperBoundError", "BelowIntrinsicError", "DomainError", "StepFunctionEdge",
     "Model", "PricingInputs", "parse_flag", "SolverResult", "SolverStatus", "chain_csv",
+    "set_devices", "get_devices",
 ]

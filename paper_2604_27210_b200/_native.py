@@ -48,6 +48,8 @@ SIGNATURES = {
                         ctypes.c_int),
     "fv_set_stream": ([_P], ctypes.c_int),
     "fv_device_count": ([], ctypes.c_int),
+    "fv_set_devices": ([_P, ctypes.c_int], ctypes.c_int),
+    "fv_get_devices": ([_P, ctypes.c_int], ctypes.c_int),
     "fv_version": ([], ctypes.c_char_p),
     "fv_set_chunk_rows": ([_I64], ctypes.c_int),
     "fv_last_launch_count": ([], _I64),
@@ -80,11 +82,26 @@ def load(path=LIB_PATH):
         return lib
 
 
+ENV_DEVICES = "FASTVOL_DEVICES"     # e.g. "0,1,2,3": host-buffer calls shard over these GPUs
+_env_applied = False
+
+
 def lib_for_compute():
-    """The library, after checking a CUDA device is present (fails loudly)."""
+    """The library, after checking a CUDA device is present (fails loudly).
+    The first call applies FASTVOL_DEVICES (see set_devices), the analogue of
+    the reference's FASTVOL_THREADS worker count (batch.py:166-178)."""
+    global _env_applied
     lib = load()
     if lib.fv_device_count() < 1:
         raise NativeUnavailable("no CUDA device visible: the fastvol B200 path has no CPU fallback")
+    if not _env_applied:
+        _env_applied = True
+        spec = os.environ.get(ENV_DEVICES, "").strip()
+        if spec:
+            ids = [int(x) for x in spec.split(",") if x.strip()]
+            arr = (ctypes.c_int * max(1, len(ids)))(*ids)
+            if lib.fv_set_devices(arr, len(ids)):
+                raise ValueError(f"{ENV_DEVICES}={spec!r}: not a list of visible device ids")
     return lib
 
 
@@ -127,3 +144,21 @@ def kernel_times(lib):
     if lib.fv_kernel_times(ms, ln) != 0:
         raise RuntimeError("fv_kernel_times failed")
     return {lib.fv_kernel_name(k).decode(): (ms[k], ln[k]) for k in range(NKERNEL) if ln[k]}
+
+
+def set_devices(ids=()):
+    """Devices for host-buffer batch calls (fv_set_devices): with two or more,
+    a call of at least len(ids) * 2^20 rows is split into contiguous row
+    shards, one host thread and one GPU each.  ``()`` restores the default."""
+    lib = lib_for_compute()
+    arr = (ctypes.c_int * max(1, len(ids)))(*ids)
+    rc = lib.fv_set_devices(arr, len(ids))
+    if rc:
+        raise ValueError(f"invalid device list {list(ids)!r}")
+
+
+def get_devices():
+    lib = load()
+    arr = (ctypes.c_int * 64)()
+    k = lib.fv_get_devices(arr, 64)
+    return list(arr[:min(k, 64)])

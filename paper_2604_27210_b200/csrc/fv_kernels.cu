@@ -1836,6 +1836,136 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
   return finish(w, c, ax, bcast_bits, s0, e1, e2);
 }
 
+// ---- host calls over several devices -------------------------
+// fv_set_devices(ids, n): host-pointer calls of at least n * kMinShardRows rows
+// are split into n contiguous row shards, one host thread per shard, each
+// driving its device's own chunked H2D -> kernels -> D2H pipeline into the
+// caller's buffers (no exchange on the data path: every output row depends
+// on its input row only).  The shards' outcomes merge to the single-device
+// one: the first failing check in the reference's order at its lowest global
+// row, else the lowest raising row per exception stream.
+std::mutex g_dev_mu;
+std::vector<int> g_devices;
+const int64_t kMinShardRows = 1 << 20;
+
+std::vector<int> devices_for_host_calls() {
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  return g_devices;
+}
+
+int dispatch(Call c, fv_error* e1, fv_error* e2);
+
+struct ShardOut {
+  int rc = FV_OK;
+  fv_error e1, e2;
+  int64_t check_rows[FV_NCHECK];
+  int64_t exc_row[2];
+  int32_t exc_code[2];
+  int64_t launches = 0;
+};
+
+thread_local bool t_in_shard = false;
+
+void shard_call(int dev, Call cs, ShardOut* out) {
+  t_in_shard = true;                           // a shard runs on its device only
+  cudaError_t ce = cudaSetDevice(dev);
+  if (ce != cudaSuccess) { out->rc = set_cuda_err(&out->e1, ce); return; }
+  out->rc = dispatch(cs, &out->e1, &out->e2);
+  for (int k = 0; k < FV_NCHECK; ++k) out->check_rows[k] = t_check_rows[k];
+  for (int k = 0; k < 2; ++k) { out->exc_row[k] = t_exc_row[k]; out->exc_code[k] = t_exc_code[k]; }
+  out->launches = t_launches;
+}
+
+void shift_error(fv_error* e, int64_t off) {
+  if (e->code == FV_ERR_PYEXC) {
+    e->index += off;
+    fill_exc_message(e);
+  } else if (e->code == FV_ERR_BATCH) {
+    const char* colon = strstr(e->message, ": ");
+    char detail[200];
+    snprintf(detail, sizeof(detail), "%s", colon ? colon + 2 : "");
+    const char* kindname = e->kind == FV_CHECK_BAD_FLAG ? "BadFlag"
+                           : (e->kind <= FV_CHECK_NONFINITE_LAST ? "NonFiniteInput" : "DomainError");
+    e->index += off;
+    snprintf(e->message, sizeof(e->message), "%s at row %lld: %s", kindname, (long long)e->index, detail);
+  }
+}
+
+int dispatch_sharded(const Call& c, const std::vector<int>& devs, fv_error* e1, fv_error* e2) {
+  const int64_t G = (int64_t)devs.size();
+  const size_t in_sz[7] = {1, 8, 8, 8, 8, 8, 8};
+  std::vector<ShardOut> outs(G);
+  std::vector<int64_t> off(G);
+  std::vector<std::thread> th;
+  for (int64_t g = 0; g < G; ++g) {
+    const int64_t lo = c.n * g / G, hi = c.n * (g + 1) / G;
+    off[g] = lo;
+    Call cs = c;
+    cs.n = hi - lo;
+    for (int i = 0; i < 7; ++i)
+      if (c.cols[i].stride != 0)
+        cs.cols[i].data = (const char*)c.cols[i].data + lo * c.cols[i].stride * (int64_t)in_sz[i];
+    for (int i = 0; i < 6; ++i) if (c.outs[i]) cs.outs[i] = c.outs[i] + lo;
+    if (c.status) cs.status = c.status + lo;
+    if (c.region) cs.region = c.region + lo;
+    set_ok(&outs[g].e1);
+    set_ok(&outs[g].e2);
+    th.emplace_back(shard_call, devs[g], cs, &outs[g]);
+  }
+  for (auto& t : th) t.join();
+  // merged thread-local outcome (fv_last_outcome) and launch count
+  int64_t launches = 0;
+  for (int k = 0; k < FV_NCHECK; ++k) t_check_rows[k] = -1;
+  for (int k = 0; k < 2; ++k) { t_exc_row[k] = -1; t_exc_code[k] = 0; }
+  for (int64_t g = 0; g < G; ++g) {
+    const ShardOut& o = outs[g];
+    launches += o.launches;
+    for (int k = 0; k < FV_NCHECK; ++k)
+      if (o.check_rows[k] >= 0 && t_check_rows[k] < 0) t_check_rows[k] = o.check_rows[k] + off[g];
+    for (int k = 0; k < 2; ++k)
+      if (o.exc_row[k] >= 0 && t_exc_row[k] < 0) { t_exc_row[k] = o.exc_row[k] + off[g]; t_exc_code[k] = o.exc_code[k]; }
+  }
+  t_launches = launches;
+  // errors: runtime / argument failures first, then the reference's order
+  for (int64_t g = 0; g < G; ++g)
+    if (outs[g].rc == FV_ERR_CUDA || outs[g].rc == FV_ERR_ARG) {
+      if (e1) *e1 = outs[g].e1;
+      if (e2) *e2 = outs[g].e2;
+      return outs[g].rc;
+    }
+  int best = -1;
+  for (int64_t g = 0; g < G; ++g) {
+    if (outs[g].rc != FV_ERR_BATCH) continue;
+    const fv_error& e = outs[g].e1.code == FV_ERR_BATCH ? outs[g].e1 : outs[g].e2;
+    if (best < 0) { best = (int)g; continue; }
+    const fv_error& b = outs[best].e1.code == FV_ERR_BATCH ? outs[best].e1 : outs[best].e2;
+    if (e.kind < b.kind) best = (int)g;          // shards in row order: equal kinds keep the earlier
+  }
+  if (best >= 0) {
+    ShardOut& o = outs[best];
+    shift_error(&o.e1, off[best]);
+    shift_error(&o.e2, off[best]);
+    if (e1) *e1 = o.e1;
+    if (e2) *e2 = o.e2;
+    return FV_ERR_BATCH;
+  }
+  int rc = FV_OK;
+  fv_error* dst[2] = {e1, e2};
+  for (int k = 0; k < 2; ++k) {
+    if (!dst[k]) continue;
+    set_ok(dst[k]);
+    for (int64_t g = 0; g < G; ++g) {
+      fv_error& e = k ? outs[g].e2 : outs[g].e1;
+      if (e.code != FV_ERR_PYEXC) continue;
+      shift_error(&e, off[g]);
+      *dst[k] = e;
+      rc = FV_ERR_PYEXC;
+      break;                                       // the earliest shard holds the lowest row
+    }
+  }
+  return rc;
+}
+
 // For host calls, broadcast columns must be readable on the device.
 int dispatch(Call c, fv_error* e1, fv_error* e2) {
   t_launches = 0;
@@ -1847,10 +1977,6 @@ int dispatch(Call c, fv_error* e1, fv_error* e2) {
     return set_arg_err(e1, "unknown IV method");
   for (int i = 0; i < 7; ++i)
     if (!c.cols[i].data) return set_arg_err(e1, "null input column");
-  DevWork* w = nullptr;
-  cudaError_t ce = get_work(&w);
-  if (ce != cudaSuccess) return set_cuda_err(e1, ce);
-  std::lock_guard<std::mutex> g(w->mu);
   // memory space: all device or all host
   int ndev = 0, nptr = 0;
   for (int i = 0; i < 7; ++i) { ++nptr; ndev += is_device_ptr(c.cols[i].data); }
@@ -1859,6 +1985,14 @@ int dispatch(Call c, fv_error* e1, fv_error* e2) {
   if (c.region) { ++nptr; ndev += is_device_ptr(c.region); }
   bool device = ndev == nptr;
   if (ndev != 0 && !device) return set_arg_err(e1, "all pointers of a call must be device pointers or all host pointers");
+  if (!device && !t_in_shard) {
+    std::vector<int> devs = devices_for_host_calls();
+    if (devs.size() > 1 && c.n >= (int64_t)devs.size() * kMinShardRows) return dispatch_sharded(c, devs, e1, e2);
+  }
+  DevWork* w = nullptr;
+  cudaError_t ce = get_work(&w);
+  if (ce != cudaSuccess) return set_cuda_err(e1, ce);
+  std::lock_guard<std::mutex> g(w->mu);
   // broadcast scalars: checked once on the host; for host calls they are
   // copied into a small device buffer.
   bool bc[7];
@@ -1979,6 +2113,23 @@ FV_API int fv_price_greeks(int model, fv_col flag, fv_col underlying, fv_col str
 FV_API int fv_set_stream(void* stream) {
   t_user_stream = (cudaStream_t)stream;
   return FV_OK;
+}
+
+FV_API int fv_set_devices(const int* ids, int n) {
+  int have = 0;
+  if (cudaGetDeviceCount(&have) != cudaSuccess) { cudaGetLastError(); have = 0; }
+  if (n < 0 || (n > 0 && !ids)) return FV_ERR_ARG;
+  for (int i = 0; i < n; ++i)
+    if (ids[i] < 0 || ids[i] >= have) return FV_ERR_ARG;
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  g_devices.assign(ids, ids + n);
+  return FV_OK;
+}
+
+FV_API int fv_get_devices(int* ids, int cap) {
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  for (int i = 0; i < (int)g_devices.size() && i < cap; ++i) ids[i] = g_devices[i];
+  return (int)g_devices.size();
 }
 
 FV_API int fv_device_count(void) {

@@ -542,3 +542,56 @@ def test_c2_full_10m_halley(fv, oracle_mod):
                            None, err) == 0, err.message
     assert torch.equal(hiv.view(torch.int64), iv.cpu().view(torch.int64))
     assert torch.equal(hst, st.cpu())
+
+
+@pytest.mark.gpu
+def test_host_calls_sharded_over_devices(fv):
+    """fv_set_devices: a host-buffer call split into row shards (here two
+    shards on device 0; on a multi-GPU box one per GPU) is bit-identical to the
+    single-device call for LBR, Halley and fused price + Greeks, and reports
+    the single-device errors (first failing check in the reference's order at
+    its lowest GLOBAL row, also when it lies in a later shard)."""
+    import torch
+    from paper_2604_27210_b200 import _native
+    from paper_2604_27210_b200 import workloads as W
+    lib = _native.lib_for_compute()
+    n = 2_500_000
+    flag, S, K, t, r, q, sig = W.chain_draws(n, seed=77)
+    px = fv.batch_price("bsm", W.flag_chars(flag), S, K, t, r, q=q, sigma=sig)["price"]
+
+    def run(devs, method, price):
+        _native.set_devices(devs)
+        try:
+            return fv.batch_iv("bsm", method, W.flag_chars(flag), S, K, t, r, price=price, q=q)
+        finally:
+            _native.set_devices(())
+
+    for method in ("lbr", "halley"):
+        one = run((), method, px)
+        two = run((0, 0), method, px)
+        assert np.array_equal(one["iv"].view(np.int64), two["iv"].view(np.int64)), method
+        assert list(one["status"][:1000]) == list(two["status"][:1000])
+        assert (np.asarray(one["status"]) == np.asarray(two["status"])).all()
+    _native.set_devices((0, 0))
+    try:
+        g2 = fv.batch_greeks("bsm", W.flag_chars(flag), S, K, t, r, q=q, sigma=sig)
+    finally:
+        _native.set_devices(())
+    g1 = fv.batch_greeks("bsm", W.flag_chars(flag), S, K, t, r, q=q, sigma=sig)
+    for c in ("delta", "gamma", "theta", "rho", "vega"):
+        assert np.array_equal(g1[c].view(np.int64), g2[c].view(np.int64)), c
+    # errors: a non-finite price in the second shard and a negative t (a later
+    # check) in the first: the non-finite row wins, at its global index
+    bad_px = px.copy()
+    bad_px[2_000_000] = np.nan
+    bad_t = t.copy()
+    bad_t[10] = -1.0
+    for devs in ((), (0, 0)):
+        _native.set_devices(devs)
+        try:
+            with pytest.raises(fv.BatchError) as ei:
+                fv.batch_iv("bsm", "lbr", W.flag_chars(flag), S, K, bad_t, r, price=bad_px, q=q)
+        finally:
+            _native.set_devices(())
+        assert ei.value.index == 2_000_000 and ei.value.kind == "NonFiniteInput", (devs, str(ei.value))
+    assert _native.get_devices() == []
