@@ -421,6 +421,19 @@ def run_ours(args):
             dominant = {"kernel": kname, "share_of_call": kernels[kname]["share"], "units": n_far_low,
                         "W_per_unit": w_solve, "ms_per_launch": t_k * 1e3,
                         "achieved": w_solve * n_far_low / t_k / 1e12}
+        kname = "k_halley_iter"
+        if args.workload == "c2" and kernels and kname in kernels:
+            # the Halley-step phase (solver.py:115-144) of the reference, per quote
+            # that reaches it (tools/w_count_halley.py on the C2 generator);
+            # units = rows x the sample's share of such quotes
+            ph = wp["phases"]["halley"]
+            units = int(round(n * ph["share_reaching"]))
+            t_k = kernels[kname]["ms_per_step"] * 1e-3
+            dominant = {"kernel": kname, "share_of_call": kernels[kname]["share"], "units": units,
+                        "W_per_unit": ph["W_per_reaching_quote"], "ms_per_launch": t_k * 1e3,
+                        "achieved": ph["W_per_reaching_quote"] * units / t_k / 1e12,
+                        "units_source": "rows x share of quotes reaching the Halley loop in a %d-row "
+                                        "reference sample (profiles/w_phases_c2.json)" % wp["rows"]}
     except (OSError, ValueError, KeyError):
         pass
 
