@@ -35,7 +35,9 @@ sys.path.insert(0, REPO)
 
 # Weighted distinct FP64 ops per quote the reference executes (SURVEY.md 8(d),
 # Appendix B.3): the algorithmic work per unit for the roofline.
-W_OPS = {"c4": 1443.0, "c1": 1405.0, "c2": 1476.0, "c3": 298.0, "c5": 347.0}
+# rt (the reference's bench harness: synthetic_chain's BSM pricing + run_bench's
+# Halley inversion, one fused fv_price_iv call): price 200 + C2 Halley 1476.
+W_OPS = {"c4": 1443.0, "c1": 1405.0, "c2": 1476.0, "c3": 298.0, "c5": 347.0, "rt": 1676.0}
 METRIC = "fp64 IV solves/sec (LBR, 100M quotes) at 1/2/4/8 B200 vs host-CPU ref"
 
 
@@ -45,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c4", choices=["c4", "c1", "c2", "c3", "c5"])
+    ap.add_argument("--workload", default="c4", choices=["c4", "c1", "c2", "c3", "c5", "rt"])
     ap.add_argument("--rows", type=int, default=0, help="rows per rank (default: workload size)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -57,7 +59,7 @@ def parse():
 
 def default_rows(workload):
     return {"c4": 100_000_000, "c1": 1_000_000, "c2": 10_000_000, "c3": 10_000_000,
-            "c5": 10_000_000}[workload]
+            "c5": 10_000_000, "rt": 10_000_000}[workload]
 
 
 # ---------------------------------------------------------------------------
@@ -296,6 +298,7 @@ def run_ours(args):
     lib.fv_set_stream(ctypes_ptr(stream.cuda_stream))
 
     # ---- inputs resident in HBM ------------------------------------------
+    roundtrip = False
     if args.workload == "c4":
         cols = c4_device(rows, rank, dev)
         model, method, last = 0, 1, "price"
@@ -304,12 +307,13 @@ def run_ours(args):
         cols = draws_device(args.workload, rows, rank, dev)
         if args.workload in ("c1", "c5"):
             model, method = 0, 1
-        elif args.workload == "c2":
+        elif args.workload in ("c2", "rt"):
             model, method = 2, 0
         else:
             model, method = 2, -1
-        last = "sigma" if method == -1 else "price"
-        if method != -1:
+        roundtrip = args.workload == "rt"
+        last = "sigma" if (method == -1 or roundtrip) else "price"
+        if method != -1 and not roundtrip:
             cols["price"] = price_on_device(lib, model, cols, rows)
             if args.workload == "c5":
                 from paper_2604_27210_b200 import workloads as W
@@ -322,6 +326,7 @@ def run_ours(args):
     n = rows
     out_iv = torch.empty(n, dtype=torch.float64, device=dev)
     out_st = torch.empty(n, dtype=torch.int8, device=dev)
+    out_px = torch.empty(n, dtype=torch.float64, device=dev) if roundtrip else None
     greeks = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(6)]
 
     ncols = native_cols(cols, last)
@@ -329,7 +334,13 @@ def run_ours(args):
 
     def step():
         err = _native.fv_error()
-        if method >= 0:
+        if roundtrip:
+            err2 = _native.fv_error()
+            rc = lib.fv_price_iv(model, method, *ncols, n, out_px.data_ptr(), out_iv.data_ptr(),
+                                 out_st.data_ptr(), None, err, err2)
+            if rc and not err.code:
+                err = err2
+        elif method >= 0:
             rc = lib.fv_batch_iv(model, method, *ncols, n, out_iv.data_ptr(), out_st.data_ptr(),
                                  None, err)
         else:
@@ -385,7 +396,7 @@ def run_ours(args):
         lib.fv_set_kernel_timing(1)
         _native.kernel_times(lib)
         nk = max(1, min(args.steps, 3))
-        region = torch.empty(n, dtype=torch.int8, device=dev) if method == 1 else None
+        region = torch.empty(n, dtype=torch.int8, device=dev) if (method == 1 and not roundtrip) else None
         for _ in range(nk):
             if region is not None:     # LBR: also record each quote's region (far-low count)
                 err = _native.fv_error()
@@ -450,16 +461,21 @@ def run_ours(args):
             hcols[k] = v.cpu().pin_memory() if v.numel() > 1 else v.cpu()
         h_iv = torch.empty(n, dtype=torch.float64).pin_memory()
         h_st = torch.empty(n, dtype=torch.int8).pin_memory()
+        h_px = torch.empty(n, dtype=torch.float64).pin_memory() if roundtrip else None
         h_g = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(6)] if method < 0 else []
         hn = native_cols(hcols, last)
         h2d = sum(hcols[k].numel() * hcols[k].element_size()
                   for k in ("flag", "underlying", "strike", "t", "r", "q", last)
                   if hcols[k].numel() > 1)
-        d2h = n * 9 if method >= 0 else n * 49        # iv + status | price + 5 Greeks + status
+        d2h = n * (17 if roundtrip else (9 if method >= 0 else 49))   # (price +) iv + status | price + 5 Greeks + status
 
         def estep():
             err = _native.fv_error()
-            if method >= 0:
+            if roundtrip:
+                err2 = _native.fv_error()
+                rc = lib.fv_price_iv(model, method, *hn, n, h_px.data_ptr(), h_iv.data_ptr(),
+                                     h_st.data_ptr(), None, err, err2)
+            elif method >= 0:
                 rc = lib.fv_batch_iv(model, method, *hn, n, h_iv.data_ptr(), h_st.data_ptr(), None, err)
             else:
                 err2 = _native.fv_error()
@@ -484,6 +500,8 @@ def run_ours(args):
         # bit-identical to the device-resident result
         if method >= 0:
             same = bool(torch.equal(h_iv.to(dev).view(torch.int64), out_iv.view(torch.int64)))
+            if roundtrip:
+                same = same and bool(torch.equal(h_px.to(dev).view(torch.int64), out_px.view(torch.int64)))
         else:
             same = all(bool(torch.equal(h.to(dev).view(torch.int64), g.view(torch.int64)))
                        for h, g in zip(h_g, greeks))
@@ -519,7 +537,7 @@ def run_ours(args):
     in_bytes = sum(cols[k].numel() * cols[k].element_size()
                    for k in ("flag", "underlying", "strike", "t", "r", "q", last)
                    if torch.is_tensor(cols[k]) and cols[k].numel() > 1)
-    out_bytes = n * (9 if method >= 0 else 49)
+    out_bytes = n * (17 if roundtrip else (9 if method >= 0 else 49))
     hbm_gbs = (in_bytes + out_bytes) / (float(np.mean(per_call_ms)) * 1e-3) / 1e9
     peaks = {}
     try:
@@ -550,7 +568,9 @@ def run_ours(args):
                    "c1": "C1: LBR Black-76 1M synthetic quotes",
                    "c2": "C2: Halley BSM with dividend yield, 10M quotes",
                    "c3": "C3: fused BSM price + all Greeks, 10M quotes",
-                   "c5": "C5: wing-stress set, LBR Black-76"}[args.workload]
+                   "c5": "C5: wing-stress set, LBR Black-76",
+                   "rt": "RT: the reference bench harness's round trip (bench.py:19-40) on 10M C2 draws: "
+                         "BSM price -> Halley IV in one fused fv_price_iv call"}[args.workload]
         line = {
             "metric": METRIC if args.workload == "c4" else f"fp64 quotes/sec ({args.workload})",
             "value": value, "unit": "quotes/s", "n_gpus": world, "steps": args.steps,

@@ -13,6 +13,10 @@
  *   fv_batch_greeks  <- batch.py:250-280  batch_greeks  (fill :263-274)
  *   fv_price_greeks  <- batch_price + batch_greeks on the same columns, one
  *                       fused pass (shared d1/d2/Phi/phi), two error records
+ *   fv_price_iv      <- batch_price then batch_iv on the price column it
+ *                       produced (bench.py:19-40 synthetic_chain + run_bench,
+ *                       SURVEY 8(f) rank 3): one call, the price column stays
+ *                       on the device between the stages, two error records
  *
  * Columns are structure-of-arrays: a column is a pointer
  * plus an element stride; stride 0 broadcasts element 0 (the reference's
@@ -142,6 +146,20 @@ FV_API int fv_price_greeks(int model, fv_col flag, fv_col underlying, fv_col str
                            double* delta, double* gamma, double* theta, double* rho,
                            double* vega, int8_t* status, fv_error* err_price,
                            fv_error* err_greeks);
+
+/* Price -> IV round trip (the reference's bench harness,
+ * bench.py:19-40): price[i] = batch_price(model, ..., sigma)[i], then
+ * iv[i] / status[i] / region[i] = batch_iv(model, method, ..., price=price)
+ * on that column.  One call: the inputs are read (host calls: copied) once,
+ * the price column goes from the pricing kernel to the IV passes in device
+ * memory, and price + iv + status come back together.  err_price is
+ * batch_price's outcome; err_iv is batch_iv's on the produced prices, which
+ * the reference only reaches when batch_price succeeded -- the return code is
+ * err_price's when it failed, else err_iv's.  region may be NULL. */
+FV_API int fv_price_iv(int model, int method, fv_col flag, fv_col underlying, fv_col strike,
+                       fv_col t, fv_col r, fv_col q, fv_col sigma, int64_t n, double* price,
+                       double* iv, int8_t* status, int8_t* region, fv_error* err_price,
+                       fv_error* err_iv);
 
 /* Stream used by device-pointer calls made from the calling thread
  * (cudaStream_t; NULL = the library's own non-blocking stream). */

@@ -11,9 +11,9 @@ with return_as containers) live in ``paper_2604_27210_b200.fast_vollib``; the
 chain CSV reader of the reference's CLI (cli.py:140-173) in ``chain_csv``.
 """
 
-from . import chain_csv
+from . import bench, chain_csv
 from .batch import (BatchError, ChainTable, batch_greeks, batch_iv, batch_price, broadcast,
-                    format_output, parse_flags, validate)
+                    format_output, parse_flags, price_iv, validate)
 from .errors import AboveUpperBoundError, BelowIntrinsicError, DomainError, StepFunctionEdge
 from .models import Model, PricingInputs, parse_flag
 from .solver import SolverResult, SolverStatus
@@ -23,8 +23,8 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BatchError", "ChainTable", "batch_greeks", "batch_iv", "batch_price", "broadcast",
-    "format_output", "parse_flags", "validate",
+    "format_output", "parse_flags", "price_iv", "validate",
     "AboveUpperBoundError", "BelowIntrinsicError", "DomainError", "StepFunctionEdge",
-    "Model", "PricingInputs", "parse_flag", "SolverResult", "SolverStatus", "chain_csv",
+    "Model", "PricingInputs", "parse_flag", "SolverResult", "SolverStatus", "chain_csv", "bench",
     "set_devices", "get_devices",
 ]

@@ -46,6 +46,8 @@ SIGNATURES = {
     "fv_batch_greeks": ([ctypes.c_int] + [_COL] * 7 + [_I64] + [_P] * 6 + [_ERR], ctypes.c_int),
     "fv_price_greeks": ([ctypes.c_int] + [_COL] * 7 + [_I64] + [_P] * 7 + [_ERR, _ERR],
                         ctypes.c_int),
+    "fv_price_iv": ([ctypes.c_int, ctypes.c_int] + [_COL] * 7 + [_I64, _P, _P, _P, _P, _ERR, _ERR],
+                    ctypes.c_int),
     "fv_set_stream": ([_P], ctypes.c_int),
     "fv_device_count": ([], ctypes.c_int),
     "fv_set_devices": ([_P, ctypes.c_int], ctypes.c_int),

@@ -346,6 +346,44 @@ def batch_iv(model, method: str, flag, underlying, strike, t, r, price=None, q=0
     return ChainTable(cols_out)
 
 
+def price_iv(model, method: str, flag, underlying, strike, t, r, q=0.0, sigma=None) -> ChainTable:
+    """Price -> IV round trip in one C-ABI call (``fv_price_iv``; SURVEY 8(f)
+    rank 3): the reference's ``batch_price(model, ..., sigma=sigma)`` followed
+    by ``batch_iv(model, method, ..., price=<that price column>, q=q)``, as its
+    bench harness runs them (bench.py:19-40).  Returns the input columns
+    (sigma included), then ``price``, ``iv`` and ``status``; values, statuses
+    and the exception raised are those of the two reference calls in sequence
+    (batch_price's errors first, then the method check, then batch_iv's)."""
+    model = as_model(model)
+    if method not in ("halley", "lbr"):
+        batch_price(model, flag, underlying, strike, t, r, q, sigma=sigma)
+        raise BatchError("DomainError", 0, f"unknown IV method {method!r}")
+    n, table = _assemble(model, flag, underlying, strike, t, r, q, sigma=sigma)
+    if "sigma" not in table:
+        validate_order_then(table, model, need="sigma")
+        raise BatchError("DomainError", 0, "batch_price requires sigma")
+    price = np.empty(n, dtype=np.float64)
+    iv = np.empty(n, dtype=np.float64)
+    codes = np.empty(n, dtype=np.int8)
+    if n:
+        lib = _native.lib_for_compute()
+        keep, cols = _columns(table, "sigma")
+        ep, ei = _native.fv_error(), _native.fv_error()
+        rc = lib.fv_price_iv(model.code, 1 if method == "lbr" else 0, *cols, n, price.ctypes.data,
+                             iv.ctypes.data, codes.ctypes.data, None, ep, ei)
+        if rc in (_native.FV_ERR_CUDA, _native.FV_ERR_ARG):
+            _raise_for(ep, table, "sigma")
+        _ok_or_raise(ep.code, ep, table, model, "sigma")          # batch_price
+        iv_table = dict(table)
+        iv_table["price"] = price
+        _ok_or_raise(ei.code, ei, iv_table, model, "price")       # batch_iv
+    cols_out = dict(table)
+    cols_out["price"] = price
+    cols_out["iv"] = iv
+    cols_out["status"] = _status_column(_IV_STATUS, codes)
+    return ChainTable(cols_out)
+
+
 def batch_greeks(model, flag, underlying, strike, t, r, q=0.0, sigma=None) -> ChainTable:
     """All five Greeks per row; zero-vol / zero-time rows carry NaNs plus a
     ``step_function_edge`` status."""

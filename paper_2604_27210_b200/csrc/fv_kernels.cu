@@ -1192,8 +1192,8 @@ struct DevWork {
   int dev = -1;
   int sm_count = 0;
   cudaStream_t streams[FV_NSLOT] = {};
-  FvDevStatus* st = nullptr;            // device
-  FvDevStatus* st_host = nullptr;       // pinned mirror
+  FvDevStatus* st = nullptr;            // device, [2]: call (or price stage), IV stage of fv_price_iv
+  FvDevStatus* st_host = nullptr;       // pinned mirror [2]
   // chunk buffers for host-pointer calls
   char* chunk[FV_NSLOT] = {};
   int64_t chunk_cap_rows[FV_NSLOT] = {};
@@ -1240,8 +1240,8 @@ cudaError_t get_work(DevWork** out) {
     w->dev = dev;
     CK(cudaDeviceGetAttribute(&w->sm_count, cudaDevAttrMultiProcessorCount, dev));
     for (int s = 0; s < FV_NSLOT; ++s) CK(cudaStreamCreateWithFlags(&w->streams[s], cudaStreamNonBlocking));
-    CK(cudaMalloc(&w->st, sizeof(FvDevStatus)));
-    CK(cudaMallocHost(&w->st_host, sizeof(FvDevStatus)));
+    CK(cudaMalloc(&w->st, 2 * sizeof(FvDevStatus)));
+    CK(cudaMallocHost(&w->st_host, 2 * sizeof(FvDevStatus)));
     CK(cudaMalloc(&w->explain, sizeof(ExplainOut)));
     w->blocks_price = occupancy_blocks((const void*)k_price, w->sm_count);
     w->blocks_greeks = occupancy_blocks((const void*)k_price_greeks<true, true>, w->sm_count);
@@ -1325,7 +1325,7 @@ cudaError_t ensure_hsm(DevWork* w, int slot, int64_t rows) {
   return cudaSuccess;
 }
 
-enum Kind { KIND_PRICE, KIND_IV, KIND_GREEKS, KIND_PRICE_GREEKS };
+enum Kind { KIND_PRICE, KIND_IV, KIND_GREEKS, KIND_PRICE_GREEKS, KIND_PRICE_IV };
 
 struct Call {
   Kind kind;
@@ -1336,12 +1336,95 @@ struct Call {
   int8_t* status;
   int8_t* region;
   bool want_price, want_greeks;
+  uint32_t bbits_iv;   // KIND_PRICE_IV: host-checked broadcast-column bits of the IV stage
 };
+
+// fv_price_iv's IV stage: batch_iv over the price column the price stage
+// wrote (outs[0]), reading the same input columns; its own check mask (the
+// IV checks: no sigma check, price never broadcast) and status block.
+KArgs iv_stage_args(const KArgs& a, DevWork* w) {
+  KArgs b = a;
+  b.has_sigma = 0;
+  b.check_mask = a.check_mask & ~((1u << FV_CHECK_NONNEG_SIGMA) | (1u << FV_CHECK_NONFINITE_LAST));
+  b.check_mask |= 1u << FV_CHECK_NONFINITE_LAST;
+  b.last.p = a.o0;
+  b.last.stride = 1;
+  b.last.mode = (((uintptr_t)a.o0) & 15) == 0 ? 1 : 2;
+  b.o0 = a.o1;
+  b.o1 = nullptr;
+  b.st = w->st + 1;
+  return b;
+}
 
 int64_t blocks_for(int64_t max_blocks, int64_t n) {
   int64_t need = ((n + 1) / 2 + 255) / 256;
   if (need < 1) need = 1;
   return need < max_blocks ? need : max_blocks;
+}
+
+// The IV passes of one launch (LBR or Halley) over rows [0, a.n).
+cudaError_t launch_iv(DevWork* w, int method, const KArgs& a, int slot, cudaStream_t s) {
+  if (a.n <= 0) return cudaSuccess;
+  if (method == FV_METHOD_LBR) {
+    const int64_t chunk = a.n < kLbrChunk ? a.n : kLbrChunk;
+    CK(ensure_lbr(w, slot, chunk));
+    for (int64_t off = 0; off < a.n; off += chunk) {
+      KArgs b = sub_args(a, off, (a.n - off) < chunk ? (a.n - off) : chunk);
+      LbrQueues lq;
+      double* sb = w->lbr_state[slot];
+      const int64_t cp = w->lbr_cap[slot];
+      lq.sx = sb; lq.sbeta = sb + cp;
+      lq.sb0 = sb + 2 * cp; lq.sb1 = sb + 3 * cp; lq.sE0 = sb + 4 * cp; lq.sE1 = sb + 5 * cp;
+      for (int c3 = 0; c3 < 7; ++c3) lq.q[c3] = w->lbr_q[slot] + c3 * w->lbr_cap[slot];
+      lq.count = w->lbr_count + 16 * slot;
+      // claims as large as FV_NORM_CLAIM pairs while every warp still gets
+      // >= 4 of them: a small batch (C1: 1M rows = 141 pairs per warp) with
+      // 128-pair claims leaves a tenth of the warps a second claim to run
+      // alone after the rest are done
+      {
+        const int64_t npair = (b.n + 1) / 2, warps = (int64_t)w->blocks_lbr_norm * 8;
+        unsigned cl = FV_NORM_CLAIM;
+        while (cl > 32 && npair < warps * (int64_t)cl * 4) cl /= 2;
+        lq.norm_claim = cl;
+      }
+      CK(cudaMemsetAsync(lq.count, 0, 16 * sizeof(unsigned int), s));
+      const int64_t cap1 = (b.n + 255) / 256;
+      auto g = [cap1](int blocks) { return (int)(cap1 < blocks ? cap1 : blocks); };
+      FV_LAUNCH(FV_KID_LBR_NORM, s, k_lbr_normalize<<<blocks_for(w->blocks_lbr_norm, b.n), 256, 0, s>>>(b, lq));
+      // the three replay passes usually find an empty queue: one CTA per SM
+      // keeps their launch + drain short (a full occupancy grid costs ~7 us)
+      FV_LAUNCH(FV_KID_LBR_NREP, s, k_lbr_normalize_replay<<<g(w->sm_count), 256, 0, s>>>(b, lq));
+      FV_LAUNCH(FV_KID_LBR_ANCH, s, k_lbr_anchors<<<g(w->blocks_lbr_anch), 256, 0, s>>>(b, lq));
+      FV_LAUNCH(FV_KID_LBR_FAST, s, k_lbr_far_low_fast<<<g(w->blocks_lbr_fast), 256, 0, s>>>(b, lq));
+      FV_LAUNCH(FV_KID_LBR_FL, s, k_lbr_solve<FV_FAR_LOW><<<g(w->sm_count), 256, 0, s>>>(b, lq));
+      FV_LAUNCH(FV_KID_LBR_NEAR_FAST, s, k_lbr_near_fast<<<g(w->blocks_lbr_nfast), 256, 0, s>>>(b, lq));
+      FV_LAUNCH(FV_KID_LBR_NEAR, s, k_lbr_solve<FV_NEAR_LOW><<<g(w->sm_count), 256, 0, s>>>(b, lq));
+      FV_LAUNCH(FV_KID_LBR_FH, s, k_lbr_solve<FV_FAR_HIGH><<<g(w->blocks_lbr_fh), 256, 0, s>>>(b, lq));
+    }
+  } else {
+    // chunks of <= 2^26 rows: int32 row indices in the queues, bounded buffers
+    const int64_t chunk = a.n < kHalleyChunk ? a.n : kHalleyChunk;
+    CK(ensure_hsm(w, slot, chunk));
+    for (int64_t off = 0; off < a.n; off += chunk) {
+      KArgs b = sub_args(a, off, (a.n - off) < chunk ? (a.n - off) : chunk);
+      unsigned long long* ctr = w->work_ctr + 2 * slot;   // [0] Halley, [1] bisection claims
+      unsigned int* cnt = w->hsm_count + 4 * slot;         // [0] records, [1] handed back, [2] bisection
+      int32_t* hrow = w->hsm_ridx[slot];
+      int32_t* bis = w->hsm_ridx[slot] + w->hsm_cap[slot];
+      CK(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s));
+      CK(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned int), s));
+      const int64_t need = (b.n + 255) / 256;
+      auto g = [need](int blocks) { return (int)(need < blocks ? need : blocks); };
+      FV_LAUNCH(FV_KID_HALLEY_SETUP, s, k_halley_bracket<<<blocks_for(w->blocks_hset, b.n), 256, 0, s>>>(
+          b, w->hsm_recs[slot], w->hsm_rrow[slot], cnt, hrow));
+      FV_LAUNCH(FV_KID_HALLEY_SM, s, k_halley_iter<<<g(w->blocks_hiter), 256, 0, s>>>(
+          b, w->hsm_recs[slot], w->hsm_rrow[slot], cnt, ctr, bis, cnt + 2, hrow, cnt + 1));
+      FV_LAUNCH(FV_KID_HALLEY_BISECT, s, k_halley_bisect<<<g(w->blocks_hbis), 256, 0, s>>>(
+          b, w->hsm_recs[slot], w->hsm_rrow[slot], bis, cnt + 2, ctr + 1, hrow, cnt + 1));
+      FV_LAUNCH(FV_KID_HALLEY_SM2, s, k_halley_careful<<<g(w->sm_count), 256, 0, s>>>(b, hrow, cnt + 1));
+    }
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStream_t s) {
@@ -1362,65 +1445,11 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
         FV_LAUNCH(FV_KID_PRICE_GREEKS, s, k_price_greeks<true, false><<<blocks_for(w->blocks_greeks, a.n), 256, 0, s>>>(a));
       break;
     case KIND_IV:
-      if (c.method == FV_METHOD_LBR) {
-        const int64_t chunk = a.n < kLbrChunk ? a.n : kLbrChunk;
-        CK(ensure_lbr(w, slot, chunk));
-        for (int64_t off = 0; off < a.n; off += chunk) {
-          KArgs b = sub_args(a, off, (a.n - off) < chunk ? (a.n - off) : chunk);
-          LbrQueues lq;
-          double* sb = w->lbr_state[slot];
-          const int64_t cp = w->lbr_cap[slot];
-          lq.sx = sb; lq.sbeta = sb + cp;
-          lq.sb0 = sb + 2 * cp; lq.sb1 = sb + 3 * cp; lq.sE0 = sb + 4 * cp; lq.sE1 = sb + 5 * cp;
-          for (int c3 = 0; c3 < 7; ++c3) lq.q[c3] = w->lbr_q[slot] + c3 * w->lbr_cap[slot];
-          lq.count = w->lbr_count + 16 * slot;
-          // claims as large as FV_NORM_CLAIM pairs while every warp still gets
-          // >= 4 of them: a small batch (C1: 1M rows = 141 pairs per warp) with
-          // 128-pair claims leaves a tenth of the warps a second claim to run
-          // alone after the rest are done
-          {
-            const int64_t npair = (b.n + 1) / 2, warps = (int64_t)w->blocks_lbr_norm * 8;
-            unsigned cl = FV_NORM_CLAIM;
-            while (cl > 32 && npair < warps * (int64_t)cl * 4) cl /= 2;
-            lq.norm_claim = cl;
-          }
-          CK(cudaMemsetAsync(lq.count, 0, 16 * sizeof(unsigned int), s));
-          const int64_t cap1 = (b.n + 255) / 256;
-          auto g = [cap1](int blocks) { return (int)(cap1 < blocks ? cap1 : blocks); };
-          FV_LAUNCH(FV_KID_LBR_NORM, s, k_lbr_normalize<<<blocks_for(w->blocks_lbr_norm, b.n), 256, 0, s>>>(b, lq));
-          // the three replay passes usually find an empty queue: one CTA per SM
-          // keeps their launch + drain short (a full occupancy grid costs ~7 us)
-          FV_LAUNCH(FV_KID_LBR_NREP, s, k_lbr_normalize_replay<<<g(w->sm_count), 256, 0, s>>>(b, lq));
-          FV_LAUNCH(FV_KID_LBR_ANCH, s, k_lbr_anchors<<<g(w->blocks_lbr_anch), 256, 0, s>>>(b, lq));
-          FV_LAUNCH(FV_KID_LBR_FAST, s, k_lbr_far_low_fast<<<g(w->blocks_lbr_fast), 256, 0, s>>>(b, lq));
-          FV_LAUNCH(FV_KID_LBR_FL, s, k_lbr_solve<FV_FAR_LOW><<<g(w->sm_count), 256, 0, s>>>(b, lq));
-          FV_LAUNCH(FV_KID_LBR_NEAR_FAST, s, k_lbr_near_fast<<<g(w->blocks_lbr_nfast), 256, 0, s>>>(b, lq));
-          FV_LAUNCH(FV_KID_LBR_NEAR, s, k_lbr_solve<FV_NEAR_LOW><<<g(w->sm_count), 256, 0, s>>>(b, lq));
-          FV_LAUNCH(FV_KID_LBR_FH, s, k_lbr_solve<FV_FAR_HIGH><<<g(w->blocks_lbr_fh), 256, 0, s>>>(b, lq));
-        }
-      } else {
-        // chunks of <= 2^26 rows: int32 row indices in the queues, bounded buffers
-        const int64_t chunk = a.n < kHalleyChunk ? a.n : kHalleyChunk;
-        CK(ensure_hsm(w, slot, chunk));
-        for (int64_t off = 0; off < a.n; off += chunk) {
-          KArgs b = sub_args(a, off, (a.n - off) < chunk ? (a.n - off) : chunk);
-          unsigned long long* ctr = w->work_ctr + 2 * slot;   // [0] Halley, [1] bisection claims
-          unsigned int* cnt = w->hsm_count + 4 * slot;         // [0] records, [1] handed back, [2] bisection
-          int32_t* hrow = w->hsm_ridx[slot];
-          int32_t* bis = w->hsm_ridx[slot] + w->hsm_cap[slot];
-          CK(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s));
-          CK(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned int), s));
-          const int64_t need = (b.n + 255) / 256;
-          auto g = [need](int blocks) { return (int)(need < blocks ? need : blocks); };
-          FV_LAUNCH(FV_KID_HALLEY_SETUP, s, k_halley_bracket<<<blocks_for(w->blocks_hset, b.n), 256, 0, s>>>(
-              b, w->hsm_recs[slot], w->hsm_rrow[slot], cnt, hrow));
-          FV_LAUNCH(FV_KID_HALLEY_SM, s, k_halley_iter<<<g(w->blocks_hiter), 256, 0, s>>>(
-              b, w->hsm_recs[slot], w->hsm_rrow[slot], cnt, ctr, bis, cnt + 2, hrow, cnt + 1));
-          FV_LAUNCH(FV_KID_HALLEY_BISECT, s, k_halley_bisect<<<g(w->blocks_hbis), 256, 0, s>>>(
-              b, w->hsm_recs[slot], w->hsm_rrow[slot], bis, cnt + 2, ctr + 1, hrow, cnt + 1));
-          FV_LAUNCH(FV_KID_HALLEY_SM2, s, k_halley_careful<<<g(w->sm_count), 256, 0, s>>>(b, hrow, cnt + 1));
-        }
-      }
+      CK(launch_iv(w, c.method, a, slot, s));
+      break;
+    case KIND_PRICE_IV:
+      FV_LAUNCH(FV_KID_PRICE, s, k_price<<<blocks_for(w->blocks_price, a.n), 256, 0, s>>>(a));
+      CK(launch_iv(w, c.method, iv_stage_args(a, w), slot, s));
       break;
   }
   return cudaGetLastError();
@@ -1512,8 +1541,7 @@ uint32_t bcast_checks(const Call& c, const double vals[7], int flag_val, const b
 
 // Resolve the device status into the two fv_error records.
 int finish(DevWork* w, const Call& c, const KArgs& a0, uint32_t bcast_bits, cudaStream_t s,
-           fv_error* e1, fv_error* e2) {
-  FvDevStatus& st = *w->st_host;
+           fv_error* e1, fv_error* e2, const FvDevStatus& st) {
   bool has_sigma = c.kind != KIND_IV;
   for (int ck = 0; ck < FV_NCHECK; ++ck) {
     unsigned long long row = st.check_first[ck];
@@ -1572,6 +1600,28 @@ int finish(DevWork* w, const Call& c, const KArgs& a0, uint32_t bcast_bits, cuda
     fill_exc_message(e);
   }
   return rc;
+}
+
+// fv_price_iv: the price stage's outcome (st_host[0]) is the call's when it
+// failed -- the reference's batch_price raises before batch_iv runs; else the
+// IV stage's (st_host[1]).  fv_last_outcome: check rows of the stage that
+// decides, exception stream [0] price, [1] IV.
+int finish_price_iv(DevWork* w, const Call& c, const KArgs& ap, const KArgs& ai, uint32_t bbits,
+                    cudaStream_t s, fv_error* ep, fv_error* ei) {
+  Call cp = c, ci = c;
+  cp.kind = KIND_PRICE;
+  ci.kind = KIND_IV;
+  const int rci = finish(w, ci, ai, c.bbits_iv, s, ei, nullptr, w->st_host[1]);
+  int64_t rows_i[FV_NCHECK];
+  for (int k = 0; k < FV_NCHECK; ++k) rows_i[k] = t_check_rows[k];
+  const int64_t xr = t_exc_row[0];
+  const int32_t xc = t_exc_code[0];
+  const int rcp = finish(w, cp, ap, bbits, s, ep, nullptr, w->st_host[0]);
+  if (rcp == FV_OK)
+    for (int k = 0; k < FV_NCHECK; ++k) t_check_rows[k] = rows_i[k];
+  t_exc_row[1] = xr;
+  t_exc_code[1] = xc;
+  return rcp != FV_OK ? rcp : rci;
 }
 
 DCol make_dcol(const fv_col& c, const void* base_override) {
@@ -1635,12 +1685,13 @@ int run_device(DevWork* w, const Call& c, cudaStream_t s, uint32_t bcast_bits, f
   a.row0 = 0;
   a.o0 = c.outs[0]; a.o1 = c.outs[1]; a.o2 = c.outs[2];
   a.o3 = c.outs[3]; a.o4 = c.outs[4]; a.o5 = c.outs[5];
-  if ((ce = cudaMemsetAsync(w->st, 0xff, sizeof(FvDevStatus), s)) != cudaSuccess) return set_cuda_err(e1, ce);
+  if ((ce = cudaMemsetAsync(w->st, 0xff, 2 * sizeof(FvDevStatus), s)) != cudaSuccess) return set_cuda_err(e1, ce);
   if ((ce = launch(w, c, a, 0, s)) != cudaSuccess) return set_cuda_err(e1, ce);
-  if ((ce = cudaMemcpyAsync(w->st_host, w->st, sizeof(FvDevStatus), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+  if ((ce = cudaMemcpyAsync(w->st_host, w->st, 2 * sizeof(FvDevStatus), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return set_cuda_err(e1, ce);
   if ((ce = cudaStreamSynchronize(s)) != cudaSuccess) return set_cuda_err(e1, ce);
-  return finish(w, c, a, bcast_bits, s, e1, e2);
+  if (c.kind == KIND_PRICE_IV) return finish_price_iv(w, c, a, iv_stage_args(a, w), bcast_bits, s, e1, e2);
+  return finish(w, c, a, bcast_bits, s, e1, e2, w->st_host[0]);
 }
 
 // Host-pointer path: chunked H2D -> kernel -> D2H, FV_NSLOT streams.
@@ -1737,7 +1788,7 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
     if (stage_region) par_memcpy((char*)(c.region + r0), st + off_region, rn);
     slot_chunk[s] = -1;
   };
-  if ((ce = cudaMemsetAsync(w->st, 0xff, sizeof(FvDevStatus), w->streams[0])) != cudaSuccess)
+  if ((ce = cudaMemsetAsync(w->st, 0xff, 2 * sizeof(FvDevStatus), w->streams[0])) != cudaSuccess)
     return set_cuda_err(e1, ce);
   cudaEvent_t ready;
   cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
@@ -1803,25 +1854,29 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
   }
   cudaEventDestroy(ready);
   cudaStream_t s0 = w->streams[0];
-  if ((ce = cudaMemcpyAsync(w->st_host, w->st, sizeof(FvDevStatus), cudaMemcpyDeviceToHost, s0)) != cudaSuccess)
+  if ((ce = cudaMemcpyAsync(w->st_host, w->st, 2 * sizeof(FvDevStatus), cudaMemcpyDeviceToHost, s0)) != cudaSuccess)
     return set_cuda_err(e1, ce);
   if ((ce = cudaStreamSynchronize(s0)) != cudaSuccess) return set_cuda_err(e1, ce);
   for (int s = 1; s < FV_NSLOT; ++s)
     if ((ce = cudaStreamSynchronize(w->streams[s])) != cudaSuccess) return set_cuda_err(e1, ce);
   if ((ce = cudaGetLastError()) != cudaSuccess) return set_cuda_err(e1, ce);
   // exceptions in later chunks: the explain kernel needs that chunk's inputs;
-  // re-stage the offending row alone.
-  FvDevStatus& st = *w->st_host;
+  // re-stage the offending row alone (fv_price_iv: the IV stage's row, its
+  // price from the caller's price column).
+  const bool piv = c.kind == KIND_PRICE_IV;
+  const FvDevStatus& st = w->st_host[piv ? 1 : 0];
   unsigned long long ex = st.exc_first;
   KArgs ax = a_first;
-  if (ex != ~0ull && c.kind == KIND_IV && (int)(ex & 0xff) >= FV_EXC_DOM_ATM_BETA) {
+  if (ex != ~0ull && (c.kind == KIND_IV || piv) && (int)(ex & 0xff) >= FV_EXC_DOM_ATM_BETA) {
     int64_t row = (int64_t)(ex >> 8);
     char* base = w->chunk[0];
     void* dev_in[7];
     for (int col = 0; col < 7; ++col) {
-      if (c.cols[col].stride == 0) { dev_in[col] = nullptr; continue; }
+      if (c.cols[col].stride == 0 && !(piv && col == 6)) { dev_in[col] = nullptr; continue; }
       dev_in[col] = base + off_in[col];
-      cudaMemcpy(dev_in[col], (const char*)c.cols[col].data + row * in_sz[col], in_sz[col], cudaMemcpyHostToDevice);
+      const void* src = (piv && col == 6) ? (const void*)(c.outs[0] + row)
+                                          : (const void*)((const char*)c.cols[col].data + row * in_sz[col]);
+      cudaMemcpy(dev_in[col], src, in_sz[col], cudaMemcpyHostToDevice);
     }
     ax.flag = make_dflag(c.cols[0], dev_in[0]);
     ax.un = make_dcol(c.cols[1], dev_in[1]);
@@ -1829,11 +1884,20 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
     ax.t = make_dcol(c.cols[3], dev_in[3]);
     ax.r = make_dcol(c.cols[4], dev_in[4]);
     ax.q = make_dcol(c.cols[5], dev_in[5]);
-    ax.last = make_dcol(c.cols[6], dev_in[6]);
+    if (piv) {
+      ax = iv_stage_args(ax, w);
+      ax.last.p = (const double*)dev_in[6];
+      ax.last.mode = 2;
+    } else {
+      ax.last = make_dcol(c.cols[6], dev_in[6]);
+    }
     ax.n = 1;
     ax.row0 = row;
+  } else if (piv) {
+    ax = iv_stage_args(a_first, w);
   }
-  return finish(w, c, ax, bcast_bits, s0, e1, e2);
+  if (piv) return finish_price_iv(w, c, a_first, ax, bcast_bits, s0, e1, e2);
+  return finish(w, c, ax, bcast_bits, s0, e1, e2, w->st_host[0]);
 }
 
 // ---- host calls over several devices -------------------------
@@ -1933,37 +1997,39 @@ int dispatch_sharded(const Call& c, const std::vector<int>& devs, fv_error* e1, 
       if (e2) *e2 = outs[g].e2;
       return outs[g].rc;
     }
-  int best = -1;
-  for (int64_t g = 0; g < G; ++g) {
-    if (outs[g].rc != FV_ERR_BATCH) continue;
-    const fv_error& e = outs[g].e1.code == FV_ERR_BATCH ? outs[g].e1 : outs[g].e2;
-    if (best < 0) { best = (int)g; continue; }
-    const fv_error& b = outs[best].e1.code == FV_ERR_BATCH ? outs[best].e1 : outs[best].e2;
-    if (e.kind < b.kind) best = (int)g;          // shards in row order: equal kinds keep the earlier
-  }
-  if (best >= 0) {
-    ShardOut& o = outs[best];
-    shift_error(&o.e1, off[best]);
-    shift_error(&o.e2, off[best]);
-    if (e1) *e1 = o.e1;
-    if (e2) *e2 = o.e2;
-    return FV_ERR_BATCH;
-  }
-  int rc = FV_OK;
+  // each error record merges on its own: the first failing check in the
+  // reference's order at its lowest global row, else the lowest raising row
+  // (shards are in row order, so the earliest shard holding one wins)
+  bool any_batch[2] = {false, false}, any_exc[2] = {false, false};
   fv_error* dst[2] = {e1, e2};
   for (int k = 0; k < 2; ++k) {
-    if (!dst[k]) continue;
-    set_ok(dst[k]);
+    int best = -1;
     for (int64_t g = 0; g < G; ++g) {
-      fv_error& e = k ? outs[g].e2 : outs[g].e1;
-      if (e.code != FV_ERR_PYEXC) continue;
-      shift_error(&e, off[g]);
-      *dst[k] = e;
-      rc = FV_ERR_PYEXC;
-      break;                                       // the earliest shard holds the lowest row
+      const fv_error& e = k ? outs[g].e2 : outs[g].e1;
+      if (e.code != FV_ERR_BATCH) continue;
+      const fv_error& b = k ? outs[best < 0 ? 0 : best].e2 : outs[best < 0 ? 0 : best].e1;
+      if (best < 0 || e.kind < b.kind) best = (int)g;
     }
+    if (best < 0)
+      for (int64_t g = 0; g < G && best < 0; ++g)
+        if ((k ? outs[g].e2 : outs[g].e1).code == FV_ERR_PYEXC) best = (int)g;
+    fv_error merged;
+    set_ok(&merged);
+    if (best >= 0) {
+      merged = k ? outs[best].e2 : outs[best].e1;
+      shift_error(&merged, off[best]);
+      any_batch[k] = merged.code == FV_ERR_BATCH;
+      any_exc[k] = merged.code == FV_ERR_PYEXC;
+    }
+    if (dst[k]) *dst[k] = merged;
   }
-  return rc;
+  if (c.kind == KIND_PRICE_IV) {          // the price stage's failure is the call's
+    if (any_batch[0]) return FV_ERR_BATCH;
+    if (any_exc[0]) return FV_ERR_PYEXC;
+    return any_batch[1] ? FV_ERR_BATCH : (any_exc[1] ? FV_ERR_PYEXC : FV_OK);
+  }
+  if (any_batch[0] || any_batch[1]) return FV_ERR_BATCH;
+  return (any_exc[0] || any_exc[1]) ? FV_ERR_PYEXC : FV_OK;
 }
 
 // For host calls, broadcast columns must be readable on the device.
@@ -1973,7 +2039,7 @@ int dispatch(Call c, fv_error* e1, fv_error* e2) {
   set_ok(e2);
   if (c.n < 0) return set_arg_err(e1, "n must be >= 0");
   if (c.model < 0 || c.model > 2) return set_arg_err(e1, "unknown model");
-  if (c.kind == KIND_IV && c.method != FV_METHOD_HALLEY && c.method != FV_METHOD_LBR)
+  if ((c.kind == KIND_IV || c.kind == KIND_PRICE_IV) && c.method != FV_METHOD_HALLEY && c.method != FV_METHOD_LBR)
     return set_arg_err(e1, "unknown IV method");
   for (int i = 0; i < 7; ++i)
     if (!c.cols[i].data) return set_arg_err(e1, "null input column");
@@ -2011,6 +2077,16 @@ int dispatch(Call c, fv_error* e1, fv_error* e2) {
       else vals[i] = *(const double*)c.cols[i].data;
     }
   uint32_t bbits = c.n > 0 ? bcast_checks(c, vals, flag_val, bc) : 0;
+  if (c.kind == KIND_PRICE_IV && c.n > 0) {
+    // the IV stage reads the same broadcast columns; its price column is the
+    // price stage's n-row output (never broadcast)
+    Call ci = c;
+    ci.kind = KIND_IV;
+    bool bci[7];
+    for (int i = 0; i < 7; ++i) bci[i] = bc[i];
+    bci[6] = false;
+    c.bbits_iv = bcast_checks(ci, vals, flag_val, bci);
+  }
   if (!device) {
     // device copies of the broadcast scalars (8 doubles, one allocation per call)
     if ((ce = cudaMalloc(&dscal, 8 * 8)) != cudaSuccess) return set_cuda_err(e1, ce);
@@ -2107,6 +2183,24 @@ FV_API int fv_price_greeks(int model, fv_col flag, fv_col underlying, fv_col str
     if (!c.want_price && err_price) set_ok(err_price);
     if (!c.want_greeks && err_greeks) set_ok(err_greeks);
   }
+  return rc;
+}
+
+FV_API int fv_price_iv(int model, int method, fv_col flag, fv_col underlying, fv_col strike,
+                       fv_col t, fv_col r, fv_col q, fv_col sigma, int64_t n, double* price,
+                       double* iv, int8_t* status, int8_t* region, fv_error* err_price,
+                       fv_error* err_iv) {
+  Call c = make_call(KIND_PRICE_IV, model, method, flag, underlying, strike, t, r, q, sigma, n);
+  c.outs[0] = price;
+  c.outs[1] = iv;
+  c.status = status;
+  c.region = region;
+  if ((!price || !iv || !status) && n > 0) return set_arg_err(err_price, "null output");
+  fv_error ep, ei;
+  const int rc = dispatch(c, &ep, &ei);
+  if (rc == FV_ERR_CUDA || rc == FV_ERR_ARG) ei = ep;
+  if (err_price) *err_price = ep;
+  if (err_iv) *err_iv = ei;
   return rc;
 }
 

@@ -27,7 +27,7 @@ def lib():
 
 def test_header_declares_the_batch_entry_points():
     names = declared()
-    for n in ("fv_batch_price", "fv_batch_iv", "fv_batch_greeks", "fv_price_greeks"):
+    for n in ("fv_batch_price", "fv_batch_iv", "fv_batch_greeks", "fv_price_greeks", "fv_price_iv"):
         assert n in names
 
 
