@@ -1192,6 +1192,10 @@ struct DevWork {
   int dev = -1;
   int sm_count = 0;
   cudaStream_t streams[FV_NSLOT] = {};
+  // per slot: a second stream and fork / join events -- the LBR far-low
+  // branch runs beside the anchors -> near -> far-high branch
+  cudaStream_t aux[FV_NSLOT] = {};
+  cudaEvent_t fork_ev[FV_NSLOT] = {}, join_ev[FV_NSLOT] = {};
   FvDevStatus* st = nullptr;            // device, [2]: call (or price stage), IV stage of fv_price_iv
   FvDevStatus* st_host = nullptr;       // pinned mirror [2]
   // chunk buffers for host-pointer calls
@@ -1239,7 +1243,12 @@ cudaError_t get_work(DevWork** out) {
     DevWork* w = new DevWork();
     w->dev = dev;
     CK(cudaDeviceGetAttribute(&w->sm_count, cudaDevAttrMultiProcessorCount, dev));
-    for (int s = 0; s < FV_NSLOT; ++s) CK(cudaStreamCreateWithFlags(&w->streams[s], cudaStreamNonBlocking));
+    for (int s = 0; s < FV_NSLOT; ++s) {
+      CK(cudaStreamCreateWithFlags(&w->streams[s], cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&w->aux[s], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&w->fork_ev[s], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&w->join_ev[s], cudaEventDisableTiming));
+    }
     CK(cudaMalloc(&w->st, 2 * sizeof(FvDevStatus)));
     CK(cudaMallocHost(&w->st_host, 2 * sizeof(FvDevStatus)));
     CK(cudaMalloc(&w->explain, sizeof(ExplainOut)));
@@ -1394,12 +1403,26 @@ cudaError_t launch_iv(DevWork* w, int method, const KArgs& a, int slot, cudaStre
       // the three replay passes usually find an empty queue: one CTA per SM
       // keeps their launch + drain short (a full occupancy grid costs ~7 us)
       FV_LAUNCH(FV_KID_LBR_NREP, s, k_lbr_normalize_replay<<<g(w->sm_count), 256, 0, s>>>(b, lq));
+      // Two independent branches after the normalize passes: the far-low
+      // solve (queue 0 -> queue 4) and anchors -> near / far-high solves
+      // (queue 3 -> queues 1, 2 -> 6); disjoint queues, counters, state rows
+      // and output rows.  Run concurrently, each fills the other's tail (a
+      // 1M-row batch is a few quotes per lane per pass).
+#ifdef FV_LBR_SERIAL
+      cudaStream_t s2 = s;                       // A/B: the branches in sequence
+#else
+      cudaStream_t s2 = w->aux[slot];
+#endif
+      CK(cudaEventRecord(w->fork_ev[slot], s));
+      CK(cudaStreamWaitEvent(s2, w->fork_ev[slot], 0));
+      FV_LAUNCH(FV_KID_LBR_FAST, s2, k_lbr_far_low_fast<<<g(w->blocks_lbr_fast), 256, 0, s2>>>(b, lq));
+      FV_LAUNCH(FV_KID_LBR_FL, s2, k_lbr_solve<FV_FAR_LOW><<<g(w->sm_count), 256, 0, s2>>>(b, lq));
       FV_LAUNCH(FV_KID_LBR_ANCH, s, k_lbr_anchors<<<g(w->blocks_lbr_anch), 256, 0, s>>>(b, lq));
-      FV_LAUNCH(FV_KID_LBR_FAST, s, k_lbr_far_low_fast<<<g(w->blocks_lbr_fast), 256, 0, s>>>(b, lq));
-      FV_LAUNCH(FV_KID_LBR_FL, s, k_lbr_solve<FV_FAR_LOW><<<g(w->sm_count), 256, 0, s>>>(b, lq));
       FV_LAUNCH(FV_KID_LBR_NEAR_FAST, s, k_lbr_near_fast<<<g(w->blocks_lbr_nfast), 256, 0, s>>>(b, lq));
       FV_LAUNCH(FV_KID_LBR_NEAR, s, k_lbr_solve<FV_NEAR_LOW><<<g(w->sm_count), 256, 0, s>>>(b, lq));
       FV_LAUNCH(FV_KID_LBR_FH, s, k_lbr_solve<FV_FAR_HIGH><<<g(w->blocks_lbr_fh), 256, 0, s>>>(b, lq));
+      CK(cudaEventRecord(w->join_ev[slot], s2));
+      CK(cudaStreamWaitEvent(s, w->join_ev[slot], 0));
     }
   } else {
     // chunks of <= 2^26 rows: int32 row indices in the queues, bounded buffers
