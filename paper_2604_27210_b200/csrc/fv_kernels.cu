@@ -1214,7 +1214,8 @@ struct DevWork {
   unsigned int* hsm_count = nullptr;        // [FV_NSLOT][4]: records, handed back, bisection queue
   HalRec* hsm_recs[FV_NSLOT] = {};
   int64_t* hsm_rrow[FV_NSLOT] = {};         // row | call bit per record
-  int32_t* hsm_ridx[FV_NSLOT] = {};         // [cap] handed-back rows, [cap] bisection queue
+  int32_t* hsm_ridx[FV_NSLOT] = {};         // [cap] rows handed back by the bracket pass, [cap]
+                                            // bisection queue, [cap] handed back later
   int64_t hsm_cap[FV_NSLOT] = {};
   int blocks_hset = 0;
   int blocks_lbr_nfast = 0;
@@ -1329,7 +1330,7 @@ cudaError_t ensure_hsm(DevWork* w, int slot, int64_t rows) {
   int64_t cap = rows < 4096 ? 4096 : rows;
   CK(cudaMalloc(&w->hsm_recs[slot], sizeof(HalRec) * cap));
   CK(cudaMalloc(&w->hsm_rrow[slot], sizeof(int64_t) * cap));
-  CK(cudaMalloc(&w->hsm_ridx[slot], sizeof(int32_t) * 2 * cap));
+  CK(cudaMalloc(&w->hsm_ridx[slot], sizeof(int32_t) * 3 * cap));
   w->hsm_cap[slot] = cap;
   return cudaSuccess;
 }
@@ -1431,20 +1432,37 @@ cudaError_t launch_iv(DevWork* w, int method, const KArgs& a, int slot, cudaStre
     for (int64_t off = 0; off < a.n; off += chunk) {
       KArgs b = sub_args(a, off, (a.n - off) < chunk ? (a.n - off) : chunk);
       unsigned long long* ctr = w->work_ctr + 2 * slot;   // [0] Halley, [1] bisection claims
-      unsigned int* cnt = w->hsm_count + 4 * slot;         // [0] records, [1] handed back, [2] bisection
+      unsigned int* cnt = w->hsm_count + 4 * slot;         // [0] records, [1] handed back by the
+                                                           // bracket pass, [2] bisection, [3] handed back later
       int32_t* hrow = w->hsm_ridx[slot];
       int32_t* bis = w->hsm_ridx[slot] + w->hsm_cap[slot];
+      int32_t* hrow2 = w->hsm_ridx[slot] + 2 * w->hsm_cap[slot];
       CK(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s));
       CK(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned int), s));
       const int64_t need = (b.n + 255) / 256;
       auto g = [need](int blocks) { return (int)(need < blocks ? need : blocks); };
       FV_LAUNCH(FV_KID_HALLEY_SETUP, s, k_halley_bracket<<<blocks_for(w->blocks_hset, b.n), 256, 0, s>>>(
           b, w->hsm_recs[slot], w->hsm_rrow[slot], cnt, hrow));
+      // The bracket pass's hand-backs (f(10) sign undecided or doubling, log(F/K)
+      // raising, range flags) are final once it ends: their careful pass runs
+      // on the second stream beside the Halley / bisection passes, which hand
+      // back into a queue of their own, drained after them.  (A careful row is
+      // long -- the whole solver on the careful routines -- and ~1 per lane.)
+#ifdef FV_HAL_SERIAL
+      cudaStream_t s2 = s;
+#else
+      cudaStream_t s2 = w->aux[slot];
+#endif
+      CK(cudaEventRecord(w->fork_ev[slot], s));
+      CK(cudaStreamWaitEvent(s2, w->fork_ev[slot], 0));
+      FV_LAUNCH(FV_KID_HALLEY_SM2, s2, k_halley_careful<<<g(w->sm_count), 256, 0, s2>>>(b, hrow, cnt + 1));
       FV_LAUNCH(FV_KID_HALLEY_SM, s, k_halley_iter<<<g(w->blocks_hiter), 256, 0, s>>>(
-          b, w->hsm_recs[slot], w->hsm_rrow[slot], cnt, ctr, bis, cnt + 2, hrow, cnt + 1));
+          b, w->hsm_recs[slot], w->hsm_rrow[slot], cnt, ctr, bis, cnt + 2, hrow2, cnt + 3));
       FV_LAUNCH(FV_KID_HALLEY_BISECT, s, k_halley_bisect<<<g(w->blocks_hbis), 256, 0, s>>>(
-          b, w->hsm_recs[slot], w->hsm_rrow[slot], bis, cnt + 2, ctr + 1, hrow, cnt + 1));
-      FV_LAUNCH(FV_KID_HALLEY_SM2, s, k_halley_careful<<<g(w->sm_count), 256, 0, s>>>(b, hrow, cnt + 1));
+          b, w->hsm_recs[slot], w->hsm_rrow[slot], bis, cnt + 2, ctr + 1, hrow2, cnt + 3));
+      FV_LAUNCH(FV_KID_HALLEY_SM2, s, k_halley_careful<<<g(w->sm_count), 256, 0, s>>>(b, hrow2, cnt + 3));
+      CK(cudaEventRecord(w->join_ev[slot], s2));
+      CK(cudaStreamWaitEvent(s, w->join_ev[slot], 0));
     }
   }
   return cudaGetLastError();
