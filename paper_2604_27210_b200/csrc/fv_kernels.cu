@@ -682,8 +682,15 @@ __device__ __forceinline__ void hal_load(const HalRec* r, int64_t rowbits, FvHal
 #ifndef FV_HSET_MINB
 #define FV_HSET_MINB 3
 #endif
-__global__ void __launch_bounds__(256, FV_HSET_MINB) k_halley_bracket(KArgs a, HalRec* recs, int64_t* rrow,
-                                                                  unsigned int* count, int32_t* hrow) {
+// kPrice (fv_price_iv): the row's price is computed here from the sigma
+// column of the price stage's arguments `pa` (its checks, status block and
+// price output) -- batch_price's row, straight-line with the careful row where
+// it flags -- written out and inverted in the same thread, instead of a
+// pricing kernel writing the column and this pass reading it back.
+template <bool kPrice>
+__global__ void __launch_bounds__(256, FV_HSET_MINB) k_halley_bracket(KArgs a, KArgs pa, HalRec* recs,
+                                                                  int64_t* rrow, unsigned int* count,
+                                                                  int32_t* hrow) {
   __shared__ double sm_x[8][64], sm_r[8][64];
   __shared__ unsigned char sm_f[8][64];
   const int wib = threadIdx.x >> 5;
@@ -692,6 +699,28 @@ __global__ void __launch_bounds__(256, FV_HSET_MINB) k_halley_bracket(KArgs a, H
   for (int64_t it = 0; it < nloop; ++it) {
     const int64_t row = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool active = row < a.n;
+    double px_fused = 0.0;
+    if (kPrice) {                                  // batch_price's row (warp-collective erfc)
+      const int64_t prow = active ? row : 0;
+      const int fl = ldf1(pa.flag, prow);
+      const double un = ld1(pa.un, prow), k = ld1(pa.k, prow), t = ld1(pa.t, prow), r = ld1(pa.r, prow);
+      const double q = ld1(pa.q, prow), sg = ld1(pa.last, prow);
+      const uint32_t pbad = active ? row_checks(pa, fl, un, k, t, r, q, sg) : 0u;
+      FxBad pflag;
+      double v = fx_price_row(pa.model, (double)fl, un, k, t, r, q, sg, pflag, active && !pbad,
+                              sm_x[wib], sm_r[wib], sm_f[wib]);
+      __syncwarp();
+      if (active) {
+        if (pbad) {
+          publish_checks(pa.st, pbad, pa.row0 + row);
+          v = __builtin_nan("");
+        } else if (pflag) {
+          v = price_row_careful(pa, row, fl, un, k, t, r, q, sg);
+        }
+        pa.o0[row] = v;
+      }
+      px_fused = v;
+    }
     bool open = false, hb = false;
     FvHalleySM m;
     m.c.th = 1.0; m.c.Fw = m.c.K = m.c.disc = m.c.sqrt_t = m.c.lnFK = m.c.target = m.c.tol_price = 0.0;
@@ -699,7 +728,7 @@ __global__ void __launch_bounds__(256, FV_HSET_MINB) k_halley_bracket(KArgs a, H
     if (active) {
       const int fl = ldf1(a.flag, row);
       const double un = ld1(a.un, row), k = ld1(a.k, row), t = ld1(a.t, row), r = ld1(a.r, row);
-      const double q = ld1(a.q, row), px = ld1(a.last, row);
+      const double q = ld1(a.q, row), px = kPrice ? px_fused : ld1(a.last, row);
       const uint32_t bad = row_checks(a, fl, un, k, t, r, q, px);
       if (bad) {
         publish_checks(a.st, bad, a.row0 + row);
@@ -1217,7 +1246,7 @@ struct DevWork {
   int32_t* hsm_ridx[FV_NSLOT] = {};         // [cap] rows handed back by the bracket pass, [cap]
                                             // bisection queue, [cap] handed back later
   int64_t hsm_cap[FV_NSLOT] = {};
-  int blocks_hset = 0;
+  int blocks_hset = 0, blocks_hset_p = 0;
   int blocks_lbr_nfast = 0;
   int blocks_lbr_norm = 0, blocks_lbr_nrep = 0, blocks_lbr_anch = 0, blocks_lbr_fast = 0, blocks_lbr_fl = 0, blocks_lbr_near = 0, blocks_lbr_fh = 0;
   std::mutex mu;
@@ -1269,7 +1298,8 @@ cudaError_t get_work(DevWork** out) {
     w->blocks_hcare = occupancy_blocks((const void*)k_halley_careful, w->sm_count);
     CK(cudaMalloc(&w->work_ctr, sizeof(unsigned long long) * 2 * FV_NSLOT));
     CK(cudaMalloc(&w->hsm_count, sizeof(unsigned int) * 4 * FV_NSLOT));
-    w->blocks_hset = occupancy_blocks((const void*)k_halley_bracket, w->sm_count);
+    w->blocks_hset = occupancy_blocks((const void*)k_halley_bracket<false>, w->sm_count);
+    w->blocks_hset_p = occupancy_blocks((const void*)k_halley_bracket<true>, w->sm_count);
     g_work[dev] = w;
   }
   *out = g_work[dev];
@@ -1373,7 +1403,8 @@ int64_t blocks_for(int64_t max_blocks, int64_t n) {
 }
 
 // The IV passes of one launch (LBR or Halley) over rows [0, a.n).
-cudaError_t launch_iv(DevWork* w, int method, const KArgs& a, int slot, cudaStream_t s) {
+cudaError_t launch_iv(DevWork* w, int method, const KArgs& a, int slot, cudaStream_t s,
+                      const KArgs* price = nullptr) {
   if (a.n <= 0) return cudaSuccess;
   if (method == FV_METHOD_LBR) {
     const int64_t chunk = a.n < kLbrChunk ? a.n : kLbrChunk;
@@ -1441,8 +1472,14 @@ cudaError_t launch_iv(DevWork* w, int method, const KArgs& a, int slot, cudaStre
       CK(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned int), s));
       const int64_t need = (b.n + 255) / 256;
       auto g = [need](int blocks) { return (int)(need < blocks ? need : blocks); };
-      FV_LAUNCH(FV_KID_HALLEY_SETUP, s, k_halley_bracket<<<blocks_for(w->blocks_hset, b.n), 256, 0, s>>>(
-          b, w->hsm_recs[slot], w->hsm_rrow[slot], cnt, hrow));
+      if (price) {                    // fv_price_iv: prices computed in the bracket pass
+        const KArgs pb = sub_args(*price, off, b.n);
+        FV_LAUNCH(FV_KID_HALLEY_SETUP, s, k_halley_bracket<true><<<blocks_for(w->blocks_hset_p, b.n), 256, 0, s>>>(
+            b, pb, w->hsm_recs[slot], w->hsm_rrow[slot], cnt, hrow));
+      } else {
+        FV_LAUNCH(FV_KID_HALLEY_SETUP, s, k_halley_bracket<false><<<blocks_for(w->blocks_hset, b.n), 256, 0, s>>>(
+            b, b, w->hsm_recs[slot], w->hsm_rrow[slot], cnt, hrow));
+      }
       // The bracket pass's hand-backs (f(10) sign undecided or doubling, log(F/K)
       // raising, range flags) are final once it ends: their careful pass runs
       // on the second stream beside the Halley / bisection passes, which hand
@@ -1489,6 +1526,16 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
       CK(launch_iv(w, c.method, a, slot, s));
       break;
     case KIND_PRICE_IV:
+#ifdef FV_RT_FUSED
+      // price computed inside the bracket pass: measured SLOWER on the rt
+      // workload (3.59 vs 3.48 ms per 10M rows, profiles/README.md) -- the
+      // pass is FP64-latency-bound either way and the pricing row's extra
+      // live state costs more than the 57 B/row of HBM traffic it saves
+      if (c.method == FV_METHOD_HALLEY) {
+        CK(launch_iv(w, c.method, iv_stage_args(a, w), slot, s, &a));
+        break;
+      }
+#endif
       FV_LAUNCH(FV_KID_PRICE, s, k_price<<<blocks_for(w->blocks_price, a.n), 256, 0, s>>>(a));
       CK(launch_iv(w, c.method, iv_stage_args(a, w), slot, s));
       break;
