@@ -187,7 +187,9 @@ FV_API int64_t fv_last_launch_count(void);
 /* Raw outcome of the calling thread's last batch call: per validation check
  * (FV_CHECK_* order) the first failing row or -1; the first raising row and
  * its FV_EXC_* code for the price/iv stream [0] and the Greeks stream [1]
- * (-1 / 0 when none).  Lets a caller that shards one logical batch over
+ * (-1 / 0 when none).  After fv_price_iv: stream [0] is the price stage,
+ * [1] the IV stage, and the check rows are the price stage's when one of its
+ * checks failed, else the IV stage's.  Lets a caller that shards one logical batch over
  * several calls/devices reproduce the reference's single first error. */
 FV_API int fv_last_outcome(int64_t* check_rows /*[FV_NCHECK]*/, int64_t* exc_rows /*[2]*/,
                            int32_t* exc_codes /*[2]*/);
