@@ -590,6 +590,9 @@ def run_ours(args):
                                  + ("; C2: the bracket pass decides f(10)'s sign in fp32 instead of evaluating "
                                     "it (~8 % of W counted but not executed)" if args.workload == "c2" else "")},
             "kernels": kernels,
+            "kernels_note": "CUDA events around each launch on its own stream; the LBR far-low branch and the "
+                            "Halley careful pass over the bracket's hand-backs run on a second stream beside the "
+                            "other passes, so those kernels' times overlap and shares are of the summed time",
             "dominant_kernel": (dict(dominant, peak=peak_tops, unit="T weighted-fp64-ops/s",
                                      frac=dominant["achieved"] / peak_tops if peak_tops else None)
                                 if dominant else None),
