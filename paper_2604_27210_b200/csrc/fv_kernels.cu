@@ -1831,11 +1831,17 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
   for (int i = 0; i < 6; ++i) { off_out[i] = slot_bytes; if (c.outs[i]) slot_bytes += align(8 * chunk); }
   off_status = slot_bytes; if (has_status) slot_bytes += align(chunk);
   off_region = slot_bytes; if (has_region) slot_bytes += align(chunk);
+  // buffers grow to the largest layout of this chunk size at once (every
+  // column streamed, six outputs, status, region): a call with more streamed
+  // columns than the last one must not pay another pinned allocation (~0.4 s
+  // for the three staging slots of 2^22 rows)
+  const size_t max_slot = align(chunk) + 6 * align(8 * chunk) + 6 * align(8 * chunk) + 2 * align(chunk);
   for (int s = 0; s < FV_NSLOT; ++s) {
     if (w->chunk_cap_rows[s] < (int64_t)slot_bytes) {
       if (w->chunk[s]) cudaFree(w->chunk[s]);
-      if ((ce = cudaMalloc(&w->chunk[s], slot_bytes)) != cudaSuccess) return set_cuda_err(e1, ce);
-      w->chunk_cap_rows[s] = (int64_t)slot_bytes;
+      w->chunk[s] = nullptr;
+      if ((ce = cudaMalloc(&w->chunk[s], max_slot)) != cudaSuccess) return set_cuda_err(e1, ce);
+      w->chunk_cap_rows[s] = (int64_t)max_slot;
     }
   }
   // pageable caller buffers go through pinned staging (parallel host copies)
@@ -1850,8 +1856,8 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
       if (w->stage_cap[s] < (int64_t)slot_bytes) {
         if (w->stage[s]) cudaFreeHost(w->stage[s]);
         w->stage[s] = nullptr;
-        if ((ce = cudaMallocHost(&w->stage[s], slot_bytes)) != cudaSuccess) return set_cuda_err(e1, ce);
-        w->stage_cap[s] = (int64_t)slot_bytes;
+        if ((ce = cudaMallocHost(&w->stage[s], max_slot)) != cudaSuccess) return set_cuda_err(e1, ce);
+        w->stage_cap[s] = (int64_t)max_slot;
       }
     }
   }

@@ -56,6 +56,29 @@ def main():
     out["quotes_per_s_python_api"] = n / out["batch_iv_total_s"]
     out["quotes_per_s_c_abi_pageable"] = n / out["c_abi_pageable_s"]
     assert np.array_equal(iv.view(np.int64), res["iv"].view(np.int64))
+    # price -> IV round trip: one price_iv call vs batch_price then batch_iv
+    fv.price_iv("black", "lbr", chars[:1000], F[:1], K[:1000], t[:1000], r[:1], sigma=sig[:1000])
+    t0 = time.perf_counter()
+    rt = fv.price_iv("black", "lbr", chars, F[:1], K, t, r[:1], sigma=sig)
+    out["price_iv_total_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    p2 = fv.batch_price("black", chars, F[:1], K, t, r[:1], sigma=sig)["price"]
+    two = fv.batch_iv("black", "lbr", chars, F[:1], K, t, r[:1], price=p2)
+    out["batch_price_then_batch_iv_s"] = time.perf_counter() - t0
+    assert np.array_equal(rt["iv"].view(np.int64), two["iv"].view(np.int64))
+    out["quotes_per_s_price_iv"] = n / out["price_iv_total_s"]
+    out["quotes_per_s_two_calls"] = n / out["batch_price_then_batch_iv_s"]
+    # the reference bench harness mirror (fastvol.bench.run_bench: batch_iv timed)
+    import contextlib
+    import io
+    from paper_2604_27210_b200 import bench as FB
+    fv.price_iv("bsm", "halley", chars[:1000], F[:1000], K[:1000], t[:1000], r[:1000], r[:1000],
+                sigma=sig[:1000])                               # warm-up (Halley workspace)
+    for runner in ("run_bench", "run_roundtrip"):
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            getattr(FB, runner)(1_000_000, "halley")
+        out[runner + "_1m_halley"] = buf.getvalue().strip().splitlines()[1]
     print(json.dumps(out))
 
 
