@@ -1223,8 +1223,9 @@ struct DevWork {
   cudaStream_t streams[FV_NSLOT] = {};
   // per slot: a second stream and fork / join events -- the LBR far-low
   // branch runs beside the anchors -> near -> far-high branch
-  cudaStream_t aux[FV_NSLOT] = {};
+  cudaStream_t aux[FV_NSLOT] = {}, aux2[FV_NSLOT] = {};
   cudaEvent_t fork_ev[FV_NSLOT] = {}, join_ev[FV_NSLOT] = {};
+  cudaEvent_t fork2_ev[FV_NSLOT] = {}, join2_ev[FV_NSLOT] = {};   // LBR far-high solve
   FvDevStatus* st = nullptr;            // device, [2]: call (or price stage), IV stage of fv_price_iv
   FvDevStatus* st_host = nullptr;       // pinned mirror [2]
   // chunk buffers for host-pointer calls
@@ -1276,6 +1277,9 @@ cudaError_t get_work(DevWork** out) {
     for (int s = 0; s < FV_NSLOT; ++s) {
       CK(cudaStreamCreateWithFlags(&w->streams[s], cudaStreamNonBlocking));
       CK(cudaStreamCreateWithFlags(&w->aux[s], cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&w->aux2[s], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&w->fork2_ev[s], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&w->join2_ev[s], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&w->fork_ev[s], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&w->join_ev[s], cudaEventDisableTiming));
     }
@@ -1450,11 +1454,22 @@ cudaError_t launch_iv(DevWork* w, int method, const KArgs& a, int slot, cudaStre
       FV_LAUNCH(FV_KID_LBR_FAST, s2, k_lbr_far_low_fast<<<g(w->blocks_lbr_fast), 256, 0, s2>>>(b, lq));
       FV_LAUNCH(FV_KID_LBR_FL, s2, k_lbr_solve<FV_FAR_LOW><<<g(w->sm_count), 256, 0, s2>>>(b, lq));
       FV_LAUNCH(FV_KID_LBR_ANCH, s, k_lbr_anchors<<<g(w->blocks_lbr_anch), 256, 0, s>>>(b, lq));
+      // the far-high solve (queue 2) depends on the anchors pass only: a third
+      // stream, beside the near solve (queues 1 -> 6)
+#if defined(FV_LBR_SERIAL) || defined(FV_LBR_FH_SERIAL)
+      cudaStream_t s3 = s;
+#else
+      cudaStream_t s3 = w->aux2[slot];
+#endif
+      CK(cudaEventRecord(w->fork2_ev[slot], s));
+      CK(cudaStreamWaitEvent(s3, w->fork2_ev[slot], 0));
+      FV_LAUNCH(FV_KID_LBR_FH, s3, k_lbr_solve<FV_FAR_HIGH><<<g(w->blocks_lbr_fh), 256, 0, s3>>>(b, lq));
       FV_LAUNCH(FV_KID_LBR_NEAR_FAST, s, k_lbr_near_fast<<<g(w->blocks_lbr_nfast), 256, 0, s>>>(b, lq));
       FV_LAUNCH(FV_KID_LBR_NEAR, s, k_lbr_solve<FV_NEAR_LOW><<<g(w->sm_count), 256, 0, s>>>(b, lq));
-      FV_LAUNCH(FV_KID_LBR_FH, s, k_lbr_solve<FV_FAR_HIGH><<<g(w->blocks_lbr_fh), 256, 0, s>>>(b, lq));
       CK(cudaEventRecord(w->join_ev[slot], s2));
       CK(cudaStreamWaitEvent(s, w->join_ev[slot], 0));
+      CK(cudaEventRecord(w->join2_ev[slot], s3));
+      CK(cudaStreamWaitEvent(s, w->join2_ev[slot], 0));
     }
   } else {
     // chunks of <= 2^26 rows: int32 row indices in the queues, bounded buffers
