@@ -55,6 +55,12 @@
 #ifndef FV_NORM_MINB
 #define FV_NORM_MINB 3
 #endif
+#ifndef FV_NORM_MINB_BIG
+#define FV_NORM_MINB_BIG 4
+#endif
+#ifndef FV_NORM_BIG_ROWS
+#define FV_NORM_BIG_ROWS (1 << 24)
+#endif
 #ifndef FV_PG_MINB
 #define FV_PG_MINB 3
 #endif
@@ -384,7 +390,12 @@ __device__ __forceinline__ void lbr_norm_row_careful(const KArgs& a, const LbrQu
 // anchor is needed, see fv_lbr_anchor_lo) or in the pending queue with (b_lo,
 // E_lo) for pass 2.  Rows the straight-line routines flag (ATM shortcut,
 // exceptions, range edges) go to queue 5 for k_lbr_normalize_replay.
-__global__ void __launch_bounds__(256, FV_NORM_MINB) k_lbr_normalize(KArgs a, LbrQueues lq) {
+// MINB: blocks per SM the register budget is cut for.  Large batches run the
+// 4-block form (64 registers, ~110 B of spills; C4 13.70 -> 13.61 ms), small
+// ones the 3-block form (80 registers; C1 is latency-bound and 2.5 % slower
+// at 4) -- see FV_NORM_BIG_ROWS.
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_lbr_normalize(KArgs a, LbrQueues lq) {
   const int64_t npair = (a.n + 1) >> 1;
   const int lane = threadIdx.x & 31;
   // dynamic distribution: each warp takes the next 32 pairs (see
@@ -1249,6 +1260,7 @@ struct DevWork {
   int64_t hsm_cap[FV_NSLOT] = {};
   int blocks_hset = 0, blocks_hset_p = 0;
   int blocks_lbr_nfast = 0;
+  int blocks_lbr_norm_big = 0;
   int blocks_lbr_norm = 0, blocks_lbr_nrep = 0, blocks_lbr_anch = 0, blocks_lbr_fast = 0, blocks_lbr_fl = 0, blocks_lbr_near = 0, blocks_lbr_fh = 0;
   std::mutex mu;
 };
@@ -1289,7 +1301,8 @@ cudaError_t get_work(DevWork** out) {
     w->blocks_price = occupancy_blocks((const void*)k_price, w->sm_count);
     w->blocks_greeks = occupancy_blocks((const void*)k_price_greeks<true, true>, w->sm_count);
     CK(cudaMalloc(&w->lbr_count, sizeof(unsigned int) * 16 * FV_NSLOT));
-    w->blocks_lbr_norm = occupancy_blocks((const void*)k_lbr_normalize, w->sm_count);
+    w->blocks_lbr_norm = occupancy_blocks((const void*)k_lbr_normalize<FV_NORM_MINB>, w->sm_count);
+    w->blocks_lbr_norm_big = occupancy_blocks((const void*)k_lbr_normalize<FV_NORM_MINB_BIG>, w->sm_count);
     w->blocks_lbr_nrep = occupancy_blocks((const void*)k_lbr_normalize_replay, w->sm_count);
     w->blocks_lbr_anch = occupancy_blocks((const void*)k_lbr_anchors, w->sm_count);
     w->blocks_lbr_fast = occupancy_blocks((const void*)k_lbr_far_low_fast, w->sm_count);
@@ -1435,7 +1448,10 @@ cudaError_t launch_iv(DevWork* w, int method, const KArgs& a, int slot, cudaStre
       CK(cudaMemsetAsync(lq.count, 0, 16 * sizeof(unsigned int), s));
       const int64_t cap1 = (b.n + 255) / 256;
       auto g = [cap1](int blocks) { return (int)(cap1 < blocks ? cap1 : blocks); };
-      FV_LAUNCH(FV_KID_LBR_NORM, s, k_lbr_normalize<<<blocks_for(w->blocks_lbr_norm, b.n), 256, 0, s>>>(b, lq));
+      if (b.n >= FV_NORM_BIG_ROWS)
+        FV_LAUNCH(FV_KID_LBR_NORM, s, k_lbr_normalize<FV_NORM_MINB_BIG><<<blocks_for(w->blocks_lbr_norm_big, b.n), 256, 0, s>>>(b, lq));
+      else
+        FV_LAUNCH(FV_KID_LBR_NORM, s, k_lbr_normalize<FV_NORM_MINB><<<blocks_for(w->blocks_lbr_norm, b.n), 256, 0, s>>>(b, lq));
       // the three replay passes usually find an empty queue: one CTA per SM
       // keeps their launch + drain short (a full occupancy grid costs ~7 us)
       FV_LAUNCH(FV_KID_LBR_NREP, s, k_lbr_normalize_replay<<<g(w->sm_count), 256, 0, s>>>(b, lq));
