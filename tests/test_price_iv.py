@@ -298,3 +298,28 @@ def test_bench_mirror_matches_reference(fv, tmp_path):
         with contextlib.redirect_stdout(buf):
             bench.run_bench(rows, method, None, None, seed)
         assert buf.getvalue().splitlines()[0] == str(g[f"{method}_report_head"])
+
+
+@pytest.mark.gpu
+def test_round_trip_edge_shapes(fv):
+    """Empty and one-row batches, broadcast-only inputs, a dividend on a
+    non-BSM model (batch_price's DomainError), a missing sigma."""
+    empty = fv.price_iv("bsm", "lbr", [], [], [], [], [], [], sigma=[])
+    assert empty["iv"].shape == (0,) and empty["status"].shape == (0,)
+    one = fv.price_iv("black", "halley", ["p"], [100.0], [90.0], [0.5], [0.01], sigma=[0.3])
+    p = fv.batch_price("black", ["p"], [100.0], [90.0], [0.5], [0.01], sigma=[0.3])["price"]
+    ref = fv.batch_iv("black", "halley", ["p"], [100.0], [90.0], [0.5], [0.01], price=p)
+    assert one["price"].tobytes() == p.tobytes() and one["iv"].tobytes() == ref["iv"].tobytes()
+    n = 5
+    bc = fv.price_iv("bsm", "lbr", ["c"] * n, 100.0, np.linspace(80, 120, n), 1.0, 0.02, 0.01,
+                     sigma=0.25)
+    p = fv.batch_price("bsm", ["c"] * n, 100.0, np.linspace(80, 120, n), 1.0, 0.02, 0.01, sigma=0.25)["price"]
+    ref = fv.batch_iv("bsm", "lbr", ["c"] * n, 100.0, np.linspace(80, 120, n), 1.0, 0.02, price=p, q=0.01)
+    assert bc["iv"].tobytes() == ref["iv"].tobytes()
+    with pytest.raises(fv.BatchError) as e:
+        fv.price_iv("bs", "lbr", ["c"] * n, 100.0, np.linspace(80, 120, n), 1.0, 0.02, 0.01, sigma=0.25)
+    with pytest.raises(fv.BatchError) as e2:
+        fv.batch_price("bs", ["c"] * n, 100.0, np.linspace(80, 120, n), 1.0, 0.02, 0.01, sigma=0.25)
+    assert str(e.value) == str(e2.value)
+    with pytest.raises(fv.BatchError, match="batch_price requires sigma"):
+        fv.price_iv("bsm", "lbr", ["c"], [100.0], [100.0], [1.0], [0.0])
