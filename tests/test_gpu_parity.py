@@ -595,3 +595,30 @@ def test_host_calls_sharded_over_devices(fv):
             _native.set_devices(())
         assert ei.value.index == 2_000_000 and ei.value.kind == "NonFiniteInput", (devs, str(ei.value))
     assert _native.get_devices() == []
+
+
+@pytest.mark.gpu
+def test_host_calls_bit_identical_for_1_2_4_8_shards(fv):
+    """results bit-identical for G in {1, 2, 4, 8} (here G host
+    shards on device 0; on a multi-GPU box one per GPU), LBR and Halley, with
+    the same status column -- the analogue of the reference's FASTVOL_THREADS
+    invariant (test_acceptance.py:211-254)."""
+    from paper_2604_27210_b200 import _native
+    from paper_2604_27210_b200 import workloads as W
+    n = 8_400_000
+    flag, S, K, t, r, q, sig = W.chain_draws(n, seed=123)
+    fl = W.flag_chars(flag)
+    px = fv.batch_price("bsm", fl, S, K, t, r, q=q, sigma=sig)["price"]
+    for method in ("lbr", "halley"):
+        ref = None
+        for g in (1, 2, 4, 8):
+            _native.set_devices((0,) * g if g > 1 else ())
+            try:
+                tb = fv.batch_iv("bsm", method, fl, S, K, t, r, price=px, q=q)
+            finally:
+                _native.set_devices(())
+            if ref is None:
+                ref = tb
+                continue
+            assert np.array_equal(ref["iv"].view(np.int64), tb["iv"].view(np.int64)), (method, g)
+            assert (ref["status"] == tb["status"]).all(), (method, g)
