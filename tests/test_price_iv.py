@@ -323,3 +323,60 @@ def test_round_trip_edge_shapes(fv):
     assert str(e.value) == str(e2.value)
     with pytest.raises(fv.BatchError, match="batch_price requires sigma"):
         fv.price_iv("bsm", "lbr", ["c"], [100.0], [100.0], [1.0], [0.0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("method,mcode", [("halley", 0), ("lbr", 1)])
+def test_round_trip_full_10m(fv, oracle_mod, method, mcode):
+    """BASELINE size for the round trip (the bench workload rt): the whole
+    10M-row C2 draw set priced and inverted in one device-resident
+    fv_price_iv call equals batch_price then batch_iv on every row (price, iv,
+    status bits); a strided 1-in-100 sample is bit-compared with the oracle;
+    the host-pointer call is bit-identical to the device-resident one."""
+    import sys
+    import torch
+    from conftest import REPO
+    if REPO not in sys.path:
+        sys.path.insert(0, REPO)
+    import bench
+    from paper_2604_27210_b200 import _native
+    lib = _native.lib_for_compute()
+    dev = torch.device("cuda", 0)
+    n = 10_000_000
+    cols = bench.draws_device("c2", n, 0, dev)
+    ncols = bench.native_cols(cols, "sigma")
+    px = torch.empty(n, dtype=torch.float64, device=dev)
+    iv = torch.empty(n, dtype=torch.float64, device=dev)
+    st = torch.empty(n, dtype=torch.int8, device=dev)
+    ep, ei = _native.fv_error(), _native.fv_error()
+    assert lib.fv_price_iv(2, mcode, *ncols, n, px.data_ptr(), iv.data_ptr(), st.data_ptr(), None,
+                           ep, ei) == 0, (ep.message, ei.message)
+    px2 = bench.price_on_device(lib, 2, cols, n)
+    cols2 = dict(cols, price=px2)
+    iv2 = torch.empty(n, dtype=torch.float64, device=dev)
+    st2 = torch.empty(n, dtype=torch.int8, device=dev)
+    err = _native.fv_error()
+    assert lib.fv_batch_iv(2, mcode, *bench.native_cols(cols2, "price"), n, iv2.data_ptr(), st2.data_ptr(),
+                           None, err) == 0, err.message
+    torch.cuda.synchronize()
+    assert torch.equal(px.view(torch.int64), px2.view(torch.int64))
+    assert torch.equal(iv.view(torch.int64), iv2.view(torch.int64))
+    assert torch.equal(st, st2)
+    idx = torch.arange(0, n, 100, device=dev)
+    samp = {k: cols[k][idx].cpu().numpy() for k in ("flag", "underlying", "strike", "t", "r", "q", "sigma")}
+    wp = oracle_mod.rows_price("bsm", samp["flag"], samp["underlying"], samp["strike"], samp["t"], samp["r"],
+                               samp["q"], samp["sigma"])
+    assert_bits(px[idx].cpu().numpy(), wp["price"], "rt-10M sample price")
+    want = oracle_mod.rows_iv("bsm", method, samp["flag"], samp["underlying"], samp["strike"], samp["t"],
+                              samp["r"], samp["q"], wp["price"])
+    assert_bits(st[idx].cpu().numpy(), want["status_code"], "rt-10M sample status")
+    assert_bits(iv[idx].cpu().numpy(), want["iv"], "rt-10M sample iv")
+    hcols = {k: (v.cpu().pin_memory() if v.numel() > 1 else v.cpu()) for k, v in cols.items() if torch.is_tensor(v)}
+    hpx = torch.empty(n, dtype=torch.float64).pin_memory()
+    hiv = torch.empty(n, dtype=torch.float64).pin_memory()
+    hst = torch.empty(n, dtype=torch.int8).pin_memory()
+    assert lib.fv_price_iv(2, mcode, *bench.native_cols(hcols, "sigma"), n, hpx.data_ptr(), hiv.data_ptr(),
+                           hst.data_ptr(), None, ep, ei) == 0, (ep.message, ei.message)
+    assert torch.equal(hpx.view(torch.int64), px.cpu().view(torch.int64))
+    assert torch.equal(hiv.view(torch.int64), iv.cpu().view(torch.int64))
+    assert torch.equal(hst, st.cpu())
