@@ -666,22 +666,28 @@ struct HalRecRow { int64_t rowbits; };   // row | (call << 62), parallel array
 
 #define FV_HAL_CALL (1ll << 62)
 
+// The record's spare slot (p[3].y) carries the row bits (row | call << 62):
+// a refill then issues the record's six 16-byte loads straight after the
+// claim, instead of a dependent load of a separate row array first (the
+// refill's load -> test chain was the top stall of k_halley_iter).
+// FV_HAL_RROW keeps the separate array (A/B).
 __device__ __forceinline__ void hal_store(HalRec* r, const FvHalleyCtx& c, double lo, double hi,
-                                          double sigma, double fval) {
+                                          double sigma, double fval, int64_t rowbits) {
   double2* p = reinterpret_cast<double2*>(r);
   p[0] = make_double2(c.Fw, c.K);
   p[1] = make_double2(c.disc, c.sqrt_t);
   p[2] = make_double2(c.lnFK, c.target);
-  p[3] = make_double2(c.tol_price, 0.0);
+  p[3] = make_double2(c.tol_price, __longlong_as_double(rowbits));
   p[4] = make_double2(lo, hi);
   p[5] = make_double2(sigma, fval);
 }
-__device__ __forceinline__ void hal_load(const HalRec* r, int64_t rowbits, FvHalleyCtx& c, double& lo,
-                                         double& hi, double& sigma, double& fval) {
+__device__ __forceinline__ void hal_load(const HalRec* r, FvHalleyCtx& c, double& lo, double& hi,
+                                         double& sigma, double& fval, int64_t& rowbits) {
   const double2* p = reinterpret_cast<const double2*>(r);
   const double2 v0 = p[0], v1 = p[1], v2 = p[2], v3 = p[3], v4 = p[4], v5 = p[5];
   c.Fw = v0.x; c.K = v0.y; c.disc = v1.x; c.sqrt_t = v1.y; c.lnFK = v2.x; c.target = v2.y;
   c.tol_price = v3.x;
+  rowbits = __double_as_longlong(v3.y);
   c.th = (rowbits & FV_HAL_CALL) ? 1.0 : -1.0;
   c.fk_bad = false;                        // such quotes never enter the queues
   lo = v4.x; hi = v4.y; sigma = v5.x; fval = v5.y;
@@ -798,8 +804,11 @@ __global__ void __launch_bounds__(256, FV_HSET_MINB) k_halley_bracket(KArgs a, K
     }
     const unsigned int slot = warp_append(count, open);
     if (open) {
-      hal_store(recs + slot, m.c, lo, hi, sigma, fval);
-      rrow[slot] = row | (m.c.th > 0.0 ? FV_HAL_CALL : 0);
+      const int64_t rb = row | (m.c.th > 0.0 ? FV_HAL_CALL : 0);
+      hal_store(recs + slot, m.c, lo, hi, sigma, fval, rb);
+#ifdef FV_HAL_RROW
+      rrow[slot] = rb;
+#endif
     }
     const unsigned int hs = warp_append(count + 1, hb);
     if (hb) hrow[hs] = (int32_t)row;
@@ -849,9 +858,15 @@ __global__ void __launch_bounds__(256, FV_HSM_MINB) k_halley_iter(KArgs a, HalRe
         exhausted = true;
       } else {
         rec = (int32_t)jq;
-        const int64_t rb = rrow[rec];
+#ifdef FV_HAL_RROW
+        const int64_t rb0 = rrow[rec];
+        row = rb0 & (FV_HAL_CALL - 1);
+#endif
+        int64_t rb;
+        hal_load(recs + rec, c, lo, hi, sigma, fval, rb);
+#ifndef FV_HAL_RROW
         row = rb & (FV_HAL_CALL - 1);
-        hal_load(recs + rec, rb, c, lo, hi, sigma, fval);
+#endif
         k = 0; midp = false; busy = true;
       }
     }
@@ -943,9 +958,15 @@ __global__ void __launch_bounds__(256, FV_HSM_MINB) k_halley_bisect(KArgs a, con
         exhausted = true;
       } else {
         const int32_t rec = bis[jq];
-        const int64_t rb = rrow[rec];
+#ifdef FV_HAL_RROW
+        const int64_t rb0 = rrow[rec];
+        row = rb0 & (FV_HAL_CALL - 1);
+#endif
+        int64_t rb;
+        hal_load(recs + rec, c, lo, hi, sigma, fval, rb);
+#ifndef FV_HAL_RROW
         row = rb & (FV_HAL_CALL - 1);
-        hal_load(recs + rec, rb, c, lo, hi, sigma, fval);
+#endif
         k = 0; busy = true;
       }
     }
