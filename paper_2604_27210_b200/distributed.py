@@ -58,18 +58,40 @@ def run_sharded(compute, n, group=None, device=None, gather=False):
     global outcome with one MIN all-reduce, and optionally all-gather the
     outputs.  Returns (outputs, outcome) where outputs are this rank's shard
     (or the full arrays with ``gather=True``)."""
+    def one_stage(lo, hi):
+        outputs, check_rows, exc_row, exc_code = compute(lo, hi)
+        return outputs, [(check_rows, exc_row, exc_code)]
+    outputs, staged = run_sharded_stages(one_stage, n, 1, group=group, device=device, gather=gather)
+    return outputs, (staged[1] if staged else None)
+
+
+def run_sharded_stages(compute, n, nstage, group=None, device=None, gather=False):
+    """``run_sharded`` for a call made of ``nstage`` stages run in sequence by
+    the reference, each with its own checks and exception stream (fv_price_iv:
+    batch_price, then batch_iv on its prices).  ``compute(lo, hi) ->
+    (outputs, [(check_rows[12], exc_row, exc_code)] * nstage)``.  One MIN
+    all-reduce over the stages' status vectors; the first stage with an
+    outcome anywhere decides, as the reference raises in the first call that
+    fails.  Returns (outputs, (stage, outcome) | None)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     lo, hi = shard_bounds(n, world, rank)
-    outputs, check_rows, exc_row, exc_code = compute(lo, hi)
-    vec = torch.from_numpy(_status_vector(check_rows, exc_row, exc_code, lo))
+    outputs, stages = compute(lo, hi)
+    assert len(stages) == nstage
+    vec = torch.from_numpy(np.concatenate([_status_vector(cr, er, ec, lo) for cr, er, ec in stages]))
     if device is not None:
         vec = vec.to(device)
     if world > 1:
         dist.all_reduce(vec, op=dist.ReduceOp.MIN, group=group)
-    outcome = merge_status(vec.cpu().numpy())
+    v = vec.cpu().numpy()
+    outcome = None
+    for s in range(nstage):
+        o = merge_status(v[s * (NCHECK + 1):(s + 1) * (NCHECK + 1)])
+        if o is not None:
+            outcome = (s, o)
+            break
     if gather and world > 1 and outcome is None:
         full = {}
         for name, shard in outputs.items():
@@ -112,3 +134,35 @@ def batch_iv_sharded(model, method, cols, n, group=None, gather=False):
         return {"iv": iv, "status": st}, cr, int(er[0]), int(ec[0])
 
     return run_sharded(compute, n, group=group, device=dev, gather=gather)
+
+
+def price_iv_sharded(model, method, cols, n, group=None, gather=False):
+    """Sharded ``price_iv`` (fv_price_iv) on device-resident torch columns
+    (``sigma`` instead of ``price``).  Returns ((price, iv, status) or the
+    gathered dict, (stage, outcome) | None) with stage 0 = batch_price, 1 =
+    batch_iv: the price stage's failure on any shard is the call's."""
+    import torch
+    from . import _native
+    from .models import as_model
+    lib = _native.lib_for_compute()
+    m = as_model(model).code
+    dev = cols["strike"].device
+    none = np.full(NCHECK, -1, np.int64)
+
+    def compute(lo, hi):
+        sl = {k: (v if v.numel() == 1 else v[lo:hi]) for k, v in cols.items()}
+        k = hi - lo
+        px = torch.empty(k, dtype=torch.float64, device=dev)
+        iv = torch.empty(k, dtype=torch.float64, device=dev)
+        st = torch.empty(k, dtype=torch.int8, device=dev)
+        ep, ei = _native.fv_error(), _native.fv_error()
+        lib.fv_price_iv(m, 1 if method == "lbr" else 0,
+                        *[_native.col(sl[c]) for c in ("flag", "underlying", "strike", "t", "r", "q", "sigma")],
+                        k, px.data_ptr(), iv.data_ptr(), st.data_ptr(), None, ep, ei)
+        cr, er, ec = _native.last_outcome(lib)
+        price_checks = ep.code == _native.FV_ERR_BATCH      # fv_last_outcome: the deciding stage's rows
+        stages = [(cr if price_checks else none, int(er[0]), int(ec[0])),
+                  (none if price_checks else cr, int(er[1]), int(ec[1]))]
+        return {"price": px, "iv": iv, "status": st}, stages
+
+    return run_sharded_stages(compute, n, 2, group=group, device=dev, gather=gather)

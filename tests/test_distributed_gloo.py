@@ -89,3 +89,60 @@ def test_first_error_is_global_reference_order():
     scen = [(800, "exc", 3), (550, "exc", 1), (20, "exc", 2)]
     for rank, outcome, _ in _run(n, scen):
         assert outcome == ("exc", 2, 20)
+
+
+def _worker_staged(rank, world, port, n, scenario, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def compute(lo, hi):
+            stages = []
+            for stage in (0, 1):
+                checks = np.full(12, -1, np.int64)
+                exc_row, exc_code = -1, 0
+                for (g_row, st, kind, code) in scenario:
+                    if st != stage or not (lo <= g_row < hi):
+                        continue
+                    if kind == "check":
+                        if checks[code] < 0 or g_row - lo < checks[code]:
+                            checks[code] = g_row - lo
+                    elif exc_row < 0 or g_row - lo < exc_row:
+                        exc_row, exc_code = g_row - lo, code
+                stages.append((checks, exc_row, exc_code))
+            return {"price": np.arange(lo, hi, dtype=np.float64)}, stages
+        outputs, outcome = D.run_sharded_stages(compute, n, 2)
+        q.put((rank, outcome, {}))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_staged(n, scenario):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_staged, args=(r, 2, port, n, scenario, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=60) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+def test_price_iv_stages_price_failure_wins():
+    """fv_price_iv sharded (distributed.price_iv_sharded): a price-stage
+    exception on rank 1 beats an IV-stage check on rank 0 at an earlier row
+    (the reference raises in batch_price before batch_iv runs); with no price
+    failure anywhere, the IV stage's first error in the reference's order."""
+    n = 1000
+    scen = [(10, 1, "check", 6), (900, 0, "exc", 1), (950, 0, "exc", 2)]
+    for rank, outcome, _ in _run_staged(n, scen):
+        assert outcome == (0, ("exc", 1, 900))
+    scen = [(10, 1, "exc", 2), (600, 1, "check", 6)]
+    for rank, outcome, _ in _run_staged(n, scen):
+        assert outcome == (1, ("batch", 6, 600))
+    for rank, outcome, _ in _run_staged(n, []):
+        assert outcome is None

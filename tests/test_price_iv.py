@@ -380,3 +380,25 @@ def test_round_trip_full_10m(fv, oracle_mod, method, mcode):
     assert torch.equal(hpx.view(torch.int64), px.cpu().view(torch.int64))
     assert torch.equal(hiv.view(torch.int64), iv.cpu().view(torch.int64))
     assert torch.equal(hst, st.cpu())
+
+
+@pytest.mark.gpu
+def test_price_iv_sharded_single_rank(fv):
+    """distributed.price_iv_sharded without a process group (one rank) equals
+    price_iv; a price-stage exception comes back as stage 0's outcome."""
+    import torch
+    from paper_2604_27210_b200 import distributed as D
+    from paper_2604_27210_b200 import workloads as W
+    flag, S, K, t, r, q, sig = W.chain_draws(50_001, seed=23)
+    ref = fv.price_iv("bsm", "halley", W.flag_chars(flag), S, K, t, r, q, sigma=sig)
+    cols = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in
+            dict(flag=flag, underlying=S, strike=K, t=t, r=r, q=q, sigma=sig).items()}
+    out, outcome = D.price_iv_sharded("bsm", "halley", cols, len(flag))
+    assert outcome is None
+    assert_bits(out["price"].cpu().numpy(), ref["price"], "sharded price")
+    assert_bits(out["iv"].cpu().numpy(), ref["iv"], "sharded iv")
+    r2 = r.copy()
+    r2[777] = -1e4                   # exp(-r t) overflows in the pricer
+    cols["r"] = torch.from_numpy(r2).cuda()
+    out, outcome = D.price_iv_sharded("bsm", "halley", cols, len(flag))
+    assert outcome == (0, ("exc", 1, 777)), outcome
