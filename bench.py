@@ -225,7 +225,7 @@ def cpu_baseline(seconds, workload="c4"):
     O.rows_iv("black", "lbr", flag, F, K, t, r, 0.0, px)
     dt = time.perf_counter() - t0
     return {"value": len(flag) / dt, "unit": "quotes/s", "cores": cores, "kind": "port",
-            "sample": f"{len(flag)} rows of the C4 chain (every {stride}th row), "
+            "sample": f"{len(flag)} rows of the C4 chain (1 row in {stride}), "
                       f"oracle/fvoracle.cpp (reference restated on glibc+scipy), "
                       f"OpenMP {cores} threads, {dt:.2f} s"}
 
@@ -267,7 +267,7 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     ms = 1e3 * float(np.mean(times))
     value = len(flag) / (ms * 1e-3)
-    sample = (f"{len(flag)} rows of the C4 chain per step (every {stride}th row), "
+    sample = (f"{len(flag)} rows of the C4 chain per step (1 row in {stride}), "
               f"oracle/fvoracle.cpp on {cores} host threads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "quotes/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
