@@ -59,7 +59,7 @@
 #define FV_NORM_MINB_BIG 4
 #endif
 #ifndef FV_NORM_BIG_ROWS
-#define FV_NORM_BIG_ROWS (1 << 24)
+#define FV_NORM_BIG_ROWS (1 << 23)
 #endif
 #ifndef FV_PG_MINB
 #define FV_PG_MINB 3
