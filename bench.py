@@ -2,28 +2,44 @@
 """Benchmark: fp64 LBR implied-vol solves/sec on the C4 100M-quote option chain.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c4|c1|c2|c3|c5] [--rows R]
+                    [--workload c4|c1|c2|c3|c5|rt] [--rows R]
+                    [--scaling strong|weak] [--shard-scheme contiguous|cyclic]
+                    [--shard g/G]
 
 Metric (BASELINE.json): "fp64 IV solves/sec (LBR, 100M quotes) at 1/2/4/8 B200
-vs host-CPU ref".  One step = one ``fv_batch_iv(BLACK76, LBR, ...)`` call over
-one rank's 100M-quote chain (2 flags x 1,000 maturities x
-50,000 strikes).  Multi-GPU: one process per GPU (torchrun); rank r solves its
-own 100M-quote chain (underlying F_r = 100 * 1.01^r, strikes scaled with it,
-so every rank has the same normalized work) -- weak scaling, no collective
-on the data path; ranks only barrier and max-reduce their timings.
+vs host-CPU ref".  One step = one ``fv_batch_iv(BLACK76, LBR, ...)`` call per
+rank over that rank's quotes of the C4 chain (2 flags x 1,000
+maturities x 50,000 strikes = 100M quotes).
+
+Multi-GPU (one process per GPU, torchrun):
+  * ``--scaling strong`` (default): ONE 100M-quote chain sharded across the N
+    ranks -- rank g solves its rows (contiguous [g N/G, (g+1) N/G), or
+    1M-row blocks dealt round-robin with ``--shard-scheme cyclic``), no
+    collective on the data path; ``value`` = 100M / the max over ranks of the
+    per-step time;
+  * ``--scaling weak``: every rank solves its own full chain (F_r = 100 *
+    1.01^r), ``value`` = N x rows / max time.
+``--shard g/G`` runs shard g of a G-way strong split on this one GPU (the
+per-shard times predict the strong-scaling imbalance on a 1-GPU pool).
 
 ``value`` is device-resident throughput (inputs already in HBM; CUDA events on
-the launching stream, max over ranks).  ``e2e`` is the same call through the
-C ABI with pinned HOST buffers (chunked H2D / kernel / D2H inside the timed
-region).  The CPU baseline is the oracle port (oracle/fvoracle.cpp -- the
-reference restated in C++ on glibc + scipy, all host threads) timed on a
-bounded strided sample of the same chain.  The inputs (2.5 GB per step) are
-larger than the 126 MB L2, so no flush is needed between steps.
+the launching stream, max over ranks).  ``e2e`` is the same call through the C
+ABI with pinned HOST buffers (chunked H2D / kernel / D2H inside the timed
+region, wall clock).  ``cpu_baseline`` is the oracle (oracle/fvoracle.cpp -- the
+reference restated in C++ on glibc + scipy, all host threads) timed on ALL rows
+of the workload; the same pass compares every row bit for bit with the GPU's
+output (``parity``).  The inputs (2.5 GB per step) are larger than the 126 MB
+L2, so no flush is needed between steps.
+
+``--impl reference`` times the reference's CPU path on the same workload and
+config (the oracle port, all host threads; /root/reference itself does not
+exist on the GPU box) without importing the product package.
 """
 
 import argparse
 import json
 import os
+import platform
 import subprocess
 import sys
 import time
@@ -33,89 +49,175 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
+import workloads as W  # noqa: E402  (numpy only; no product import)
+
 # Weighted distinct FP64 ops per quote the reference executes (SURVEY.md 8(d),
 # Appendix B.3): the algorithmic work per unit for the roofline.
 # rt (the reference's bench harness: synthetic_chain's BSM pricing + run_bench's
 # Halley inversion, one fused fv_price_iv call): price 200 + C2 Halley 1476.
 W_OPS = {"c4": 1443.0, "c1": 1405.0, "c2": 1476.0, "c3": 298.0, "c5": 347.0, "rt": 1676.0}
 METRIC = "fp64 IV solves/sec (LBR, 100M quotes) at 1/2/4/8 B200 vs host-CPU ref"
+CYCLIC_BLOCK = 1 << 20
+WL_NAMES = {"c4": "C4: jackel_iv_black (LBR) on the 100M-quote Black-76 chain "
+                  "(2 flags x 1000 maturities x 50000 strikes)",
+            "c1": "C1: LBR Black-76 1M synthetic quotes (synthetic_chain seed 0)",
+            "c2": "C2: Halley BSM with dividend yield, 10M quotes (synthetic_chain seed 0)",
+            "c3": "C3: fused BSM price + all Greeks, 10M quotes (synthetic_chain seed 0)",
+            "c5": "C5: wing-stress set, LBR Black-76 (seed 5)",
+            "rt": "RT: the reference bench harness's round trip (bench.py:19-40) on 10M C2 draws: "
+                  "BSM price -> Halley IV in one fused fv_price_iv call"}
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4", choices=["c4", "c1", "c2", "c3", "c5", "rt"])
-    ap.add_argument("--rows", type=int, default=0, help="rows per rank (default: workload size)")
+    ap.add_argument("--rows", type=int, default=0,
+                    help="rows of the logical batch (default: the workload's size; fewer C4 rows = an "
+                         "evenly strided sub-chain, for profiling)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--shard-scheme", default="contiguous", choices=["contiguous", "cyclic"])
+    ap.add_argument("--shard", default="", help="g/G: run shard g of a G-way strong split on this GPU")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the oracle pass (cpu_baseline + parity)")
     ap.add_argument("--no-kernel-timing", action="store_true",
                     help="skip the per-kernel event-timing pass (ncu traffic captures)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def default_rows(workload):
-    return {"c4": 100_000_000, "c1": 1_000_000, "c2": 10_000_000, "c3": 10_000_000,
+    return {"c4": W.C4_ROWS, "c1": 1_000_000, "c2": 10_000_000, "c3": 10_000_000,
             "c5": 10_000_000, "rt": 10_000_000}[workload]
 
 
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
 # ---------------------------------------------------------------------------
-# workload construction on the device
+# sharding (every output row depends on its input row only)
 # ---------------------------------------------------------------------------
-def c4_device(rows, rank, dev):
-    """C4 chain for one rank, built on the GPU: returns the
-    column tensors of a Black-76 LBR batch (F, r, q are broadcast scalars)."""
+def shard_ranges(n, nshard, g, scheme="contiguous", block=CYCLIC_BLOCK):
+    """Row ranges [(lo, hi), ...] of shard g of n rows split nshard ways:
+    one contiguous range, or blocks of ``block`` rows dealt round-robin."""
+    if scheme == "contiguous":
+        lo, hi = n * g // nshard, n * (g + 1) // nshard
+        return [(lo, hi)] if hi > lo else []
+    nb = (n + block - 1) // block
+    return [(b * block, min(n, (b + 1) * block)) for b in range(g, nb, nshard)]
+
+
+def plan(args, world, rank):
+    """(logical rows, this process's row ranges, shard label, F, scaling)."""
+    n_total = args.rows or default_rows(args.workload)
+    if args.shard:
+        g, G = (int(x) for x in args.shard.split("/"))
+        assert 0 <= g < G and world == 1, "--shard g/G runs one shard in one process"
+        return n_total, shard_ranges(n_total, G, g, args.shard_scheme), f"{g}/{G}", 100.0, "strong"
+    if args.scaling == "weak":
+        return n_total, [(0, n_total)], f"{rank}/{world}", 100.0 * (1.01 ** rank), "weak"
+    return n_total, shard_ranges(n_total, world, rank, args.shard_scheme), f"{rank}/{world}", 100.0, "strong"
+
+
+def c4_row_index(ranges, n_total):
+    """Chain row indices of the given logical rows (an evenly strided
+    sub-chain when the logical batch is smaller than the chain)."""
+    stride = max(1, W.C4_ROWS // n_total) if n_total < W.C4_ROWS else 1
+    return [(lo, hi, stride) for lo, hi in ranges]
+
+
+# ---------------------------------------------------------------------------
+# workload construction
+# ---------------------------------------------------------------------------
+def c4_device(rows, rank, dev, ranges=None, n_total=None, F=None):
+    """C4 chain rows built on the GPU: returns the column
+    tensors of a Black-76 LBR batch (F, r, q are broadcast scalars).  Default:
+    rows [0, rows) of rank ``rank``'s weak-scaling chain (F = 100 * 1.01^rank)."""
     import torch
-    from paper_2604_27210_b200 import workloads as W
-    F = 100.0 * (1.01 ** rank)
-    out = {}
-    flag = torch.empty(rows, dtype=torch.int8, device=dev)
-    K = torch.empty(rows, dtype=torch.float64, device=dev)
-    t = torch.empty(rows, dtype=torch.float64, device=dev)
-    sig = torch.empty(rows, dtype=torch.float64, device=dev)
+    F = (100.0 * (1.01 ** rank)) if F is None else F
+    n_total = rows if n_total is None else n_total
+    ranges = [(0, rows)] if ranges is None else ranges
+    m = sum(hi - lo for lo, hi in ranges)
+    flag = torch.empty(m, dtype=torch.int8, device=dev)
+    K = torch.empty(m, dtype=torch.float64, device=dev)
+    t = torch.empty(m, dtype=torch.float64, device=dev)
+    sig = torch.empty(m, dtype=torch.float64, device=dev)
     step = 1 << 24
-    # fewer rows than the chain: an evenly strided sub-chain (profiling runs)
-    stride = max(1, W.C4_ROWS // rows) if rows < W.C4_ROWS else 1
-    for s0 in range(0, rows, step):
-        s1 = min(rows, s0 + step)
-        row = (torch.arange(s0, s1, device=dev, dtype=torch.int64) * stride) % W.C4_ROWS
-        i = (row % W.C4_STRIKES).double()
-        j = ((row // W.C4_STRIKES) % W.C4_MATURITIES).double()
-        f = row // (W.C4_STRIKES * W.C4_MATURITIES)
-        x = -2.0 + 4.0 * i / (W.C4_STRIKES - 1)
-        K[s0:s1] = F * torch.exp(-x)
-        tt = (1.0 / 365.0) * torch.pow(torch.tensor(5.0 * 365.0, dtype=torch.float64, device=dev),
-                                       j / (W.C4_MATURITIES - 1))
-        t[s0:s1] = tt
-        sig[s0:s1] = torch.clamp(0.2 + 0.1 * x * x / torch.sqrt(tt), max=2.0)
-        flag[s0:s1] = torch.where(f == 0, 1, -1).to(torch.int8)
-    out["flag"], out["strike"], out["t"], out["sigma"] = flag, K, t, sig
-    out["underlying"] = torch.full((1,), F, dtype=torch.float64, device=dev)
-    out["r"] = torch.full((1,), 0.03, dtype=torch.float64, device=dev)
-    out["q"] = torch.zeros(1, dtype=torch.float64, device=dev)
-    return out
+    o = 0
+    for lo, hi, stride in c4_row_index(ranges, n_total):
+        for s0 in range(lo, hi, step):
+            s1 = min(hi, s0 + step)
+            row = (torch.arange(s0, s1, device=dev, dtype=torch.int64) * stride) % W.C4_ROWS
+            i = (row % W.C4_STRIKES).double()
+            j = ((row // W.C4_STRIKES) % W.C4_MATURITIES).double()
+            f = row // (W.C4_STRIKES * W.C4_MATURITIES)
+            x = -2.0 + 4.0 * i / (W.C4_STRIKES - 1)
+            k = s1 - s0
+            K[o:o + k] = F * torch.exp(-x)
+            tt = (1.0 / 365.0) * torch.pow(torch.tensor(5.0 * 365.0, dtype=torch.float64, device=dev),
+                                           j / (W.C4_MATURITIES - 1))
+            t[o:o + k] = tt
+            sig[o:o + k] = torch.clamp(0.2 + 0.1 * x * x / torch.sqrt(tt), max=2.0)
+            flag[o:o + k] = torch.where(f == 0, 1, -1).to(torch.int8)
+            o += k
+    return {"flag": flag, "strike": K, "t": t, "sigma": sig,
+            "underlying": torch.full((1,), F, dtype=torch.float64, device=dev),
+            "r": torch.full((1,), 0.03, dtype=torch.float64, device=dev),
+            "q": torch.zeros(1, dtype=torch.float64, device=dev)}
 
 
-def draws_device(workload, rows, rank, dev):
-    """C1/C2/C3/C5 columns (numpy generators, moved to the device)."""
-    import torch
-    from paper_2604_27210_b200 import workloads as W
+def c4_host(ranges, n_total, F=100.0):
+    """The same rows on the host (numpy; the reference arm / oracle)."""
+    parts = []
+    for lo, hi, stride in c4_row_index(ranges, n_total):
+        parts.append((np.arange(lo, hi, dtype=np.int64) * stride) % W.C4_ROWS)
+    row = np.concatenate(parts) if parts else np.zeros(0, np.int64)
+    flag, _, K, t, _, sig = W.c4_rows(row)
+    if F != 100.0:
+        K = K * (F / 100.0)
+    return {"flag": flag, "underlying": np.array([F]), "strike": K, "t": t, "r": np.array([0.03]),
+            "q": np.zeros(1), "sigma": sig}
+
+
+def draws_host(workload, n_total, ranges, rank_seed=0):
+    """C1/C2/C3/C5/rt columns (numpy generators of the whole logical batch,
+    sliced to this process's rows)."""
     if workload == "c5":
-        flag, F, K, t, r, s, kind, side = W.c5_params(rows, seed=5 + rank)
+        flag, F, K, t, r, s, kind, side = W.c5_params(n_total, seed=5 + rank_seed)
         q = np.zeros_like(F)
-        extra = {"kind": kind, "side": side}
+        cols = {"flag": flag, "underlying": F, "strike": K, "t": t, "r": r, "q": q, "sigma": s,
+                "kind": kind, "side": side}
     else:
-        flag, F, K, t, r, q, s = W.chain_draws(rows, seed=rank)
+        flag, F, K, t, r, q, s = W.chain_draws(n_total, seed=rank_seed)
         if workload == "c1":
             q = np.zeros_like(F)
-        extra = {}
-    cols = {"flag": flag, "underlying": F, "strike": K, "t": t, "r": r, "q": q, "sigma": s}
-    out = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in cols.items()}
-    out.update(extra)
+        cols = {"flag": flag, "underlying": F, "strike": K, "t": t, "r": r, "q": q, "sigma": s}
+    n = len(cols["flag"])
+    idx = np.concatenate([np.arange(lo, min(hi, n)) for lo, hi in ranges]) if ranges else np.zeros(0, np.int64)
+    return {k: np.ascontiguousarray(v[idx]) for k, v in cols.items()}
+
+
+def draws_device(workload, rows, rank, dev, ranges=None):
+    import torch
+    h = draws_host(workload, rows, ranges if ranges is not None else [(0, rows)], rank_seed=rank)
+    out = {k: torch.from_numpy(v).to(dev) for k, v in h.items() if k not in ("kind", "side")}
+    out["kind"], out["side"] = h.get("kind"), h.get("side")
     return out
+
+
+def cpu_sample_c4(rows):
+    """``rows`` evenly strided rows of the C4 chain (numpy):
+    (flag, F, K, t, r, sigma, stride)."""
+    stride = max(1, W.C4_ROWS // rows)
+    idx = np.arange(0, W.C4_ROWS, stride, dtype=np.int64)[:rows]
+    flag, F, K, t, r, sig = W.c4_rows(idx)
+    return flag, F, K, t, r, sig, stride
 
 
 def native_cols(cols, last):
@@ -132,6 +234,27 @@ def price_on_device(lib, model, cols, n):
     if rc:
         raise RuntimeError(err.message)
     return px
+
+
+def workload_call(workload):
+    """(model code, method code: 1 LBR / 0 Halley / -1 price+Greeks, price->IV round trip?)"""
+    if workload in ("c4", "c1", "c5"):
+        return 0, 1, False
+    if workload == "c2":
+        return 2, 0, False
+    if workload == "rt":
+        return 2, 0, True
+    return 2, -1, False
+
+
+def config_for(args, world, n_total, scaling, shard_label):
+    cfg = {"workload": WL_NAMES[args.workload], "rows_total": n_total,
+           "parallelism": f"quote-sharded x{world} ({scaling} scaling"
+                          + (f", {args.shard_scheme} shards" if scaling == "strong" else "") + ")",
+           "l2": "inputs (>= 0.5 GB/step per GPU) exceed the 126 MB L2; no flush needed"}
+    if args.shard:
+        cfg["shard"] = shard_label
+    return cfg
 
 
 # ---------------------------------------------------------------------------
@@ -159,8 +282,7 @@ class ClockSampler:
             self.proc = None
             return
         # the sampler must be live before the timed region starts (nvidia-smi
-        # takes a few hundred ms to print its first line; a short timed region
-        # would otherwise end before any sample)
+        # takes a few hundred ms to print its first line)
         t0 = time.time()
         while time.time() - t0 < 5.0 and self.proc.poll() is None:
             self.fh.flush()
@@ -198,95 +320,121 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port on the host cores
+# the oracle pass: CPU baseline timing + parity of every row
 # ---------------------------------------------------------------------------
-def cpu_sample_c4(rows, stride_rows=None):
-    from paper_2604_27210_b200 import workloads as W
-    stride = max(1, W.C4_ROWS // rows)
-    idx = np.arange(0, W.C4_ROWS, stride, dtype=np.int64)[:rows]
-    i = idx % W.C4_STRIKES
-    j = (idx // W.C4_STRIKES) % W.C4_MATURITIES
-    f = idx // (W.C4_STRIKES * W.C4_MATURITIES)
-    x = -2.0 + 4.0 * i / (W.C4_STRIKES - 1)
-    K = 100.0 * np.exp(-x)
-    t = (1.0 / 365.0) * (5.0 * 365.0) ** (j / (W.C4_MATURITIES - 1))
-    sig = np.minimum(0.2 + 0.1 * x * x / np.sqrt(t), 2.0)
-    flag = np.where(f == 0, 1, -1).astype(np.int8)
-    n = len(idx)
-    return flag, np.full(n, 100.0), K, t, np.full(n, 0.03), sig, stride
+def host_info(threads):
+    info = {"cores": threads, "host_cpus": os.cpu_count(), "cpu_model": None,
+            "glibc": "-".join(platform.libc_ver()), "numpy": np.__version__}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        import scipy
+        info["scipy"] = scipy.__version__
+    except ImportError:
+        info["scipy"] = None
+    return info
 
 
-def cpu_baseline(seconds, workload="c4"):
-    """Time the oracle (reference restated in C++, all host threads) on a
-    strided sample of the chain sized to ~``seconds`` of CPU work."""
+def oracle_run(workload, h, threads):
+    """Run the oracle (reference restated on glibc + scipy) over the host
+    columns ``h`` of one workload: returns (seconds, outputs dict).  The
+    price column of the IV workloads is an input (given in ``h``)."""
     from oracle import fvoracle as O
     O.lib()
-    cores = os.cpu_count() or 1
-    O.set_threads(cores)
-    flag, F, K, t, r, sig, stride = cpu_sample_c4(200_000)
-    px = O.rows_price("black", flag, F, K, t, r, 0.0, sig)["price"]
+    O.set_threads(threads)
+    model, method, rt = workload_call(workload)
+    mname = {0: "black", 2: "bsm"}[model]
+    a = [h[k] for k in ("flag", "underlying", "strike", "t", "r", "q")]
     t0 = time.perf_counter()
-    O.rows_iv("black", "lbr", flag, F, K, t, r, 0.0, px)
-    rate = len(flag) / (time.perf_counter() - t0)
-    rows = int(min(max(rate * seconds, 200_000), 50_000_000))
-    flag, F, K, t, r, sig, stride = cpu_sample_c4(rows)
-    px = O.rows_price("black", flag, F, K, t, r, 0.0, sig)["price"]
-    t0 = time.perf_counter()
-    O.rows_iv("black", "lbr", flag, F, K, t, r, 0.0, px)
-    dt = time.perf_counter() - t0
-    return {"value": len(flag) / dt, "unit": "quotes/s", "cores": cores, "kind": "port",
-            "sample": f"{len(flag)} rows of the C4 chain (1 row in {stride}), "
-                      f"oracle/fvoracle.cpp (reference restated on glibc+scipy), "
-                      f"OpenMP {cores} threads, {dt:.2f} s"}
+    if method == -1:
+        p = O.rows_price(mname, *a, h["sigma"])
+        g = O.rows_greeks(mname, *a, h["sigma"])
+        out = {"price": p["price"], "delta": g["delta"], "gamma": g["gamma"], "theta": g["theta"],
+               "rho": g["rho"], "vega": g["vega"], "status": g["status_code"],
+               "exc": p["exc"].astype(np.int32) + g["exc"]}
+    elif rt:
+        p = O.rows_price(mname, *a, h["sigma"])
+        w = O.rows_iv(mname, "halley" if method == 0 else "lbr", *a, p["price"])
+        out = {"price": p["price"], "iv": w["iv"], "status": w["status_code"],
+               "exc": p["exc"].astype(np.int32) + w["exc"]}
+    else:
+        w = O.rows_iv(mname, "lbr" if method == 1 else "halley", *a, h["price"])
+        out = {"iv": w["iv"], "status": w["status_code"], "exc": w["exc"].astype(np.int32)}
+    return time.perf_counter() - t0, out
+
+
+def parity_count(got, want):
+    """Rows whose outputs differ bit for bit (any NaN equals any NaN) or where
+    the reference would have raised."""
+    bad = np.asarray(want["exc"]) != 0
+    for k, v in got.items():
+        w = want[k]
+        v = np.asarray(v)
+        if v.dtype == np.float64:
+            same = (v.view(np.int64) == w.view(np.int64)) | (np.isnan(v) & np.isnan(w))
+        else:
+            same = v.astype(np.int64) == np.asarray(w).astype(np.int64)
+        bad |= ~same
+    return int(bad.sum())
 
 
 # ---------------------------------------------------------------------------
 # arms
 # ---------------------------------------------------------------------------
-def dist_setup():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
-
-
 def run_reference(args):
+    """The reference's CPU path on the same workload and config: the oracle
+    port (reference restated in C++ on glibc + scipy) on all host threads, no
+    product code imported.  Rank 0 only under torchrun."""
     world, rank, local = dist_setup()
     if rank != 0:
         return 0
-    from oracle import fvoracle as O
-    O.lib()
-    cores = os.cpu_count() or 1
-    O.set_threads(cores)
-    # size one step to a few seconds of host work
-    flag, F, K, t, r, sig, stride = cpu_sample_c4(100_000)
-    px = O.rows_price("black", flag, F, K, t, r, 0.0, sig)["price"]
-    t0 = time.perf_counter()
-    O.rows_iv("black", "lbr", flag, F, K, t, r, 0.0, px)
-    rate = len(flag) / (time.perf_counter() - t0)
-    rows = int(min(max(rate * 4.0, 100_000), 50_000_000))
-    flag, F, K, t, r, sig, stride = cpu_sample_c4(rows)
-    px = O.rows_price("black", flag, F, K, t, r, 0.0, sig)["price"]
+    assert "paper_2604_27210_b200" not in sys.modules
+    n_total = args.rows or default_rows(args.workload)
+    scaling = "weak" if args.scaling == "weak" else "strong"
+    threads = os.cpu_count() or 1
+    model, method, rt = workload_call(args.workload)
+    # the whole logical batch (strong scaling's chain; the reference has one host)
+    if args.workload == "c4":
+        h = c4_host([(0, n_total)], n_total)
+    else:
+        h = draws_host(args.workload, n_total, [(0, n_total)])
+    if method != -1 and not rt:
+        from oracle import fvoracle as O
+        O.lib()
+        O.set_threads(threads)
+        mname = {0: "black", 2: "bsm"}[model]
+        h["price"] = O.rows_price(mname, *[h[k] for k in ("flag", "underlying", "strike", "t", "r", "q")],
+                                  h["sigma"])["price"]
+        if args.workload == "c5":
+            F = np.broadcast_to(h["underlying"], h["strike"].shape)
+            h["price"] = W.c5_prices(h["flag"], F, h["strike"], h["t"], h["r"], h["kind"], h["side"], h["price"])
+    m = len(h["flag"])
+    warm = min(m, 1_000_000)
+    hw = {k: (v[:warm] if (isinstance(v, np.ndarray) and v.shape[0] == m) else v) for k, v in h.items()}
     for _ in range(args.warmup):
-        O.rows_iv("black", "lbr", flag[:10000], F[:10000], K[:10000], t[:10000], r[:10000], 0.0,
-                  px[:10000])
+        oracle_run(args.workload, hw, threads)
     times = []
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        O.rows_iv("black", "lbr", flag, F, K, t, r, 0.0, px)
-        times.append(time.perf_counter() - t0)
+        dt, _ = oracle_run(args.workload, h, threads)
+        times.append(dt)
     ms = 1e3 * float(np.mean(times))
-    value = len(flag) / (ms * 1e-3)
-    sample = (f"{len(flag)} rows of the C4 chain per step (1 row in {stride}), "
-              f"oracle/fvoracle.cpp on {cores} host threads")
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "quotes/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": "C4 LBR Black-76 chain (strided sample)"},
-            "cpu_baseline": {"value": value, "unit": "quotes/s", "cores": cores, "kind": "port",
-                             "sample": sample},
-            "e2e": {"value": value, "unit": "quotes/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+    value = m / (ms * 1e-3)
+    sample = (f"all {m} rows of the workload per step; warm-up steps on its first {warm} rows; "
+              f"oracle/fvoracle.cpp (the reference restated in C++ on glibc + scipy) on {threads} host threads")
+    cpu = dict(host_info(threads), value=value, unit="quotes/s", kind="port", sample=sample)
+    line = {"impl": "reference",
+            "metric": METRIC if args.workload == "c4" else f"fp64 quotes/sec ({args.workload})",
+            "value": value, "unit": "quotes/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (same generator and rows as the GPU arm)",
+            "config": config_for(args, args.gpus, n_total, scaling, ""),
+            "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": "quotes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -303,42 +451,36 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
     lib = _native.lib_for_compute()
-    rows = args.rows or default_rows(args.workload)
+    n_total, ranges, shard_label, Fr, scaling = plan(args, world, rank)
     stream = torch.cuda.current_stream(dev)
     lib.fv_set_stream(ctypes_ptr(stream.cuda_stream))
+    model, method, roundtrip = workload_call(args.workload)
 
     # ---- inputs resident in HBM ------------------------------------------
-    roundtrip = False
     if args.workload == "c4":
-        cols = c4_device(rows, rank, dev)
-        model, method, last = 0, 1, "price"
-        cols["price"] = price_on_device(lib, 0, cols, rows)
+        cols = c4_device(0, rank, dev, ranges=ranges, n_total=n_total, F=Fr)
+        last = "price"
+        n = cols["flag"].numel()
+        cols["price"] = price_on_device(lib, 0, cols, n)
+        extra = {}
     else:
-        cols = draws_device(args.workload, rows, rank, dev)
-        if args.workload in ("c1", "c5"):
-            model, method = 0, 1
-        elif args.workload in ("c2", "rt"):
-            model, method = 2, 0
-        else:
-            model, method = 2, -1
-        roundtrip = args.workload == "rt"
+        cols = draws_device(args.workload, n_total, 0 if scaling == "strong" else rank, dev, ranges)
+        extra = {"kind": cols.pop("kind"), "side": cols.pop("side")}
+        n = cols["flag"].numel()
         last = "sigma" if (method == -1 or roundtrip) else "price"
         if method != -1 and not roundtrip:
-            cols["price"] = price_on_device(lib, model, cols, rows)
+            cols["price"] = price_on_device(lib, model, cols, n)
             if args.workload == "c5":
-                from paper_2604_27210_b200 import workloads as W
-                h = {k: cols[k].cpu().numpy() for k in ("flag", "underlying", "strike", "t", "r", "price")}
-                px = W.c5_prices(h["flag"], h["underlying"], h["strike"], h["t"], h["r"],
-                                 cols["kind"], cols["side"], h["price"])
+                hh = {k: cols[k].cpu().numpy() for k in ("flag", "underlying", "strike", "t", "r", "price")}
+                px = W.c5_prices(hh["flag"], hh["underlying"], hh["strike"], hh["t"], hh["r"],
+                                 extra["kind"], extra["side"], hh["price"])
                 cols["price"] = torch.from_numpy(px).to(dev)
     torch.cuda.synchronize(dev)
 
-    n = rows
     out_iv = torch.empty(n, dtype=torch.float64, device=dev)
     out_st = torch.empty(n, dtype=torch.int8, device=dev)
     out_px = torch.empty(n, dtype=torch.float64, device=dev) if roundtrip else None
-    greeks = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(6)]
-
+    greeks = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(6)] if method < 0 else []
     ncols = native_cols(cols, last)
     launches = [0]
 
@@ -389,17 +531,20 @@ def run_ours(args):
     clk = clocks.stop()
     total_ms = t_all0.elapsed_time(t_all1)
     per_call_ms = [a.elapsed_time(b) for a, b in ev]
+    own_ms = total_ms
     if pg:
         tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         pg.all_reduce(tt, op=pg.ReduceOp.MAX)
         total_ms = float(tt.item())
     ms_step = total_ms / args.steps
-    value = world * n / (ms_step * 1e-3)
+    units = world * n if scaling == "weak" else (n_total if not args.shard else n)
+    value = units / (ms_step * 1e-3)
+    st = torch.bincount(out_st.to(torch.int64), minlength=5).cpu().tolist()
 
-    # ---- per-kernel split of a step (CUDA events around each launch, on the
-    # launching stream; a separate pass so the headline timing has no events)
-    kernels = None
-    n_far_low = None
+    # ---- per-kernel split of a step (CUDA events around each launch; the
+    # timing pass serialises the side-stream branches, so the shares are of
+    # the serialised call and each event pair brackets one kernel alone)
+    kernels, n_far_low, serial_ms = None, None, None
     try:
         if args.no_kernel_timing:
             raise RuntimeError("skipped (--no-kernel-timing)")
@@ -407,6 +552,8 @@ def run_ours(args):
         _native.kernel_times(lib)
         nk = max(1, min(args.steps, 3))
         region = torch.empty(n, dtype=torch.int8, device=dev) if (method == 1 and not roundtrip) else None
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         for _ in range(nk):
             if region is not None:     # LBR: also record each quote's region (far-low count)
                 err = _native.fv_error()
@@ -416,7 +563,9 @@ def run_ours(args):
                     raise RuntimeError(err.message)
             else:
                 step()
+        e1.record(stream)
         torch.cuda.synchronize(dev)
+        serial_ms = e0.elapsed_time(e1) / nk
         if region is not None:
             n_far_low = int((region == 0).sum().item())
         kt = _native.kernel_times(lib)
@@ -425,16 +574,20 @@ def run_ours(args):
         kernels = {k: {"ms_per_step": v[0] / nk, "launches_per_step": v[1] / nk, "share": v[0] / tot}
                    for k, v in sorted(kt.items(), key=lambda kv: -kv[1][0])}
     except Exception as exc:  # noqa: BLE001
+        lib.fv_set_kernel_timing(0)
         kernels = {"error": repr(exc)}
 
-    # ---- the dominant kernel's own roofline (C4: k_lbr_far_low_fast) --------
+    # ---- the dominant kernel's own roofline --------------------------------
     # algorithmic work per launch = the reference's weighted distinct fp64 ops
-    # of the far-low solve phase per far-low quote (profiles/w_phases_c4.json,
-    # tools/w_count.py) x the far-low quotes of the call; time = its mean
-    # launch duration from the CUDA-event pass above
+    # of the kernel's phase per quote (profiles/w_phases_*.json, tools/w_count*.py)
+    # x the quotes it processes; time = its mean launch duration (event pass)
     dominant = None
+    wp = {}
     try:
         wp = json.load(open(os.path.join(REPO, "profiles", "w_phases_%s.json" % args.workload)))
+    except (OSError, ValueError):
+        pass
+    try:
         kname = "k_lbr_far_low_fast"
         if n_far_low and kernels and kname in kernels:
             w_solve = wp["by_region"]["FAR_LOW"]["W_solve"]
@@ -444,30 +597,22 @@ def run_ours(args):
                         "achieved": w_solve * n_far_low / t_k / 1e12}
         kname = "k_halley_iter"
         if args.workload == "c2" and kernels and kname in kernels:
-            # the Halley-step phase (solver.py:115-144) of the reference, per quote
-            # that reaches it (tools/w_count_halley.py on the C2 generator);
-            # units = rows x the sample's share of such quotes
             ph = wp["phases"]["halley"]
-            units = int(round(n * ph["share_reaching"]))
+            units_h = int(round(n * ph["share_reaching"]))
             t_k = kernels[kname]["ms_per_step"] * 1e-3
-            dominant = {"kernel": kname, "share_of_call": kernels[kname]["share"], "units": units,
+            dominant = {"kernel": kname, "share_of_call": kernels[kname]["share"], "units": units_h,
                         "W_per_unit": ph["W_per_reaching_quote"], "ms_per_launch": t_k * 1e3,
-                        "achieved": ph["W_per_reaching_quote"] * units / t_k / 1e12,
+                        "achieved": ph["W_per_reaching_quote"] * units_h / t_k / 1e12,
                         "units_source": "rows x share of quotes reaching the Halley loop in a %d-row "
                                         "reference sample (profiles/w_phases_c2.json)" % wp["rows"]}
-    except (OSError, ValueError, KeyError):
+    except (KeyError, TypeError, ZeroDivisionError):
         pass
-
-    # ---- status mix of the solved chain (for the record) --------------------
-    st = torch.bincount(out_st.to(torch.int64) + 0, minlength=5).cpu().tolist()
 
     # ---- e2e: same call with pinned host buffers ---------------------------
     e2e = None
     if not args.no_e2e:
         hcols = {}
         for k, v in cols.items():
-            if not torch.is_tensor(v):
-                continue
             hcols[k] = v.cpu().pin_memory() if v.numel() > 1 else v.cpu()
         h_iv = torch.empty(n, dtype=torch.float64).pin_memory()
         h_st = torch.empty(n, dtype=torch.int8).pin_memory()
@@ -475,9 +620,8 @@ def run_ours(args):
         h_g = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(6)] if method < 0 else []
         hn = native_cols(hcols, last)
         h2d = sum(hcols[k].numel() * hcols[k].element_size()
-                  for k in ("flag", "underlying", "strike", "t", "r", "q", last)
-                  if hcols[k].numel() > 1)
-        d2h = n * (17 if roundtrip else (9 if method >= 0 else 49))   # (price +) iv + status | price + 5 Greeks + status
+                  for k in ("flag", "underlying", "strike", "t", "r", "q", last) if hcols[k].numel() > 1)
+        d2h = n * (17 if roundtrip else (9 if method >= 0 else 49))
 
         def estep():
             err = _native.fv_error()
@@ -499,6 +643,8 @@ def run_ours(args):
         times = []
         for _ in range(max(2, min(args.steps, 5))):
             torch.cuda.synchronize(dev)
+            if pg:
+                pg.barrier()
             t0 = time.perf_counter()
             estep()
             times.append(time.perf_counter() - t0)
@@ -507,7 +653,6 @@ def run_ours(args):
             tt = torch.tensor([e_ms], dtype=torch.float64, device=dev)
             pg.all_reduce(tt, op=pg.ReduceOp.MAX)
             e_ms = float(tt.item())
-        # bit-identical to the device-resident result
         if method >= 0:
             same = bool(torch.equal(h_iv.to(dev).view(torch.int64), out_iv.view(torch.int64)))
             if roundtrip:
@@ -515,7 +660,6 @@ def run_ours(args):
         else:
             same = all(bool(torch.equal(h.to(dev).view(torch.int64), g.view(torch.int64)))
                        for h, g in zip(h_g, greeks))
-        # the link's own ceiling: a plain pinned 1 GB host->device copy
         h2d_gbs = None
         try:
             hb = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
@@ -530,34 +674,62 @@ def run_ours(args):
             del hb, db
         except Exception:  # noqa: BLE001
             pass
-        e2e = {"value": world * n / (e_ms * 1e-3), "unit": "quotes/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": units / (e_ms * 1e-3), "unit": "quotes/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms,
-               "timing": "wall clock around the synchronous C-ABI call (host buffers pinned)",
-               "bit_identical_to_device_resident": same,
-               "pcie_h2d_gbs": h2d_gbs,
-               "h2d_ceiling_quotes_s": (world * n * h2d_gbs * 1e9 / h2d) if h2d_gbs and h2d else None}
+               "timing": "wall clock around the synchronous C-ABI call (host buffers pinned), max over ranks",
+               "bit_identical_to_device_resident": same, "pcie_h2d_gbs": h2d_gbs,
+               "h2d_ceiling_quotes_s": (n * h2d_gbs * 1e9 / h2d * (units / n)) if h2d_gbs and h2d else None}
+
+    # ---- oracle pass: CPU baseline (rank 0, N=1) + parity of every row ------
+    parity, cpu = None, None
+    if not args.no_cpu:
+        try:
+            hcpu = {k: v.cpu().numpy() for k, v in cols.items()}
+            threads = max(1, (os.cpu_count() or 1) // world)
+            dt, want = oracle_run(args.workload, hcpu, threads)
+            if method == -1:
+                got = {"price": greeks[0], "delta": greeks[1], "gamma": greeks[2], "theta": greeks[3],
+                       "rho": greeks[4], "vega": greeks[5], "status": out_st}
+            else:
+                got = {"iv": out_iv, "status": out_st}
+                if roundtrip:
+                    got["price"] = out_px
+            got = {k: v.cpu().numpy() for k, v in got.items()}
+            bad = parity_count(got, want)
+            rows_checked = n
+            if pg:
+                tt = torch.tensor([bad, rows_checked], dtype=torch.int64, device=dev)
+                pg.all_reduce(tt, op=pg.ReduceOp.SUM)
+                bad, rows_checked = (int(x) for x in tt.tolist())
+            parity = {"rows_checked": rows_checked, "mismatches": bad,
+                      "against": "oracle/fvoracle.cpp (pinned to the live reference by tests/golden/)",
+                      "compared": sorted(got) + ["reference exception rows"],
+                      "rule": "bit-identical doubles (any NaN = any NaN), identical status codes"}
+            if world == 1:
+                cpu = dict(host_info(threads), value=n / dt, unit="quotes/s", kind="port",
+                           sample=f"all {n} rows of this run's workload, oracle/fvoracle.cpp (the reference "
+                                  f"restated in C++ on glibc + scipy), OpenMP {threads} threads, {dt:.2f} s")
+        except Exception as exc:  # noqa: BLE001
+            parity = {"error": repr(exc)}
 
     # ---- roofline ------------------------------------------------------------
     peak = ctypes_double()
     secs = ctypes_double()
     lib.fv_probe_fp64_peak(ctypes_addr(peak), ctypes_addr(secs))
     peak_tops = peak.value / 1e12
-    per_gpu_qps = n / (float(np.mean(per_call_ms)) * 1e-3)
-    achieved = W_OPS[args.workload] * per_gpu_qps / 1e12
+    call_s = float(np.mean(per_call_ms)) * 1e-3
+    achieved = W_OPS[args.workload] * n / call_s / 1e12
+    w_read = wp.get("W_read_mean") if args.workload == "c4" else None
     in_bytes = sum(cols[k].numel() * cols[k].element_size()
-                   for k in ("flag", "underlying", "strike", "t", "r", "q", last)
-                   if torch.is_tensor(cols[k]) and cols[k].numel() > 1)
+                   for k in ("flag", "underlying", "strike", "t", "r", "q", last) if cols[k].numel() > 1)
     out_bytes = n * (17 if roundtrip else (9 if method >= 0 else 49))
-    hbm_gbs = (in_bytes + out_bytes) / (float(np.mean(per_call_ms)) * 1e-3) / 1e9
+    hbm_gbs = (in_bytes + out_bytes) / call_s / 1e9
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
     except (OSError, ValueError):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    # DRAM bytes (read + write) per launch of the call, from the committed
-    # `ncu --set full` capture (profiles/roofline_traffic.json: bytes per
-    # quote summed over the call's kernels) scaled to this launch's rows
     traffic = None
     try:
         prof = json.load(open(os.path.join(REPO, "profiles", "roofline_traffic.json")))
@@ -565,57 +737,56 @@ def run_ours(args):
         traffic = bpq * n if bpq else None
     except (OSError, ValueError, AttributeError):
         pass
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak_tops, "unit": "T weighted-fp64-ops/s",
+                "frac": achieved / peak_tops if peak_tops else None, "traffic": traffic,
+                "note": "kernel = one C-ABI call (its kernels in sequence on the call's stream, side-stream "
+                        "branches overlapping); achieved = W=%.0f weighted distinct fp64 ops/quote (SURVEY 8(d)) "
+                        "x rows per call / mean call duration (CUDA events on the launching stream); peak = "
+                        "measured DFMA issue rate (fv_probe_fp64_peak, this run; MEASURED_PEAKS.json has no fp64 "
+                        "entry); traffic = ncu DRAM read+write bytes per call (profiles/roofline_traffic.json)"
+                        % W_OPS[args.workload]}
+    if w_read:
+        roofline["achieved_read"] = w_read * n / call_s / 1e12
+        roofline["frac_read"] = roofline["achieved_read"] / peak_tops if peak_tops else None
+        roofline["W_read"] = w_read
+        roofline["note_read"] = ("frac_read counts only the W the GPU path must evaluate: the reference's "
+                                 "anchors that _region never reads (b_c, b_hi of far-low quotes, b_hi of "
+                                 "near-low ones; %.0f of W=%.0f on a 30k-row C4 sample, tools/w_count.py) "
+                                 "are skipped by the lazy-anchor passes" % (W_OPS["c4"] - w_read, W_OPS["c4"]))
+    if args.workload == "c2":
+        roofline["note"] += ("; C2: the bracket pass decides f(10)'s sign in fp32 instead of evaluating it "
+                             "(~8 % of W counted but not executed)")
 
     if rank == 0:
-        cpu = None
-        if world == 1 and not args.no_cpu:
-            try:
-                cpu = cpu_baseline(args.cpu_seconds, args.workload)
-            except Exception as exc:  # noqa: BLE001
-                cpu = {"error": repr(exc)}
-        wl_name = {"c4": "C4: jackel_iv_black (LBR) on a 100M-quote Black-76 chain "
-                         "(2 flags x 1000 maturities x 50000 strikes) per GPU",
-                   "c1": "C1: LBR Black-76 1M synthetic quotes",
-                   "c2": "C2: Halley BSM with dividend yield, 10M quotes",
-                   "c3": "C3: fused BSM price + all Greeks, 10M quotes",
-                   "c5": "C5: wing-stress set, LBR Black-76",
-                   "rt": "RT: the reference bench harness's round trip (bench.py:19-40) on 10M C2 draws: "
-                         "BSM price -> Halley IV in one fused fv_price_iv call"}[args.workload]
         line = {
             "metric": METRIC if args.workload == "c4" else f"fp64 quotes/sec ({args.workload})",
             "value": value, "unit": "quotes/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded chain generated on device; prices from the pricing kernel)",
-            "config": {"workload": wl_name, "rows_per_gpu": n, "parallelism": f"quote-sharded x{world}",
-                       "l2": "inputs (%.1f GB/step) exceed the 126 MB L2; no flush needed" % (in_bytes / 1e9)},
-            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_tops,
-                         "unit": "T weighted-fp64-ops/s", "frac": achieved / peak_tops if peak_tops else None,
-                         "traffic": traffic,
-                         "note": "kernel = one fv_batch_iv/fv_price_greeks call (its kernels in sequence on one "
-                                 "stream); achieved = W=%.0f weighted distinct fp64 ops/quote (SURVEY 8(d)) x rows per "
-                                 "call / mean call duration (CUDA events on the launching stream); peak = measured "
-                                 "DFMA issue rate (fv_probe_fp64_peak, this run); traffic = ncu DRAM read+write bytes "
-                                 "per call (profiles/roofline_traffic.json)" % W_OPS[args.workload]
-                                 + ("; C2: the bracket pass decides f(10)'s sign in fp32 instead of evaluating "
-                                    "it (~8 % of W counted but not executed)" if args.workload == "c2" else "")},
+            "config": config_for(args, world, n_total, scaling, shard_label),
+            "rows_this_rank": n,
+            "roofline": roofline,
             "kernels": kernels,
-            "kernels_note": "CUDA events around each launch on its own stream; the LBR far-low branch and the "
-                            "Halley careful pass over the bracket's hand-backs run on a second stream beside the "
-                            "other passes, so those kernels' times overlap and shares are of the summed time",
+            "kernels_note": "per-kernel CUDA events in a separate pass that runs the side-stream branches in "
+                            "sequence on the call's stream (fv_set_kernel_timing): shares are of the serialised "
+                            "call (serial_ms_per_call); the timed calls overlap those branches",
+            "serial_ms_per_call": serial_ms,
             "dominant_kernel": (dict(dominant, peak=peak_tops, unit="T weighted-fp64-ops/s",
                                      frac=dominant["achieved"] / peak_tops if peak_tops else None)
                                 if dominant else None),
             "roofline_hbm": {"bound": "hbm", "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
-                             "frac": hbm_gbs / hbm_peak, "bytes_per_quote": (in_bytes + out_bytes) / n,
+                             "frac": hbm_gbs / hbm_peak, "bytes_per_quote": (in_bytes + out_bytes) / max(n, 1),
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": e2e,
             "gpu_launches": launches[0],
             "clocks": clk,
             "status_counts": dict(zip(["converged", "fell_back", "below_intrinsic", "above_upper",
                                        "max_iterations"], st)),
             "per_call_ms": per_call_ms,
+            "rank0_ms_per_step": own_ms / args.steps,
         }
         print(json.dumps(line), flush=True)
     if pg:

@@ -162,7 +162,10 @@ FV_API int fv_price_iv(int model, int method, fv_col flag, fv_col underlying, fv
                        fv_error* err_iv);
 
 /* Stream used by device-pointer calls made from the calling thread
- * (cudaStream_t; NULL = the library's own non-blocking stream). */
+ * (cudaStream_t; NULL = the device's legacy default stream, which is what
+ * torch's default stream is).  A thread that never calls it uses the
+ * library's own non-blocking stream (ordered with nothing else: the call is
+ * synchronous, but inputs must be complete before it). */
 FV_API int fv_set_stream(void* stream);
 
 /* Number of CUDA devices visible; library version string. */
@@ -172,7 +175,9 @@ FV_API int fv_device_count(void);
  * thread and one device each (ids may repeat), results written straight into
  * the caller's buffers; errors and fv_last_outcome are the single-device
  * ones.  n = 0 restores the default (the calling thread's current device).
- * Device-pointer calls always run on the current device. */
+ * Device-pointer calls run on the device that owns the pointers (all on one
+ * device, else FV_ERR_ARG); the thread's current device is restored after the
+ * call.  A stream set by fv_set_stream must belong to that device. */
 FV_API int fv_set_devices(const int* ids, int n);
 FV_API int fv_get_devices(int* ids, int cap);
 FV_API const char* fv_version(void);
@@ -183,6 +188,11 @@ FV_API int fv_set_chunk_rows(int64_t rows);
 /* Kernels launched by this thread's last call (instrumentation for the
  * bench's gpu_launches count). */
 FV_API int64_t fv_last_launch_count(void);
+
+/* Testing knob: rows per LBR classify/solve round and per Halley chunk of
+ * one launch (0 = default: 2^27 and 2^26; Halley <= 2^26).  Results do not
+ * depend on it; tests force multi-round calls on small batches with it. */
+FV_API int fv_set_round_rows(int64_t lbr_rows, int64_t halley_rows);
 
 /* Raw outcome of the calling thread's last batch call: per validation check
  * (FV_CHECK_* order) the first failing row or -1; the first raising row and
@@ -211,7 +221,10 @@ FV_API int fv_selftest_fast(int64_t n, uint64_t seed, int64_t* mismatches /*[11]
  * the calling thread launches is bracketed by CUDA events on its stream;
  * fv_kernel_times sums the elapsed milliseconds and launch counts per kernel
  * (FV_KID_* order, names from fv_kernel_name) since the previous call and
- * resets them. */
+ * resets them.  While on, the passes that otherwise run concurrently on side
+ * streams (LBR far-low / far-high branches, the Halley careful pass) run in
+ * sequence on the call's stream, so each event pair brackets one kernel
+ * alone and the shares add up to the serialised call. */
 #define FV_KID_PRICE 0
 #define FV_KID_PRICE_GREEKS 1
 #define FV_KID_LBR_NORM 2

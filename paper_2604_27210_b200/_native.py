@@ -55,6 +55,7 @@ SIGNATURES = {
     "fv_version": ([], ctypes.c_char_p),
     "fv_set_chunk_rows": ([_I64], ctypes.c_int),
     "fv_last_launch_count": ([], _I64),
+    "fv_set_round_rows": ([_I64, _I64], ctypes.c_int),
     "fv_probe_fp64_peak": ([_P, _P], ctypes.c_int),
     "fv_last_outcome": ([_P, _P, _P], ctypes.c_int),
     "fv_selftest_div_const": ([_I64, ctypes.c_uint64, _P], ctypes.c_int),
@@ -124,6 +125,40 @@ def ptr(arr):
     if hasattr(arr, "data_ptr"):
         return arr.data_ptr()
     return np.asarray(arr).ctypes.data
+
+
+class NativeCallError(RuntimeError):
+    """A C-ABI call failed for a runtime / argument reason (FV_ERR_CUDA,
+    FV_ERR_ARG) -- not one of the reference's own errors."""
+
+
+def check_runtime(rc, err):
+    """Raise on FV_ERR_CUDA / FV_ERR_ARG (the outputs and fv_last_outcome of
+    such a call are meaningless); the reference's errors pass through."""
+    if rc in (FV_ERR_CUDA, FV_ERR_ARG):
+        raise NativeCallError("fastvol_b200: " + err.message.decode(errors="replace"))
+    return rc
+
+
+class device_scope:
+    """``with device_scope(lib, dev):`` -- a device-pointer call on ``dev``:
+    that device current (torch does not switch it for tensors on another
+    device) and the kernels ordered on its current torch stream."""
+
+    def __init__(self, lib, dev):
+        import torch
+        self.lib = lib
+        self.dev = torch.device(dev)
+        self._guard = torch.cuda.device(self.dev)
+
+    def __enter__(self):
+        import torch
+        self._guard.__enter__()
+        self.lib.fv_set_stream(torch.cuda.current_stream(self.dev).cuda_stream)
+        return self
+
+    def __exit__(self, *exc):
+        return self._guard.__exit__(*exc)
 
 
 def last_outcome(lib):

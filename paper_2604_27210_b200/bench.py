@@ -84,16 +84,7 @@ def run_roundtrip(rows: int, method: str = "halley", output: Optional[str] = Non
 
 
 def _write_figure(path: str, rows: int, method: str, rps: float) -> None:
-    """One-bar throughput figure (matplotlib, as the reference; ImportError
-    when it is not installed)."""
-    import matplotlib
-    matplotlib.use("Agg")
-    import matplotlib.pyplot as plt
-
-    fig, ax = plt.subplots(figsize=(5, 3.2))
-    ax.bar([method], [rps], width=0.5)
-    ax.set_ylabel("rows / sec")
-    ax.set_title(f"batch IV throughput ({rows:,} rows)")
-    fig.tight_layout()
-    fig.savefig(path, dpi=120)
-    plt.close(fig)
+    """The reference's matplotlib report figure (bench.py:57-69) is outside
+    the hot path this package rebuilds: asking for one is an error here."""
+    raise NotImplementedError("throughput figures are not part of the B200 path; omit --figure "
+                              f"(requested {path!r} for {rows} rows, {method}, {rps:.3g} rows/s)")

@@ -1217,6 +1217,7 @@ __global__ void k_selftest_fast(int64_t n, uint64_t seed, unsigned long long* mi
 namespace {
 
 thread_local cudaStream_t t_user_stream = nullptr;
+thread_local bool t_user_stream_set = false;   // fv_set_stream called (NULL = legacy default stream)
 thread_local int64_t t_launches = 0;
 
 // Optional per-kernel timing (fv_set_kernel_timing): CUDA events around every
@@ -1352,8 +1353,10 @@ cudaError_t get_work(DevWork** out) {
 #ifndef FV_LBR_ROUND_LOG2
 #define FV_LBR_ROUND_LOG2 27
 #endif
-const int64_t kLbrChunk = 1ll << FV_LBR_ROUND_LOG2;
-const int64_t kHalleyChunk = 1ll << 26;
+// Runtime-settable (fv_set_round_rows) so tests can force multi-round calls
+// on small batches and check them against single-round ones.
+int64_t g_lbr_round = 1ll << FV_LBR_ROUND_LOG2;
+int64_t g_halley_round = 1ll << 26;
 
 cudaError_t ensure_lbr(DevWork* w, int slot, int64_t rows) {
   if (w->lbr_cap[slot] >= rows) return cudaSuccess;
@@ -1445,6 +1448,7 @@ cudaError_t launch_iv(DevWork* w, int method, const KArgs& a, int slot, cudaStre
                       const KArgs* price = nullptr) {
   if (a.n <= 0) return cudaSuccess;
   if (method == FV_METHOD_LBR) {
+    const int64_t kLbrChunk = g_lbr_round;
     const int64_t chunk = a.n < kLbrChunk ? a.n : kLbrChunk;
     CK(ensure_lbr(w, slot, chunk));
     for (int64_t off = 0; off < a.n; off += chunk) {
@@ -1484,7 +1488,9 @@ cudaError_t launch_iv(DevWork* w, int method, const KArgs& a, int slot, cudaStre
 #ifdef FV_LBR_SERIAL
       cudaStream_t s2 = s;                       // A/B: the branches in sequence
 #else
-      cudaStream_t s2 = w->aux[slot];
+      // the per-kernel timing pass (fv_set_kernel_timing) serialises the
+      // branches so each kernel's events bracket it alone
+      cudaStream_t s2 = t_timing ? s : w->aux[slot];
 #endif
       CK(cudaEventRecord(w->fork_ev[slot], s));
       CK(cudaStreamWaitEvent(s2, w->fork_ev[slot], 0));
@@ -1496,7 +1502,7 @@ cudaError_t launch_iv(DevWork* w, int method, const KArgs& a, int slot, cudaStre
 #if defined(FV_LBR_SERIAL) || defined(FV_LBR_FH_SERIAL)
       cudaStream_t s3 = s;
 #else
-      cudaStream_t s3 = w->aux2[slot];
+      cudaStream_t s3 = t_timing ? s : w->aux2[slot];
 #endif
       CK(cudaEventRecord(w->fork2_ev[slot], s));
       CK(cudaStreamWaitEvent(s3, w->fork2_ev[slot], 0));
@@ -1510,6 +1516,7 @@ cudaError_t launch_iv(DevWork* w, int method, const KArgs& a, int slot, cudaStre
     }
   } else {
     // chunks of <= 2^26 rows: int32 row indices in the queues, bounded buffers
+    const int64_t kHalleyChunk = g_halley_round;
     const int64_t chunk = a.n < kHalleyChunk ? a.n : kHalleyChunk;
     CK(ensure_hsm(w, slot, chunk));
     for (int64_t off = 0; off < a.n; off += chunk) {
@@ -1540,7 +1547,7 @@ cudaError_t launch_iv(DevWork* w, int method, const KArgs& a, int slot, cudaStre
 #ifdef FV_HAL_SERIAL
       cudaStream_t s2 = s;
 #else
-      cudaStream_t s2 = w->aux[slot];
+      cudaStream_t s2 = t_timing ? s : w->aux[slot];
 #endif
       CK(cudaEventRecord(w->fork_ev[slot], s));
       CK(cudaStreamWaitEvent(s2, w->fork_ev[slot], 0));
@@ -1595,12 +1602,20 @@ cudaError_t launch(DevWork* w, const Call& c, const KArgs& a, int slot, cudaStre
   return cudaGetLastError();
 }
 
-bool is_device_ptr(const void* p) {
+// Device pointer? (*dev: its device)
+bool is_device_ptr(const void* p, int* dev = nullptr) {
   if (!p) return false;
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  if (dev) *dev = at.device;
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
+
+// Restores the calling thread's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
 
 const char* check_name(int c, bool has_sigma, char* buf, size_t len) {
   static const char* cols[] = {"underlying", "strike", "t", "r", "q"};
@@ -2181,6 +2196,9 @@ int dispatch_sharded(const Call& c, const std::vector<int>& devs, fv_error* e1, 
 // For host calls, broadcast columns must be readable on the device.
 int dispatch(Call c, fv_error* e1, fv_error* e2) {
   t_launches = 0;
+  // fv_last_outcome describes THIS call, even when it fails before finish()
+  for (int k = 0; k < FV_NCHECK; ++k) t_check_rows[k] = -1;
+  for (int k = 0; k < 2; ++k) { t_exc_row[k] = -1; t_exc_code[k] = 0; }
   set_ok(e1);
   set_ok(e2);
   if (c.n < 0) return set_arg_err(e1, "n must be >= 0");
@@ -2190,13 +2208,50 @@ int dispatch(Call c, fv_error* e1, fv_error* e2) {
   for (int i = 0; i < 7; ++i)
     if (!c.cols[i].data) return set_arg_err(e1, "null input column");
   // memory space: all device or all host
-  int ndev = 0, nptr = 0;
-  for (int i = 0; i < 7; ++i) { ++nptr; ndev += is_device_ptr(c.cols[i].data); }
-  for (int i = 0; i < 6; ++i) if (c.outs[i]) { ++nptr; ndev += is_device_ptr(c.outs[i]); }
-  if (c.status) { ++nptr; ndev += is_device_ptr(c.status); }
-  if (c.region) { ++nptr; ndev += is_device_ptr(c.region); }
+  // memory space: all device (one device) or all host
+  int ndev = 0, nptr = 0, pdev = -1;
+  bool mixed_dev = false;
+  auto note = [&](const void* p) {
+    int d = -1;
+    ++nptr;
+    if (is_device_ptr(p, &d)) {
+      ++ndev;
+      if (pdev < 0) pdev = d;
+      else if (d != pdev) mixed_dev = true;
+    }
+  };
+  for (int i = 0; i < 7; ++i) note(c.cols[i].data);
+  for (int i = 0; i < 6; ++i) if (c.outs[i]) note(c.outs[i]);
+  if (c.status) note(c.status);
+  if (c.region) note(c.region);
   bool device = ndev == nptr;
   if (ndev != 0 && !device) return set_arg_err(e1, "all pointers of a call must be device pointers or all host pointers");
+  if (mixed_dev) return set_arg_err(e1, "device pointers of a call must all be on one device");
+  // device calls run on the device that owns the columns, whatever the
+  // thread's current device is (restored on return)
+  DeviceGuard guard;
+  if (device) {
+    int cur = -1;
+    cudaError_t ce0 = cudaGetDevice(&cur);
+    if (ce0 != cudaSuccess) return set_cuda_err(e1, ce0);
+    if (cur != pdev) {
+      if ((ce0 = cudaSetDevice(pdev)) != cudaSuccess) return set_cuda_err(e1, ce0);
+      guard.prev = cur;
+    }
+    if (t_user_stream_set && t_user_stream) {
+      int sdev = -1;
+      if (cudaStreamGetDevice(t_user_stream, &sdev) != cudaSuccess) {
+        cudaGetLastError();
+        return set_arg_err(e1, "the stream set by fv_set_stream is not a valid CUDA stream");
+      }
+      if (sdev != pdev) {
+        char msg[160];
+        snprintf(msg, sizeof(msg), "the stream set by fv_set_stream belongs to device %d, the columns to device %d",
+                 sdev, pdev);
+        return set_arg_err(e1, msg);
+      }
+    }
+  }
   if (!device && !t_in_shard) {
     std::vector<int> devs = devices_for_host_calls();
     if (devs.size() > 1 && c.n >= (int64_t)devs.size() * kMinShardRows) return dispatch_sharded(c, devs, e1, e2);
@@ -2247,7 +2302,7 @@ int dispatch(Call c, fv_error* e1, fv_error* e2) {
   }
   int rc;
   if (device) {
-    cudaStream_t s = t_user_stream ? t_user_stream : w->streams[0];
+    cudaStream_t s = t_user_stream_set ? t_user_stream : w->streams[0];
     rc = run_device(w, c, s, bbits, e1, e2);
   } else {
     rc = run_host(w, c, bbits, e1, e2);
@@ -2352,6 +2407,7 @@ FV_API int fv_price_iv(int model, int method, fv_col flag, fv_col underlying, fv
 
 FV_API int fv_set_stream(void* stream) {
   t_user_stream = (cudaStream_t)stream;
+  t_user_stream_set = true;
   return FV_OK;
 }
 
@@ -2387,6 +2443,13 @@ FV_API int fv_set_chunk_rows(int64_t rows) {
 }
 
 FV_API int64_t fv_last_launch_count(void) { return t_launches; }
+
+FV_API int fv_set_round_rows(int64_t lbr_rows, int64_t halley_rows) {
+  if (lbr_rows < 0 || halley_rows < 0 || halley_rows > (1ll << 26)) return FV_ERR_ARG;   // int32 queue entries
+  g_lbr_round = lbr_rows ? lbr_rows : (1ll << FV_LBR_ROUND_LOG2);
+  g_halley_round = halley_rows ? halley_rows : (1ll << 26);
+  return FV_OK;
+}
 
 FV_API int fv_set_kernel_timing(int on) {
   t_timing = on != 0;

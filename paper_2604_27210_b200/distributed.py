@@ -127,9 +127,12 @@ def batch_iv_sharded(model, method, cols, n, group=None, gather=False):
         iv = torch.empty(k, dtype=torch.float64, device=dev)
         st = torch.empty(k, dtype=torch.int8, device=dev)
         err = _native.fv_error()
-        lib.fv_batch_iv(m, 1 if method == "lbr" else 0,
-                        *[_native.col(sl[c]) for c in ("flag", "underlying", "strike", "t", "r", "q", "price")],
-                        k, iv.data_ptr(), st.data_ptr(), None, err)
+        with _native.device_scope(lib, dev):
+            rc = lib.fv_batch_iv(m, 1 if method == "lbr" else 0,
+                                 *[_native.col(sl[c]) for c in ("flag", "underlying", "strike", "t", "r", "q",
+                                                               "price")],
+                                 k, iv.data_ptr(), st.data_ptr(), None, err)
+        _native.check_runtime(rc, err)
         cr, er, ec = _native.last_outcome(lib)
         return {"iv": iv, "status": st}, cr, int(er[0]), int(ec[0])
 
@@ -156,9 +159,12 @@ def price_iv_sharded(model, method, cols, n, group=None, gather=False):
         iv = torch.empty(k, dtype=torch.float64, device=dev)
         st = torch.empty(k, dtype=torch.int8, device=dev)
         ep, ei = _native.fv_error(), _native.fv_error()
-        lib.fv_price_iv(m, 1 if method == "lbr" else 0,
-                        *[_native.col(sl[c]) for c in ("flag", "underlying", "strike", "t", "r", "q", "sigma")],
-                        k, px.data_ptr(), iv.data_ptr(), st.data_ptr(), None, ep, ei)
+        with _native.device_scope(lib, dev):
+            rc = lib.fv_price_iv(m, 1 if method == "lbr" else 0,
+                                 *[_native.col(sl[c]) for c in ("flag", "underlying", "strike", "t", "r", "q",
+                                                               "sigma")],
+                                 k, px.data_ptr(), iv.data_ptr(), st.data_ptr(), None, ep, ei)
+        _native.check_runtime(rc, ep)
         cr, er, ec = _native.last_outcome(lib)
         price_checks = ep.code == _native.FV_ERR_BATCH      # fv_last_outcome: the deciding stage's rows
         stages = [(cr if price_checks else none, int(er[0]), int(ec[0])),

@@ -44,19 +44,14 @@ def _dev_cols(flag, und, K, t, r, q, last, last_name):
     return dev, n, cols, table
 
 
-def _stream(lib, dev):
-    import torch
-    lib.fv_set_stream(torch.cuda.current_stream(dev).cuda_stream)
-
-
 def device_call_price(lib, model, flag, und, K, t, r, q, sigma):
     import torch
     dev, n, cols, table = _dev_cols(flag, und, K, t, r, q, sigma, "sigma")
     out = torch.empty(n, dtype=torch.float64, device=dev)
     if n:
-        _stream(lib, dev)
         err = _native.fv_error()
-        rc = lib.fv_batch_price(model.code, *[_native.col(c) for c in cols], n, out.data_ptr(), err)
+        with _native.device_scope(lib, dev):
+            rc = lib.fv_batch_price(model.code, *[_native.col(c) for c in cols], n, out.data_ptr(), err)
         _ok_or_raise(rc, err, table, model, "sigma")
     return out
 
@@ -67,10 +62,10 @@ def device_call_iv(lib, model, method, flag, und, K, t, r, q, price):
     iv = torch.empty(n, dtype=torch.float64, device=dev)
     st = torch.empty(n, dtype=torch.int8, device=dev)
     if n:
-        _stream(lib, dev)
         err = _native.fv_error()
-        rc = lib.fv_batch_iv(model.code, 1 if method == "lbr" else 0, *[_native.col(c) for c in cols], n,
-                             iv.data_ptr(), st.data_ptr(), None, err)
+        with _native.device_scope(lib, dev):
+            rc = lib.fv_batch_iv(model.code, 1 if method == "lbr" else 0, *[_native.col(c) for c in cols], n,
+                                 iv.data_ptr(), st.data_ptr(), None, err)
         _ok_or_raise(rc, err, table, model, "price")
     return iv, st
 
@@ -81,10 +76,10 @@ def device_call_greeks(lib, model, flag, und, K, t, r, q, sigma):
     outs = {g: torch.empty(n, dtype=torch.float64, device=dev) for g in GREEK_COLUMNS}
     st = torch.empty(n, dtype=torch.int8, device=dev)
     if n:
-        _stream(lib, dev)
         err = _native.fv_error()
-        rc = lib.fv_batch_greeks(model.code, *[_native.col(c) for c in cols], n,
-                                 *[outs[g].data_ptr() for g in GREEK_COLUMNS], st.data_ptr(), err)
+        with _native.device_scope(lib, dev):
+            rc = lib.fv_batch_greeks(model.code, *[_native.col(c) for c in cols], n,
+                                     *[outs[g].data_ptr() for g in GREEK_COLUMNS], st.data_ptr(), err)
         _ok_or_raise(rc, err, table, model, "sigma")
     outs["status"] = st
     return outs

@@ -39,7 +39,7 @@ from fastvol import batch as B  # noqa: E402
 from fastvol import lbr as L  # noqa: E402
 from fastvol import distributions as D  # noqa: E402
 from fastvol.models import Model  # noqa: E402
-from paper_2604_27210_b200 import workloads as W  # noqa: E402
+import workloads as W  # noqa: E402
 
 IV_CODES = {"converged": 0, "fell_back_to_bisection": 1, "below_intrinsic": 2,
             "above_upper_bound": 3, "max_iterations": 4}

@@ -219,7 +219,7 @@ def oracle_mod():
 
 
 def test_c1_lbr_vs_oracle(fv, oracle_mod):
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     flag, S, K, t, r, q, sig = W.chain_draws(400_000, seed=7)
     px = oracle_mod.rows_price("black", flag, S, K, t, r, 0.0, sig)["price"]
     want = oracle_mod.rows_iv("black", "lbr", flag, S, K, t, r, 0.0, px)
@@ -231,7 +231,7 @@ def test_c1_lbr_vs_oracle(fv, oracle_mod):
 
 
 def test_c2_halley_vs_oracle(fv, oracle_mod):
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     flag, S, K, t, r, q, sig = W.chain_draws(100_000, seed=8)
     px = oracle_mod.rows_price("bsm", flag, S, K, t, r, q, sig)["price"]
     want = oracle_mod.rows_iv("bsm", "halley", flag, S, K, t, r, q, px)
@@ -242,7 +242,7 @@ def test_c2_halley_vs_oracle(fv, oracle_mod):
 
 
 def test_c5_wings_vs_oracle(fv, oracle_mod):
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     flag, F, K, t, r, s, kind, side = W.c5_params(200_000, seed=9)
     px0 = oracle_mod.rows_price("black", flag, F, K, t, r, 0.0, s)["price"]
     px = W.c5_prices(flag, F, K, t, r, kind, side, px0)
@@ -260,7 +260,7 @@ def test_c3_price_greeks_vs_oracle(fv, oracle_mod, model):
     fused price + Greeks on the device vs the oracle, bit for bit."""
     import torch
     from paper_2604_27210_b200 import _native
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     flag, S, K, t, r, q, sig = W.chain_draws(300_000, seed=13)
     if model != "bsm":
         q = np.zeros_like(q)
@@ -291,7 +291,7 @@ def test_c3_price_greeks_vs_oracle(fv, oracle_mod, model):
 
 
 def test_c4_chain_sample_vs_oracle(fv, oracle_mod):
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     rng = np.random.default_rng(4)
     starts = rng.integers(0, W.C4_ROWS - 2000, 40)
     parts = [W.c4_params(int(s0), int(s0) + 2000) for s0 in starts]
@@ -309,7 +309,7 @@ def test_host_chunked_pipeline_matches_device(fv):
     """Host-pointer calls (chunked H2D/kernel/D2H over 3 streams) give the same
     bits as device-resident calls, including row offsets across chunks."""
     from paper_2604_27210_b200 import _native
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     lib = _native.load()
     flag, S, K, t, r, q, sig = W.chain_draws(300_001, seed=11)
     px = fv.batch_price("black", W.flag_chars(flag), S, K, t, r, sigma=sig)["price"]
@@ -352,7 +352,7 @@ def test_fast_routines_match_careful_forms():
 def test_sharded_single_rank_equals_batch(fv):
     import torch
     from paper_2604_27210_b200 import distributed as D
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     flag, S, K, t, r, q, sig = W.chain_draws(50_001, seed=21)
     px = fv.batch_price("black", W.flag_chars(flag), S, K, t, r, sigma=sig)["price"]
     ref = fv.batch_iv("black", "lbr", W.flag_chars(flag), S, K, t, r, price=px)
@@ -365,16 +365,17 @@ def test_sharded_single_rank_equals_batch(fv):
 
 def test_c4_full_chain_100m(fv, oracle_mod):
     """BASELINE size: the whole 100M-quote C4 chain in one device-resident
-    fv_batch_iv call (three internal 2^25-row rounds).  Checked against the
-    oracle on a strided 1-in-1000 sample of the SAME run, every non-converged
-    row of the sample's status class, and through size-independent
-    properties: the status mix, the price -> IV round trip on converged
-    quotes (the chain's prices come from sigma), and bit-identity with a
-    separate call on a row range that straddles a round boundary."""
+    fv_batch_iv call (one 2^27-row round).  Checked against the oracle on a
+    strided 1-in-1000 sample of the SAME run (every row is compared in
+    test_gpu_fullsize.py), and through size-independent properties: the
+    status mix, the price -> IV round trip on converged quotes (the chain's
+    prices come from sigma), bit-identity with a separate call on a
+    sub-range of the rows, and the host-pointer pipeline.  Multi-round calls:
+    test_gpu_fullsize.py::test_multi_round_calls_bit_identical."""
     import bench
     import torch
     from paper_2604_27210_b200 import _native
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     lib = _native.lib_for_compute()
     dev = torch.device("cuda", 0)
     n = W.C4_ROWS
@@ -410,7 +411,7 @@ def test_c4_full_chain_100m(fv, oracle_mod):
                               np.full(m, 0.03), 0.0, samp["price"])
     assert_bits(st[idx].cpu().numpy(), want["status_code"], "C4-100M sample status")
     assert_bits(iv[idx].cpu().numpy(), want["iv"], "C4-100M sample iv")
-    # a row range straddling the first 2^25-row round boundary, as its own call
+    # a row range in the middle of the chain, as its own call
     lo, hi = (1 << 25) - 70_000, (1 << 25) + 70_000
     sub = {k: (v[lo:hi] if v.numel() > 1 else v) for k, v in cols.items() if torch.is_tensor(v)}
     iv2 = torch.empty(hi - lo, dtype=torch.float64, device=dev)
@@ -435,7 +436,7 @@ def test_fast_vollib_facade_device(fv, oracle_mod):
     device-resident path), bit-identical to the oracle."""
     import torch
     from paper_2604_27210_b200 import fast_vollib as FV
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     flag, S, K, t, r, q, sig = W.chain_draws(50_000, seed=31)
     chars = W.flag_chars(flag)
     # pricing
@@ -471,7 +472,7 @@ def test_odd_sizes_and_strided_device_columns(fv, oracle_mod, n):
     tensor): LBR, Halley, price and Greeks, bit for bit against the oracle."""
     import torch
     from paper_2604_27210_b200 import _native
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     lib = _native.lib_for_compute()
     flag, S, K, t, r, q, sig = W.chain_draws(n, seed=1000 + n)
     px = oracle_mod.rows_price("bsm", flag, S, K, t, r, q, sig)["price"]
@@ -553,7 +554,7 @@ def test_host_calls_sharded_over_devices(fv):
     its lowest GLOBAL row, also when it lies in a later shard)."""
     import torch
     from paper_2604_27210_b200 import _native
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     lib = _native.lib_for_compute()
     n = 2_500_000
     flag, S, K, t, r, q, sig = W.chain_draws(n, seed=77)
@@ -604,7 +605,7 @@ def test_host_calls_bit_identical_for_1_2_4_8_shards(fv):
     the same status column -- the analogue of the reference's FASTVOL_THREADS
     invariant (test_acceptance.py:211-254)."""
     from paper_2604_27210_b200 import _native
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     n = 8_400_000
     flag, S, K, t, r, q, sig = W.chain_draws(n, seed=123)
     fl = W.flag_chars(flag)

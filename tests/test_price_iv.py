@@ -93,7 +93,7 @@ def _price_iv_native(model, method, cols, device, region=True):
     (2, "bsm", "halley", 0), (2, "bsm", "lbr", 1), (0, "black", "lbr", 1), (0, "black", "halley", 0),
     (1, "bs", "lbr", 1)])
 def test_round_trip_vs_oracle(fv, oracle_mod, device, model, mname, method, mcode):
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     flag, S, K, t, r, q, sig = W.chain_draws(150_001, seed=21 + model)
     if model != 2:
         q = np.zeros_like(S)
@@ -114,7 +114,7 @@ def test_round_trip_host_chunks_and_broadcast(fv):
     """Host pipeline over many chunks (chunk rows not a multiple of anything)
     with broadcast r / q / sigma columns equals the device-resident call."""
     from paper_2604_27210_b200 import _native
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     lib = _native.load()
     n = 300_001
     flag, S, K, t, r, q, sig = W.chain_draws(n, seed=5)
@@ -133,7 +133,7 @@ def test_round_trip_host_chunks_and_broadcast(fv):
 
 @pytest.mark.gpu
 def test_python_round_trip_equals_two_calls(fv):
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     flag, S, K, t, r, q, sig = W.chain_draws(70_000, seed=9)
     fl = W.flag_chars(flag)
     for method in ("halley", "lbr"):
@@ -253,7 +253,7 @@ def test_round_trip_sharded_over_devices(fv):
     """Two host shards on device 0: same bits, and the merged error is the
     price stage's when it failed in either shard."""
     from paper_2604_27210_b200 import _native
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     n = 2_400_000
     flag, S, K, t, r, q, sig = W.chain_draws(n, seed=31)
     fl = W.flag_chars(flag)
@@ -388,7 +388,7 @@ def test_price_iv_sharded_single_rank(fv):
     price_iv; a price-stage exception comes back as stage 0's outcome."""
     import torch
     from paper_2604_27210_b200 import distributed as D
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     flag, S, K, t, r, q, sig = W.chain_draws(50_001, seed=23)
     ref = fv.price_iv("bsm", "halley", W.flag_chars(flag), S, K, t, r, q, sigma=sig)
     cols = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in

@@ -126,7 +126,7 @@ def test_exception_rows(Q):
 
 def test_fused_far_low_matches_reference_order(Q):
     from oracle import fvoracle as O
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     Q.qh_far_low_fused_check.restype = ctypes.c_int64
     flag, S, K, t, r, q, sig = W.chain_draws(100_000, seed=3)
     px = O.rows_price("black", flag, S, K, t, r, 0.0, sig)["price"]
@@ -142,7 +142,7 @@ def test_straight_line_far_low_matches_careful(Q, seed):
     back to the careful solver is bit-identical to it (sigma, status,
     iterations), on C1-like draws and on the C4 chain."""
     from oracle import fvoracle as O
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     Q.qh_far_low_fast_check.restype = ctypes.c_int64
     if seed == 3:
         flag, S, K, t, r, q, sig = W.chain_draws(100_000, seed=seed)
@@ -163,7 +163,7 @@ def test_straight_line_classify_matches_careful(Q, case):
     """fv_fast.h's first pass (normalize_quote, bounds, first anchor, far-low
     test): every row it does not flag reproduces the careful pass exactly
     (classification, outputs of finished rows, the state handed on)."""
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     from oracle import fvoracle as O
     Q.qh_classify_fast_check.restype = ctypes.c_int64
     model, q = 0, None
@@ -197,7 +197,7 @@ def test_straight_line_classify_matches_careful(Q, case):
 def test_straight_line_price_greeks_match_careful(Q, model):
     """fv_fast.h's price and fused price+Greeks rows: every row they do not
     flag is bit-identical to the careful rows (all six outputs + status)."""
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     Q.qh_price_greeks_fast_check.restype = ctypes.c_int64
     flag, S, K, t, r, q, sig = W.chain_draws(100_000, seed=30 + model)
     if model != 2:
@@ -227,7 +227,7 @@ def test_straight_line_halley_matches_careful(Q, case):
     """fv_fast.h's Halley step (fx_hsm_pre / fx_halley_f): every quote it does
     not flag ends with the careful solver's status and sigma bits."""
     from oracle import fvoracle as O
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     Q.qh_halley_fast_check.restype = ctypes.c_int64
     if case == "c5":
         flag, S, K, t, r, sig, kind, side = W.c5_params(20_000, seed=5)
@@ -255,7 +255,7 @@ def test_straight_line_near_matches_careful(Q, case):
     middle objective, all three normalized_black branches): every quote it
     does not flag is bit-identical to the careful solver."""
     from oracle import fvoracle as O
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     Q.qh_near_fast_check.restype = ctypes.c_int64
     flag, S, K, t, r, q, sig = W.chain_draws(100_000, seed=50)
     if case == "wide":                     # deep strikes, long/short maturities, high vols
@@ -278,7 +278,7 @@ def test_straight_line_anchor_rest_matches_careful(Q, case):
     anchor values as the careful stage on every unflagged quote (the central
     anchor's erfcx argument is 0 up to rounding: erfcx's y100 == 100 case)."""
     from oracle import fvoracle as O
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     Q.qh_anchor_rest_fast_check.restype = ctypes.c_int64
     flag, S, K, t, r, q, sig = W.chain_draws(100_000, seed=60)
     if case == "wide":
@@ -322,7 +322,7 @@ def test_halley_fp32_sign_matches_careful(Q, case):
     (F + K)) never decides a sign the careful f disagrees with; checked at
     sigma = 10 and at values where f is small (near the solution)."""
     from oracle import fvoracle as O
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     Q.qh_halley_sign_check.restype = ctypes.c_int64
     rng = np.random.default_rng(21)
     if case == "c5":

@@ -15,7 +15,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2604_27210_b200 as fv                      # noqa: E402
 from paper_2604_27210_b200 import batch as B            # noqa: E402
-from paper_2604_27210_b200 import workloads as W        # noqa: E402
+import workloads as W        # noqa: E402
 
 
 def main():

@@ -54,7 +54,7 @@ def main():
         return tracer
 
     from oracle import fvoracle as O
-    from paper_2604_27210_b200 import workloads as W
+    import workloads as W
     O.lib()
     flag, Su, K, t, r, q, sig = W.chain_draws(rows, seed=0)
     px = O.rows_price("bsm", flag, Su, K, t, r, q, sig)["price"]

@@ -39,7 +39,12 @@ def c4_params(start, stop):
     """Rows [start, stop) of the C4 chain: 2 flags x 1,000 maturities x
     50,000 strikes, row = (f*1000 + j)*50000 + i.  Returns
     (flag, F, K, t, r, sigma) as numpy arrays (F = 100, r = 0.03)."""
-    row = np.arange(start, stop, dtype=np.int64)
+    return c4_rows(np.arange(start, stop, dtype=np.int64))
+
+
+def c4_rows(row):
+    """The C4 chain's rows at the given (int64) row indices."""
+    row = np.asarray(row, dtype=np.int64)
     i = row % C4_STRIKES
     j = (row // C4_STRIKES) % C4_MATURITIES
     f = row // (C4_STRIKES * C4_MATURITIES)
@@ -48,7 +53,7 @@ def c4_params(start, stop):
     t = (1.0 / 365.0) * (5.0 * 365.0) ** (j / (C4_MATURITIES - 1))
     sigma = np.minimum(0.2 + 0.1 * x * x / np.sqrt(t), 2.0)
     flag = np.where(f == 0, 1, -1).astype(np.int8)
-    n = stop - start
+    n = row.shape[0]
     return flag, np.full(n, 100.0), K, t, np.full(n, 0.03), sigma
 
 
