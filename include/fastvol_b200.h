@@ -161,6 +161,42 @@ FV_API int fv_price_iv(int model, int method, fv_col flag, fv_col underlying, fv
                        double* iv, int8_t* status, int8_t* region, fv_error* err_price,
                        fv_error* err_iv);
 
+/* ---- one logical batch over several devices, device-resident
+ * Each shard is a contiguous row range of the logical batch (shards in row
+ * order) whose columns and outputs live on `device`; every shard runs from
+ * its own host thread on its device and stream (NULL = that device's legacy
+ * default stream).  No exchange between shards: every output row depends on
+ * its input row only.  The outcome is the single-call one -- the first
+ * failing check in the reference's order at its lowest GLOBAL row, else the
+ * lowest raising row -- with err1 = the price / IV (price stage of
+ * FV_KIND_PRICE_IV) record and err2 = the Greeks (IV stage) record, as the
+ * single-device entry points report them.  fv_last_outcome is the merged
+ * one, in global rows. */
+#define FV_KIND_PRICE 0          /* fv_batch_price:  outs[0] = price */
+#define FV_KIND_IV 1             /* fv_batch_iv:     outs[0] = iv, status (+ region) */
+#define FV_KIND_GREEKS 2         /* fv_batch_greeks: outs[1..5], status */
+#define FV_KIND_PRICE_GREEKS 3   /* fv_price_greeks: outs[0] and/or outs[1..5] + status */
+#define FV_KIND_PRICE_IV 4       /* fv_price_iv:     outs[0] = price, outs[1] = iv, status (+ region) */
+typedef struct fv_shard {
+  int device;          /* CUDA device owning this shard's pointers */
+  void* stream;        /* cudaStream_t on that device (NULL = its legacy default stream) */
+  fv_col cols[7];      /* flag, underlying, strike, t, r, q, sigma | price */
+  int64_t n;           /* rows of this shard */
+  double* outs[6];     /* price|iv, delta, gamma, theta, rho, vega (FV_KIND_PRICE_IV: price, iv) */
+  int8_t* status;
+  int8_t* region;      /* optional (IV kinds) */
+} fv_shard;
+FV_API int fv_run_shards(int kind, int model, int method, int nshard, const fv_shard* shards,
+                         fv_error* err1, fv_error* err2);
+
+/* Gather per-shard device buffers into one buffer on dst_device (NVLink /
+ * NVSwitch peer copies where peer access is available, else staged by the
+ * driver): src[g] (bytes[g] bytes on src_device[g]) lands at dst + the sum of
+ * the previous bytes.  Ordered on dst_stream (a stream of dst_device, NULL =
+ * its legacy default stream); returns when the data is in place. */
+FV_API int fv_gather(void* dst, int dst_device, void* dst_stream, int nshard, const void* const* src,
+                     const int* src_device, const int64_t* bytes);
+
 /* Stream used by device-pointer calls made from the calling thread
  * (cudaStream_t; NULL = the device's legacy default stream, which is what
  * torch's default stream is).  A thread that never calls it uses the

@@ -27,6 +27,15 @@ class fv_error(ctypes.Structure):
                 ("value", ctypes.c_double), ("message", ctypes.c_char * 256)]
 
 
+class fv_shard(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("cols", fv_col * 7),
+                ("n", ctypes.c_int64), ("outs", ctypes.c_void_p * 6), ("status", ctypes.c_void_p),
+                ("region", ctypes.c_void_p)]
+
+
+FV_KIND_PRICE, FV_KIND_IV, FV_KIND_GREEKS, FV_KIND_PRICE_GREEKS, FV_KIND_PRICE_IV = range(5)
+
+
 class NativeUnavailable(RuntimeError):
     """The CUDA extension is not built or cannot run here."""
 
@@ -49,6 +58,8 @@ SIGNATURES = {
     "fv_price_iv": ([ctypes.c_int, ctypes.c_int] + [_COL] * 7 + [_I64, _P, _P, _P, _P, _ERR, _ERR],
                     ctypes.c_int),
     "fv_set_stream": ([_P], ctypes.c_int),
+    "fv_run_shards": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _ERR, _ERR], ctypes.c_int),
+    "fv_gather": ([_P, ctypes.c_int, _P, ctypes.c_int, _P, _P, _P], ctypes.c_int),
     "fv_device_count": ([], ctypes.c_int),
     "fv_set_devices": ([_P, ctypes.c_int], ctypes.c_int),
     "fv_get_devices": ([_P, ctypes.c_int], ctypes.c_int),

@@ -2091,10 +2091,11 @@ struct ShardOut {
 
 thread_local bool t_in_shard = false;
 
-void shard_call(int dev, Call cs, ShardOut* out) {
+void shard_call(int dev, Call cs, ShardOut* out, bool set_stream = false, void* stream = nullptr) {
   t_in_shard = true;                           // a shard runs on its device only
   cudaError_t ce = cudaSetDevice(dev);
   if (ce != cudaSuccess) { out->rc = set_cuda_err(&out->e1, ce); return; }
+  if (set_stream) { t_user_stream = (cudaStream_t)stream; t_user_stream_set = true; }
   out->rc = dispatch(cs, &out->e1, &out->e2);
   for (int k = 0; k < FV_NCHECK; ++k) out->check_rows[k] = t_check_rows[k];
   for (int k = 0; k < 2; ++k) { out->exc_row[k] = t_exc_row[k]; out->exc_code[k] = t_exc_code[k]; }
@@ -2116,6 +2117,9 @@ void shift_error(fv_error* e, int64_t off) {
   }
 }
 
+int merge_shards(Kind kind, const std::vector<ShardOut>& outs, const std::vector<int64_t>& off, fv_error* e1,
+                 fv_error* e2);
+
 int dispatch_sharded(const Call& c, const std::vector<int>& devs, fv_error* e1, fv_error* e2) {
   const int64_t G = (int64_t)devs.size();
   const size_t in_sz[7] = {1, 8, 8, 8, 8, 8, 8};
@@ -2135,10 +2139,17 @@ int dispatch_sharded(const Call& c, const std::vector<int>& devs, fv_error* e1, 
     if (c.region) cs.region = c.region + lo;
     set_ok(&outs[g].e1);
     set_ok(&outs[g].e2);
-    th.emplace_back(shard_call, devs[g], cs, &outs[g]);
+    th.emplace_back(shard_call, devs[g], cs, &outs[g], false, nullptr);
   }
   for (auto& t : th) t.join();
-  // merged thread-local outcome (fv_last_outcome) and launch count
+  return merge_shards(c.kind, outs, off, e1, e2);
+}
+
+// The shards' outcomes (shards in row order, row offsets off[g]) merged into
+// the single-call one, and into this thread's fv_last_outcome.
+int merge_shards(Kind kind, const std::vector<ShardOut>& outs, const std::vector<int64_t>& off, fv_error* e1,
+                 fv_error* e2) {
+  const int64_t G = (int64_t)outs.size();
   int64_t launches = 0;
   for (int k = 0; k < FV_NCHECK; ++k) t_check_rows[k] = -1;
   for (int k = 0; k < 2; ++k) { t_exc_row[k] = -1; t_exc_code[k] = 0; }
@@ -2184,7 +2195,7 @@ int dispatch_sharded(const Call& c, const std::vector<int>& devs, fv_error* e1, 
     }
     if (dst[k]) *dst[k] = merged;
   }
-  if (c.kind == KIND_PRICE_IV) {          // the price stage's failure is the call's
+  if (kind == KIND_PRICE_IV) {            // the price stage's failure is the call's
     if (any_batch[0]) return FV_ERR_BATCH;
     if (any_exc[0]) return FV_ERR_PYEXC;
     return any_batch[1] ? FV_ERR_BATCH : (any_exc[1] ? FV_ERR_PYEXC : FV_OK);
@@ -2403,6 +2414,102 @@ FV_API int fv_price_iv(int model, int method, fv_col flag, fv_col underlying, fv
   if (err_price) *err_price = ep;
   if (err_iv) *err_iv = ei;
   return rc;
+}
+
+FV_API int fv_run_shards(int kind, int model, int method, int nshard, const fv_shard* shards,
+                         fv_error* err1, fv_error* err2) {
+  set_ok(err1);
+  set_ok(err2);
+  for (int k = 0; k < FV_NCHECK; ++k) t_check_rows[k] = -1;
+  for (int k = 0; k < 2; ++k) { t_exc_row[k] = -1; t_exc_code[k] = 0; }
+  t_launches = 0;
+  if (kind < FV_KIND_PRICE || kind > FV_KIND_PRICE_IV) return set_arg_err(err1, "unknown call kind");
+  if (nshard < 1 || !shards) return set_arg_err(err1, "no shards");
+  int have = 0;
+  if (cudaGetDeviceCount(&have) != cudaSuccess) { cudaGetLastError(); have = 0; }
+  std::vector<ShardOut> outs(nshard);
+  std::vector<int64_t> off(nshard);
+  std::vector<Call> calls(nshard);
+  int64_t row = 0;
+  for (int g = 0; g < nshard; ++g) {
+    const fv_shard& sh = shards[g];
+    if (sh.device < 0 || sh.device >= have) return set_arg_err(err1, "shard device out of range");
+    if (sh.n < 0) return set_arg_err(err1, "shard n must be >= 0");
+    Call& c = calls[g];
+    c = make_call((Kind)kind, model, method, sh.cols[0], sh.cols[1], sh.cols[2], sh.cols[3], sh.cols[4],
+                  sh.cols[5], sh.cols[6], sh.n);
+    for (int i = 0; i < 6; ++i) c.outs[i] = sh.outs[i];
+    c.status = sh.status;
+    c.region = (kind == FV_KIND_IV || kind == FV_KIND_PRICE_IV) ? sh.region : nullptr;
+    bool ok = true;
+    switch (kind) {
+      case FV_KIND_PRICE: ok = sh.outs[0] != nullptr; break;
+      case FV_KIND_IV: ok = sh.outs[0] && sh.status; break;
+      case FV_KIND_GREEKS:
+        c.outs[0] = nullptr;
+        ok = sh.outs[1] && sh.outs[2] && sh.outs[3] && sh.outs[4] && sh.outs[5] && sh.status;
+        c.want_greeks = true;
+        break;
+      case FV_KIND_PRICE_GREEKS:
+        c.want_price = sh.outs[0] != nullptr;
+        c.want_greeks = sh.outs[1] || sh.outs[2] || sh.outs[3] || sh.outs[4] || sh.outs[5] || sh.status;
+        ok = (c.want_price || c.want_greeks) &&
+             (!c.want_greeks || (sh.outs[1] && sh.outs[2] && sh.outs[3] && sh.outs[4] && sh.outs[5] && sh.status));
+        break;
+      case FV_KIND_PRICE_IV: ok = sh.outs[0] && sh.outs[1] && sh.status; break;
+    }
+    if (!ok && sh.n > 0) return set_arg_err(err1, "shard outputs missing for this call kind");
+    off[g] = row;
+    row += sh.n;
+    set_ok(&outs[g].e1);
+    set_ok(&outs[g].e2);
+  }
+  // one host thread per shard, each on its shard's device and stream (the
+  // shards of one device run one after the other on it: DevWork's lock)
+  std::vector<std::thread> th;
+  for (int g = 0; g < nshard; ++g)
+    th.emplace_back(shard_call, shards[g].device, calls[g], &outs[g], true, shards[g].stream);
+  for (auto& t : th) t.join();
+  fv_error m1, m2;
+  int rc = merge_shards((Kind)kind, outs, off, &m1, &m2);
+  if (kind == FV_KIND_PRICE_GREEKS && rc == FV_ERR_PYEXC) {
+    const bool wp = calls[0].want_price, wg = calls[0].want_greeks;
+    if (!((wp && m1.code) || (wg && m2.code))) rc = FV_OK;
+    if (!wp) set_ok(&m1);
+    if (!wg) set_ok(&m2);
+  }
+  if (kind == FV_KIND_PRICE_IV && (rc == FV_ERR_CUDA || rc == FV_ERR_ARG)) m2 = m1;
+  if (err1) *err1 = m1;
+  if (err2) *err2 = m2;
+  return rc;
+}
+
+FV_API int fv_gather(void* dst, int dst_device, void* dst_stream, int nshard, const void* const* src,
+                     const int* src_device, const int64_t* bytes) {
+  if (nshard < 0 || (nshard > 0 && (!src || !src_device || !bytes)) || !dst) return FV_ERR_ARG;
+  int prev = 0;
+  if (cudaGetDevice(&prev) != cudaSuccess) return FV_ERR_CUDA;
+  DeviceGuard guard;
+  guard.prev = prev;
+  if (cudaSetDevice(dst_device) != cudaSuccess) { cudaGetLastError(); return FV_ERR_ARG; }
+  cudaStream_t s = (cudaStream_t)dst_stream;
+  int64_t o = 0;
+  for (int g = 0; g < nshard; ++g) {
+    if (bytes[g] < 0) return FV_ERR_ARG;
+    if (src_device[g] != dst_device) {
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, dst_device, src_device[g]);
+      if (can) {
+        cudaError_t pe = cudaDeviceEnablePeerAccess(src_device[g], 0);
+        if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      }
+    }
+    if (bytes[g] && cudaMemcpyPeerAsync((char*)dst + o, dst_device, src[g], src_device[g], (size_t)bytes[g], s) !=
+                        cudaSuccess)
+      return FV_ERR_CUDA;
+    o += bytes[g];
+  }
+  return cudaStreamSynchronize(s) == cudaSuccess ? FV_OK : FV_ERR_CUDA;
 }
 
 FV_API int fv_set_stream(void* stream) {

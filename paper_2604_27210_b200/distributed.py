@@ -11,7 +11,14 @@ on the data path.  The only cross-rank traffic is
     the whole result on every rank (NCCL over NVLink / NVSwitch).
 
 ``run_sharded`` holds the merge logic and is backend-agnostic (tested on CPU
-with gloo); ``batch_iv_sharded`` binds it to the CUDA C ABI.
+with gloo); ``batch_iv_sharded`` binds it to the CUDA C ABI.  ``gather_to``
+brings the shards to ONE rank only (point-to-point sends, NCCL over NVLink /
+NVSwitch on a GPU box) when the caller asks for the result on one device.
+
+Inside one process, ``run_device_shards`` drives several GPUs from one call
+(``fv_run_shards``: one host thread per device-resident shard, outcome merged
+in C) and ``gather_device`` copies the shards' results into one device's
+memory (``fv_gather``: peer copies over NVLink).
 """
 
 import numpy as np
@@ -52,6 +59,36 @@ def merge_status(vec):
     return None
 
 
+def gather_to(shard, n, dst=0, group=None):
+    """The full n-row result on rank ``dst`` only (None elsewhere): rank r's
+    ``shard`` holds rows shard_bounds(n, world, r).  Point-to-point: every
+    other rank sends its shard once (NCCL: over NVLink / NVSwitch), so the
+    traffic is the gathered bytes, not world x them as an all-gather."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    t = shard if torch.is_tensor(shard) else torch.from_numpy(np.ascontiguousarray(shard))
+    if world == 1:
+        return t
+    if rank != dst:
+        dist.send(t.contiguous(), dst=dist.get_global_rank(group, dst) if group is not None else dst,
+                  group=group)
+        return None
+    full = torch.empty(n, dtype=t.dtype, device=t.device)
+    reqs = []
+    for r in range(world):
+        lo, hi = shard_bounds(n, world, r)
+        if r == rank:
+            full[lo:hi] = t
+        elif hi > lo:
+            src = dist.get_global_rank(group, r) if group is not None else r
+            reqs.append(dist.irecv(full[lo:hi], src=src, group=group))
+    for q in reqs:
+        q.wait()
+    return full
+
+
 def run_sharded(compute, n, group=None, device=None, gather=False):
     """Run ``compute(lo, hi) -> (outputs: dict of 1-D arrays/tensors,
     check_rows[12], exc_row, exc_code)`` on this rank's shard, agree on the
@@ -72,7 +109,10 @@ def run_sharded_stages(compute, n, nstage, group=None, device=None, gather=False
     (outputs, [(check_rows[12], exc_row, exc_code)] * nstage)``.  One MIN
     all-reduce over the stages' status vectors; the first stage with an
     outcome anywhere decides, as the reference raises in the first call that
-    fails.  Returns (outputs, (stage, outcome) | None)."""
+    fails.  ``gather``: False (each rank keeps its shard), True / "all" (every
+    rank gets the full arrays: all-gather), or an int rank (only that rank
+    gets them, ``gather_to``; the others get None).  Returns (outputs,
+    (stage, outcome) | None)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -92,7 +132,15 @@ def run_sharded_stages(compute, n, nstage, group=None, device=None, gather=False
         if o is not None:
             outcome = (s, o)
             break
-    if gather and world > 1 and outcome is None:
+    if gather is not False and gather is not None and not isinstance(gather, bool) and gather != "all" \
+            and world > 1 and outcome is None:
+        dst = int(gather)
+        outputs = {name: gather_to(shard if device is None or not torch.is_tensor(shard) else shard.to(device),
+                                   n, dst=dst, group=group)
+                   for name, shard in outputs.items()}
+        if rank != dst:
+            outputs = None
+    elif gather and world > 1 and outcome is None:
         full = {}
         for name, shard in outputs.items():
             t = shard if torch.is_tensor(shard) else torch.from_numpy(np.ascontiguousarray(shard))
@@ -172,3 +220,87 @@ def price_iv_sharded(model, method, cols, n, group=None, gather=False):
         return {"price": px, "iv": iv, "status": st}, stages
 
     return run_sharded_stages(compute, n, 2, group=group, device=dev, gather=gather)
+
+
+# ---------------------------------------------------------------------------
+# several GPUs from one process (fv_run_shards / fv_gather)
+# ---------------------------------------------------------------------------
+_KIND_LAST = {0: "sigma", 1: "price", 2: "sigma", 3: "sigma", 4: "sigma"}
+
+
+def run_device_shards(kind, model, method, shards):
+    """One logical batch whose row ranges live on several devices (``shards``:
+    list, in row order, of dicts of device-resident torch columns -- flag,
+    underlying, strike, t, r, q and sigma | price -- all on one device each).
+    Runs every shard on its own device from its own host thread (one
+    ``fv_run_shards`` call), on each device's current torch stream.  Returns
+    (per-shard output dicts, rc, err1, err2): outputs are allocated on each
+    shard's device; rc / err1 / err2 as the single-device entry point (the
+    merged outcome in GLOBAL rows; ``_native.last_outcome`` likewise)."""
+    import torch
+    from . import _native
+    from .models import as_model
+    lib = _native.lib_for_compute()
+    m = as_model(model).code
+    last = _KIND_LAST[kind]
+    arr = (_native.fv_shard * len(shards))()
+    outs = []
+    for g, cols in enumerate(shards):
+        dev = cols["strike"].device
+        n = cols["flag"].numel() if cols["flag"].numel() > 1 else max(
+            c.numel() for c in cols.values())
+        sh = arr[g]
+        sh.device = dev.index
+        sh.stream = torch.cuda.current_stream(dev).cuda_stream
+        for i, k in enumerate(("flag", "underlying", "strike", "t", "r", "q", last)):
+            sh.cols[i] = _native.col(cols[k])
+        sh.n = n
+        o = {}
+        if kind in (_native.FV_KIND_PRICE, _native.FV_KIND_PRICE_GREEKS, _native.FV_KIND_PRICE_IV):
+            o["price"] = torch.empty(n, dtype=torch.float64, device=dev)
+        if kind in (_native.FV_KIND_IV, _native.FV_KIND_PRICE_IV):
+            o["iv"] = torch.empty(n, dtype=torch.float64, device=dev)
+        if kind in (_native.FV_KIND_GREEKS, _native.FV_KIND_PRICE_GREEKS):
+            for name in ("delta", "gamma", "theta", "rho", "vega"):
+                o[name] = torch.empty(n, dtype=torch.float64, device=dev)
+        if kind != _native.FV_KIND_PRICE:
+            o["status"] = torch.empty(n, dtype=torch.int8, device=dev)
+        slots = {"price": 0, "delta": 1, "gamma": 2, "theta": 3, "rho": 4, "vega": 5}
+        if kind == _native.FV_KIND_IV:
+            slots = {"iv": 0}
+        elif kind == _native.FV_KIND_PRICE_IV:
+            slots = {"price": 0, "iv": 1}
+        for name, j in slots.items():
+            if name in o:
+                sh.outs[j] = o[name].data_ptr()
+        if "status" in o:
+            sh.status = o["status"].data_ptr()
+        outs.append(o)
+    e1, e2 = _native.fv_error(), _native.fv_error()
+    rc = lib.fv_run_shards(kind, m, 1 if method == "lbr" else 0, len(shards), arr, e1, e2)
+    _native.check_runtime(rc, e1)
+    return outs, rc, e1, e2
+
+
+def gather_device(tensors, dst_device):
+    """Concatenate per-device 1-D tensors (in order) into one tensor on
+    ``dst_device`` with peer copies (``fv_gather``: NVLink / NVSwitch P2P)."""
+    import ctypes
+    import torch
+    from . import _native
+    lib = _native.lib_for_compute()
+    dst_device = torch.device(dst_device)
+    dtype = tensors[0].dtype
+    n = sum(t.numel() for t in tensors)
+    out = torch.empty(n, dtype=dtype, device=dst_device)
+    k = len(tensors)
+    src = (ctypes.c_void_p * k)(*[t.data_ptr() for t in tensors])
+    sdev = (ctypes.c_int * k)(*[t.device.index for t in tensors])
+    nb = (ctypes.c_int64 * k)(*[t.numel() * t.element_size() for t in tensors])
+    for t in tensors:                     # the shards' producers are done before the copies start
+        torch.cuda.current_stream(t.device).synchronize()
+    rc = lib.fv_gather(out.data_ptr(), dst_device.index, torch.cuda.current_stream(dst_device).cuda_stream,
+                       k, src, sdev, nb)
+    if rc:
+        raise _native.NativeCallError(f"fv_gather failed (rc={rc})")
+    return out

@@ -22,7 +22,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, scenario, q):
+def _worker(rank, world, port, n, scenario, q, gather=True):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -41,17 +41,17 @@ def _worker(rank, world, port, n, scenario, q):
                     elif exc_row < 0 or g_row - lo < exc_row:
                         exc_row, exc_code = g_row - lo, code
             return out, checks, exc_row, exc_code
-        outputs, outcome = D.run_sharded(compute, n, gather=True)
-        q.put((rank, outcome, {k: np.asarray(v) for k, v in outputs.items()}))
+        outputs, outcome = D.run_sharded(compute, n, gather=gather)
+        q.put((rank, outcome, None if outputs is None else {k: np.asarray(v) for k, v in outputs.items()}))
     finally:
         dist.destroy_process_group()
 
 
-def _run(n, scenario):
+def _run(n, scenario, gather=True, world=2):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, scenario, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, scenario, q, gather)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=60) for _ in procs]
@@ -76,6 +76,32 @@ def test_clean_run_gathers_full_result():
         assert outcome is None
         assert np.array_equal(out["iv"], np.arange(n) * 0.5)
         assert np.array_equal(out["status"], (np.arange(n) % 5).astype(np.int8))
+
+
+def test_gather_to_one_rank_only():
+    """gather=<rank>: the full result lands on that rank only (point-to-point
+    sends; NCCL over NVLink on a GPU box), the others keep nothing -- the
+    north star's "NVLink only to gather results when the caller asks for
+    them on one device"."""
+    n = 1001
+    for dst in (0, 1):
+        res = _run(n, [], gather=dst)
+        for rank, outcome, out in res:
+            assert outcome is None
+            if rank == dst:
+                assert np.array_equal(out["iv"], np.arange(n) * 0.5)
+                assert np.array_equal(out["status"], (np.arange(n) % 5).astype(np.int8))
+            else:
+                assert out is None
+
+
+def test_gather_to_one_rank_world3_uneven():
+    n = 1000                                  # 334 / 333 / 333 rows
+    for rank, outcome, out in _run(n, [], gather=2, world=3):
+        if rank == 2:
+            assert np.array_equal(out["iv"], np.arange(n) * 0.5)
+        else:
+            assert out is None
 
 
 def test_first_error_is_global_reference_order():
