@@ -13,10 +13,13 @@ maturities x 50,000 strikes = 100M quotes).
 
 Multi-GPU (one process per GPU, torchrun):
   * ``--scaling strong`` (default): ONE 100M-quote chain sharded across the N
-    ranks -- rank g solves its rows (contiguous [g N/G, (g+1) N/G), or
-    1M-row blocks dealt round-robin with ``--shard-scheme cyclic``), no
-    collective on the data path; ``value`` = 100M / the max over ranks of the
-    per-step time;
+    ranks -- rank g solves its rows: 1M-row blocks dealt round-robin
+    (``--shard-scheme cyclic``, default) or one contiguous range [g N/G,
+    (g+1) N/G) (``contiguous``; the chain's (flag, maturity, strike) order
+    gives contiguous shards different region mixes: 7.6 / 8.4 % imbalance at
+    G = 4 / 8 against 1.1 / 2.3 % cyclic, profiles/r2/shard_times_c4.json),
+    no collective on the data path; ``value`` = 100M / the max over ranks of
+    the per-step time;
   * ``--scaling weak``: every rank solves its own full chain (F_r = 100 *
     1.01^r), ``value`` = N x rows / max time.
 ``--shard g/G`` runs shard g of a G-way strong split on this one GPU (the
@@ -79,7 +82,7 @@ def parse(argv=None):
                     help="rows of the logical batch (default: the workload's size; fewer C4 rows = an "
                          "evenly strided sub-chain, for profiling)")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
-    ap.add_argument("--shard-scheme", default="contiguous", choices=["contiguous", "cyclic"])
+    ap.add_argument("--shard-scheme", default="cyclic", choices=["contiguous", "cyclic"])
     ap.add_argument("--shard", default="", help="g/G: run shard g of a G-way strong split on this GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle pass (cpu_baseline + parity)")

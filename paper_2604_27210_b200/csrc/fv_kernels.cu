@@ -830,6 +830,29 @@ __device__ __forceinline__ unsigned long long claim(bool need, unsigned long lon
 #ifndef FV_HSM_MINB
 #define FV_HSM_MINB 3
 #endif
+#ifndef FV_HAL_PREFETCH
+#define FV_HAL_PREFETCH 1
+#endif
+
+// One-record-ahead prefetch for the Halley passes' refill: each lane claims
+// its NEXT record while it still works on the current one and copies it into
+// its shared-memory slot with cp.async (16-byte, L2-only), so a lane whose
+// quote finishes takes the next one from shared memory instead of waiting on
+// the claim atomic and a dependent HBM load (the refill's load -> test chain
+// was the top stall of k_halley_iter).
+__device__ __forceinline__ void hal_prefetch(double* slot, const HalRec* r) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(slot);
+  const char* g = reinterpret_cast<const char*>(r);
+#pragma unroll
+  for (int k = 0; k < 6; ++k)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa + 16 * k), "l"(g + 16 * k) : "memory");
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void hal_take(const double* slot, FvHalleyCtx& c, double& lo, double& hi, double& sigma,
+                                         double& fval, int64_t& rowbits) {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  hal_load(reinterpret_cast<const HalRec*>(slot), c, lo, hi, sigma, fval, rowbits);
+}
 // Halley steps (:115-144) over the bracket pass's queue.  One f evaluation
 // per loop trip: at the Halley candidate when it lies inside the bracket,
 // else (and after a candidate that did not improve |f|) at the midpoint.
@@ -850,7 +873,36 @@ __global__ void __launch_bounds__(256, FV_HSM_MINB) k_halley_iter(KArgs a, HalRe
   int64_t row = 0;
   int32_t rec = 0;
   bool busy = false, exhausted = false, midp = false;
+#if FV_HAL_PREFETCH
+  // 12 doubles of record + the record index per lane (14 x 8 B: the slot
+  // holds the index too, so it does not occupy a register across the trip)
+  __shared__ __align__(16) double sm_next[256 * 14];
+  bool has_next = false;
+#endif
   for (;;) {
+#if FV_HAL_PREFETCH
+    const bool need = !has_next && !exhausted;
+    const unsigned long long jq = claim(need, next, lane);
+    if (need) {
+      if (jq >= n) {
+        exhausted = true;
+      } else {
+        double* my_next = sm_next + 14 * threadIdx.x;   // 16-byte aligned 112-byte slot
+        reinterpret_cast<int32_t*>(my_next + 12)[0] = (int32_t)jq;
+        hal_prefetch(my_next, recs + jq);
+        has_next = true;
+      }
+    }
+    if (!busy && has_next) {
+      const double* my_next = sm_next + 14 * threadIdx.x;
+      rec = reinterpret_cast<const int32_t*>(my_next + 12)[0];
+      int64_t rb;
+      hal_take(my_next, c, lo, hi, sigma, fval, rb);
+      row = rb & (FV_HAL_CALL - 1);
+      has_next = false;
+      k = 0; midp = false; busy = true;
+    }
+#else
     const bool need = !busy && !exhausted;
     const unsigned long long jq = claim(need, next, lane);
     if (need) {
@@ -870,6 +922,7 @@ __global__ void __launch_bounds__(256, FV_HSM_MINB) k_halley_iter(KArgs a, HalRe
         k = 0; midp = false; busy = true;
       }
     }
+#endif
     if (!__any_sync(0xffffffffu, busy)) break;
     // next evaluation point (:118-128)
     double x = 0.5 * (lo + hi);
