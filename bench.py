@@ -506,14 +506,16 @@ def run_ours(args):
             raise RuntimeError(f"fv call failed rc={rc}: {err.message}")
         launches[0] += lib.fv_last_launch_count()
 
+    # the clock sampler starts first: the warm-up steps then also bring the
+    # GPU back from the idle of the sampler's start-up (a first call right
+    # after an idle period runs ~15 % slow)
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
     if pg:
         pg.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
     launches[0] = 0
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -579,6 +581,20 @@ def run_ours(args):
     except Exception as exc:  # noqa: BLE001
         lib.fv_set_kernel_timing(0)
         kernels = {"error": repr(exc)}
+
+    # ---- device span of a call (events around its launches, nothing
+    # serialised): per_call_ms - span = host overhead of the synchronous call
+    span_ms = None
+    try:
+        lib.fv_set_span_timing(1)
+        spans = []
+        for _ in range(max(1, min(args.steps, 5))):
+            step()
+            spans.append(lib.fv_last_span_ms())
+        lib.fv_set_span_timing(0)
+        span_ms = float(np.mean(spans)) if min(spans) >= 0 else None
+    except Exception:  # noqa: BLE001
+        lib.fv_set_span_timing(0)
 
     # ---- the dominant kernel's own roofline --------------------------------
     # algorithmic work per launch = the reference's weighted distinct fp64 ops
@@ -775,6 +791,10 @@ def run_ours(args):
                             "sequence on the call's stream (fv_set_kernel_timing): shares are of the serialised "
                             "call (serial_ms_per_call); the timed calls overlap those branches",
             "serial_ms_per_call": serial_ms,
+            "device_span_ms_per_call": span_ms,
+            "device_span_note": "CUDA events on the call's stream before its first and after its last launch "
+                                "(fv_set_span_timing); mean per-call time minus this = host overhead of the "
+                                "synchronous C-ABI call",
             "dominant_kernel": (dict(dominant, peak=peak_tops, unit="T weighted-fp64-ops/s",
                                      frac=dominant["achieved"] / peak_tops if peak_tops else None)
                                 if dominant else None),

@@ -277,6 +277,14 @@ FV_API int fv_selftest_fast(int64_t n, uint64_t seed, int64_t* mismatches /*[11]
 #define FV_KID_HALLEY_BISECT 13
 #define FV_NKERNEL 14
 FV_API int fv_set_kernel_timing(int on);
+
+/* Device span of this thread's last device-pointer call (diagnostics; off by
+ * default): milliseconds between CUDA events recorded on the call's stream
+ * before its first and after its last launch (side streams joined), nothing
+ * serialised.  The caller's own per-call time minus this is host overhead
+ * (argument checks, launches, the status read-back).  -1 when not recorded. */
+FV_API int fv_set_span_timing(int on);
+FV_API double fv_last_span_ms(void);
 FV_API int fv_kernel_times(double* ms /*[FV_NKERNEL]*/, int64_t* launches /*[FV_NKERNEL]*/);
 FV_API const char* fv_kernel_name(int id);
 

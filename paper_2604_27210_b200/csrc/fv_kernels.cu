@@ -665,6 +665,12 @@ struct HalRec {            // 96 bytes, 16-byte aligned: a quote between passes
 struct HalRecRow { int64_t rowbits; };   // row | (call << 62), parallel array
 
 #define FV_HAL_CALL (1ll << 62)
+// rowbits = row | k << 56 | midp << 61 | call << 62: the record also carries
+// the Halley step count and the pending-midpoint flag of a quote whose first
+// steps ran in the bracket pass (FV_HAL_BRACKET_TRIPS)
+#define FV_HAL_ROWMASK ((1ll << 56) - 1)
+#define FV_HAL_KSHIFT 56
+#define FV_HAL_MIDP (1ll << 61)
 
 // The record's spare slot (p[3].y) carries the row bits (row | call << 62):
 // a refill then issues the record's six 16-byte loads straight after the
@@ -693,8 +699,71 @@ __device__ __forceinline__ void hal_load(const HalRec* r, FvHalleyCtx& c, double
   lo = v4.x; hi = v4.y; sigma = v5.x; fval = v5.y;
 }
 
+// One trip of the Halley loop (solver.py:115-144) for the lanes with `busy`
+// (warp-collective: all 32 lanes call it): the next evaluation point -- the
+// Halley candidate, or the midpoint after a rejected candidate (`midp`) --
+// f there, and the bracket / iterate update.  fin >= 0: the quote finished
+// with that status at `sigma`; to_bis: the 16 Halley steps are spent
+// (bisection next); hb: a straight-line routine flagged (careful pass).
+// busy is cleared for all three.
+__device__ __forceinline__ void hal_trip(bool& busy, bool& midp, int& k, const FvHalleyCtx& c, double& lo,
+                                         double& hi, double& sigma, double& fval, int& fin, bool& to_bis,
+                                         bool& hb, double* sm_x, double* sm_r, unsigned char* sm_f) {
+  double x = 0.5 * (lo + hi);
+  bool chk = false;
+  hb = false;
+  fin = -1;
+  to_bis = false;
+  if (busy && !midp) {
+    FxBad vb;
+    const double s = sigma * c.sqrt_t;
+    double vega = 0.0, d1 = 0.0;
+    if (!(s < FV_K_1EM12)) {
+      d1 = fx_div0(c.lnFK + 0.5 * s * s, s, vb);
+      vega = c.disc * c.Fw * fx_norm_pdf(d1, vb) * c.sqrt_t;
+    }
+    double cn = __builtin_nan("");
+    if (vega > 0.0) {
+      const double d2 = d1 - s;
+      const double vomma = fx_div0(vega * d1 * d2, sigma, vb);
+      const double denom = 2.0 * vega * vega - fval * vomma;
+      if (denom != 0.0) cn = sigma - fx_div0(2.0 * fval * vega, denom, vb);
+    }
+    if (fv_isfinite(cn) && lo < cn && cn < hi) { x = cn; chk = true; }
+    if (vb) hb = true;
+  }
+  if (hb) busy = false;
+  __syncwarp();
+  FxBad fb;
+  const double fx = fx_halley_f_warp(busy, c, x, fb, sm_x, sm_r, sm_f);
+  __syncwarp();
+  if (busy && fb) { hb = true; busy = false; }
+  if (busy) {
+    if (chk && !(fv_fabs(fx) < fv_fabs(fval))) {          // :129-135: rejected -> f(mid) next
+      midp = true;
+    } else {                                               // :136-144
+      midp = false;
+      if (fx > 0.0) hi = x;
+      else if (fx < 0.0) lo = x;
+      const double step = x - sigma;
+      sigma = x; fval = fx;
+      if (fv_fabs(step) <= FV_K_1EM12 * py_max(1.0, sigma)) fin = FV_IV_CONVERGED;
+      else if (++k == 16) to_bis = true;
+      else if (fv_fabs(fval) <= c.tol_price) fin = FV_IV_CONVERGED;   // :116-117 of the next step
+    }
+  }
+  if (fin >= 0 || to_bis) busy = false;
+}
+
 #ifndef FV_HAL_SIGN32
 #define FV_HAL_SIGN32 1
+#endif
+// Halley trips run by the bracket pass itself, one row per thread, before a
+// quote is queued: nearly every quote needs its first steps (C2: 99.3 % reach
+// the loop, mode 3 steps), and here they run with all lanes of a warp busy and
+// no claim / record reload, against ~24 of 32 lanes in the refill loop.
+#ifndef FV_HAL_BRACKET_TRIPS
+#define FV_HAL_BRACKET_TRIPS 2
 #endif
 #ifndef FV_HSET_MINB
 #define FV_HSET_MINB 3
@@ -802,10 +871,27 @@ __global__ void __launch_bounds__(256, FV_HSET_MINB) k_halley_bracket(KArgs a, K
       a.status[row] = (int8_t)FV_IV_CONVERGED;
       open = false;
     }
+    // the first Halley trips, row per thread (all lanes call: f is warp-collective)
+    double sg = sigma, fv = fval;
+    int kst = 0;
+    bool midp = false;
+#pragma unroll 1
+    for (int trip = 0; trip < FV_HAL_BRACKET_TRIPS; ++trip) {
+      if (!__any_sync(0xffffffffu, open)) break;
+      int fin;
+      bool to_bis, hbt;
+      hal_trip(open, midp, kst, m.c, lo, hi, sg, fv, fin, to_bis, hbt, sm_x[wib], sm_r[wib], sm_f[wib]);
+      if (fin >= 0) {
+        a.o0[row] = sg;
+        a.status[row] = (int8_t)fin;
+      }
+      if (hbt) hb = true;
+    }
     const unsigned int slot = warp_append(count, open);
     if (open) {
-      const int64_t rb = row | (m.c.th > 0.0 ? FV_HAL_CALL : 0);
-      hal_store(recs + slot, m.c, lo, hi, sigma, fval, rb);
+      const int64_t rb = row | (m.c.th > 0.0 ? FV_HAL_CALL : 0) | ((int64_t)kst << FV_HAL_KSHIFT) |
+                         (midp ? FV_HAL_MIDP : 0);
+      hal_store(recs + slot, m.c, lo, hi, sg, fv, rb);
 #ifdef FV_HAL_RROW
       rrow[slot] = rb;
 #endif
@@ -831,7 +917,7 @@ __device__ __forceinline__ unsigned long long claim(bool need, unsigned long lon
 #define FV_HSM_MINB 3
 #endif
 #ifndef FV_HAL_PREFETCH
-#define FV_HAL_PREFETCH 1
+#define FV_HAL_PREFETCH 0
 #endif
 
 // One-record-ahead prefetch for the Halley passes' refill: each lane claims
@@ -898,9 +984,11 @@ __global__ void __launch_bounds__(256, FV_HSM_MINB) k_halley_iter(KArgs a, HalRe
       rec = reinterpret_cast<const int32_t*>(my_next + 12)[0];
       int64_t rb;
       hal_take(my_next, c, lo, hi, sigma, fval, rb);
-      row = rb & (FV_HAL_CALL - 1);
+      row = rb & FV_HAL_ROWMASK;
       has_next = false;
-      k = 0; midp = false; busy = true;
+      k = (int)((rb >> FV_HAL_KSHIFT) & 31);
+      midp = (rb & FV_HAL_MIDP) != 0;
+      busy = true;
     }
 #else
     const bool need = !busy && !exhausted;
@@ -912,72 +1000,35 @@ __global__ void __launch_bounds__(256, FV_HSM_MINB) k_halley_iter(KArgs a, HalRe
         rec = (int32_t)jq;
 #ifdef FV_HAL_RROW
         const int64_t rb0 = rrow[rec];
-        row = rb0 & (FV_HAL_CALL - 1);
+        row = rb0 & FV_HAL_ROWMASK;
 #endif
         int64_t rb;
         hal_load(recs + rec, c, lo, hi, sigma, fval, rb);
 #ifndef FV_HAL_RROW
-        row = rb & (FV_HAL_CALL - 1);
+        row = rb & FV_HAL_ROWMASK;
 #endif
-        k = 0; midp = false; busy = true;
+        k = (int)((rb >> FV_HAL_KSHIFT) & 31);
+        midp = (rb & FV_HAL_MIDP) != 0;
+        busy = true;
       }
     }
 #endif
+#if FV_ERFC_CTA
+    if (!__syncthreads_or(busy)) break;          // the block's warps share the erfc rounds
+#else
     if (!__any_sync(0xffffffffu, busy)) break;
-    // next evaluation point (:118-128)
-    double x = 0.5 * (lo + hi);
-    bool chk = false;
-    bool hb = false;
-    if (busy && !midp) {
-      FxBad vb;
-      const double s = sigma * c.sqrt_t;
-      double vega = 0.0, d1 = 0.0;
-      if (!(s < FV_K_1EM12)) {
-        d1 = fx_div0(c.lnFK + 0.5 * s * s, s, vb);
-        vega = c.disc * c.Fw * fx_norm_pdf(d1, vb) * c.sqrt_t;
-      }
-      double cn = __builtin_nan("");
-      if (vega > 0.0) {
-        const double d2 = d1 - s;
-        const double vomma = fx_div0(vega * d1 * d2, sigma, vb);
-        const double denom = 2.0 * vega * vega - fval * vomma;
-        if (denom != 0.0) cn = sigma - fx_div0(2.0 * fval * vega, denom, vb);
-      }
-      if (fv_isfinite(cn) && lo < cn && cn < hi) { x = cn; chk = true; }
-      if (vb) hb = true;
-    }
-    if (hb) busy = false;
-    __syncwarp();
-    FxBad fb;
-    const double fx = fx_halley_f_warp(busy, c, x, fb, sm_x[wib], sm_r[wib], sm_f[wib]);
-    __syncwarp();
-    if (busy && fb) { hb = true; busy = false; }
-    int fin = -1;
-    bool to_bis = false;
-    if (busy) {
-      if (chk && !(fv_fabs(fx) < fv_fabs(fval))) {          // :129-135: rejected -> f(mid) next
-        midp = true;
-      } else {                                               // :136-144
-        midp = false;
-        if (fx > 0.0) hi = x;
-        else if (fx < 0.0) lo = x;
-        const double step = x - sigma;
-        sigma = x; fval = fx;
-        if (fv_fabs(step) <= FV_K_1EM12 * py_max(1.0, sigma)) fin = FV_IV_CONVERGED;
-        else if (++k == 16) to_bis = true;
-        else if (fv_fabs(fval) <= c.tol_price) fin = FV_IV_CONVERGED;   // :116-117 of the next step
-      }
-    }
+#endif
+    int fin;
+    bool to_bis, hb;
+    hal_trip(busy, midp, k, c, lo, hi, sigma, fval, fin, to_bis, hb, sm_x[wib], sm_r[wib], sm_f[wib]);
     if (fin >= 0) {
       a.o0[row] = sigma;
       a.status[row] = (int8_t)fin;
-      busy = false;
     }
     if (to_bis) {
       double2* p = reinterpret_cast<double2*>(recs + rec);
       p[4] = make_double2(lo, hi);
       p[5] = make_double2(sigma, fval);
-      busy = false;
     }
     const unsigned int bs = warp_append(nbis, to_bis);
     if (to_bis) bis[bs] = rec;
@@ -1013,17 +1064,21 @@ __global__ void __launch_bounds__(256, FV_HSM_MINB) k_halley_bisect(KArgs a, con
         const int32_t rec = bis[jq];
 #ifdef FV_HAL_RROW
         const int64_t rb0 = rrow[rec];
-        row = rb0 & (FV_HAL_CALL - 1);
+        row = rb0 & FV_HAL_ROWMASK;
 #endif
         int64_t rb;
         hal_load(recs + rec, c, lo, hi, sigma, fval, rb);
 #ifndef FV_HAL_RROW
-        row = rb & (FV_HAL_CALL - 1);
+        row = rb & FV_HAL_ROWMASK;
 #endif
         k = 0; busy = true;
       }
     }
+#if FV_ERFC_CTA
+    if (!__syncthreads_or(busy)) break;          // the block's warps share the erfc rounds
+#else
     if (!__any_sync(0xffffffffu, busy)) break;
+#endif
     if (busy && (fv_fabs(fval) <= c.tol_price || (hi - lo) <= FV_K_1EM12 * py_max(1.0, sigma))) {
       a.o0[row] = sigma;                                     // :147-149
       a.status[row] = (int8_t)FV_IV_FELL_BACK;
@@ -1281,6 +1336,11 @@ const char* const kKernelNames[FV_NKERNEL] = {
     "k_halley_bracket", "k_halley_iter", "k_halley_careful", "k_lbr_near_fast", "k_halley_bisect"};
 struct TimedLaunch { int id; cudaEvent_t a, b; };
 thread_local bool t_timing = false;
+// Device span of a device-pointer call (fv_set_span_timing): events around
+// its launches on the call's stream, without serialising anything -- the
+// difference to the caller's own per-call time is host overhead.
+thread_local bool t_span = false;
+thread_local float t_span_ms = -1.0f;
 thread_local std::vector<TimedLaunch> t_timed;
 inline void time_begin(int id, cudaStream_t s) {
   if (!t_timing) return;
@@ -1320,6 +1380,7 @@ struct DevWork {
   char* stage[FV_NSLOT] = {};              // pinned host staging (pageable callers)
   int64_t stage_cap[FV_NSLOT] = {};
   ExplainOut* explain = nullptr;
+  double* scal = nullptr;               // device copies of a host call's broadcast scalars
   // LBR classify -> solve workspace (per slot)
   double* lbr_state[FV_NSLOT] = {};     // 8 SoA fields x lbr_cap
   int32_t* lbr_q[FV_NSLOT] = {};        // 6 queues of lbr_cap entries each
@@ -1373,6 +1434,7 @@ cudaError_t get_work(DevWork** out) {
     CK(cudaMalloc(&w->st, 2 * sizeof(FvDevStatus)));
     CK(cudaMallocHost(&w->st_host, 2 * sizeof(FvDevStatus)));
     CK(cudaMalloc(&w->explain, sizeof(ExplainOut)));
+    CK(cudaMalloc(&w->scal, 8 * sizeof(double)));
     w->blocks_price = occupancy_blocks((const void*)k_price, w->sm_count);
     w->blocks_greeks = occupancy_blocks((const void*)k_price_greeks<true, true>, w->sm_count);
     CK(cudaMalloc(&w->lbr_count, sizeof(unsigned int) * 16 * FV_NSLOT));
@@ -1471,6 +1533,7 @@ struct Call {
   int8_t* region;
   bool want_price, want_greeks;
   uint32_t bbits_iv;   // KIND_PRICE_IV: host-checked broadcast-column bits of the IV stage
+  bool bcast_dev;      // device call: broadcast columns are checked by the kernels (row 0 wins)
 };
 
 // fv_price_iv's IV stage: batch_iv over the price column the price stage
@@ -1867,7 +1930,7 @@ KArgs base_args(const Call& c, DevWork* w) {
                                 {FV_CHECK_NONFINITE_Q, FV_CHECK_DIVIDEND, -1},
                                 {FV_CHECK_NONFINITE_LAST, FV_CHECK_NONNEG_SIGMA, -1}};
   for (int col = 0; col < 7; ++col)
-    if (c.cols[col].stride == 0)
+    if (c.cols[col].stride == 0 && !c.bcast_dev)
       for (int j = 0; j < 3; ++j)
         if (col_checks[col][j] >= 0) mask &= ~(1u << col_checks[col][j]);
   a.check_mask = mask;
@@ -1893,11 +1956,24 @@ int run_device(DevWork* w, const Call& c, cudaStream_t s, uint32_t bcast_bits, f
   a.row0 = 0;
   a.o0 = c.outs[0]; a.o1 = c.outs[1]; a.o2 = c.outs[2];
   a.o3 = c.outs[3]; a.o4 = c.outs[4]; a.o5 = c.outs[5];
+  cudaEvent_t sp0 = nullptr, sp1 = nullptr;
+  if (t_span) {
+    cudaEventCreate(&sp0);
+    cudaEventCreate(&sp1);
+    cudaEventRecord(sp0, s);
+  }
   if ((ce = cudaMemsetAsync(w->st, 0xff, 2 * sizeof(FvDevStatus), s)) != cudaSuccess) return set_cuda_err(e1, ce);
   if ((ce = launch(w, c, a, 0, s)) != cudaSuccess) return set_cuda_err(e1, ce);
+  if (t_span) cudaEventRecord(sp1, s);
   if ((ce = cudaMemcpyAsync(w->st_host, w->st, 2 * sizeof(FvDevStatus), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return set_cuda_err(e1, ce);
   if ((ce = cudaStreamSynchronize(s)) != cudaSuccess) return set_cuda_err(e1, ce);
+  if (t_span) {
+    t_span_ms = -1.0f;
+    cudaEventElapsedTime(&t_span_ms, sp0, sp1);
+    cudaEventDestroy(sp0);
+    cudaEventDestroy(sp1);
+  }
   if (c.kind == KIND_PRICE_IV) return finish_price_iv(w, c, a, iv_stage_args(a, w), bcast_bits, s, e1, e2);
   return finish(w, c, a, bcast_bits, s, e1, e2, w->st_host[0]);
 }
@@ -2324,25 +2400,23 @@ int dispatch(Call c, fv_error* e1, fv_error* e2) {
   cudaError_t ce = get_work(&w);
   if (ce != cudaSuccess) return set_cuda_err(e1, ce);
   std::lock_guard<std::mutex> g(w->mu);
-  // broadcast scalars: checked once on the host; for host calls they are
-  // copied into a small device buffer.
+  // broadcast scalars of a host call: checked once on the host and copied
+  // into the device's scalar slot.  A device call does not read them back
+  // (a synchronous device -> host copy per column, ~10 us each, before any
+  // launch): its kernels check them like any column, and every row failing
+  // such a check puts the reported row at 0, as the host check does.
   bool bc[7];
   double vals[7] = {0, 0, 0, 0, 0, 0, 0};
   int flag_val = 0;
   for (int i = 0; i < 7; ++i) bc[i] = c.cols[i].stride == 0;
-  double* dscal = nullptr;
-  int8_t* dflag = nullptr;
-  if (bc[0]) {
-    if (device) cudaMemcpy(&flag_val, c.cols[0].data, 1, cudaMemcpyDeviceToHost), flag_val = (int)(int8_t)flag_val;
-    else flag_val = *(const int8_t*)c.cols[0].data;
+  c.bcast_dev = device;
+  if (!device) {
+    if (bc[0]) flag_val = *(const int8_t*)c.cols[0].data;
+    for (int i = 1; i < 7; ++i)
+      if (bc[i]) vals[i] = *(const double*)c.cols[i].data;
   }
-  for (int i = 1; i < 7; ++i)
-    if (bc[i]) {
-      if (device) cudaMemcpy(&vals[i], c.cols[i].data, 8, cudaMemcpyDeviceToHost);
-      else vals[i] = *(const double*)c.cols[i].data;
-    }
-  uint32_t bbits = c.n > 0 ? bcast_checks(c, vals, flag_val, bc) : 0;
-  if (c.kind == KIND_PRICE_IV && c.n > 0) {
+  uint32_t bbits = (c.n > 0 && !device) ? bcast_checks(c, vals, flag_val, bc) : 0;
+  if (c.kind == KIND_PRICE_IV && c.n > 0 && !device) {
     // the IV stage reads the same broadcast columns; its price column is the
     // price stage's n-row output (never broadcast)
     Call ci = c;
@@ -2353,16 +2427,17 @@ int dispatch(Call c, fv_error* e1, fv_error* e2) {
     c.bbits_iv = bcast_checks(ci, vals, flag_val, bci);
   }
   if (!device) {
-    // device copies of the broadcast scalars (8 doubles, one allocation per call)
-    if ((ce = cudaMalloc(&dscal, 8 * 8)) != cudaSuccess) return set_cuda_err(e1, ce);
+    // device copies of the broadcast scalars (the DevWork's slot; host calls
+    // are synchronous, so the slot is free again when the next one starts)
     double tmp[8] = {0};
     int8_t f8 = (int8_t)flag_val;
     memcpy(&tmp[7], &f8, 1);
     for (int i = 1; i < 7; ++i) tmp[i] = vals[i];
-    cudaMemcpy(dscal, tmp, sizeof(tmp), cudaMemcpyHostToDevice);
-    dflag = (int8_t*)(dscal + 7);
+    if ((ce = cudaMemcpy(w->scal, tmp, sizeof(tmp), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return set_cuda_err(e1, ce);
+    const int8_t* dflag = (const int8_t*)(w->scal + 7);
     for (int i = 0; i < 7; ++i)
-      if (bc[i]) c.cols[i].data = (i == 0) ? (const void*)dflag : (const void*)(dscal + i);
+      if (bc[i]) c.cols[i].data = (i == 0) ? (const void*)dflag : (const void*)(w->scal + i);
   }
   int rc;
   if (device) {
@@ -2371,7 +2446,6 @@ int dispatch(Call c, fv_error* e1, fv_error* e2) {
   } else {
     rc = run_host(w, c, bbits, e1, e2);
   }
-  if (dscal) cudaFree(dscal);
   return rc;
 }
 
@@ -2610,6 +2684,13 @@ FV_API int fv_set_round_rows(int64_t lbr_rows, int64_t halley_rows) {
   g_halley_round = halley_rows ? halley_rows : (1ll << 26);
   return FV_OK;
 }
+
+FV_API int fv_set_span_timing(int on) {
+  t_span = on != 0;
+  return FV_OK;
+}
+
+FV_API double fv_last_span_ms(void) { return (double)t_span_ms; }
 
 FV_API int fv_set_kernel_timing(int on) {
   t_timing = on != 0;

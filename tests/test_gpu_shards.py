@@ -108,3 +108,45 @@ def test_gather_uneven_sources(setup):
     parts = [torch.arange(k, dtype=torch.float64, device=dev) + 1000 * i for i, k in enumerate((5, 0, 17, 1))]
     g = D.gather_device(parts, dev)
     assert torch.equal(g, torch.cat(parts))
+
+
+@pytest.mark.parametrize("case", ["neg_underlying", "nan_r", "dividend_black", "bad_flag", "neg_t_and_nan_k"])
+def test_device_broadcast_column_checks_match_host(setup, case):
+    """Device calls check broadcast (stride-0) columns in the kernels instead
+    of reading them back to the host: the reported BatchError (check, row 0,
+    message) is the host call's, also when a row-wise column fails a LATER
+    check at an earlier row."""
+    import torch
+    from paper_2604_27210_b200 import _native
+    lib, dev, bench, cols, n = setup
+    m = 2000
+    h = {k: (v[:m].cpu().numpy().copy() if v.numel() > 1 else v.cpu().numpy().copy()) for k, v in cols.items()}
+    model = 2
+    if case == "neg_underlying":
+        h["underlying"] = np.array([-1.0])
+    elif case == "nan_r":
+        h["r"] = np.array([np.nan])
+    elif case == "dividend_black":
+        model = 0
+        h["q"] = np.array([0.01])
+    elif case == "bad_flag":
+        h["flag"] = np.array([3], np.int8)
+    else:
+        h["t"] = np.array([-0.5])
+        h["strike"][7] = np.nan
+    d = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in h.items()}
+    res = []
+    for src in (h, d):
+        for method in (1, 0):
+            iv = (torch.empty(m, dtype=torch.float64, device=dev) if src is d else np.empty(m))
+            st = (torch.empty(m, dtype=torch.int8, device=dev) if src is d else np.empty(m, np.int8))
+            err = _native.fv_error()
+            rc = lib.fv_batch_iv(model, method, *bench.native_cols(src, "price"), m, _native.ptr(iv),
+                                 _native.ptr(st), None, err)
+            res.append((rc, err.kind, err.index, err.message))
+    assert all(r == res[0] for r in res), res
+    assert res[0][0] == _native.FV_ERR_BATCH
+    if case == "neg_t_and_nan_k":
+        assert res[0][2] == 7                    # NonFinite strike (earlier check) at row 7 beats t < 0 at row 0
+    else:
+        assert res[0][2] == 0
