@@ -34,6 +34,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -763,7 +765,7 @@ __device__ __forceinline__ void hal_trip(bool& busy, bool& midp, int& k, const F
 // the loop, mode 3 steps), and here they run with all lanes of a warp busy and
 // no claim / record reload, against ~24 of 32 lanes in the refill loop.
 #ifndef FV_HAL_BRACKET_TRIPS
-#define FV_HAL_BRACKET_TRIPS 2
+#define FV_HAL_BRACKET_TRIPS 0
 #endif
 #ifndef FV_HSET_MINB
 #define FV_HSET_MINB 3
@@ -1982,23 +1984,80 @@ int run_device(DevWork* w, const Call& c, cudaStream_t s, uint32_t bcast_bits, f
 // Host memcpy split over threads: pageable caller buffers are moved through
 // pinned staging slots, and one thread's memcpy (~11 GB/s) would otherwise
 // cap the pipeline far below the link (~50 GB/s pinned).
+// A persistent pool of host copy workers (created on first use): a pageable
+// call's staging copies are split into 8 MB+ parts spread over the workers and
+// the calling thread, without creating threads per copy (thread start-up was
+// ~50 us per thread per column per chunk).
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool* pool = new CopyPool();      // never destroyed: workers outlive static teardown
+    return *pool;
+  }
+  int workers() const { return (int)th_.size(); }
+  // runs fn(0..parts-1), part 0 on the caller; returns when all are done
+  void run(int parts, const std::function<void(int)>& fn) {
+    std::unique_lock<std::mutex> lk(mu_);
+    job_ = &fn;
+    next_ = 1;
+    parts_ = parts;
+    pending_ = parts - 1;
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    fn(0);
+    lk.lock();
+    done_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  CopyPool() {
+    unsigned nt = std::thread::hardware_concurrency();
+    if (nt > 8) nt = 8;
+    for (unsigned k = 1; k < nt; ++k) th_.emplace_back([this] { loop(); });
+  }
+  void loop() {
+    unsigned long long seen = 0;
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+      cv_.wait(lk, [&] { return gen_ != seen && job_ && next_ < parts_; });
+      seen = gen_;
+      while (job_ && next_ < parts_) {
+        const int part = next_++;
+        const std::function<void(int)>* fn = job_;
+        lk.unlock();
+        (*fn)(part);
+        lk.lock();
+        if (--pending_ == 0) done_.notify_all();
+      }
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int next_ = 0, parts_ = 0, pending_ = 0;
+  unsigned long long gen_ = 0;
+};
+std::mutex g_copy_mu;     // one pooled copy at a time (calls on several devices share the pool)
+
 void par_memcpy(char* dst, const char* src, size_t bytes) {
   const size_t kMin = (size_t)8 << 20;
-  unsigned nt = std::thread::hardware_concurrency();
-  if (nt > 8) nt = 8;
-  if (nt < 2 || bytes < 2 * kMin) { memcpy(dst, src, bytes); return; }
+  if (bytes < 2 * kMin) { memcpy(dst, src, bytes); return; }
+  CopyPool& pool = CopyPool::get();
   size_t parts = bytes / kMin;
-  if (parts > nt) parts = nt;
+  const size_t cap = (size_t)pool.workers() + 1;
+  if (parts > cap) parts = cap;
+  if (parts < 2) { memcpy(dst, src, bytes); return; }
   const size_t per = ((bytes / parts) + 4095) & ~(size_t)4095;
-  std::vector<std::thread> th;
-  for (size_t k = 1; k < parts; ++k) {
-    const size_t o = k * per;
-    if (o >= bytes) break;
+  std::lock_guard<std::mutex> g(g_copy_mu);
+  pool.run((int)parts, [=](int k) {
+    const size_t o = (size_t)k * per;
+    if (o >= bytes) return;
     const size_t len = (o + per <= bytes) ? per : bytes - o;
-    th.emplace_back([=] { memcpy(dst + o, src + o, len); });
-  }
-  memcpy(dst, src, per < bytes ? per : bytes);
-  for (auto& t : th) t.join();
+    memcpy(dst + o, src + o, len);
+  });
 }
 
 bool is_pageable(const void* p) {
