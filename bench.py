@@ -87,7 +87,8 @@ def parse(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle pass (cpu_baseline + parity)")
     ap.add_argument("--no-kernel-timing", action="store_true",
-                    help="skip the per-kernel event-timing pass (ncu traffic captures)")
+                    help="skip the per-kernel event-timing and device-span passes (ncu traffic captures: "
+                         "only the timed calls run)")
     return ap.parse_args(argv)
 
 
@@ -586,6 +587,8 @@ def run_ours(args):
     # serialised): per_call_ms - span = host overhead of the synchronous call
     span_ms = None
     try:
+        if args.no_kernel_timing:
+            raise RuntimeError("skipped (--no-kernel-timing)")
         lib.fv_set_span_timing(1)
         spans = []
         for _ in range(max(1, min(args.steps, 5))):

@@ -29,9 +29,13 @@ def main():
     thr_op = Counter()
     stall_op = Counter()
     insts = []
+    seen = set()
     for r in rows[hdr + 1:]:
         if len(r) <= ci:
             continue
+        if r[0] in seen:           # the source page can list a kernel's SASS twice
+            continue
+        seen.add(r[0])
         try:
             n = int(r[ci]); nt = int(r[ct]); st = int(r[cst] or 0)
         except ValueError:

@@ -54,7 +54,7 @@ def main(tag):
         if os.path.exists(path):
             lines.append(open(path).read().strip().splitlines()[-1])
     open(os.path.join(P, f"{tag}_bench_lines.jsonl"), "w").write("\n".join(lines) + "\n")
-    for rep, name in (("prof", "lbr"), ("profh", "halley")):
+    for rep, name in (("prof", "lbr"), ("profh", "halley"), ("profg", "price_greeks")):
         src = os.path.join(G, f"{rep}_{tag}.ncu-rep")
         if os.path.exists(src):
             out = subprocess.run([sys.executable, os.path.join(REPO, "tools", "ncu_summary.py"), src],
@@ -62,6 +62,11 @@ def main(tag):
             open(os.path.join(P, f"{tag}_ncu_{name}.txt"), "w").write(out)
     if os.path.exists(os.path.join(G, f"launches_{tag}.csv")):
         launches(tag)
+    for name in (f"api_e2e_{tag}.json", f"pytest_gpu_{tag}.txt", f"smoke_{tag}.txt", f"cpu_{tag}.txt",
+                 f"gpu_{tag}.txt"):
+        src = os.path.join(G, name)
+        if os.path.exists(src):
+            shutil.copy(src, os.path.join(P, name))
     specs = []
     for w, n in ROWS.items():
         src = os.path.join(G, f"traffic_{tag}_{w}.csv")
