@@ -1983,7 +1983,7 @@ int run_device(DevWork* w, const Call& c, cudaStream_t s, uint32_t bcast_bits, f
 // Host-pointer path: chunked H2D -> kernel -> D2H, FV_NSLOT streams.
 // Host memcpy split over threads: pageable caller buffers are moved through
 // pinned staging slots, and one thread's memcpy (~11 GB/s) would otherwise
-// cap the pipeline far below the link (~50 GB/s pinned).
+// cap the pipeline far below the link (~55 GB/s pinned).
 // A persistent pool of host copy workers (created on first use): a pageable
 // call's staging copies are split into 8 MB+ parts spread over the workers and
 // the calling thread, without creating threads per copy (thread start-up was
@@ -2014,7 +2014,7 @@ class CopyPool {
  private:
   CopyPool() {
     unsigned nt = std::thread::hardware_concurrency();
-    if (nt > 8) nt = 8;
+    if (nt > 16) nt = 16;
     for (unsigned k = 1; k < nt; ++k) th_.emplace_back([this] { loop(); });
   }
   void loop() {
@@ -2042,23 +2042,35 @@ class CopyPool {
 };
 std::mutex g_copy_mu;     // one pooled copy at a time (calls on several devices share the pool)
 
-void par_memcpy(char* dst, const char* src, size_t bytes) {
-  const size_t kMin = (size_t)8 << 20;
-  if (bytes < 2 * kMin) { memcpy(dst, src, bytes); return; }
+// A batch of copies (the staged columns of one chunk) as one pool job: every
+// segment is cut into ~2 MB parts and all parts share the workers, so a chunk's
+// columns are copied together instead of one fork / join per column.
+struct CopySeg { char* dst; const char* src; size_t bytes; };
+void par_memcpy_batch(const std::vector<CopySeg>& segs) {
+  const size_t kPart = (size_t)2 << 20;
+  struct Part { char* dst; const char* src; size_t bytes; };
+  std::vector<Part> parts;
+  size_t total = 0;
+  for (const CopySeg& g : segs) {
+    total += g.bytes;
+    for (size_t o = 0; o < g.bytes; o += kPart)
+      parts.push_back({g.dst + o, g.src + o, (o + kPart <= g.bytes) ? kPart : g.bytes - o});
+  }
+  if (parts.empty()) return;
+  if (total < ((size_t)4 << 20) || parts.size() < 2) {
+    for (const Part& q : parts) memcpy(q.dst, q.src, q.bytes);
+    return;
+  }
   CopyPool& pool = CopyPool::get();
-  size_t parts = bytes / kMin;
-  const size_t cap = (size_t)pool.workers() + 1;
-  if (parts > cap) parts = cap;
-  if (parts < 2) { memcpy(dst, src, bytes); return; }
-  const size_t per = ((bytes / parts) + 4095) & ~(size_t)4095;
+  const int nw = pool.workers() + 1;
+  const int nparts = (int)parts.size();
+  const int ntask = nparts < nw ? nparts : nw;
   std::lock_guard<std::mutex> g(g_copy_mu);
-  pool.run((int)parts, [=](int k) {
-    const size_t o = (size_t)k * per;
-    if (o >= bytes) return;
-    const size_t len = (o + per <= bytes) ? per : bytes - o;
-    memcpy(dst + o, src + o, len);
+  pool.run(ntask, [&](int k) {                       // task k: parts k, k + ntask, ...
+    for (int i = k; i < nparts; i += ntask) memcpy(parts[i].dst, parts[i].src, parts[i].bytes);
   });
 }
+
 
 bool is_pageable(const void* p) {
   cudaPointerAttributes at;
@@ -2131,10 +2143,12 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
     cudaEventSynchronize(slot_done[s]);
     const int64_t r0 = ci * chunk, rn = (r0 + chunk < n ? chunk : n - r0);
     char* st = w->stage[s];
+    std::vector<CopySeg> segs;
     for (int i = 0; i < 6; ++i)
-      if (stage_out[i]) par_memcpy((char*)(c.outs[i] + r0), st + off_out[i], 8 * rn);
-    if (stage_status) par_memcpy((char*)(c.status + r0), st + off_status, rn);
-    if (stage_region) par_memcpy((char*)(c.region + r0), st + off_region, rn);
+      if (stage_out[i]) segs.push_back({(char*)(c.outs[i] + r0), st + off_out[i], (size_t)(8 * rn)});
+    if (stage_status) segs.push_back({(char*)(c.status + r0), st + off_status, (size_t)rn});
+    if (stage_region) segs.push_back({(char*)(c.region + r0), st + off_region, (size_t)rn});
+    par_memcpy_batch(segs);
     slot_chunk[s] = -1;
   };
   if ((ce = cudaMemsetAsync(w->st, 0xff, 2 * sizeof(FvDevStatus), w->streams[0])) != cudaSuccess)
@@ -2153,15 +2167,20 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
     char* base = w->chunk[slot];
     char* stg = w->stage[slot];
     if (any_stage) drain(slot);               // the slot's previous chunk is done with staging
+    {                                         // the chunk's pageable input columns, one pool job
+      std::vector<CopySeg> segs;
+      for (int col = 0; col < 7; ++col)
+        if (c.cols[col].stride != 0 && stage_in[col])
+          segs.push_back({stg + off_in[col], (const char*)c.cols[col].data + r0 * in_sz[col],
+                          (size_t)(rn * in_sz[col])});
+      par_memcpy_batch(segs);
+    }
     void* dev_in[7];
     for (int col = 0; col < 7; ++col) {
       if (c.cols[col].stride == 0) { dev_in[col] = nullptr; continue; }
       dev_in[col] = base + off_in[col];
       const char* src = (const char*)c.cols[col].data + r0 * in_sz[col];
-      if (stage_in[col]) {
-        par_memcpy(stg + off_in[col], src, rn * in_sz[col]);
-        src = stg + off_in[col];
-      }
+      if (stage_in[col]) src = stg + off_in[col];
       if ((ce = cudaMemcpyAsync(dev_in[col], src, rn * in_sz[col], cudaMemcpyHostToDevice, s)) != cudaSuccess) {
         cudaEventDestroy(ready);
         return set_cuda_err(e1, ce);
