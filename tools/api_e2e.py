@@ -34,9 +34,16 @@ def main():
     B.parse_flags(chars)
     B._fvhost = _fvh
     out["parse_flags_numpy_s"] = time.perf_counter() - t0
+    ts = []
+    for _ in range(3):                       # first call of this size pays one-time costs
+        t0 = time.perf_counter()
+        res = fv.batch_iv("black", "lbr", chars, F[:1], K, t, r[:1], price=px)
+        ts.append(time.perf_counter() - t0)
+    out["batch_iv_total_s"] = min(ts)
+    out["batch_iv_total_s_runs"] = ts
     t0 = time.perf_counter()
-    res = fv.batch_iv("black", "lbr", chars, F[:1], K, t, r[:1], price=px)
-    out["batch_iv_total_s"] = time.perf_counter() - t0
+    B._assemble(B.as_model("black"), chars, F[:1], K, t, r[:1], 0.0, price=px)
+    out["assemble_s"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     _ = B._status_column(B._IV_STATUS, np.zeros(n, np.int8))
     out["status_strings_s"] = time.perf_counter() - t0
@@ -53,6 +60,9 @@ def main():
     t0 = time.perf_counter()
     lib.fv_batch_iv(0, 1, *cols, n, iv.ctypes.data, st.ctypes.data, None, err)
     out["c_abi_pageable_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    lib.fv_batch_iv(0, 1, *cols, n, iv.ctypes.data, st.ctypes.data, None, err)
+    out["c_abi_pageable_touched_out_s"] = time.perf_counter() - t0
     out["quotes_per_s_python_api"] = n / out["batch_iv_total_s"]
     out["quotes_per_s_c_abi_pageable"] = n / out["c_abi_pageable_s"]
     assert np.array_equal(iv.view(np.int64), res["iv"].view(np.int64))
