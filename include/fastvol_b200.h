@@ -230,11 +230,6 @@ FV_API int64_t fv_last_launch_count(void);
  * depend on it; tests force multi-round calls on small batches with it. */
 FV_API int fv_set_round_rows(int64_t lbr_rows, int64_t halley_rows);
 
-/* LBR rounds of fewer rows than this take the small-batch path: the
- * remaining anchors inside the normalize pass and the far-low + near solves
- * in one kernel (default 2^23; 0 = never).  Results do not depend on it. */
-FV_API int fv_set_lbr_eager_rows(int64_t rows);
-
 /* Raw outcome of the calling thread's last batch call: per validation check
  * (FV_CHECK_* order) the first failing row or -1; the first raising row and
  * its FV_EXC_* code for the price/iv stream [0] and the Greeks stream [1]
@@ -280,8 +275,7 @@ FV_API int fv_selftest_fast(int64_t n, uint64_t seed, int64_t* mismatches /*[11]
 #define FV_KID_HALLEY_SM2 11
 #define FV_KID_LBR_NEAR_FAST 12
 #define FV_KID_HALLEY_BISECT 13
-#define FV_KID_LBR_SOLVE_FAST 14
-#define FV_NKERNEL 15
+#define FV_NKERNEL 14
 FV_API int fv_set_kernel_timing(int on);
 
 /* Device span of this thread's last device-pointer call (diagnostics; off by

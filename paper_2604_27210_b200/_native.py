@@ -67,7 +67,6 @@ SIGNATURES = {
     "fv_set_chunk_rows": ([_I64], ctypes.c_int),
     "fv_last_launch_count": ([], _I64),
     "fv_set_round_rows": ([_I64, _I64], ctypes.c_int),
-    "fv_set_lbr_eager_rows": ([_I64], ctypes.c_int),
     "fv_probe_fp64_peak": ([_P, _P], ctypes.c_int),
     "fv_last_outcome": ([_P, _P, _P], ctypes.c_int),
     "fv_selftest_div_const": ([_I64, ctypes.c_uint64, _P], ctypes.c_int),
@@ -184,7 +183,7 @@ def last_outcome(lib):
     return cr, er, ec
 
 
-NKERNEL = 15
+NKERNEL = 14
 
 
 def kernel_times(lib):

@@ -396,41 +396,7 @@ __device__ __forceinline__ void lbr_norm_row_careful(const KArgs& a, const LbrQu
 // 4-block form (64 registers, ~110 B of spills; C4 13.70 -> 13.61 ms), small
 // ones the 3-block form (80 registers; C1 is latency-bound and 2.5 % slower
 // at 4) -- see FV_NORM_BIG_ROWS.
-__device__ __noinline__ int anchor_rest_careful(FvLbrState& st, FvExc& e);
-
-// The rest of _region for one pending row (lbr.py:231-248): b_c, and b_hi only
-// if beta >= b_c, straight-line with the careful form where it flags; state
-// (b0 / E0, b1 / E1) as k_lbr_solve / k_lbr_near_fast read it, region out.
-// Returns the region class (1 near, 2 far-high) or -1 (the row is finished:
-// the careful form raised).  Shared by k_lbr_anchors and the eager normalize.
-__device__ __noinline__ int lbr_anchor_row(const KArgs& a, const LbrQueues& lq, int32_t row, FvLbrState& st,
-                                           int& region) {
-  FvExc e = {0, 0, 0.0};
-  FxBad flagged;
-  FvLbrState sf = st;
-  region = fx_lbr_anchor_rest(sf, flagged);            // straight-line form
-  if (flagged) region = anchor_rest_careful(st, e);   // range edge: careful form
-  else st = sf;
-  if (region < 0) {
-    publish_exc(&a.st->exc_first, e.code, a.row0 + row);
-    a.o0[row] = __builtin_nan("");
-    a.status[row] = (int8_t)FV_IV_MAX_ITER;
-    return -1;
-  }
-  if (region != FV_FAR_HIGH) {
-    if (region == FV_NEAR_HIGH) { lq.sb0[row] = st.b0; lq.sE0[row] = st.E0; }
-    lq.sb1[row] = st.b1; lq.sE1[row] = st.E1;
-  }
-  if (a.region) a.region[row] = (int8_t)region;
-  return region_class(region);
-}
-
-// kEager (small batches, FV_LBR_EAGER_ROWS): the pending rows' remaining
-// anchors are computed here, in the same pass, and the rows go straight to
-// the near / far-high queues (1, 2) -- one dependent pass fewer on the way to
-// the solves, which then run as one kernel (k_lbr_solve_fast); without it
-// they go to queue 3 for k_lbr_anchors.
-template <int MINB, bool kEager>
+template <int MINB>
 __global__ void __launch_bounds__(256, MINB) k_lbr_normalize(KArgs a, LbrQueues lq) {
   const int64_t npair = (a.n + 1) >> 1;
   const int lane = threadIdx.x & 31;
@@ -451,7 +417,6 @@ __global__ void __launch_bounds__(256, MINB) k_lbr_normalize(KArgs a, LbrQueues 
     const int64_t i = 2 * j;
     const bool two = active && (i + 1 < a.n);
     bool pend[2] = {false, false}, flow[2] = {false, false}, rep[2] = {false, false};
-    int ncls[2] = {0, 0}, nreg[2] = {0, 0};          // kEager: class (1 near, 2 far-high) / region
     Pair p;
     if (active) load_pair(a, i, two, p);
 #pragma unroll 1
@@ -485,12 +450,6 @@ __global__ void __launch_bounds__(256, MINB) k_lbr_normalize(KArgs a, LbrQueues 
         lq.sx[row] = st.x; lq.sbeta[row] = st.beta;
         if (pending) { lq.sb0[row] = st.b0; lq.sE0[row] = st.E0; }   // read by pass 2
       }
-      if (kEager && pending) {
-        int region = -1;
-        const int cls = lbr_anchor_row(a, lq, (int32_t)row, st, region);
-        if (u) { ncls[1] = cls; nreg[1] = region; } else { ncls[0] = cls; nreg[0] = region; }
-        pending = false;
-      }
       // outputs of finished rows only: far-low / pending rows get theirs from
       // the solve that finishes them (one writer per row, no placeholder
       // write of 9 B per quote), flagged rows from the replay pass
@@ -507,18 +466,9 @@ __global__ void __launch_bounds__(256, MINB) k_lbr_normalize(KArgs a, LbrQueues 
     unsigned int slot = warp_append2(lq.count + 0, flow[0], flow[1]);
     if (flow[0]) { lq.q[0][slot++] = (int32_t)(2 * i); }
     if (flow[1]) { lq.q[0][slot] = (int32_t)(2 * (i + 1)); }
-    if (kEager) {
-#pragma unroll
-      for (int c = 1; c < 3; ++c) {
-        slot = warp_append2(lq.count + c, ncls[0] == c, ncls[1] == c);
-        if (ncls[0] == c) lq.q[c][slot++] = (int32_t)(2 * i + (nreg[0] == FV_NEAR_HIGH ? 1 : 0));
-        if (ncls[1] == c) lq.q[c][slot] = (int32_t)(2 * (i + 1) + (nreg[1] == FV_NEAR_HIGH ? 1 : 0));
-      }
-    } else {
-      slot = warp_append2(lq.count + 3, pend[0], pend[1]);
-      if (pend[0]) { lq.q[3][slot++] = (int32_t)i; }
-      if (pend[1]) { lq.q[3][slot] = (int32_t)(i + 1); }
-    }
+    slot = warp_append2(lq.count + 3, pend[0], pend[1]);
+    if (pend[0]) { lq.q[3][slot++] = (int32_t)i; }
+    if (pend[1]) { lq.q[3][slot] = (int32_t)(i + 1); }
     if (__any_sync(0xffffffffu, rep[0] || rep[1])) {
       slot = warp_append2(lq.count + 5, rep[0], rep[1]);
       if (rep[0]) { lq.q[5][slot++] = (int32_t)i; }
@@ -568,7 +518,23 @@ __global__ void __launch_bounds__(256, FV_ANCH_MINB) k_lbr_anchors(KArgs a, LbrQ
       st.x = lq.sx[row]; st.beta = lq.sbeta[row];
       { FvExc e0 = {0, 0, 0.0}; st.s_c = py_sqrt(2.0 * fv_fabs(st.x), e0); }
       st.b0 = lq.sb0[row]; st.E0 = lq.sE0[row];
-      cls = lbr_anchor_row(a, lq, row, st, region);
+      FvExc e = {0, 0, 0.0};
+      FxBad flagged;
+      FvLbrState sf = st;
+      region = fx_lbr_anchor_rest(sf, flagged);            // straight-line form
+      if (flagged) region = anchor_rest_careful(st, e);   // range edge: careful form
+      else st = sf;
+      if (region < 0) {
+        publish_exc(&a.st->exc_first, e.code, a.row0 + row);
+        a.o0[row] = __builtin_nan("");
+        a.status[row] = (int8_t)FV_IV_MAX_ITER;
+      } else {
+        cls = region_class(region);
+        if (region != FV_FAR_HIGH) {
+          if (region == FV_NEAR_HIGH) { lq.sb0[row] = st.b0; lq.sE0[row] = st.E0; }
+          lq.sb1[row] = st.b1; lq.sE1[row] = st.E1;
+        }
+      }
     }
 #pragma unroll
     for (int c = 1; c < 3; ++c) {
@@ -576,6 +542,7 @@ __global__ void __launch_bounds__(256, FV_ANCH_MINB) k_lbr_anchors(KArgs a, LbrQ
       // entry = local row * 2 + near-high bit (the near class holds both)
       if (cls == c) lq.q[c][slot] = (int32_t)(2 * row + (region == FV_NEAR_HIGH ? 1 : 0));
     }
+    if (j < n && a.region && cls >= 0) a.region[row] = (int8_t)region;
   }
 }
 
@@ -647,53 +614,6 @@ __global__ void __launch_bounds__(256, FV_FAST_MINB) k_lbr_near_fast(KArgs a, Lb
     }
     const unsigned int slot = warp_append(lq.count + 6, (bool)bad);
     if (bad) lq.q[6][slot] = ent;
-  }
-}
-
-// Far-low and near solves in ONE launch (small batches, with the eager
-// normalize): warps claim 32 entries at a time from queue 0 then queue 1, so
-// the two solves share one ramp and one tail instead of two kernels each
-// with their own (a 1M-row batch is ~3 quotes per lane per solve).  Hand-backs
-// to queues 4 / 6 as in the two kernels.
-#ifndef FV_SFAST_MINB
-#define FV_SFAST_MINB 3
-#endif
-__global__ void __launch_bounds__(256, FV_SFAST_MINB) k_lbr_solve_fast(KArgs a, LbrQueues lq) {
-  const unsigned int n0 = lq.count[0], n = n0 + lq.count[1];
-  const int lane = threadIdx.x & 31;
-  for (;;) {
-    unsigned int base = 0;
-    if (lane == 0) base = atomicAdd(lq.count + 7, 32u);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (base >= n) break;
-    const unsigned int j = base + lane;
-    const bool fl = j < n0;
-    FxBad bad;
-    int32_t ent = 0;
-    if (j < n) {
-      ent = fl ? lq.q[0][j] : lq.q[1][j - n0];
-      const int32_t row = ent >> 1;
-      FvLbrState st;
-      st.x = lq.sx[row]; st.beta = lq.sbeta[row];
-      st.sqrt_t = fx_sqrt(ld1(a.t, row), bad);
-      st.s_c = fx_sqrt(2.0 * fv_fabs(st.x), bad);
-      FvLbrOut o;
-      if (fl) {
-        st.b0 = st.b1 = st.E0 = st.E1 = 0.0;
-        o = fx_lbr_far_low(st, bad);
-      } else {
-        st.b0 = lq.sb0[row]; st.b1 = lq.sb1[row]; st.E0 = lq.sE0[row]; st.E1 = lq.sE1[row];
-        o = fx_lbr_near((ent & 1) ? FV_NEAR_HIGH : FV_NEAR_LOW, st, bad);
-      }
-      if (!bad) {
-        a.o0[row] = (o.status == FV_IV_CONVERGED) ? o.sigma : __builtin_nan("");
-        a.status[row] = (int8_t)o.status;
-      }
-    }
-    unsigned int slot = warp_append(lq.count + 4, bad && fl);
-    if (bad && fl) lq.q[4][slot] = ent;
-    slot = warp_append(lq.count + 6, bad && !fl);
-    if (bad && !fl) lq.q[6][slot] = ent;
   }
 }
 
@@ -1415,8 +1335,7 @@ thread_local int64_t t_launches = 0;
 const char* const kKernelNames[FV_NKERNEL] = {
     "k_price", "k_price_greeks", "k_lbr_normalize", "k_lbr_normalize_replay", "k_lbr_anchors",
     "k_lbr_far_low_fast", "k_lbr_solve<FAR_LOW>", "k_lbr_solve<NEAR>", "k_lbr_solve<FAR_HIGH>",
-    "k_halley_bracket", "k_halley_iter", "k_halley_careful", "k_lbr_near_fast", "k_halley_bisect",
-    "k_lbr_solve_fast"};
+    "k_halley_bracket", "k_halley_iter", "k_halley_careful", "k_lbr_near_fast", "k_halley_bisect"};
 struct TimedLaunch { int id; cudaEvent_t a, b; };
 thread_local bool t_timing = false;
 // Device span of a device-pointer call (fv_set_span_timing): events around
@@ -1479,7 +1398,7 @@ struct DevWork {
   int64_t hsm_cap[FV_NSLOT] = {};
   int blocks_hset = 0, blocks_hset_p = 0;
   int blocks_lbr_nfast = 0;
-  int blocks_lbr_norm_big = 0, blocks_lbr_norm_eager = 0, blocks_lbr_sfast = 0;
+  int blocks_lbr_norm_big = 0;
   int blocks_lbr_norm = 0, blocks_lbr_nrep = 0, blocks_lbr_anch = 0, blocks_lbr_fast = 0, blocks_lbr_fl = 0, blocks_lbr_near = 0, blocks_lbr_fh = 0;
   std::mutex mu;
 };
@@ -1521,11 +1440,9 @@ cudaError_t get_work(DevWork** out) {
     w->blocks_price = occupancy_blocks((const void*)k_price, w->sm_count);
     w->blocks_greeks = occupancy_blocks((const void*)k_price_greeks<true, true>, w->sm_count);
     CK(cudaMalloc(&w->lbr_count, sizeof(unsigned int) * 16 * FV_NSLOT));
-    w->blocks_lbr_norm = occupancy_blocks((const void*)k_lbr_normalize<FV_NORM_MINB, false>, w->sm_count);
-    w->blocks_lbr_norm_big = occupancy_blocks((const void*)k_lbr_normalize<FV_NORM_MINB_BIG, false>, w->sm_count);
+    w->blocks_lbr_norm = occupancy_blocks((const void*)k_lbr_normalize<FV_NORM_MINB>, w->sm_count);
+    w->blocks_lbr_norm_big = occupancy_blocks((const void*)k_lbr_normalize<FV_NORM_MINB_BIG>, w->sm_count);
     w->blocks_lbr_nrep = occupancy_blocks((const void*)k_lbr_normalize_replay, w->sm_count);
-    w->blocks_lbr_norm_eager = occupancy_blocks((const void*)k_lbr_normalize<FV_NORM_MINB, true>, w->sm_count);
-    w->blocks_lbr_sfast = occupancy_blocks((const void*)k_lbr_solve_fast, w->sm_count);
     w->blocks_lbr_anch = occupancy_blocks((const void*)k_lbr_anchors, w->sm_count);
     w->blocks_lbr_fast = occupancy_blocks((const void*)k_lbr_far_low_fast, w->sm_count);
     w->blocks_lbr_fl = occupancy_blocks((const void*)k_lbr_solve<FV_FAR_LOW>, w->sm_count);
@@ -1556,12 +1473,6 @@ cudaError_t get_work(DevWork** out) {
 // Runtime-settable (fv_set_round_rows) so tests can force multi-round calls
 // on small batches and check them against single-round ones.
 int64_t g_lbr_round = 1ll << FV_LBR_ROUND_LOG2;
-// LBR rounds below this many rows take the eager path (anchors inside the
-// normalize pass, far-low + near solves in one kernel); fv_set_lbr_eager_rows.
-#ifndef FV_LBR_EAGER_ROWS
-#define FV_LBR_EAGER_ROWS (1ll << 23)
-#endif
-int64_t g_lbr_eager_rows = FV_LBR_EAGER_ROWS;
 int64_t g_halley_round = 1ll << 26;
 
 cudaError_t ensure_lbr(DevWork* w, int slot, int64_t rows) {
@@ -1680,28 +1591,10 @@ cudaError_t launch_iv(DevWork* w, int method, const KArgs& a, int slot, cudaStre
       CK(cudaMemsetAsync(lq.count, 0, 16 * sizeof(unsigned int), s));
       const int64_t cap1 = (b.n + 255) / 256;
       auto g = [cap1](int blocks) { return (int)(cap1 < blocks ? cap1 : blocks); };
-      if (b.n < g_lbr_eager_rows) {
-        // small round: normalize + anchors in one pass, then the far-low and near
-        // solves in one kernel beside the far-high solve
-        FV_LAUNCH(FV_KID_LBR_NORM, s, k_lbr_normalize<FV_NORM_MINB, true><<<blocks_for(w->blocks_lbr_norm_eager, b.n), 256, 0, s>>>(b, lq));
-        FV_LAUNCH(FV_KID_LBR_NREP, s, k_lbr_normalize_replay<<<g(w->sm_count), 256, 0, s>>>(b, lq));
-        // the replay's pending rows (normally none) still need their anchors
-        FV_LAUNCH(FV_KID_LBR_ANCH, s, k_lbr_anchors<<<g(w->sm_count), 256, 0, s>>>(b, lq));
-        cudaStream_t s3 = t_timing ? s : w->aux2[slot];
-        CK(cudaEventRecord(w->fork2_ev[slot], s));
-        CK(cudaStreamWaitEvent(s3, w->fork2_ev[slot], 0));
-        FV_LAUNCH(FV_KID_LBR_FH, s3, k_lbr_solve<FV_FAR_HIGH><<<g(w->blocks_lbr_fh), 256, 0, s3>>>(b, lq));
-        FV_LAUNCH(FV_KID_LBR_SOLVE_FAST, s, k_lbr_solve_fast<<<g(w->blocks_lbr_sfast), 256, 0, s>>>(b, lq));
-        FV_LAUNCH(FV_KID_LBR_FL, s, k_lbr_solve<FV_FAR_LOW><<<g(w->sm_count), 256, 0, s>>>(b, lq));
-        FV_LAUNCH(FV_KID_LBR_NEAR, s, k_lbr_solve<FV_NEAR_LOW><<<g(w->sm_count), 256, 0, s>>>(b, lq));
-        CK(cudaEventRecord(w->join2_ev[slot], s3));
-        CK(cudaStreamWaitEvent(s, w->join2_ev[slot], 0));
-        continue;
-      }
       if (b.n >= FV_NORM_BIG_ROWS)
-        FV_LAUNCH(FV_KID_LBR_NORM, s, k_lbr_normalize<FV_NORM_MINB_BIG, false><<<blocks_for(w->blocks_lbr_norm_big, b.n), 256, 0, s>>>(b, lq));
+        FV_LAUNCH(FV_KID_LBR_NORM, s, k_lbr_normalize<FV_NORM_MINB_BIG><<<blocks_for(w->blocks_lbr_norm_big, b.n), 256, 0, s>>>(b, lq));
       else
-        FV_LAUNCH(FV_KID_LBR_NORM, s, k_lbr_normalize<FV_NORM_MINB, false><<<blocks_for(w->blocks_lbr_norm, b.n), 256, 0, s>>>(b, lq));
+        FV_LAUNCH(FV_KID_LBR_NORM, s, k_lbr_normalize<FV_NORM_MINB><<<blocks_for(w->blocks_lbr_norm, b.n), 256, 0, s>>>(b, lq));
       // the three replay passes usually find an empty queue: one CTA per SM
       // keeps their launch + drain short (a full occupancy grid costs ~7 us)
       FV_LAUNCH(FV_KID_LBR_NREP, s, k_lbr_normalize_replay<<<g(w->sm_count), 256, 0, s>>>(b, lq));
@@ -2862,12 +2755,6 @@ FV_API int fv_set_chunk_rows(int64_t rows) {
 }
 
 FV_API int64_t fv_last_launch_count(void) { return t_launches; }
-
-FV_API int fv_set_lbr_eager_rows(int64_t rows) {
-  if (rows < 0) return FV_ERR_ARG;
-  g_lbr_eager_rows = rows;
-  return FV_OK;
-}
 
 FV_API int fv_set_round_rows(int64_t lbr_rows, int64_t halley_rows) {
   if (lbr_rows < 0 || halley_rows < 0 || halley_rows > (1ll << 26)) return FV_ERR_ARG;   // int32 queue entries
