@@ -2072,6 +2072,26 @@ void par_memcpy_batch(const std::vector<CopySeg>& segs) {
 }
 
 
+std::vector<std::pair<int64_t, int64_t>> chunk_plan(int64_t n, int64_t chunk) {
+  std::vector<std::pair<int64_t, int64_t>> plan;
+  if (n <= 0) return plan;
+  if (n <= 3 * chunk) {                        // small calls: plain chunks
+    for (int64_t r0 = 0; r0 < n; r0 += chunk) plan.push_back({r0, (r0 + chunk < n) ? chunk : n - r0});
+    return plan;
+  }
+  const int64_t q = chunk / 4, h = chunk / 2;
+  int64_t r0 = 0;
+  plan.push_back({r0, q}); r0 += q;
+  plan.push_back({r0, h}); r0 += h;
+  const int64_t tail = h + q;                  // the last two chunks: 1/2 and 1/4
+  while (n - r0 - tail > chunk) { plan.push_back({r0, chunk}); r0 += chunk; }
+  const int64_t mid = n - r0 - tail;           // 0 < mid <= chunk
+  if (mid > 0) { plan.push_back({r0, mid}); r0 += mid; }
+  plan.push_back({r0, h}); r0 += h;
+  plan.push_back({r0, n - r0});
+  return plan;
+}
+
 bool is_pageable(const void* p) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return true; }
@@ -2134,6 +2154,11 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
     ~SlotEvents() { for (auto& e : ev) cudaEventDestroy(e); }
   } sev;
   cudaEvent_t* slot_done = sev.ev;
+  // chunk plan: full-size chunks in the middle, a ramp of 1/4- and 1/2-size
+  // chunks at both ends -- the first chunk's H2D and the last chunk's kernels
+  // + D2H are not overlapped with anything, so smaller end chunks shorten the
+  // pipeline's fill and drain (C4 100M rows: ~3 ms of a ~49 ms call)
+  std::vector<std::pair<int64_t, int64_t>> plan = chunk_plan(n, chunk);
   int64_t slot_chunk[FV_NSLOT];
   for (int s = 0; s < FV_NSLOT; ++s) slot_chunk[s] = -1;
   // results of chunk `ci` (in slot s) from pinned staging to the caller
@@ -2141,7 +2166,7 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
     const int64_t ci = slot_chunk[s];
     if (ci < 0) return;
     cudaEventSynchronize(slot_done[s]);
-    const int64_t r0 = ci * chunk, rn = (r0 + chunk < n ? chunk : n - r0);
+    const int64_t r0 = plan[ci].first, rn = plan[ci].second;
     char* st = w->stage[s];
     std::vector<CopySeg> segs;
     for (int i = 0; i < 6; ++i)
@@ -2159,11 +2184,11 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
   for (int s = 1; s < FV_NSLOT; ++s) cudaStreamWaitEvent(w->streams[s], ready, 0);
   KArgs a_first;
   memset(&a_first, 0, sizeof(a_first));
-  int64_t nchunks = (n + chunk - 1) / chunk;
+  const int64_t nchunks = (int64_t)plan.size();
   for (int64_t ci = 0; ci < nchunks; ++ci) {
     int slot = (int)(ci % FV_NSLOT);
     cudaStream_t s = w->streams[slot];
-    int64_t r0 = ci * chunk, rn = (r0 + chunk < n ? chunk : n - r0);
+    const int64_t r0 = plan[ci].first, rn = plan[ci].second;
     char* base = w->chunk[slot];
     char* stg = w->stage[slot];
     if (any_stage) drain(slot);               // the slot's previous chunk is done with staging
