@@ -136,7 +136,11 @@ def run_chain(input: str, model: str, compute: str = "price", method: str = "hal
 
 
 def _emit(text: str, output: Optional[str]) -> str:
+    """cli.py:95-100: the text to ``output`` (an ASCII str is written as its
+    bytes by the host extension, GIL released -- the same file contents as
+    the text-mode write, without its encode copy)."""
     if output:
-        with open(output, "w") as fh:
-            fh.write(text)
+        if B._fvhost is None or B._fvhost.write_text(output, text) is None:
+            with open(output, "w") as fh:
+                fh.write(text)
     return text

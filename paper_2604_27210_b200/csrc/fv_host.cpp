@@ -26,8 +26,13 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <errno.h>
+#include <fcntl.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <charconv>
+#include <memory>
 #include <string>
 #include <thread>
 #include <vector>
@@ -226,7 +231,137 @@ struct CsvCol {
   bool is_signed;
   std::vector<PyObject*> objs;          // COL_STR: distinct objects ...
   std::vector<std::string> text;        // ... and their UTF-8
+  size_t maxlen = 0;                    // longest text
 };
+
+// ---- threaded text output ---------------------------------------------------
+// Workers for `work` units with at least `min_per` units each (<= 16).
+int parts_for(int64_t work, int64_t min_per) {
+  unsigned nt = std::thread::hardware_concurrency();
+  if (nt > 16) nt = 16;
+  if (nt < 1) nt = 1;
+  int64_t p = work / min_per;
+  if (p > (int64_t)nt) p = nt;
+  if (p < 1) p = 1;
+  return (int)p;
+}
+template <class F>
+void run_parts(int parts, F fn) {
+  std::vector<std::thread> th;
+  for (int k = 1; k < parts; ++k) th.emplace_back(fn, k);
+  fn(0);
+  for (auto& t : th) t.join();
+}
+// A growable byte buffer written through a raw pointer: reserve() the bound
+// of the next record, then append with put()/ptr (no per-character capacity
+// checks; the std::string appends of the first form ran at ~250 MB/s).
+struct OutBuf {
+  std::unique_ptr<char[]> b;
+  size_t cap = 0, n = 0;
+  void reserve(size_t more) {
+    if (n + more <= cap) return;
+    size_t nc = cap ? cap : 1 << 16;
+    while (nc < n + more) nc *= 2;
+    std::unique_ptr<char[]> nb(new char[nc]);
+    if (n) memcpy(nb.get(), b.get(), n);
+    b.swap(nb);
+    cap = nc;
+  }
+  char* ptr() { return b.get() + n; }
+  void put(const char* p, size_t k) { memcpy(b.get() + n, p, k); n += k; }
+  void put(char c) { b[n++] = c; }
+};
+bool ascii_text(const char* p, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if ((unsigned char)p[i] >= 0x80) return false;
+  return true;
+}
+// The pieces, in order, as one str: ASCII text becomes a compact 1-byte
+// PyUnicode filled by parallel copies (no concatenated copy, no UTF-8
+// decode pass); anything else goes through the UTF-8 decoder.
+PyObject* str_from_pieces(const std::vector<std::pair<const char*, size_t>>& pcs, bool ascii) {
+  size_t total = 0;
+  for (auto& pc : pcs) total += pc.second;
+  if (!ascii) {
+    std::string all;
+    all.reserve(total);
+    for (auto& pc : pcs) all.append(pc.first, pc.second);
+    return PyUnicode_DecodeUTF8(all.data(), (Py_ssize_t)all.size(), "strict");
+  }
+  PyObject* out = PyUnicode_New((Py_ssize_t)total, 127);
+  if (!out) return nullptr;
+  char* dst = (char*)PyUnicode_1BYTE_DATA(out);
+  std::vector<size_t> off(pcs.size() + 1, 0);
+  for (size_t i = 0; i < pcs.size(); ++i) off[i + 1] = off[i] + pcs[i].second;
+  const int parts = parts_for((int64_t)total, 1 << 22);
+  Py_BEGIN_ALLOW_THREADS
+  run_parts(parts, [&](int k) {                      // byte range [a, b) of the output
+    const size_t a = total * k / parts, b = total * (k + 1) / parts;
+    for (size_t i = 0; i < pcs.size(); ++i) {
+      const size_t lo = std::max(a, off[i]), hi = std::min(b, off[i + 1]);
+      if (lo < hi) memcpy(dst + lo, pcs[i].first + (lo - off[i]), hi - lo);
+    }
+  });
+  Py_END_ALLOW_THREADS
+  return out;
+}
+// Column setup shared by the CSV and JSON formatters: false -> the caller
+// returns None (Python path); sets an exception and returns false with
+// `err` when the C API failed.
+bool setup_col(PyObject* o, int64_t& n, CsvCol& c, bool int_ok, bool& err) {
+  err = false;
+  if (!PyArray_Check(o)) return false;
+  PyArrayObject* a = (PyArrayObject*)o;
+  if (PyArray_NDIM(a) != 1) return false;
+  if (n < 0) n = PyArray_DIM(a, 0);
+  if (PyArray_DIM(a, 0) != n) return false;
+  c.base = (const char*)PyArray_DATA(a);
+  c.stride = PyArray_STRIDE(a, 0);
+  const int t = PyArray_TYPE(a);
+  if (t == NPY_FLOAT64 && PyArray_ISNOTSWAPPED(a)) {
+    c.kind = COL_F64;
+    c.maxlen = 24;                                   // -d.ddddddddddddddddde-308
+    return true;
+  }
+  if (PyArray_ISFLOAT(a)) return false;              // other float widths: Python path
+  if (int_ok && PyArray_ISINTEGER(a) && PyArray_ISNOTSWAPPED(a) && PyArray_ITEMSIZE(a) <= 8) {
+    c.kind = COL_INT;
+    c.isize = (int)PyArray_ITEMSIZE(a);
+    c.is_signed = PyArray_ISSIGNED(a);
+    c.maxlen = 1;
+    return true;
+  }
+  if (t != NPY_OBJECT) return false;
+  c.kind = COL_STR;
+  for (int64_t i = 0; i < n; ++i) {                  // distinct objects (a status column has <= 5)
+    PyObject* v = *(PyObject* const*)(c.base + i * c.stride);
+    bool seen = false;
+    for (PyObject* w : c.objs) if (w == v) { seen = true; break; }
+    if (seen) continue;
+    if (c.objs.size() >= 16 || !v || !PyUnicode_CheckExact(v)) return false;
+    Py_ssize_t len;
+    const char* u = PyUnicode_AsUTF8AndSize(v, &len);
+    if (!u) { err = true; return false; }
+    c.objs.push_back(v);
+    c.text.emplace_back(u, len);
+    c.maxlen = std::max(c.maxlen, (size_t)len);
+  }
+  return true;
+}
+inline bool int_pos(const CsvCol& c, const char* p) {
+  switch (c.isize) {
+    case 1: return c.is_signed ? *(const int8_t*)p > 0 : *(const uint8_t*)p > 0;
+    case 2: return c.is_signed ? *(const int16_t*)p > 0 : *(const uint16_t*)p > 0;
+    case 4: return c.is_signed ? *(const int32_t*)p > 0 : *(const uint32_t*)p > 0;
+    default: return c.is_signed ? *(const int64_t*)p > 0 : *(const uint64_t*)p > 0;
+  }
+}
+inline const std::string& str_of(const CsvCol& c, const char* p) {
+  PyObject* v = *(PyObject* const*)p;
+  size_t w = 0;
+  while (c.objs[w] != v) ++w;
+  return c.text[w];
+}
 
 // format_csv(names, columns) -> str, or None when a column is outside the
 // fast path (the caller then runs the Python loop).
@@ -247,94 +382,54 @@ PyObject* format_csv(PyObject*, PyObject* args) {
     header.append(u, len);
   }
   header += '\n';
+  bool ascii = ascii_text(header.data(), header.size());
   int64_t n = -1;
   std::vector<CsvCol> cc(m);
+  size_t rowmax = (size_t)m;                         // separators
   for (Py_ssize_t j = 0; j < m; ++j) {
-    PyObject* o = PyTuple_GET_ITEM(cols, j);
-    if (!PyArray_Check(o)) Py_RETURN_NONE;
-    PyArrayObject* a = (PyArrayObject*)o;
-    if (PyArray_NDIM(a) != 1) Py_RETURN_NONE;
-    if (n < 0) n = PyArray_DIM(a, 0);
-    if (PyArray_DIM(a, 0) != n) Py_RETURN_NONE;
-    CsvCol& c = cc[j];
-    c.base = (const char*)PyArray_DATA(a);
-    c.stride = PyArray_STRIDE(a, 0);
-    const int t = PyArray_TYPE(a);
-    if (t == NPY_FLOAT64 && PyArray_ISNOTSWAPPED(a)) {
-      c.kind = COL_F64;
-    } else if (PyArray_ISINTEGER(a) && PyArray_ISNOTSWAPPED(a) && PyArray_ITEMSIZE(a) <= 8) {
-      c.kind = COL_INT;
-      c.isize = (int)PyArray_ITEMSIZE(a);
-      c.is_signed = PyArray_ISSIGNED(a);
-    } else if (t == NPY_OBJECT) {
-      c.kind = COL_STR;
-      for (int64_t i = 0; i < n; ++i) {                 // distinct objects (a status column has <= 5)
-        PyObject* v = *(PyObject* const*)(c.base + i * c.stride);
-        bool seen = false;
-        for (PyObject* w : c.objs) if (w == v) { seen = true; break; }
-        if (seen) continue;
-        if (c.objs.size() >= 16 || !v || !PyUnicode_CheckExact(v)) Py_RETURN_NONE;
-        Py_ssize_t len;
-        const char* u = PyUnicode_AsUTF8AndSize(v, &len);
-        if (!u) return nullptr;
-        c.objs.push_back(v);
-        c.text.emplace_back(u, len);
-      }
-    } else {
+    bool err;
+    if (!setup_col(PyTuple_GET_ITEM(cols, j), n, cc[j], true, err)) {
+      if (err) return nullptr;
       Py_RETURN_NONE;
     }
+    rowmax += cc[j].maxlen;
+    for (auto& t : cc[j].text) ascii = ascii && ascii_text(t.data(), t.size());
   }
-  unsigned nt = std::thread::hardware_concurrency();
-  if (nt > 16) nt = 16;
-  int64_t parts = n / 65536;
-  if (parts > (int64_t)nt) parts = nt;
-  if (parts < 1) parts = 1;
-  std::vector<std::string> chunk(parts);
+  const int parts = parts_for(n, 65536);
+  std::vector<OutBuf> buf(parts);
   Py_BEGIN_ALLOW_THREADS
-  auto work = [&](int64_t k) {
+  run_parts(parts, [&](int k) {
     const int64_t a = n * k / parts, b = n * (k + 1) / parts;
-    std::string& s = chunk[k];
-    s.reserve((size_t)(b - a) * (size_t)m * 20);
-    char buf[48];
+    OutBuf& s = buf[k];
+    s.reserve((size_t)(b - a) * (size_t)m * 18);
     for (int64_t i = a; i < b; ++i) {
+      s.reserve(rowmax);
+      char* w = s.ptr();                 // a local cursor: stores through char*
+                                         // would otherwise reload s.n each time
       for (Py_ssize_t j = 0; j < m; ++j) {
         const CsvCol& c = cc[j];
         const char* p = c.base + i * c.stride;
         if (c.kind == COL_F64) {
           double v;
           memcpy(&v, p, 8);
-          s.append(buf, repr_double(v, buf));
+          w += repr_double(v, w);
         } else if (c.kind == COL_INT) {
-          bool pos;
-          switch (c.isize) {
-            case 1: pos = c.is_signed ? *(const int8_t*)p > 0 : *(const uint8_t*)p > 0; break;
-            case 2: pos = c.is_signed ? *(const int16_t*)p > 0 : *(const uint16_t*)p > 0; break;
-            case 4: pos = c.is_signed ? *(const int32_t*)p > 0 : *(const uint32_t*)p > 0; break;
-            default: pos = c.is_signed ? *(const int64_t*)p > 0 : *(const uint64_t*)p > 0; break;
-          }
-          s += pos ? 'c' : 'p';
+          *w++ = int_pos(c, p) ? 'c' : 'p';
         } else {
-          PyObject* v = *(PyObject* const*)p;
-          size_t w = 0;
-          while (c.objs[w] != v) ++w;
-          s += c.text[w];
+          const std::string& t = str_of(c, p);
+          memcpy(w, t.data(), t.size());
+          w += t.size();
         }
-        s += (j + 1 < m) ? ',' : '\n';
+        *w++ = (j + 1 < m) ? ',' : '\n';
       }
+      s.n = (size_t)(w - s.b.get());
     }
-  };
-  std::vector<std::thread> th;
-  for (int64_t k = 1; k < parts; ++k) th.emplace_back(work, k);
-  work(0);
-  for (auto& t : th) t.join();
+  });
   Py_END_ALLOW_THREADS
-  size_t total = header.size();
-  for (auto& s : chunk) total += s.size();
-  std::string all;
-  all.reserve(total);
-  all += header;
-  for (auto& s : chunk) { all += s; std::string().swap(s); }
-  return PyUnicode_DecodeUTF8(all.data(), (Py_ssize_t)all.size(), "strict");
+  std::vector<std::pair<const char*, size_t>> pcs;
+  pcs.emplace_back(header.data(), header.size());
+  for (auto& s : buf) pcs.emplace_back(s.b.get(), s.n);
+  return str_from_pieces(pcs, ascii);
 }
 
 // ---- CSV chain input (cli.py:140-173 _read_chain + _numeric) ---------------
@@ -376,16 +471,37 @@ PyObject* parse_chain_csv(PyObject*, PyObject* args) {
   struct Release { Py_buffer* b; ~Release() { PyBuffer_Release(b); } } rel{&buf};
   const char* d = (const char*)buf.buf;
   const int64_t len = buf.len;
-  for (int64_t i = 0; i < len; ++i) {
-    const unsigned char ch = (unsigned char)d[i];
-    if (ch == '"' || ch == '\r' || ch >= 0x80) Py_RETURN_NONE;
-  }
-  // line starts
-  std::vector<int64_t> ls;
-  ls.push_back(0);
-  for (int64_t i = 0; i < len; ++i)
-    if (d[i] == '\n' && i + 1 < len) ls.push_back(i + 1);
   if (len == 0) Py_RETURN_NONE;
+  // the byte screen and the line starts, on byte ranges in parallel
+  const int sparts = parts_for(len, 1 << 22);
+  std::vector<std::vector<int64_t>> nl(sparts);
+  std::vector<char> odd(sparts, 0);
+  Py_BEGIN_ALLOW_THREADS
+  run_parts(sparts, [&](int k) {
+    const int64_t a = len * k / sparts, b = len * (k + 1) / sparts;
+    std::vector<int64_t>& v = nl[k];
+    v.reserve((size_t)((b - a) / 48 + 16));
+    unsigned char acc = 0;
+    for (int64_t i = a; i < b; ++i) {
+      const unsigned char ch = (unsigned char)d[i];
+      acc |= (unsigned char)(ch == '"' || ch == '\r' || ch >= 0x80);
+      if (ch == '\n') v.push_back(i);
+    }
+    odd[k] = (char)acc;
+  });
+  Py_END_ALLOW_THREADS
+  for (char o : odd) if (o) Py_RETURN_NONE;
+  std::vector<int64_t> ls;
+  {
+    size_t cnt = 1;
+    for (auto& v : nl) cnt += v.size();
+    ls.reserve(cnt);
+  }
+  ls.push_back(0);
+  for (auto& v : nl)
+    for (int64_t i : v)
+      if (i + 1 < len) ls.push_back(i + 1);
+  std::vector<std::vector<int64_t>>().swap(nl);
   auto line_end = [&](size_t k) {
     int64_t e = (k + 1 < ls.size()) ? ls[k + 1] - 1 : len;
     if (e > ls[k] && d[e - 1] == '\n') --e;         // the final line's '\n'
@@ -416,15 +532,11 @@ PyObject* parse_chain_csv(PyObject*, PyObject* args) {
   uint32_t* flag_out = flag_col >= 0 ? (uint32_t*)PyArray_DATA((PyArrayObject*)arrays[flag_col]) : nullptr;
   for (int64_t j = 0; j < m; ++j)
     if (j != flag_col) out[j] = (double*)PyArray_DATA((PyArrayObject*)arrays[j]);
-  unsigned nt = std::thread::hardware_concurrency();
-  if (nt > 16) nt = 16;
-  int64_t parts = n / 65536;
-  if (parts > (int64_t)nt) parts = nt;
-  if (parts < 1) parts = 1;
+  const int parts = parts_for(n, 65536);
   std::vector<std::vector<std::pair<int64_t, int64_t>>> bad(parts);
   std::vector<char> fallback(parts, 0);
   Py_BEGIN_ALLOW_THREADS
-  auto work = [&](int64_t k) {
+  run_parts(parts, [&](int k) {
     const int64_t r0 = n * k / parts, r1 = n * (k + 1) / parts;
     for (int64_t r = r0; r < r1 && !fallback[k]; ++r) {
       const int64_t a = ls[r + 1], e = line_end(r + 1);
@@ -453,11 +565,7 @@ PyObject* parse_chain_csv(PyObject*, PyObject* args) {
       }
       if (j != m) fallback[k] = 1;
     }
-  };
-  std::vector<std::thread> th;
-  for (int64_t k = 1; k < parts; ++k) th.emplace_back(work, k);
-  work(0);
-  for (auto& t : th) t.join();
+  });
   Py_END_ALLOW_THREADS
   bool fb = false;
   for (char f : fallback) fb = fb || f;
@@ -497,6 +605,7 @@ PyObject* format_json(PyObject*, PyObject* args) {
   const Py_ssize_t m = PyTuple_GET_SIZE(keys);
   if (m != PyTuple_GET_SIZE(cols)) Py_RETURN_NONE;
   std::vector<std::string> kenc(m);
+  bool ascii = true;
   for (Py_ssize_t j = 0; j < m; ++j) {
     PyObject* k = PyTuple_GET_ITEM(keys, j);
     if (!PyUnicode_CheckExact(k)) Py_RETURN_NONE;
@@ -504,105 +613,111 @@ PyObject* format_json(PyObject*, PyObject* args) {
     const char* u = PyUnicode_AsUTF8AndSize(k, &len);
     if (!u) return nullptr;
     kenc[j].assign(u, len);
+    ascii = ascii && ascii_text(u, (size_t)len);
   }
   int64_t n = -1;
   std::vector<CsvCol> cc(m);
   for (Py_ssize_t j = 0; j < m; ++j) {
+    bool err;
     PyObject* o = PyTuple_GET_ITEM(cols, j);
-    if (!PyArray_Check(o)) Py_RETURN_NONE;
-    PyArrayObject* a = (PyArrayObject*)o;
-    if (PyArray_NDIM(a) != 1) Py_RETURN_NONE;
-    if (n < 0) n = PyArray_DIM(a, 0);
-    if (PyArray_DIM(a, 0) != n) Py_RETURN_NONE;
-    CsvCol& c = cc[j];
-    c.base = (const char*)PyArray_DATA(a);
-    c.stride = PyArray_STRIDE(a, 0);
-    const int t = PyArray_TYPE(a);
-    if (t == NPY_FLOAT64 && PyArray_ISNOTSWAPPED(a)) {
-      c.kind = COL_F64;
-    } else if (PyArray_ISFLOAT(a)) {
-      Py_RETURN_NONE;                                  // other float widths: Python path
-    } else if (j == flag_index && PyArray_ISINTEGER(a) && PyArray_ISNOTSWAPPED(a) && PyArray_ITEMSIZE(a) <= 8) {
-      c.kind = COL_INT;
-      c.isize = (int)PyArray_ITEMSIZE(a);
-      c.is_signed = PyArray_ISSIGNED(a);
-    } else if (t == NPY_OBJECT && j != flag_index) {
-      c.kind = COL_STR;
-      for (int64_t i = 0; i < n; ++i) {
-        PyObject* v = *(PyObject* const*)(c.base + i * c.stride);
-        bool seen = false;
-        for (PyObject* w : c.objs) if (w == v) { seen = true; break; }
-        if (seen) continue;
-        if (c.objs.size() >= 16 || !v || !PyUnicode_CheckExact(v)) Py_RETURN_NONE;
-        Py_ssize_t len;
-        const char* u = PyUnicode_AsUTF8AndSize(v, &len);
-        if (!u) return nullptr;
-        std::string q = "\"";
-        q.append(u, len);
-        if (!json_plain(q.substr(1))) Py_RETURN_NONE;
-        q += '"';
-        c.objs.push_back(v);
-        c.text.push_back(q);
-      }
-    } else {
+    if (j != flag_index && PyArray_Check(o) && PyArray_TYPE((PyArrayObject*)o) != NPY_FLOAT64 &&
+        PyArray_TYPE((PyArrayObject*)o) != NPY_OBJECT)
+      Py_RETURN_NONE;
+    if (!setup_col(o, n, cc[j], j == flag_index, err)) {
+      if (err) return nullptr;
       Py_RETURN_NONE;
     }
+    if (j == flag_index && cc[j].kind == COL_STR) Py_RETURN_NONE;   // Python's "c" / "p" mapping
+    for (auto& t : cc[j].text) {
+      if (!json_plain(t)) Py_RETURN_NONE;
+      t = "\"" + t + "\"";
+    }
+    cc[j].maxlen += 2;
+    if (cc[j].kind == COL_INT) cc[j].maxlen = 3;
   }
-  unsigned nt = std::thread::hardware_concurrency();
-  if (nt > 16) nt = 16;
-  int64_t parts = n / 65536;
-  if (parts > (int64_t)nt) parts = nt;
-  if (parts < 1) parts = 1;
-  std::vector<std::string> chunk((size_t)m * parts);
+  if (n < 0) n = 0;
+  const int parts = parts_for(n, 65536);
+  std::vector<OutBuf> chunk((size_t)m * parts);
   Py_BEGIN_ALLOW_THREADS
-  auto work = [&](int64_t k) {
+  run_parts(parts, [&](int k) {
     const int64_t a = n * k / parts, b = n * (k + 1) / parts;
-    char buf[48];
     for (Py_ssize_t j = 0; j < m; ++j) {
       const CsvCol& c = cc[j];
-      std::string& s = chunk[(size_t)j * parts + k];
-      s.reserve((size_t)(b - a) * 22);
-      for (int64_t i = a; i < b; ++i) {
-        if (i) { s += ','; s += ' '; }
-        const char* p = c.base + i * c.stride;
-        if (c.kind == COL_F64) {
-          double v;
-          memcpy(&v, p, 8);
-          if (v - v != 0.0) s.append("null", 4);         // nan, inf
-          else s.append(buf, repr_double(v, buf));
-        } else if (c.kind == COL_INT) {
-          bool pos;
-          switch (c.isize) {
-            case 1: pos = c.is_signed ? *(const int8_t*)p > 0 : *(const uint8_t*)p > 0; break;
-            case 2: pos = c.is_signed ? *(const int16_t*)p > 0 : *(const uint16_t*)p > 0; break;
-            case 4: pos = c.is_signed ? *(const int32_t*)p > 0 : *(const uint32_t*)p > 0; break;
-            default: pos = c.is_signed ? *(const int64_t*)p > 0 : *(const uint64_t*)p > 0; break;
+      OutBuf& s = chunk[(size_t)j * parts + k];
+      s.reserve((size_t)(b - a) * (c.kind == COL_F64 ? 20 : c.maxlen + 2));
+      const int64_t blk = 4096;
+      for (int64_t i0 = a; i0 < b; i0 += blk) {
+        const int64_t i1 = std::min(b, i0 + blk);
+        s.reserve((size_t)(i1 - i0) * (c.maxlen + 2));
+        char* w = s.ptr();
+        for (int64_t i = i0; i < i1; ++i) {
+          if (i) { *w++ = ','; *w++ = ' '; }
+          const char* p = c.base + i * c.stride;
+          if (c.kind == COL_F64) {
+            double v;
+            memcpy(&v, p, 8);
+            if (v - v != 0.0) { memcpy(w, "null", 4); w += 4; }   // nan, inf
+            else w += repr_double(v, w);
+          } else if (c.kind == COL_INT) {
+            memcpy(w, int_pos(c, p) ? "\"c\"" : "\"p\"", 3);
+            w += 3;
+          } else {
+            const std::string& t = str_of(c, p);
+            memcpy(w, t.data(), t.size());
+            w += t.size();
           }
-          s.append(pos ? "\"c\"" : "\"p\"", 3);
-        } else {
-          PyObject* v = *(PyObject* const*)p;
-          size_t w = 0;
-          while (c.objs[w] != v) ++w;
-          s += c.text[w];
         }
+        s.n = (size_t)(w - s.b.get());
       }
     }
-  };
-  std::vector<std::thread> th;
-  for (int64_t k = 1; k < parts; ++k) th.emplace_back(work, k);
-  work(0);
-  for (auto& t : th) t.join();
+  });
   Py_END_ALLOW_THREADS
-  std::string all = "{";
+  std::vector<std::string> glue((size_t)m + 1);
+  std::vector<std::pair<const char*, size_t>> pcs;
   for (Py_ssize_t j = 0; j < m; ++j) {
-    if (j) all += ", ";
-    all += kenc[j];
-    all += ": [";
-    for (int64_t k = 0; k < parts; ++k) { all += chunk[(size_t)j * parts + k]; std::string().swap(chunk[(size_t)j * parts + k]); }
-    all += ']';
+    glue[j] = (j ? std::string(", ") : std::string("{")) + kenc[j] + ": [";
+    pcs.emplace_back(glue[j].data(), glue[j].size());
+    for (int k = 0; k < parts; ++k) {
+      OutBuf& s = chunk[(size_t)j * parts + k];
+      pcs.emplace_back(s.b.get(), s.n);
+    }
+    pcs.emplace_back("]", 1);
   }
-  all += '}';
-  return PyUnicode_DecodeUTF8(all.data(), (Py_ssize_t)all.size(), "strict");
+  glue[m] = m ? "}" : "{}";
+  pcs.emplace_back(glue[m].data(), glue[m].size());
+  return str_from_pieces(pcs, ascii);
+}
+
+// write_text(path, text) -> True, or None for text that is not compact ASCII
+// (the caller writes it itself): the bytes of an ASCII str are its UTF-8, so
+// they go to the file as they are, without the text layer's encode copy,
+// with the GIL released.  Same file contents as open(path, "w").write(text).
+PyObject* write_text(PyObject*, PyObject* args) {
+  PyObject* path;
+  PyObject* text;
+  if (!PyArg_ParseTuple(args, "O&U", PyUnicode_FSConverter, &path, &text)) return nullptr;
+  struct Drop { PyObject* o; ~Drop() { Py_DECREF(o); } } drop{path};
+  if (!PyUnicode_IS_COMPACT_ASCII(text)) Py_RETURN_NONE;
+  const char* p = (const char*)PyUnicode_DATA(text);
+  size_t left = (size_t)PyUnicode_GET_LENGTH(text);
+  const char* fn = PyBytes_AS_STRING(path);
+  int rc = 0, e = 0;
+  Py_BEGIN_ALLOW_THREADS
+  const int fd = open(fn, O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0666);
+  if (fd < 0) { rc = -1; e = errno; }
+  while (fd >= 0 && left) {
+    const ssize_t w = write(fd, p, left > (1u << 30) ? (1u << 30) : left);
+    if (w < 0) { if (errno == EINTR) continue; rc = -1; e = errno; break; }
+    p += w;
+    left -= (size_t)w;
+  }
+  if (fd >= 0 && close(fd) != 0 && rc == 0) { rc = -1; e = errno; }
+  Py_END_ALLOW_THREADS
+  if (rc) {
+    errno = e;
+    return PyErr_SetFromErrnoWithFilenameObject(PyExc_OSError, PyTuple_GET_ITEM(args, 0));
+  }
+  Py_RETURN_TRUE;
 }
 
 PyMethodDef kMethods[] = {
@@ -612,6 +727,7 @@ PyMethodDef kMethods[] = {
     {"repr_doubles", repr_doubles, METH_VARARGS, "repr(float(v)) for each element (test hook)"},
     {"parse_flags_u", parse_flags_u, METH_VARARGS, "case-insensitive c/p -> int8 +1/-1; (flags, first_bad)"},
     {"status_objects", status_objects, METH_VARARGS, "object array names[codes]"},
+    {"write_text", write_text, METH_VARARGS, "write an ASCII str to a file (GIL released), or None"},
     {nullptr, nullptr, 0, nullptr}};
 
 PyModuleDef kModule = {PyModuleDef_HEAD_INIT, "_fvhost", "fastvol_b200 batch front-end host loops", -1, kMethods};
