@@ -253,6 +253,13 @@ FV_API int fv_selftest_div_const(int64_t n, uint64_t seed, int64_t* mismatches);
 FV_API int fv_selftest_fast(int64_t n, uint64_t seed, int64_t* mismatches /*[11]*/,
                             int64_t* flagged /*[11]*/);
 
+/* Exhaustive check of the lower-bound table behind the quick far-low
+ * decision of the LBR normalize pass (fv_fast.h g_qlo_tab): over every fp32
+ * |x| in [2^-13, 2^5), the points where the exact first anchor b_lo(x) is
+ * below its bin's bound (must be 0), the smallest b_lo / bound ratio (>= 1:
+ * the bound's tightness) and the number of points.  Diagnostics / tests. */
+FV_API int fv_selftest_qlo(int64_t* violations, double* min_ratio, int64_t* points);
+
 /* Per-kernel timing (diagnostics; off by default).  While on, every kernel
  * the calling thread launches is bracketed by CUDA events on its stream;
  * fv_kernel_times sums the elapsed milliseconds and launch counts per kernel

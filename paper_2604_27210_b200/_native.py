@@ -71,6 +71,7 @@ SIGNATURES = {
     "fv_last_outcome": ([_P, _P, _P], ctypes.c_int),
     "fv_selftest_div_const": ([_I64, ctypes.c_uint64, _P], ctypes.c_int),
     "fv_selftest_fast": ([_I64, ctypes.c_uint64, _P, _P], ctypes.c_int),
+    "fv_selftest_qlo": ([_P, _P, _P], ctypes.c_int),
     "fv_set_kernel_timing": ([ctypes.c_int], ctypes.c_int),
     "fv_set_span_timing": ([ctypes.c_int], ctypes.c_int),
     "fv_last_span_ms": ([], ctypes.c_double),

@@ -439,7 +439,8 @@ __global__ void __launch_bounds__(256, MINB) k_lbr_normalize(KArgs a, LbrQueues 
         publish_checks(a.st, badc, a.row0 + row);
       } else {
         FvLbrOut o;
-        const int cls = fx_lbr_classify_lo(a.model, (double)fl, un, k, t, r, q, px, st, o, flagged);
+        const int cls = fx_lbr_classify_lo<MINB == FV_NORM_MINB_BIG>(a.model, (double)fl, un, k, t, r, q, px,
+                                                                    st, o, flagged);
         if (!flagged) {
           if (cls == FV_FAR_LOW) far_low = true;
           else if (cls == FV_NEAR_LOW) pending = true;
@@ -1408,6 +1409,30 @@ std::vector<DevWork*> g_work;
 
 #define CK(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) return _e; } while (0)
 
+// The quick far-low table (fv_fast.h g_qlo_tab): one thread per bin.
+__device__ double qlo_b_lo(double ax) {       // the exact first anchor at x = -ax
+  FvExc e = {0, 0, 0.0};
+  const double x = -ax;
+  const double s_c = py_sqrt(2.0 * ax, e);
+  double E = 0.0;
+  return py_max(fv_normalized_black(x, s_c * 0.5, false, e, &E, nullptr), 0.0);
+}
+__global__ void k_qlo_table() {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= FV_QLO_NBIN) return;
+  const int oct = k / FV_QLO_PER, m = k % FV_QLO_PER;
+  const double base = ldexp(1.0, oct - 13);
+  const double lo = base * (1.0 + (double)m / FV_QLO_PER), hi = base * (1.0 + (double)(m + 1) / FV_QLO_PER);
+  double mn = 1e300;
+  for (int j = 0; j <= 16; ++j) mn = fmin(mn, qlo_b_lo(lo + (hi - lo) * j / 16.0));
+  const double D = 17.0 / 16.0 + 0.5 / lo;
+  const double L = mn * exp(-D * (hi - lo) / 32.0) * (1.0 - 1e-4);
+  g_qlo_tab[k] = (L > 0.0 && L == L) ? __double2float_rd(L) : 0.0f;
+}
+cudaError_t qlo_table_init() {
+  k_qlo_table<<<(FV_QLO_NBIN + 127) / 128, 128>>>();
+  return cudaDeviceSynchronize();
+}
 int occupancy_blocks(const void* fn, int sm) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
@@ -1456,6 +1481,7 @@ cudaError_t get_work(DevWork** out) {
     CK(cudaMalloc(&w->hsm_count, sizeof(unsigned int) * 4 * FV_NSLOT));
     w->blocks_hset = occupancy_blocks((const void*)k_halley_bracket<false>, w->sm_count);
     w->blocks_hset_p = occupancy_blocks((const void*)k_halley_bracket<true>, w->sm_count);
+    CK(qlo_table_init());                     // the quick far-low bounds (fv_fast.h)
     g_work[dev] = w;
   }
   *out = g_work[dev];
@@ -2831,6 +2857,48 @@ FV_API int fv_selftest_div_const(int64_t n, uint64_t seed, int64_t* mismatches) 
   if (ce != cudaSuccess) return FV_ERR_CUDA;
   *mismatches = (int64_t)h;
   return FV_OK;
+}
+
+// Exhaustive check of the table: every fp32 |x| in [2^-13, 2^5): violations
+// of b_lo(x) >= g_qlo_tab[bin(x)] -> out[0]; the smallest b_lo / bound ratio
+// seen (as ordered bits of a positive double) -> out[1]; points -> out[2].
+__global__ void k_selftest_qlo(uint32_t lo_bits, uint32_t hi_bits, unsigned long long* out) {
+  unsigned long long bad = 0, cnt = 0;
+  double worst = 1e300;
+  for (uint64_t b = lo_bits + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < hi_bits;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    const double ax = (double)__uint_as_float((uint32_t)b);
+    const int k = fx_qlo_bin(ax);
+    const double L = (k >= 0) ? (double)g_qlo_tab[k] : 0.0;
+    const double ex = qlo_b_lo(ax);
+    if (!(ex >= L)) ++bad;
+    if (L > 0.0) worst = fmin(worst, ex / L);
+    ++cnt;
+  }
+  atomicAdd(out, bad);
+  atomicMin(out + 1, (unsigned long long)__double_as_longlong(worst));
+  atomicAdd(out + 2, cnt);
+}
+FV_API int fv_selftest_qlo(int64_t* violations, double* min_ratio, int64_t* points) {
+  DevWork* w = nullptr;
+  if (get_work(&w) != cudaSuccess) return FV_ERR_CUDA;
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, 3 * sizeof(unsigned long long)) != cudaSuccess) return FV_ERR_CUDA;
+  unsigned long long init[3] = {0, ~0ull, 0};
+  cudaMemcpy(d, init, sizeof(init), cudaMemcpyHostToDevice);
+  const float lo = 0x1p-13f, hi = 0x1p5f;
+  uint32_t lob, hib;
+  memcpy(&lob, &lo, 4);
+  memcpy(&hib, &hi, 4);
+  k_selftest_qlo<<<148 * 16, 256>>>(lob, hib, d);
+  unsigned long long h[3] = {0, 0, 0};
+  const cudaError_t ce = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (ce != cudaSuccess) return FV_ERR_CUDA;
+  *violations = (int64_t)h[0];
+  memcpy(min_ratio, &h[1], 8);
+  *points = (int64_t)h[2];
+  return 0;
 }
 
 FV_API int fv_selftest_fast(int64_t n, uint64_t seed, int64_t* mismatches, int64_t* flagged) {

@@ -333,6 +333,19 @@ def test_device_constant_division_is_ieee(fv):
     assert bad.value == 0
 
 
+def test_quick_far_low_bound_exhaustive(fv):
+    """The lower-bound table behind the normalize pass's quick far-low
+    decision (fv_fast.h g_qlo_tab) holds on EVERY fp32 |x| of its range:
+    b_lo(x) >= bound(bin(x)), with the exact anchor of the careful routine."""
+    from paper_2604_27210_b200 import _native
+    lib = _native.lib_for_compute()
+    bad, ratio, pts = ctypes.c_int64(), ctypes.c_double(), ctypes.c_int64()
+    assert lib.fv_selftest_qlo(ctypes.byref(bad), ctypes.byref(ratio), ctypes.byref(pts)) == 0
+    assert pts.value > 150_000_000
+    assert bad.value == 0, (bad.value, ratio.value)
+    assert 1.0 <= ratio.value < 1.1, ratio.value
+
+
 def test_fast_routines_match_careful_forms():
     """fv_fast.h: every unflagged result of the straight-line routines equals
     the careful routine bit for bit (and the flagged share stays small)."""

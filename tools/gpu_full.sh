@@ -33,3 +33,10 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_price_greeks -c 1 -o gpurun_out/profg_${TAG} python bench.py --workload c3 --steps 1 --warmup 0 --no-e2e --no-cpu --no-kernel-timing > gpurun_out/ncug_${TAG}.log 2>&1
   tail -1 gpurun_out/ncug_${TAG}.log
 fi
+if [ "${SAN:-1}" = "1" ]; then
+  for tool in memcheck racecheck synccheck initcheck; do
+    timeout 1200 compute-sanitizer --tool $tool --error-exitcode 1 python tools/sanitize.py > gpurun_out/sanitize_${TAG}_$tool.log 2>&1
+    echo "sanitize $tool rc=$? $(tail -1 gpurun_out/sanitize_${TAG}_$tool.log)"
+  done
+fi
+timeout 600 python tools/chain_e2e.py 1000000 "price,iv,greeks" > gpurun_out/chain_e2e_${TAG}.json 2>> gpurun_out/bench_${TAG}.err
