@@ -449,9 +449,27 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (same generator and rows as the GPU arm)",
             "config": config_for(args, args.gpus, n_total, scaling, ""),
             "cpu_baseline": cpu,
-            "e2e": {"value": value, "unit": "quotes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": value, "unit": "quotes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "repo_libs_loaded": repo_libs_loaded()}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def repo_libs_loaded():
+    """The repo's shared objects mapped into this process (/proc/self/maps):
+    the evidence of which native code a line's numbers came from -- the
+    product library and host extension for our arm, oracle/ for the reference
+    arm."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for ln in fh:
+                path = ln.split()[-1] if ln.strip() else ""
+                if path.endswith(".so") and os.path.realpath(path).startswith(os.path.realpath(REPO)):
+                    libs.add(os.path.relpath(os.path.realpath(path), os.path.realpath(REPO)))
+    except OSError:
+        return None
+    return sorted(libs)
 
 
 def run_ours(args):
@@ -838,6 +856,7 @@ def run_ours(args):
                                        "max_iterations"], st)),
             "per_call_ms": per_call_ms,
             "rank0_ms_per_step": own_ms / args.steps,
+            "repo_libs_loaded": repo_libs_loaded(),
         }
         print(json.dumps(line), flush=True)
     if pg:
