@@ -476,12 +476,21 @@ def run_ours(args):
     import torch
     from paper_2604_27210_b200 import _native
     world, rank, local = dist_setup()
+    # FV_BENCH_SHARE_GPUS=1 (tests only): ranks share the visible GPUs (local
+    # rank mod device count) over gloo, so the N > 1 code path runs on a
+    # 1-GPU box; its timings are not scaling numbers
+    share = os.environ.get("FV_BENCH_SHARE_GPUS") == "1"
+    if share:
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         pg = dist
     lib = _native.lib_for_compute()
     n_total, ranges, shard_label, Fr, scaling = plan(args, world, rank)
