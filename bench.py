@@ -794,6 +794,7 @@ def run_ours(args):
     call_s = float(np.mean(per_call_ms)) * 1e-3
     achieved = W_OPS[args.workload] * n / call_s / 1e12
     w_read = wp.get("W_read_mean") if args.workload == "c4" else None
+    w_done = wp.get("W_done_mean") if args.workload == "c4" else None
     in_bytes = sum(cols[k].numel() * cols[k].element_size()
                    for k in ("flag", "underlying", "strike", "t", "r", "q", last) if cols[k].numel() > 1)
     out_bytes = n * (17 if roundtrip else (9 if method >= 0 else 49))
@@ -827,6 +828,13 @@ def run_ours(args):
                                  "anchors that _region never reads (b_c, b_hi of far-low quotes, b_hi of "
                                  "near-low ones; %.0f of W=%.0f on a 30k-row C4 sample, tools/w_count.py) "
                                  "are skipped by the lazy-anchor passes" % (W_OPS["c4"] - w_read, W_OPS["c4"]))
+    if w_done:
+        roofline["frac_done"] = w_done * n / call_s / 1e12 / peak_tops if peak_tops else None
+        roofline["W_done"] = w_done
+        roofline["note_done"] = ("frac_done also leaves out the first anchor b_lo of every far-low quote "
+                                 "(%.0f of W per quote on average): the normalize pass's table bound proves "
+                                 "beta < b_lo without it for whole warps of the chain, so this is a lower "
+                                 "bound of the work done" % (w_read - w_done))
     if args.workload == "c2":
         roofline["note"] += ("; C2: the bracket pass decides f(10)'s sign in fp32 instead of evaluating it "
                              "(~8 % of W counted but not executed)")

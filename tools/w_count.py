@@ -119,7 +119,7 @@ def main():
         calls = [0]
 
         def nb(*aa, **kk):
-            STATE["phase"] = (outer, "anchor_c", "anchor_hi")[min(calls[0], 2)]
+            STATE["phase"] = ("anchor_lo", "anchor_c", "anchor_hi")[min(calls[0], 2)]
             calls[0] += 1
             try:
                 return real_nb(*aa, **kk)
@@ -150,19 +150,22 @@ def main():
         reg = seen_region.get("r", "FINISHED")
         w = STATE["w"]
         totals.append(sum(w.values()))
-        d = by.setdefault(reg, {"n": 0, "classify": 0.0, "solve": 0.0, "anchor_c": 0.0, "anchor_hi": 0.0})
+        d = by.setdefault(reg, {"n": 0, "classify": 0.0, "solve": 0.0, "anchor_lo": 0.0, "anchor_c": 0.0,
+                                "anchor_hi": 0.0})
         d["n"] += 1
-        # b_c / b_hi: classification work (as before), also reported apart
-        d["classify"] += w.get("classify", 0.0) + w.get("anchor_c", 0.0) + w.get("anchor_hi", 0.0)
+        # b_lo / b_c / b_hi: classification work (as before), also reported apart
+        d["classify"] += (w.get("classify", 0.0) + w.get("anchor_lo", 0.0) + w.get("anchor_c", 0.0)
+                          + w.get("anchor_hi", 0.0))
         d["solve"] += w.get("solve", 0.0)
+        d["anchor_lo"] += w.get("anchor_lo", 0.0)
         d["anchor_c"] += w.get("anchor_c", 0.0)
         d["anchor_hi"] += w.get("anchor_hi", 0.0)
     out = {"workload": "c4", "rows": len(totals), "sample": f"every {stride}th row of the C4 chain",
            "W_total_mean": float(np.mean(totals)), "by_region": {}}
     for k, d in by.items():
         out["by_region"][k] = {"share": d["n"] / len(totals), "W_classify": d["classify"] / d["n"],
-                               "W_solve": d["solve"] / d["n"], "W_anchor_c": d["anchor_c"] / d["n"],
-                               "W_anchor_hi": d["anchor_hi"] / d["n"]}
+                               "W_solve": d["solve"] / d["n"], "W_anchor_lo": d["anchor_lo"] / d["n"],
+                               "W_anchor_c": d["anchor_c"] / d["n"], "W_anchor_hi": d["anchor_hi"] / d["n"]}
     # W of the anchors the lazy-anchor path does not evaluate: far-low quotes
     # skip b_c and b_hi, near-low quotes b_hi (lbr.py:241-248 never reads them)
     skip = 0.0
@@ -173,6 +176,11 @@ def main():
             skip += d["anchor_hi"]
     out["W_anchors_not_read_mean"] = skip / len(totals)
     out["W_read_mean"] = out["W_total_mean"] - out["W_anchors_not_read_mean"]
+    # the first anchor of far-low quotes as well (round 2: a table bound decides
+    # beta < b_lo without it for whole warps of the chain): a lower bound of the
+    # work the GPU path evaluates
+    fl = by.get("FAR_LOW")
+    out["W_done_mean"] = out["W_read_mean"] - (fl["anchor_lo"] / len(totals) if fl else 0.0)
     print(json.dumps(out, indent=1))
 
 
