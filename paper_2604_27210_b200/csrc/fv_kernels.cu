@@ -2124,9 +2124,28 @@ bool is_pageable(const void* p) {
   return at.type == cudaMemoryTypeUnregistered;
 }
 
+// Rows per chunk of a host-buffer call: the configured size (2^22 by default,
+// fv_set_chunk_rows), but at least 8 chunks when the call is smaller than 8 of
+// them, down to 2^18 rows: the first chunk's H2D and the last chunk's kernels
+// + D2H overlap nothing, so a 10M-row call in three 4M-row chunks spent a
+// third of its time filling and draining the pipeline.
+#ifndef FV_HOST_AUTO_CHUNK
+#define FV_HOST_AUTO_CHUNK 1
+#endif
+int64_t host_chunk_rows(int64_t n) {
+  int64_t c = g_chunk_rows;
+#if FV_HOST_AUTO_CHUNK
+  const int64_t eighth = ((n / 8 + 65535) / 65536) * 65536;
+  const int64_t want = eighth > (1ll << 18) ? eighth : (1ll << 18);
+  if (want < c) c = want;
+#endif
+  (void)n;
+  return c;
+}
+
 int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_error* e2) {
   cudaError_t ce;
-  const int64_t chunk = g_chunk_rows;
+  const int64_t chunk = host_chunk_rows(c.n);
   const int64_t n = c.n;
   // column element sizes and whether each is streamed
   const size_t in_sz[7] = {1, 8, 8, 8, 8, 8, 8};
@@ -2148,7 +2167,10 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
   // column streamed, six outputs, status, region): a call with more streamed
   // columns than the last one must not pay another pinned allocation (~0.4 s
   // for the three staging slots of 2^22 rows)
-  const size_t max_slot = align(chunk) + 6 * align(8 * chunk) + 6 * align(8 * chunk) + 2 * align(chunk);
+  // (sized for the configured chunk, so smaller auto-sized chunks of a
+  // mid-size call never shrink the buffers a large call needs)
+  const int64_t cap_rows = g_chunk_rows > chunk ? g_chunk_rows : chunk;
+  const size_t max_slot = align(cap_rows) + 6 * align(8 * cap_rows) + 6 * align(8 * cap_rows) + 2 * align(cap_rows);
   for (int s = 0; s < FV_NSLOT; ++s) {
     if (w->chunk_cap_rows[s] < (int64_t)slot_bytes) {
       if (w->chunk[s]) cudaFree(w->chunk[s]);
