@@ -3019,13 +3019,20 @@ FV_API int fv_probe_fp64_peak(double* dfma_per_s, double* seconds) {
   const int iters = 4096;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
+  // alone on the device (work still draining on the library's non-blocking
+  // streams would share the SMs), the fastest of three timed runs
+  cudaError_t ce = cudaDeviceSynchronize();
   k_fp64_probe<<<blocks, 256>>>(out, 64, 0.999999, 1e-7);          // warm-up
-  cudaEventRecord(e0);
-  k_fp64_probe<<<blocks, 256>>>(out, iters, 0.999999, 1e-7);
-  cudaEventRecord(e1);
-  cudaError_t ce = cudaEventSynchronize(e1);
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
+  for (int rep = 0; rep < 3 && ce == cudaSuccess; ++rep) {
+    cudaEventRecord(e0);
+    k_fp64_probe<<<blocks, 256>>>(out, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    ce = cudaEventSynchronize(e1);
+    float m = 0.f;
+    cudaEventElapsedTime(&m, e0, e1);
+    if (rep == 0 || m < ms) ms = m;
+  }
   cudaEventDestroy(e0); cudaEventDestroy(e1);
   cudaFree(out);
   if (ce != cudaSuccess) return FV_ERR_CUDA;
