@@ -343,7 +343,10 @@ def test_quick_far_low_bound_exhaustive(fv):
     assert lib.fv_selftest_qlo(ctypes.byref(bad), ctypes.byref(ratio), ctypes.byref(pts)) == 0
     assert pts.value > 150_000_000
     assert bad.value == 0, (bad.value, ratio.value)
-    assert 1.0 <= ratio.value < 1.1, ratio.value
+    # every fp32 point clears its bound by more than b_lo can move between two
+    # consecutive fp32 points (|d ln b_lo / dx| |x| 2^-23 <= 5e-6 for |x| < 32),
+    # so every double x of the range does too
+    assert 1.0 + 2e-5 <= ratio.value < 1.1, ratio.value
 
 
 def test_fast_routines_match_careful_forms():
