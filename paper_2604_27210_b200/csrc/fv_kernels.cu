@@ -419,6 +419,9 @@ __device__ __forceinline__ void lbr_norm_row_careful(const KArgs& a, const LbrQu
 // 4-block form (64 registers, ~110 B of spills; C4 13.70 -> 13.61 ms), small
 // ones the 3-block form (80 registers; C1 is latency-bound and 2.5 % slower
 // at 4) -- see FV_NORM_BIG_ROWS.
+#ifndef FV_NORM_DEFER_FL
+#define FV_NORM_DEFER_FL 1
+#endif
 template <int MINB>
 __global__ void __launch_bounds__(256, MINB) k_lbr_normalize(KArgs a, LbrQueues lq) {
   pdl_wait();
@@ -433,6 +436,9 @@ __global__ void __launch_bounds__(256, MINB) k_lbr_normalize(KArgs a, LbrQueues 
     if (lane == 0) claim = atomicAdd(lq.count + 8, lq.norm_claim);
     claim = __shfl_sync(0xffffffffu, claim, 0);
     if ((int64_t)claim >= npair) break;
+#if FV_NORM_DEFER_FL
+    unsigned flbits = 0;            // far-low rows of the claim: bit 2 sub + u
+#endif
 #pragma unroll 1
   for (int sub = 0; sub < (int)(lq.norm_claim / 32); ++sub) {
     const unsigned int base = claim + 32u * sub;
@@ -489,9 +495,14 @@ __global__ void __launch_bounds__(256, MINB) k_lbr_normalize(KArgs a, LbrQueues 
     }
     // queue appends in row order (lane 0's pair, lane 1's pair, ...); far-low
     // entries are 2 * row (the solve's entry format), the others plain rows
+#if FV_NORM_DEFER_FL
+    flbits |= ((unsigned)flow[0] | ((unsigned)flow[1] << 1)) << (2 * sub);
+    unsigned int slot;
+#else
     unsigned int slot = warp_append2(lq.count + 0, flow[0], flow[1]);
     if (flow[0]) { lq.q[0][slot++] = (int32_t)(2 * i); }
     if (flow[1]) { lq.q[0][slot] = (int32_t)(2 * (i + 1)); }
+#endif
     slot = warp_append2(lq.count + 3, pend[0], pend[1]);
     if (pend[0]) { lq.q[3][slot++] = (int32_t)i; }
     if (pend[1]) { lq.q[3][slot] = (int32_t)(i + 1); }
@@ -501,6 +512,30 @@ __global__ void __launch_bounds__(256, MINB) k_lbr_normalize(KArgs a, LbrQueues 
       if (rep[1]) { lq.q[5][slot] = (int32_t)(i + 1); }
     }
   }
+#if FV_NORM_DEFER_FL
+    // the claim's far-low rows in one append (one atomic per claim instead of
+    // one per 32 pairs); entries in (sub, lane, u) order, 2 * row each
+    {
+      const unsigned lt = (1u << lane) - 1;
+      unsigned total = 0;
+      for (int b = 0; b < 8; ++b) total += __popc(__ballot_sync(0xffffffffu, (flbits >> b) & 1u));
+      unsigned int base0 = 0;
+      if (total) {
+        if (lane == 0) base0 = atomicAdd(lq.count + 0, total);
+        base0 = __shfl_sync(0xffffffffu, base0, 0);
+      }
+      unsigned off = 0;
+      for (int sb = 0; sb < 4; ++sb) {
+        const unsigned m0 = __ballot_sync(0xffffffffu, (flbits >> (2 * sb)) & 1u);
+        const unsigned m1 = __ballot_sync(0xffffffffu, (flbits >> (2 * sb + 1)) & 1u);
+        unsigned slot = base0 + off + __popc(m0 & lt) + __popc(m1 & lt);
+        const int64_t ii = 2 * ((int64_t)claim + 32 * sb + lane);
+        if ((flbits >> (2 * sb)) & 1u) lq.q[0][slot++] = (int32_t)(2 * ii);
+        if ((flbits >> (2 * sb + 1)) & 1u) lq.q[0][slot] = (int32_t)(2 * (ii + 1));
+        off += __popc(m0) + __popc(m1);
+      }
+    }
+#endif
   }
 }
 
