@@ -422,6 +422,30 @@ __device__ __forceinline__ void lbr_norm_row_careful(const KArgs& a, const LbrQu
 #ifndef FV_NORM_DEFER_FL
 #define FV_NORM_DEFER_FL 1
 #endif
+// One queue append for a whole normalize claim (warp-collective): bits =
+// this lane's rows of the claim (bit 2 sub + u for row 2 (claim + 32 sub +
+// lane) + u); entries in (sub, lane, u) order, row * mul each.
+__device__ __forceinline__ void claim_append(unsigned bits, unsigned int* counter, int32_t* q, unsigned claim,
+                                             int mul, int lane) {
+  const unsigned lt = (1u << lane) - 1;
+  unsigned m[8];
+  unsigned total = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) { m[b] = __ballot_sync(0xffffffffu, (bits >> b) & 1u); total += __popc(m[b]); }
+  if (!total) return;
+  unsigned int base0 = 0;
+  if (lane == 0) base0 = atomicAdd(counter, total);
+  base0 = __shfl_sync(0xffffffffu, base0, 0);
+  unsigned off = 0;
+#pragma unroll
+  for (int sb = 0; sb < 4; ++sb) {
+    unsigned slot = base0 + off + __popc(m[2 * sb] & lt) + __popc(m[2 * sb + 1] & lt);
+    const int64_t ii = 2 * ((int64_t)claim + 32 * sb + lane);
+    if ((bits >> (2 * sb)) & 1u) q[slot++] = (int32_t)(mul * ii);
+    if ((bits >> (2 * sb + 1)) & 1u) q[slot] = (int32_t)(mul * (ii + 1));
+    off += __popc(m[2 * sb]) + __popc(m[2 * sb + 1]);
+  }
+}
 template <int MINB>
 __global__ void __launch_bounds__(256, MINB) k_lbr_normalize(KArgs a, LbrQueues lq) {
   pdl_wait();
@@ -437,7 +461,7 @@ __global__ void __launch_bounds__(256, MINB) k_lbr_normalize(KArgs a, LbrQueues 
     claim = __shfl_sync(0xffffffffu, claim, 0);
     if ((int64_t)claim >= npair) break;
 #if FV_NORM_DEFER_FL
-    unsigned flbits = 0;            // far-low rows of the claim: bit 2 sub + u
+    unsigned flbits = 0, pdbits = 0;   // far-low / pending rows of the claim: bit 2 sub + u
 #endif
 #pragma unroll 1
   for (int sub = 0; sub < (int)(lq.norm_claim / 32); ++sub) {
@@ -497,15 +521,16 @@ __global__ void __launch_bounds__(256, MINB) k_lbr_normalize(KArgs a, LbrQueues 
     // entries are 2 * row (the solve's entry format), the others plain rows
 #if FV_NORM_DEFER_FL
     flbits |= ((unsigned)flow[0] | ((unsigned)flow[1] << 1)) << (2 * sub);
+    pdbits |= ((unsigned)pend[0] | ((unsigned)pend[1] << 1)) << (2 * sub);
     unsigned int slot;
 #else
     unsigned int slot = warp_append2(lq.count + 0, flow[0], flow[1]);
     if (flow[0]) { lq.q[0][slot++] = (int32_t)(2 * i); }
     if (flow[1]) { lq.q[0][slot] = (int32_t)(2 * (i + 1)); }
-#endif
     slot = warp_append2(lq.count + 3, pend[0], pend[1]);
     if (pend[0]) { lq.q[3][slot++] = (int32_t)i; }
     if (pend[1]) { lq.q[3][slot] = (int32_t)(i + 1); }
+#endif
     if (__any_sync(0xffffffffu, rep[0] || rep[1])) {
       slot = warp_append2(lq.count + 5, rep[0], rep[1]);
       if (rep[0]) { lq.q[5][slot++] = (int32_t)i; }
@@ -513,28 +538,11 @@ __global__ void __launch_bounds__(256, MINB) k_lbr_normalize(KArgs a, LbrQueues 
     }
   }
 #if FV_NORM_DEFER_FL
-    // the claim's far-low rows in one append (one atomic per claim instead of
-    // one per 32 pairs); entries in (sub, lane, u) order, 2 * row each
-    {
-      const unsigned lt = (1u << lane) - 1;
-      unsigned total = 0;
-      for (int b = 0; b < 8; ++b) total += __popc(__ballot_sync(0xffffffffu, (flbits >> b) & 1u));
-      unsigned int base0 = 0;
-      if (total) {
-        if (lane == 0) base0 = atomicAdd(lq.count + 0, total);
-        base0 = __shfl_sync(0xffffffffu, base0, 0);
-      }
-      unsigned off = 0;
-      for (int sb = 0; sb < 4; ++sb) {
-        const unsigned m0 = __ballot_sync(0xffffffffu, (flbits >> (2 * sb)) & 1u);
-        const unsigned m1 = __ballot_sync(0xffffffffu, (flbits >> (2 * sb + 1)) & 1u);
-        unsigned slot = base0 + off + __popc(m0 & lt) + __popc(m1 & lt);
-        const int64_t ii = 2 * ((int64_t)claim + 32 * sb + lane);
-        if ((flbits >> (2 * sb)) & 1u) lq.q[0][slot++] = (int32_t)(2 * ii);
-        if ((flbits >> (2 * sb + 1)) & 1u) lq.q[0][slot] = (int32_t)(2 * (ii + 1));
-        off += __popc(m0) + __popc(m1);
-      }
-    }
+    // the claim's far-low and pending rows, one append each (one atomic ->
+    // shfl -> store chain per claim instead of one per 32 pairs); far-low
+    // entries are 2 * row (the solve's entry format), pending ones plain rows
+    claim_append(flbits, lq.count + 0, lq.q[0], claim, 2, lane);
+    claim_append(pdbits, lq.count + 3, lq.q[3], claim, 1, lane);
 #endif
   }
 }
