@@ -2423,7 +2423,8 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
       dev_in[col] = base + off_in[col];
       const void* src = (piv && col == 6) ? (const void*)(c.outs[0] + row)
                                           : (const void*)((const char*)c.cols[col].data + row * in_sz[col]);
-      cudaMemcpy(dev_in[col], src, in_sz[col], cudaMemcpyHostToDevice);
+      cudaMemcpyAsync(dev_in[col], src, in_sz[col], cudaMemcpyHostToDevice, s0);   // ordered before the
+                                                                                // explain kernel on s0
     }
     ax.flag = make_dflag(c.cols[0], dev_in[0]);
     ax.un = make_dcol(c.cols[1], dev_in[1]);
@@ -2690,7 +2691,13 @@ int dispatch(Call c, fv_error* e1, fv_error* e2) {
     int8_t f8 = (int8_t)flag_val;
     memcpy(&tmp[7], &f8, 1);
     for (int i = 1; i < 7; ++i) tmp[i] = vals[i];
-    if ((ce = cudaMemcpy(w->scal, tmp, sizeof(tmp), cudaMemcpyHostToDevice)) != cudaSuccess)
+    // On the host pipeline's first stream, ahead of its status reset and the
+    // `ready` event every slot stream waits on: a synchronous cudaMemcpy from
+    // pageable memory may return before its DMA lands, and the library's
+    // streams do not synchronise with the legacy default stream, so a
+    // kernel could read the previous call's scalars (seen once in ~10^6 calls:
+    // a 1-row batch_iv solving the preceding batch_price's sigma).
+    if ((ce = cudaMemcpyAsync(w->scal, tmp, sizeof(tmp), cudaMemcpyHostToDevice, w->streams[0])) != cudaSuccess)
       return set_cuda_err(e1, ce);
     const int8_t* dflag = (const int8_t*)(w->scal + 7);
     for (int i = 0; i < 7; ++i)
