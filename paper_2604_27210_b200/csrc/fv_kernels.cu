@@ -34,6 +34,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <chrono>
 #include <condition_variable>
 #include <functional>
 #include <mutex>
@@ -2238,11 +2239,61 @@ bool is_pageable(const void* p) {
 #ifndef FV_HOST_AUTO_CHUNK
 #define FV_HOST_AUTO_CHUNK 1
 #endif
+#ifndef FV_HOST_CHUNK_DIV
+#define FV_HOST_CHUNK_DIV 8
+#endif
+#ifndef FV_HOST_CHUNK_MIN_LOG2
+#define FV_HOST_CHUNK_MIN_LOG2 18
+#endif
+// FV_HOST_TRACE (diagnostic builds only): per-call host timestamps and a
+// device timeline of each chunk's H2D / kernels / D2H on stderr
+#ifndef FV_HOST_TRACE
+#define FV_HOST_TRACE 0
+#endif
+#if FV_HOST_TRACE
+__device__ unsigned long long g_stamps[512];
+__global__ void k_stamp(int i) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_stamps[i] = t;
+}
+struct HostTrace {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  std::vector<std::pair<const char*, double>> marks;
+  std::vector<const char*> names;
+  std::vector<std::pair<int64_t, int>> ev_chunk;
+  void mark(const char* m) {
+    marks.push_back({m, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count()});
+  }
+  void ev(const char* name, int64_t ci, int slot, cudaStream_t s) {
+    if (names.size() >= 512) return;
+    k_stamp<<<1, 1, 0, s>>>((int)names.size());
+    names.push_back(name);
+    ev_chunk.push_back({ci, slot});
+  }
+  ~HostTrace() {
+    mark("trace_end");
+    for (auto& m : marks) fprintf(stderr, "host %-14s %9.1f us\n", m.first, m.second);
+    if (names.empty()) return;
+    cudaDeviceSynchronize();
+    unsigned long long st[512];
+    cudaMemcpyFromSymbol(st, g_stamps, sizeof(st));
+    for (size_t i = 0; i < names.size(); ++i)
+      fprintf(stderr, "dev  chunk %3lld slot %d %-10s %9.1f us\n", (long long)ev_chunk[i].first, ev_chunk[i].second,
+              names[i], 1e-3 * (double)(st[i] - st[0]));
+  }
+};
+#define TR_MARK(x) tr.mark(x)
+#define TR_EV(n, ci, sl, st) tr.ev(n, ci, sl, st)
+#else
+#define TR_MARK(x) ((void)0)
+#define TR_EV(n, ci, sl, st) ((void)0)
+#endif
 int64_t host_chunk_rows(int64_t n) {
   int64_t c = g_chunk_rows;
 #if FV_HOST_AUTO_CHUNK
-  const int64_t eighth = ((n / 8 + 65535) / 65536) * 65536;
-  const int64_t want = eighth > (1ll << 18) ? eighth : (1ll << 18);
+  const int64_t eighth = ((n / FV_HOST_CHUNK_DIV + 65535) / 65536) * 65536;
+  const int64_t want = eighth > (1ll << FV_HOST_CHUNK_MIN_LOG2) ? eighth : (1ll << FV_HOST_CHUNK_MIN_LOG2);
   if (want < c) c = want;
 #endif
   (void)n;
@@ -2251,6 +2302,9 @@ int64_t host_chunk_rows(int64_t n) {
 
 int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_error* e2) {
   cudaError_t ce;
+#if FV_HOST_TRACE
+  HostTrace tr;
+#endif
   const int64_t chunk = host_chunk_rows(c.n);
   const int64_t n = c.n;
   // column element sizes and whether each is streamed
@@ -2302,6 +2356,7 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
       }
     }
   }
+  TR_MARK("buffers_ready");
   struct SlotEvents {
     cudaEvent_t ev[FV_NSLOT];
     SlotEvents() { for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming); }
@@ -2339,6 +2394,8 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
   KArgs a_first;
   memset(&a_first, 0, sizeof(a_first));
   const int64_t nchunks = (int64_t)plan.size();
+  TR_MARK("setup_done");
+  TR_EV("start", -1, 0, w->streams[0]);
   for (int64_t ci = 0; ci < nchunks; ++ci) {
     int slot = (int)(ci % FV_NSLOT);
     cudaStream_t s = w->streams[slot];
@@ -2355,6 +2412,7 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
       par_memcpy_batch(segs);
     }
     void* dev_in[7];
+    TR_EV("h2d_start", ci, slot, s);
     for (int col = 0; col < 7; ++col) {
       if (c.cols[col].stride == 0) { dev_in[col] = nullptr; continue; }
       dev_in[col] = base + off_in[col];
@@ -2381,7 +2439,9 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
     a.status = has_status ? (int8_t*)(base + off_status) : nullptr;
     a.region = has_region ? (int8_t*)(base + off_region) : nullptr;
     if (ci == 0) a_first = a;
+    TR_EV("h2d_done", ci, slot, s);
     if ((ce = launch(w, c, a, slot, s)) != cudaSuccess) { cudaEventDestroy(ready); return set_cuda_err(e1, ce); }
+    TR_EV("kern_done", ci, slot, s);
     for (int i = 0; i < 6; ++i)
       if (c.outs[i])
         cudaMemcpyAsync(stage_out[i] ? (void*)(stg + off_out[i]) : (void*)(c.outs[i] + r0), douts[i], 8 * rn,
@@ -2393,6 +2453,8 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
       cudaMemcpyAsync(stage_region ? (void*)(stg + off_region) : (void*)(c.region + r0), a.region, rn,
                       cudaMemcpyDeviceToHost, s);
     if (any_stage) { cudaEventRecord(slot_done[slot], s); slot_chunk[slot] = ci; }
+    TR_EV("d2h_done", ci, slot, s);
+    TR_MARK("chunk_issued");
   }
   if (any_stage) for (int s = 0; s < FV_NSLOT; ++s) drain(s);
   for (int s = 1; s < FV_NSLOT; ++s) {
@@ -2407,6 +2469,7 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
   for (int s = 1; s < FV_NSLOT; ++s)
     if ((ce = cudaStreamSynchronize(w->streams[s])) != cudaSuccess) return set_cuda_err(e1, ce);
   if ((ce = cudaGetLastError()) != cudaSuccess) return set_cuda_err(e1, ce);
+  TR_MARK("synced");
   // exceptions in later chunks: the explain kernel needs that chunk's inputs;
   // re-stage the offending row alone (fv_price_iv: the IV stage's row, its
   // price from the caller's price column).
