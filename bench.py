@@ -712,6 +712,8 @@ def run_ours(args):
             if rc:
                 raise RuntimeError(err.message)
         estep()
+        h2d_logical = h2d
+        h2d = int(lib.fv_last_h2d_bytes())          # what crossed the link (runs for piecewise-constant columns)
         if pg:
             pg.barrier()
         times = []
@@ -749,6 +751,10 @@ def run_ours(args):
         except Exception:  # noqa: BLE001
             pass
         e2e = {"value": units / (e_ms * 1e-3), "unit": "quotes/s", "h2d_bytes_per_step": int(h2d),
+               "h2d_bytes_per_step_logical": int(h2d_logical),
+               "h2d_note": "h2d_bytes_per_step = bytes the call moved host -> device (fv_last_h2d_bytes): "
+                           "streamed columns, piecewise-constant columns as (first row, value) runs "
+                           "rebuilt on the device, broadcast scalars; _logical = the input arrays' bytes",
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms,
                "timing": "wall clock around the synchronous C-ABI call (host buffers pinned), max over ranks",
                "bit_identical_to_device_resident": same, "pcie_h2d_gbs": h2d_gbs,

@@ -225,6 +225,13 @@ FV_API int fv_set_chunk_rows(int64_t rows);
  * bench's gpu_launches count). */
 FV_API int64_t fv_last_launch_count(void);
 
+/* Bytes this thread's last host-pointer call moved host -> device: streamed
+ * columns, the run-length form of piecewise-constant ones (a chunk whose
+ * column is at most rows/64 runs of one value travels as (first row, value)
+ * runs and is rebuilt in device memory), broadcast scalars.  0 for
+ * device-pointer calls. */
+FV_API int64_t fv_last_h2d_bytes(void);
+
 /* Testing knob: rows per LBR classify/solve round and per Halley chunk of
  * one launch (0 = default: 2^27 and 2^26; Halley <= 2^26).  Results do not
  * depend on it; tests force multi-round calls on small batches with it. */

@@ -34,9 +34,11 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
 #include <chrono>
 #include <condition_variable>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <utility>
@@ -1417,6 +1419,7 @@ namespace {
 thread_local cudaStream_t t_user_stream = nullptr;
 thread_local bool t_user_stream_set = false;   // fv_set_stream called (NULL = legacy default stream)
 thread_local int64_t t_launches = 0;
+thread_local int64_t t_h2d_bytes = 0;       // host calls: bytes this thread's last call moved host -> device
 
 // Optional per-kernel timing (fv_set_kernel_timing): CUDA events around every
 // launch on the launching stream, summed per kernel by fv_kernel_times.
@@ -1489,6 +1492,9 @@ struct DevWork {
   int64_t chunk_cap_rows[FV_NSLOT] = {};
   char* stage[FV_NSLOT] = {};              // pinned host staging (pageable callers)
   int64_t stage_cap[FV_NSLOT] = {};
+  char* rle_host[FV_NSLOT] = {};           // pinned: a chunk's column runs (run-length transport)
+  char* rle_dev[FV_NSLOT] = {};
+  int64_t rle_cap[FV_NSLOT] = {};
   ExplainOut* explain = nullptr;
   double* scal = nullptr;               // device copies of a host call's broadcast scalars
   // LBR classify -> solve workspace (per slot)
@@ -2128,23 +2134,37 @@ class CopyPool {
     return *pool;
   }
   int workers() const { return (int)th_.size(); }
-  // runs fn(0..parts-1), part 0 on the caller; returns when all are done
+  // runs fn(0..parts-1), part 0 on the caller; returns when all are done.
+  // Workers spin for a while after each job and the caller spins on the
+  // completion count before sleeping: a host call hands the pool one job per
+  // chunk, and a futex wake-up (tens of us on the bench boxes) per job and per
+  // join showed up as host-side gaps in the pipeline.
   void run(int parts, const std::function<void(int)>& fn) {
     std::unique_lock<std::mutex> lk(mu_);
     job_ = &fn;
     next_ = 1;
     parts_ = parts;
-    pending_ = parts - 1;
+    pending_.store(parts - 1, std::memory_order_relaxed);
     ++gen_;
+    agen_.store(gen_, std::memory_order_release);
     cv_.notify_all();
     lk.unlock();
     fn(0);
+    const auto t0 = std::chrono::steady_clock::now();
+    while (pending_.load(std::memory_order_acquire) != 0 &&
+           std::chrono::steady_clock::now() - t0 < std::chrono::milliseconds(5))
+      cpu_relax();
     lk.lock();
-    done_.wait(lk, [&] { return pending_ == 0; });
+    done_.wait(lk, [&] { return pending_.load(std::memory_order_acquire) == 0; });
     job_ = nullptr;
   }
 
  private:
+  static void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+  }
   CopyPool() {
     unsigned nt = std::thread::hardware_concurrency();
     if (nt > 16) nt = 16;
@@ -2152,9 +2172,13 @@ class CopyPool {
   }
   void loop() {
     unsigned long long seen = 0;
-    std::unique_lock<std::mutex> lk(mu_);
     for (;;) {
-      cv_.wait(lk, [&] { return gen_ != seen && job_ && next_ < parts_; });
+      const auto t0 = std::chrono::steady_clock::now();
+      while (agen_.load(std::memory_order_acquire) == seen &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(500))
+        cpu_relax();
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return gen_ != seen; });
       seen = gen_;
       while (job_ && next_ < parts_) {
         const int part = next_++;
@@ -2162,7 +2186,7 @@ class CopyPool {
         lk.unlock();
         (*fn)(part);
         lk.lock();
-        if (--pending_ == 0) done_.notify_all();
+        if (pending_.fetch_sub(1, std::memory_order_acq_rel) == 1) done_.notify_all();
       }
     }
   }
@@ -2170,8 +2194,10 @@ class CopyPool {
   std::mutex mu_;
   std::condition_variable cv_, done_;
   const std::function<void(int)>* job_ = nullptr;
-  int next_ = 0, parts_ = 0, pending_ = 0;
+  int next_ = 0, parts_ = 0;
+  std::atomic<int> pending_{0};
   unsigned long long gen_ = 0;
+  std::atomic<unsigned long long> agen_{0};
 };
 std::mutex g_copy_mu;     // one pooled copy at a time (calls on several devices share the pool)
 
@@ -2223,6 +2249,179 @@ std::vector<std::pair<int64_t, int64_t>> chunk_plan(int64_t n, int64_t chunk) {
   plan.push_back({r0, h}); r0 += h;
   plan.push_back({r0, n - r0});
   return plan;
+}
+
+// ---- run-length transport of piecewise-constant host columns ---------------
+// A host call's input column whose chunk is a few runs of one value (an option
+// chain's maturity column, a flag column sorted by side, one value repeated as
+// an array) crosses the link as (first row, value) runs and k_expand_runs
+// rebuilds the chunk's column in HBM: the kernels read the same bits, the link
+// carries 12 bytes per run instead of 8 per row (C4's chain: t and flag, 9 of
+// its 25 bytes per quote).  A chunk uses it when it has at most
+// rows / kRleRowsPerRun runs; the scan runs on the copy pool, each part giving
+// up past its share of that budget, so a column of distinct values costs about
+// 1/kRleRowsPerRun of a pass over it.
+#ifndef FV_HOST_RLE
+#define FV_HOST_RLE 1
+#endif
+const int64_t kRleRowsPerRun = 64;
+const int64_t kRleMinRows = 1 << 14;
+
+// bytes of one column's runs area for a chunk of `rows` rows: int32 starts
+// [budget + 1] then the values [budget], 256-byte aligned
+size_t rle_starts_bytes(int64_t rows) {
+  const int64_t b = rows / kRleRowsPerRun + 1;
+  return (4 * (size_t)(b + 1) + 255) & ~(size_t)255;
+}
+size_t rle_col_bytes(int64_t rows, size_t elem) {
+  const int64_t b = rows / kRleRowsPerRun + 1;
+  return rle_starts_bytes(rows) + ((elem * (size_t)b + 255) & ~(size_t)255);
+}
+
+// row i of the chunk takes the value of the last run starting at or before i;
+// each block covers a contiguous tile, so a thread searches only the runs
+// that meet its block's tile
+template <typename T>
+__global__ void __launch_bounds__(256) k_expand_runs(const int32_t* __restrict__ starts, const T* __restrict__ vals,
+                                                     int nruns, T* __restrict__ out, int64_t n) {
+  const int64_t tile = (int64_t)blockDim.x * 8;
+  __shared__ int s_r0, s_r1;
+  for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < n; t0 += (int64_t)gridDim.x * tile) {
+    const int64_t t1 = (t0 + tile < n ? t0 + tile : n) - 1;
+    if (threadIdx.x < 2) {
+      const int64_t row = threadIdx.x ? t1 : t0;
+      int lo = 0, hi = nruns - 1;                 // last run with starts[r] <= row
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (starts[mid] <= row) lo = mid; else hi = mid - 1;
+      }
+      if (threadIdx.x) s_r1 = lo; else s_r0 = lo;
+    }
+    __syncthreads();
+    const int r0 = s_r0, r1 = s_r1;
+    for (int64_t i = t0 + threadIdx.x; i <= t1; i += blockDim.x) {
+      int lo = r0, hi = r1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (starts[mid] <= i) lo = mid; else hi = mid - 1;
+      }
+      out[i] = vals[lo];
+    }
+    __syncthreads();
+  }
+}
+
+// One chunk's candidate columns scanned for runs in ONE pool job (a fork /
+// join per column cost ~40 us each): every column is cut into parts of >= 32K
+// rows (a thread scans ~10 GB/s), each part gives up past its share of the
+// column's budget.  Per column: nr runs into starts / vals (starts[nr] = n),
+// or nr = -1 when the column has more than `budget` runs.
+struct RunScan {
+  const void* p;
+  int elem;                 // 8 (double bits) or 1 (flag)
+  int64_t n, budget;
+  int32_t* starts;
+  void* vals;
+  int64_t nr;
+  char* copy_to;            // pageable column: also copied here (pinned staging) in the same pass
+};
+
+// rows [lo, hi) of one column: its runs (the first entry may continue the
+// previous part's last run; the merge drops it).  Runs that start in this
+// part are published to the column's total 64 at a time, and the scan stops
+// once that total passes the budget (a lower bound of the true count, so
+// stopping is always right; the exact count is checked after the join).
+template <typename T>
+void scan_part(const T* p, int64_t lo, int64_t hi, int64_t budget, std::atomic<int64_t>& total,
+               std::atomic<bool>& over, std::vector<std::pair<int64_t, uint64_t>>& v, int64_t& mine) {
+  T cur = p[lo];
+  v.push_back({lo, (uint64_t)cur});
+  int64_t counted = (lo == 0 || p[lo - 1] != cur) ? 1 : 0, pending = counted;
+  for (int64_t i = lo + 1; i < hi;) {
+    if (i + 8 <= hi) {                           // eight rows of the current run at a time
+      T acc = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc |= (T)(p[i + u] ^ cur);
+      if (acc == 0) { i += 8; continue; }
+    }
+    if (p[i] == cur) { ++i; continue; }
+    ++counted;
+    if (++pending == 64) {
+      if (total.fetch_add(pending, std::memory_order_relaxed) + pending > budget ||
+          over.load(std::memory_order_relaxed)) {
+        over.store(true, std::memory_order_relaxed);
+        return;
+      }
+      pending = 0;
+    }
+    cur = p[i];
+    v.push_back({i, (uint64_t)cur});
+    ++i;
+  }
+  total.fetch_add(pending, std::memory_order_relaxed);
+  mine = counted;
+}
+
+void find_runs_batch(std::vector<RunScan>& jobs) {
+  if (jobs.empty()) return;
+  CopyPool& pool = CopyPool::get();
+  const int nw = pool.workers() + 1;
+  struct Task { int job; int64_t lo, hi; };
+  std::vector<Task> tasks;
+  for (int j = 0; j < (int)jobs.size(); ++j) {
+    const RunScan& r = jobs[j];
+    int parts = (int)(r.n >> 15);                // >= 32K rows per part (a thread scans ~10 GB/s)
+    if (parts > nw) parts = nw;
+    if (parts < 1) parts = 1;
+    for (int k = 0; k < parts; ++k) tasks.push_back({j, r.n * k / parts, r.n * (k + 1) / parts});
+  }
+  const int nt = (int)tasks.size();
+  std::vector<std::vector<std::pair<int64_t, uint64_t>>> found(nt);
+  std::vector<int64_t> counted(nt, 0);
+  std::unique_ptr<std::atomic<bool>[]> over(new std::atomic<bool>[jobs.size()]);
+  std::unique_ptr<std::atomic<int64_t>[]> total(new std::atomic<int64_t>[jobs.size()]);
+  for (size_t j = 0; j < jobs.size(); ++j) {
+    over[j].store(jobs[j].budget < 1 || jobs[j].n <= 0);
+    total[j].store(0);
+  }
+  auto run_task = [&](int t) {
+    const Task& k = tasks[t];
+    const RunScan& r = jobs[k.job];
+    if (r.copy_to)
+      memcpy(r.copy_to + k.lo * r.elem, (const char*)r.p + k.lo * r.elem, (size_t)((k.hi - k.lo) * r.elem));
+    if (over[k.job].load(std::memory_order_relaxed)) return;
+    if (r.elem == 8)
+      scan_part((const uint64_t*)r.p, k.lo, k.hi, r.budget, total[k.job], over[k.job], found[t], counted[t]);
+    else
+      scan_part((const uint8_t*)r.p, k.lo, k.hi, r.budget, total[k.job], over[k.job], found[t], counted[t]);
+  };
+  const int ntask = nt < nw ? nt : nw;
+  if (ntask <= 1) {
+    for (int t = 0; t < nt; ++t) run_task(t);
+  } else {
+    std::lock_guard<std::mutex> g(g_copy_mu);
+    pool.run(ntask, [&](int w) { for (int t = w; t < nt; t += ntask) run_task(t); });
+  }
+  std::vector<int64_t> exact(jobs.size(), 0);
+  for (int t = 0; t < nt; ++t) exact[tasks[t].job] += counted[t];
+  for (size_t j = 0; j < jobs.size(); ++j)
+    jobs[j].nr = (over[j].load() || exact[j] > jobs[j].budget) ? -1 : 0;
+  for (int t = 0; t < nt; ++t) {                 // tasks are in row order within a column
+    RunScan& r = jobs[tasks[t].job];
+    if (r.nr < 0) continue;
+    for (const auto& run : found[t]) {
+      if (r.nr > 0) {                             // the previous part's last run continues here
+        const uint64_t last = r.elem == 8 ? ((const uint64_t*)r.vals)[r.nr - 1] : ((const uint8_t*)r.vals)[r.nr - 1];
+        if (last == run.second) continue;
+      }
+      r.starts[r.nr] = (int32_t)run.first;
+      if (r.elem == 8) ((uint64_t*)r.vals)[r.nr] = run.second;
+      else ((uint8_t*)r.vals)[r.nr] = (uint8_t)run.second;
+      ++r.nr;
+    }
+  }
+  for (RunScan& r : jobs)
+    if (r.nr >= 0) r.starts[r.nr] = (int32_t)r.n;
 }
 
 bool is_pageable(const void* p) {
@@ -2356,13 +2555,42 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
       }
     }
   }
+  // run-length transport: candidate columns (the streamed ones) and each
+  // slot's runs areas, pinned and on the device
+  bool rle_cand[7] = {};
+  size_t off_rle[7] = {};
+  bool any_rle_cand = false;
+#if FV_HOST_RLE
+  if (n >= kRleMinRows && cap_rows < ((int64_t)1 << 31)) {
+    size_t rle_bytes = 0;
+    for (int col = 0; col < 7; ++col) {
+      off_rle[col] = rle_bytes;
+      rle_bytes += rle_col_bytes(cap_rows, in_sz[col]);
+      any_rle_cand |= (rle_cand[col] = c.cols[col].stride != 0);
+    }
+    for (int s = 0; any_rle_cand && s < FV_NSLOT; ++s) {
+      if (w->rle_cap[s] < (int64_t)rle_bytes) {
+        if (w->rle_host[s]) cudaFreeHost(w->rle_host[s]);
+        if (w->rle_dev[s]) cudaFree(w->rle_dev[s]);
+        w->rle_host[s] = nullptr;
+        w->rle_dev[s] = nullptr;
+        w->rle_cap[s] = 0;
+        if ((ce = cudaMallocHost(&w->rle_host[s], rle_bytes)) != cudaSuccess) return set_cuda_err(e1, ce);
+        if ((ce = cudaMalloc(&w->rle_dev[s], rle_bytes)) != cudaSuccess) return set_cuda_err(e1, ce);
+        w->rle_cap[s] = (int64_t)rle_bytes;
+      }
+    }
+  }
+#endif
   TR_MARK("buffers_ready");
   struct SlotEvents {
     cudaEvent_t ev[FV_NSLOT];
     SlotEvents() { for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming); }
     ~SlotEvents() { for (auto& e : ev) cudaEventDestroy(e); }
-  } sev;
+  } sev, rev;
   cudaEvent_t* slot_done = sev.ev;
+  cudaEvent_t* rle_sent = rev.ev;            // a slot's runs have left its pinned area
+  bool rle_inflight[FV_NSLOT] = {};
   // chunk plan: full-size chunks in the middle, a ramp of 1/4- and 1/2-size
   // chunks at both ends -- the first chunk's H2D and the last chunk's kernels
   // + D2H are not overlapped with anything, so smaller end chunks shorten the
@@ -2403,26 +2631,74 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
     char* base = w->chunk[slot];
     char* stg = w->stage[slot];
     if (any_stage) drain(slot);               // the slot's previous chunk is done with staging
+    // the chunk's piecewise-constant columns as runs
+    bool rle[7] = {}, scanned[7] = {};
+    int64_t nrun[7] = {};
+    if (any_rle_cand && rn >= kRleMinRows) {
+      if (rle_inflight[slot]) { cudaEventSynchronize(rle_sent[slot]); rle_inflight[slot] = false; }
+      std::vector<RunScan> jobs;
+      int jcol[7];
+      for (int col = 0; col < 7; ++col) {
+        if (!rle_cand[col]) continue;
+        char* area = w->rle_host[slot] + off_rle[col];
+        jcol[jobs.size()] = col;
+        jobs.push_back({(const char*)c.cols[col].data + r0 * in_sz[col], (int)in_sz[col], rn,
+                        rn / kRleRowsPerRun, (int32_t*)area, area + rle_starts_bytes(cap_rows), -1,
+                        stage_in[col] ? stg + off_in[col] : nullptr});
+        scanned[col] = true;
+      }
+      find_runs_batch(jobs);
+      for (size_t j = 0; j < jobs.size(); ++j) {
+        nrun[jcol[j]] = jobs[j].nr;
+        rle[jcol[j]] = jobs[j].nr > 0;
+      }
+    }
     {                                         // the chunk's pageable input columns, one pool job
       std::vector<CopySeg> segs;
       for (int col = 0; col < 7; ++col)
-        if (c.cols[col].stride != 0 && stage_in[col])
+        if (c.cols[col].stride != 0 && stage_in[col] && !scanned[col])
           segs.push_back({stg + off_in[col], (const char*)c.cols[col].data + r0 * in_sz[col],
                           (size_t)(rn * in_sz[col])});
       par_memcpy_batch(segs);
     }
     void* dev_in[7];
     TR_EV("h2d_start", ci, slot, s);
+    bool any_rle = false;
     for (int col = 0; col < 7; ++col) {
       if (c.cols[col].stride == 0) { dev_in[col] = nullptr; continue; }
       dev_in[col] = base + off_in[col];
+      if (rle[col]) {                         // runs over the link, the column rebuilt in HBM
+        const size_t vat = rle_starts_bytes(cap_rows);
+        const char* hs = w->rle_host[slot] + off_rle[col];
+        char* ds = w->rle_dev[slot] + off_rle[col];
+        const size_t sb = 4 * (size_t)(nrun[col] + 1), vb = in_sz[col] * (size_t)nrun[col];
+        if ((ce = cudaMemcpyAsync(ds, hs, sb, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+            (ce = cudaMemcpyAsync(ds + vat, hs + vat, vb, cudaMemcpyHostToDevice, s)) != cudaSuccess) {
+          cudaEventDestroy(ready);
+          return set_cuda_err(e1, ce);
+        }
+        t_h2d_bytes += (int64_t)(sb + vb);
+        int64_t blocks = (rn + 2047) / 2048;
+        if (blocks > 8 * (int64_t)w->sm_count) blocks = 8 * (int64_t)w->sm_count;
+        if (in_sz[col] == 8)
+          k_expand_runs<uint64_t><<<(unsigned)blocks, 256, 0, s>>>((const int32_t*)ds, (const uint64_t*)(ds + vat),
+                                                                   (int)nrun[col], (uint64_t*)dev_in[col], rn);
+        else
+          k_expand_runs<uint8_t><<<(unsigned)blocks, 256, 0, s>>>((const int32_t*)ds, (const uint8_t*)(ds + vat),
+                                                                  (int)nrun[col], (uint8_t*)dev_in[col], rn);
+        ++t_launches;
+        any_rle = true;
+        continue;
+      }
       const char* src = (const char*)c.cols[col].data + r0 * in_sz[col];
       if (stage_in[col]) src = stg + off_in[col];
       if ((ce = cudaMemcpyAsync(dev_in[col], src, rn * in_sz[col], cudaMemcpyHostToDevice, s)) != cudaSuccess) {
         cudaEventDestroy(ready);
         return set_cuda_err(e1, ce);
       }
+      t_h2d_bytes += rn * (int64_t)in_sz[col];
     }
+    if (any_rle) { cudaEventRecord(rle_sent[slot], s); rle_inflight[slot] = true; }
     KArgs a = base_args(c, w);
     a.flag = make_dflag(c.cols[0], dev_in[0]);
     a.un = make_dcol(c.cols[1], dev_in[1]);
@@ -2537,6 +2813,7 @@ struct ShardOut {
   int64_t exc_row[2];
   int32_t exc_code[2];
   int64_t launches = 0;
+  int64_t h2d_bytes = 0;
 };
 
 thread_local bool t_in_shard = false;
@@ -2550,6 +2827,7 @@ void shard_call(int dev, Call cs, ShardOut* out, bool set_stream = false, void* 
   for (int k = 0; k < FV_NCHECK; ++k) out->check_rows[k] = t_check_rows[k];
   for (int k = 0; k < 2; ++k) { out->exc_row[k] = t_exc_row[k]; out->exc_code[k] = t_exc_code[k]; }
   out->launches = t_launches;
+  out->h2d_bytes = t_h2d_bytes;
 }
 
 void shift_error(fv_error* e, int64_t off) {
@@ -2600,18 +2878,20 @@ int dispatch_sharded(const Call& c, const std::vector<int>& devs, fv_error* e1, 
 int merge_shards(Kind kind, const std::vector<ShardOut>& outs, const std::vector<int64_t>& off, fv_error* e1,
                  fv_error* e2) {
   const int64_t G = (int64_t)outs.size();
-  int64_t launches = 0;
+  int64_t launches = 0, h2d = 0;
   for (int k = 0; k < FV_NCHECK; ++k) t_check_rows[k] = -1;
   for (int k = 0; k < 2; ++k) { t_exc_row[k] = -1; t_exc_code[k] = 0; }
   for (int64_t g = 0; g < G; ++g) {
     const ShardOut& o = outs[g];
     launches += o.launches;
+    h2d += o.h2d_bytes;
     for (int k = 0; k < FV_NCHECK; ++k)
       if (o.check_rows[k] >= 0 && t_check_rows[k] < 0) t_check_rows[k] = o.check_rows[k] + off[g];
     for (int k = 0; k < 2; ++k)
       if (o.exc_row[k] >= 0 && t_exc_row[k] < 0) { t_exc_row[k] = o.exc_row[k] + off[g]; t_exc_code[k] = o.exc_code[k]; }
   }
   t_launches = launches;
+  t_h2d_bytes = h2d;
   // errors: runtime / argument failures first, then the reference's order
   for (int64_t g = 0; g < G; ++g)
     if (outs[g].rc == FV_ERR_CUDA || outs[g].rc == FV_ERR_ARG) {
@@ -2657,6 +2937,7 @@ int merge_shards(Kind kind, const std::vector<ShardOut>& outs, const std::vector
 // For host calls, broadcast columns must be readable on the device.
 int dispatch(Call c, fv_error* e1, fv_error* e2) {
   t_launches = 0;
+  t_h2d_bytes = 0;
   // fv_last_outcome describes THIS call, even when it fails before finish()
   for (int k = 0; k < FV_NCHECK; ++k) t_check_rows[k] = -1;
   for (int k = 0; k < 2; ++k) { t_exc_row[k] = -1; t_exc_code[k] = 0; }
@@ -2762,6 +3043,7 @@ int dispatch(Call c, fv_error* e1, fv_error* e2) {
     // a 1-row batch_iv solving the preceding batch_price's sigma).
     if ((ce = cudaMemcpyAsync(w->scal, tmp, sizeof(tmp), cudaMemcpyHostToDevice, w->streams[0])) != cudaSuccess)
       return set_cuda_err(e1, ce);
+    t_h2d_bytes += (int64_t)sizeof(tmp);
     const int8_t* dflag = (const int8_t*)(w->scal + 7);
     for (int i = 0; i < 7; ++i)
       if (bc[i]) c.cols[i].data = (i == 0) ? (const void*)dflag : (const void*)(w->scal + i);
@@ -2877,6 +3159,7 @@ FV_API int fv_run_shards(int kind, int model, int method, int nshard, const fv_s
   for (int k = 0; k < FV_NCHECK; ++k) t_check_rows[k] = -1;
   for (int k = 0; k < 2; ++k) { t_exc_row[k] = -1; t_exc_code[k] = 0; }
   t_launches = 0;
+  t_h2d_bytes = 0;
   if (kind < FV_KIND_PRICE || kind > FV_KIND_PRICE_IV) return set_arg_err(err1, "unknown call kind");
   if (nshard < 1 || !shards) return set_arg_err(err1, "no shards");
   int have = 0;
@@ -3004,6 +3287,8 @@ FV_API int fv_set_chunk_rows(int64_t rows) {
 }
 
 FV_API int64_t fv_last_launch_count(void) { return t_launches; }
+
+FV_API int64_t fv_last_h2d_bytes(void) { return t_h2d_bytes; }
 
 FV_API int fv_set_round_rows(int64_t lbr_rows, int64_t halley_rows) {
   if (lbr_rows < 0 || halley_rows < 0 || halley_rows > (1ll << 26)) return FV_ERR_ARG;   // int32 queue entries
