@@ -2648,6 +2648,7 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
         scanned[col] = true;
       }
       find_runs_batch(jobs);
+      TR_MARK("runs_scanned");
       for (size_t j = 0; j < jobs.size(); ++j) {
         nrun[jcol[j]] = jobs[j].nr;
         rle[jcol[j]] = jobs[j].nr > 0;

@@ -92,6 +92,24 @@ def main():
                                  st.data_ptr(), None, ep, ei)
             assert rc in (0, 2)
             checked += n
+    # run-length transport: piecewise-constant host columns (flag, S, t, r, q,
+    # sigma) shipped as runs and rebuilt by k_expand_runs, three chunks
+    lib.fv_set_chunk_rows(20_000)
+    n = 60_000
+    fl = np.where(np.arange(n) < 30_000, 1, -1).astype(np.int8)
+    S, r, q = np.full(n, 100.0), np.full(n, 0.01), np.zeros(n)
+    t = np.repeat([0.25, 0.5, 1.0], 20_000)
+    K = 100.0 * np.exp(np.linspace(-0.3, 0.3, n))
+    sg = np.repeat([0.2, 0.35], 30_000)
+    px = O.rows_price("bsm", fl, S, K, t, r, q, sg)["price"]
+    want = O.rows_iv("bsm", "lbr", fl, S, K, t, r, q, px)
+    iv, st = np.empty(n), np.empty(n, np.int8)
+    err = _native.fv_error()
+    assert lib.fv_batch_iv(2, 1, *[_native.col(c) for c in (fl, S, K, t, r, q, px)], n, iv.ctypes.data,
+                           st.ctypes.data, None, err) == 0, err.message
+    assert same(iv, want["iv"]) and same(st, want["status_code"])
+    assert lib.fv_last_h2d_bytes() < n * 17, lib.fv_last_h2d_bytes()      # K and price whole, the rest as runs
+    checked += n
     # host call split into shards; device shards + gather
     _native.set_devices((0, 0))
     lib.fv_set_chunk_rows(1 << 20)
