@@ -232,6 +232,13 @@ FV_API int64_t fv_last_launch_count(void);
  * device-pointer calls. */
 FV_API int64_t fv_last_h2d_bytes(void);
 
+/* The host side of that transport on its own (no device needed): the runs of
+ * data[0, n) (elem 8: 64-bit values compared bit for bit; elem 1: flags) into
+ * starts[0..nr] (starts[nr] = n) and vals[0..nr), on the library's copy
+ * threads.  *nruns = nr, or -1 when the column has more than `budget` runs. */
+FV_API int fv_host_find_runs(const void* data, int elem, int64_t n, int64_t budget, int32_t* starts,
+                             void* vals, int64_t* nruns);
+
 /* Testing knob: rows per LBR classify/solve round and per Halley chunk of
  * one launch (0 = default: 2^27 and 2^26; Halley <= 2^26).  Results do not
  * depend on it; tests force multi-round calls on small batches with it. */

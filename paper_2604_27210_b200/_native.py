@@ -67,6 +67,7 @@ SIGNATURES = {
     "fv_set_chunk_rows": ([_I64], ctypes.c_int),
     "fv_last_launch_count": ([], _I64),
     "fv_last_h2d_bytes": ([], _I64),
+    "fv_host_find_runs": ([_P, ctypes.c_int, _I64, _I64, _P, _P, _P], ctypes.c_int),
     "fv_set_round_rows": ([_I64, _I64], ctypes.c_int),
     "fv_probe_fp64_peak": ([_P, _P], ctypes.c_int),
     "fv_last_outcome": ([_P, _P, _P], ctypes.c_int),

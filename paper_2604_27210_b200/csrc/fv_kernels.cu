@@ -2135,10 +2135,10 @@ class CopyPool {
   }
   int workers() const { return (int)th_.size(); }
   // runs fn(0..parts-1), part 0 on the caller; returns when all are done.
-  // Workers spin for a while after each job and the caller spins on the
-  // completion count before sleeping: a host call hands the pool one job per
-  // chunk, and a futex wake-up (tens of us on the bench boxes) per job and per
-  // join showed up as host-side gaps in the pipeline.
+  // Workers spin (yielding) for a while after each job and the caller spins
+  // on the completion count before sleeping: a host call hands the pool one
+  // job per chunk, and a futex wake-up per job and per join showed up as
+  // host-side gaps in the pipeline.
   void run(int parts, const std::function<void(int)>& fn) {
     std::unique_lock<std::mutex> lk(mu_);
     job_ = &fn;
@@ -2160,11 +2160,10 @@ class CopyPool {
   }
 
  private:
-  static void cpu_relax() {
-#if defined(__x86_64__) || defined(__i386__)
-    __builtin_ia32_pause();
-#endif
-  }
+  // a yielding spin: a pause-only spin starved the calling thread for whole
+  // scheduler slices (~3.5 ms per job) whenever the box had other runnable
+  // threads (tools: the pool harness in profiles/r2/ab_session3.txt item 7)
+  static void cpu_relax() { std::this_thread::yield(); }
   CopyPool() {
     unsigned nt = std::thread::hardware_concurrency();
     if (nt > 16) nt = 16;
@@ -2376,7 +2375,12 @@ void find_runs_batch(std::vector<RunScan>& jobs) {
     for (int k = 0; k < parts; ++k) tasks.push_back({j, r.n * k / parts, r.n * (k + 1) / parts});
   }
   const int nt = (int)tasks.size();
-  std::vector<std::vector<std::pair<int64_t, uint64_t>>> found(nt);
+  // the parts' run lists keep their capacity from call to call: fresh vectors
+  // page-faulted on every call (~0.5 ms per 2.5M-row column that gives up)
+  std::lock_guard<std::mutex> g(g_copy_mu);
+  static std::vector<std::vector<std::pair<int64_t, uint64_t>>> found;
+  if ((int)found.size() < nt) found.resize(nt);
+  for (int t = 0; t < nt; ++t) found[t].clear();
   std::vector<int64_t> counted(nt, 0);
   std::unique_ptr<std::atomic<bool>[]> over(new std::atomic<bool>[jobs.size()]);
   std::unique_ptr<std::atomic<int64_t>[]> total(new std::atomic<int64_t>[jobs.size()]);
@@ -2399,7 +2403,6 @@ void find_runs_batch(std::vector<RunScan>& jobs) {
   if (ntask <= 1) {
     for (int t = 0; t < nt; ++t) run_task(t);
   } else {
-    std::lock_guard<std::mutex> g(g_copy_mu);
     pool.run(ntask, [&](int w) { for (int t = w; t < nt; t += ntask) run_task(t); });
   }
   std::vector<int64_t> exact(jobs.size(), 0);
@@ -2664,33 +2667,28 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
     }
     void* dev_in[7];
     TR_EV("h2d_start", ci, slot, s);
+    // runs first (a few KB), then the streamed columns, then the expansions:
+    // an expansion waits for SMs the previous chunk's kernels still hold, and
+    // a copy queued behind it on this stream would leave the link idle
     bool any_rle = false;
+    const size_t vat = rle_starts_bytes(cap_rows);
     for (int col = 0; col < 7; ++col) {
-      if (c.cols[col].stride == 0) { dev_in[col] = nullptr; continue; }
-      dev_in[col] = base + off_in[col];
-      if (rle[col]) {                         // runs over the link, the column rebuilt in HBM
-        const size_t vat = rle_starts_bytes(cap_rows);
-        const char* hs = w->rle_host[slot] + off_rle[col];
-        char* ds = w->rle_dev[slot] + off_rle[col];
-        const size_t sb = 4 * (size_t)(nrun[col] + 1), vb = in_sz[col] * (size_t)nrun[col];
-        if ((ce = cudaMemcpyAsync(ds, hs, sb, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
-            (ce = cudaMemcpyAsync(ds + vat, hs + vat, vb, cudaMemcpyHostToDevice, s)) != cudaSuccess) {
-          cudaEventDestroy(ready);
-          return set_cuda_err(e1, ce);
-        }
-        t_h2d_bytes += (int64_t)(sb + vb);
-        int64_t blocks = (rn + 2047) / 2048;
-        if (blocks > 8 * (int64_t)w->sm_count) blocks = 8 * (int64_t)w->sm_count;
-        if (in_sz[col] == 8)
-          k_expand_runs<uint64_t><<<(unsigned)blocks, 256, 0, s>>>((const int32_t*)ds, (const uint64_t*)(ds + vat),
-                                                                   (int)nrun[col], (uint64_t*)dev_in[col], rn);
-        else
-          k_expand_runs<uint8_t><<<(unsigned)blocks, 256, 0, s>>>((const int32_t*)ds, (const uint8_t*)(ds + vat),
-                                                                  (int)nrun[col], (uint8_t*)dev_in[col], rn);
-        ++t_launches;
-        any_rle = true;
-        continue;
+      dev_in[col] = c.cols[col].stride == 0 ? nullptr : base + off_in[col];
+      if (!rle[col]) continue;
+      const char* hs = w->rle_host[slot] + off_rle[col];
+      char* ds = w->rle_dev[slot] + off_rle[col];
+      const size_t sb = 4 * (size_t)(nrun[col] + 1), vb = in_sz[col] * (size_t)nrun[col];
+      if ((ce = cudaMemcpyAsync(ds, hs, sb, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+          (ce = cudaMemcpyAsync(ds + vat, hs + vat, vb, cudaMemcpyHostToDevice, s)) != cudaSuccess) {
+        cudaEventDestroy(ready);
+        return set_cuda_err(e1, ce);
       }
+      t_h2d_bytes += (int64_t)(sb + vb);
+      any_rle = true;
+    }
+    if (any_rle) { cudaEventRecord(rle_sent[slot], s); rle_inflight[slot] = true; }
+    for (int col = 0; col < 7; ++col) {
+      if (c.cols[col].stride == 0 || rle[col]) continue;
       const char* src = (const char*)c.cols[col].data + r0 * in_sz[col];
       if (stage_in[col]) src = stg + off_in[col];
       if ((ce = cudaMemcpyAsync(dev_in[col], src, rn * in_sz[col], cudaMemcpyHostToDevice, s)) != cudaSuccess) {
@@ -2699,7 +2697,19 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
       }
       t_h2d_bytes += rn * (int64_t)in_sz[col];
     }
-    if (any_rle) { cudaEventRecord(rle_sent[slot], s); rle_inflight[slot] = true; }
+    for (int col = 0; col < 7; ++col) {
+      if (!rle[col]) continue;
+      const char* ds = w->rle_dev[slot] + off_rle[col];
+      int64_t blocks = (rn + 2047) / 2048;
+      if (blocks > 8 * (int64_t)w->sm_count) blocks = 8 * (int64_t)w->sm_count;
+      if (in_sz[col] == 8)
+        k_expand_runs<uint64_t><<<(unsigned)blocks, 256, 0, s>>>((const int32_t*)ds, (const uint64_t*)(ds + vat),
+                                                                 (int)nrun[col], (uint64_t*)dev_in[col], rn);
+      else
+        k_expand_runs<uint8_t><<<(unsigned)blocks, 256, 0, s>>>((const int32_t*)ds, (const uint8_t*)(ds + vat),
+                                                                (int)nrun[col], (uint8_t*)dev_in[col], rn);
+      ++t_launches;
+    }
     KArgs a = base_args(c, w);
     a.flag = make_dflag(c.cols[0], dev_in[0]);
     a.un = make_dcol(c.cols[1], dev_in[1]);
@@ -3290,6 +3300,17 @@ FV_API int fv_set_chunk_rows(int64_t rows) {
 FV_API int64_t fv_last_launch_count(void) { return t_launches; }
 
 FV_API int64_t fv_last_h2d_bytes(void) { return t_h2d_bytes; }
+
+FV_API int fv_host_find_runs(const void* data, int elem, int64_t n, int64_t budget, int32_t* starts, void* vals,
+                             int64_t* nruns) {
+  if (!data || !starts || !vals || !nruns || (elem != 1 && elem != 8) || n < 1 || n >= ((int64_t)1 << 31))
+    return FV_ERR_ARG;
+  std::vector<RunScan> jobs(1);
+  jobs[0] = {data, elem, n, budget, starts, vals, -1, nullptr};
+  find_runs_batch(jobs);
+  *nruns = jobs[0].nr;
+  return FV_OK;
+}
 
 FV_API int fv_set_round_rows(int64_t lbr_rows, int64_t halley_rows) {
   if (lbr_rows < 0 || halley_rows < 0 || halley_rows > (1ll << 26)) return FV_ERR_ARG;   // int32 queue entries

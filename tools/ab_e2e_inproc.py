@@ -1,0 +1,91 @@
+#!/usr/bin/env python3
+"""e2e A/B of several builds of the library IN ONE PROCESS: each
+variants/lib_*.so is loaded with its own ctypes handle (RTLD_LOCAL), the
+workload's pinned host buffers are made once, and the builds' host-buffer
+C-ABI calls alternate round by round, so box-to-box and drift noise cancel.
+Prints the median and min call time per build and workload.
+
+    python tools/ab_e2e_inproc.py [workloads...]     (default: c4 c5 c1 c2 c3 rt)
+"""
+import ctypes
+import glob
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+import bench  # noqa: E402
+from paper_2604_27210_b200 import _native  # noqa: E402
+
+
+def load(path):
+    lib = ctypes.CDLL(path)
+    for name, (args, res) in _native.SIGNATURES.items():
+        fn = getattr(lib, name, None)
+        if fn is not None:
+            fn.argtypes, fn.restype = args, res
+    return lib
+
+
+def main():
+    wls = sys.argv[1:] or ["c4", "c5", "c1", "c2", "c3", "rt"]
+    paths = sorted(glob.glob(os.path.join(REPO, "variants", "lib_*.so")))
+    libs = [(os.path.basename(p)[4:-3], load(p)) for p in paths]
+    ref = _native.lib_for_compute()
+    dev = torch.device("cuda", 0)
+    for wl in wls:
+        model, method, roundtrip = bench.workload_call(wl)
+        if wl == "c4":
+            n = 100_000_000
+            cols = bench.c4_device(n, 0, dev)
+        else:
+            n = bench.default_rows(wl)
+            cols = bench.draws_device(wl, n, 0, dev)
+        last = "sigma"
+        if method >= 0 and not roundtrip:
+            cols["price"] = bench.price_on_device(ref, model, cols, n)
+            last = "price"
+        h = {k: (v.cpu().pin_memory() if v.numel() > 1 else v.cpu()) for k, v in cols.items() if torch.is_tensor(v)}
+        del cols
+        torch.cuda.empty_cache()
+        hn = bench.native_cols(h, last)
+        outs = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(6 if method < 0 else 2)]
+        st = torch.empty(n, dtype=torch.int8).pin_memory()
+
+        def call(lib):
+            e1, e2 = _native.fv_error(), _native.fv_error()
+            if roundtrip:
+                rc = lib.fv_price_iv(model, method, *hn, n, outs[0].data_ptr(), outs[1].data_ptr(), st.data_ptr(),
+                                     None, e1, e2)
+            elif method >= 0:
+                rc = lib.fv_batch_iv(model, method, *hn, n, outs[0].data_ptr(), st.data_ptr(), None, e1)
+            else:
+                rc = lib.fv_price_greeks(model, *hn, n, *[o.data_ptr() for o in outs], st.data_ptr(), e1, e2)
+            if rc not in (0,):
+                raise RuntimeError(e1.message)
+
+        times = {name: [] for name, _ in libs}
+        for name, lib in libs:
+            call(lib)
+        rounds = 6 if wl == "c4" else 15
+        for r in range(rounds):
+            order = libs if r % 2 == 0 else libs[::-1]
+            for name, lib in order:
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                call(lib)
+                times[name].append(time.perf_counter() - t0)
+        for name, _ in libs:
+            ts = np.array(times[name])
+            print("%-3s %-10s e2e median %.3f G/s (%.2f ms)  best %.3f G/s" %
+                  (wl, name, n / np.median(ts) / 1e9, 1e3 * np.median(ts), n / ts.min() / 1e9), flush=True)
+        del h, hn, outs, st
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
