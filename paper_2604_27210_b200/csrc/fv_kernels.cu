@@ -2264,6 +2264,11 @@ std::vector<std::pair<int64_t, int64_t>> chunk_plan(int64_t n, int64_t chunk) {
 #define FV_HOST_RLE 1
 #endif
 const int64_t kRleRowsPerRun = 64;
+// pageable columns: staging copy made in the scan's pass (1) or after it, for
+// the columns that did not go as runs (0)
+#ifndef FV_SCAN_COPY
+#define FV_SCAN_COPY 0
+#endif
 const int64_t kRleMinRows = 1 << 14;
 
 // bytes of one column's runs area for a chunk of `rows` rows: int32 starts
@@ -2647,7 +2652,7 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
         jcol[jobs.size()] = col;
         jobs.push_back({(const char*)c.cols[col].data + r0 * in_sz[col], (int)in_sz[col], rn,
                         rn / kRleRowsPerRun, (int32_t*)area, area + rle_starts_bytes(cap_rows), -1,
-                        stage_in[col] ? stg + off_in[col] : nullptr});
+                        (FV_SCAN_COPY && stage_in[col]) ? stg + off_in[col] : nullptr});
         scanned[col] = true;
       }
       find_runs_batch(jobs);
@@ -2660,7 +2665,7 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
     {                                         // the chunk's pageable input columns, one pool job
       std::vector<CopySeg> segs;
       for (int col = 0; col < 7; ++col)
-        if (c.cols[col].stride != 0 && stage_in[col] && !scanned[col])
+        if (c.cols[col].stride != 0 && stage_in[col] && !(FV_SCAN_COPY ? scanned[col] : rle[col]))
           segs.push_back({stg + off_in[col], (const char*)c.cols[col].data + r0 * in_sz[col],
                           (size_t)(rn * in_sz[col])});
       par_memcpy_batch(segs);
