@@ -5,7 +5,7 @@ workload's pinned host buffers are made once, and the builds' host-buffer
 C-ABI calls alternate round by round, so box-to-box and drift noise cancel.
 Prints the median and min call time per build and workload.
 
-    python tools/ab_e2e_inproc.py [workloads...]     (default: c4 c5 c1 c2 c3 rt)
+    [AB_LIBS=a,b] python tools/ab_e2e_inproc.py [workloads...]     (default: c4 c5 c1 c2 c3 rt)
 """
 import ctypes
 import glob
@@ -34,6 +34,8 @@ def load(path):
 def main():
     wls = sys.argv[1:] or ["c4", "c5", "c1", "c2", "c3", "rt"]
     paths = sorted(glob.glob(os.path.join(REPO, "variants", "lib_*.so")))
+    if os.environ.get("AB_LIBS"):                     # e.g. AB_LIBS=a,b: only variants/lib_a.so, lib_b.so
+        paths = [os.path.join(REPO, "variants", "lib_%s.so" % x) for x in os.environ["AB_LIBS"].split(",")]
     libs = [(os.path.basename(p)[4:-3], load(p)) for p in paths]
     ref = _native.lib_for_compute()
     dev = torch.device("cuda", 0)
