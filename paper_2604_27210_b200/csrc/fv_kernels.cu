@@ -30,7 +30,9 @@
 //     copies) so copies overlap compute.
 // All arithmetic is bit-faithful to the reference; compile with -fmad=false.
 #include <cuda_runtime.h>
+#include <sched.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -2164,9 +2166,22 @@ class CopyPool {
   // scheduler slices (~3.5 ms per job) whenever the box had other runnable
   // threads (tools: the pool harness in profiles/r2/ab_session3.txt item 7)
   static void cpu_relax() { std::this_thread::yield(); }
-  CopyPool() {
+  // threads: the cores this process may run on (its affinity mask, not the
+  // machine's count), shared with the other ranks on this host when launched
+  // one process per GPU (LOCAL_WORLD_SIZE, set by torchrun), at most 16
+  static unsigned host_threads() {
     unsigned nt = std::thread::hardware_concurrency();
-    if (nt > 16) nt = 16;
+    cpu_set_t set;
+    if (sched_getaffinity(0, sizeof(set), &set) == 0 && CPU_COUNT(&set) > 0) nt = (unsigned)CPU_COUNT(&set);
+    if (const char* e = getenv("LOCAL_WORLD_SIZE")) {
+      const long k = atol(e);
+      if (k > 1) nt = nt / (unsigned)k;
+    }
+    if (nt < 2) nt = 2;
+    return nt > 16 ? 16 : nt;
+  }
+  CopyPool() {
+    const unsigned nt = host_threads();
     for (unsigned k = 1; k < nt; ++k) th_.emplace_back([this] { loop(); });
   }
   void loop() {
