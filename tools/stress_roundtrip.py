@@ -1,3 +1,6 @@
+"""Repeat tests/test_price_iv.py::test_round_trip_exceptions_match_two_calls N times
+(python tools/stress_roundtrip.py [N]) and count failures: the flake hunt behind the
+broadcast-scalar ordering fix (profiles/README.md, r2f)."""
 import sys, os, time
 sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
 import paper_2604_27210_b200 as fv
