@@ -190,3 +190,33 @@ def test_random_columns_fall_back(lib):
     for a, b in zip(got[2], want[2]):
         assert_bits(a, b, "random columns")
     assert got[3] >= n * (1 + 6 * 8)
+
+
+def test_concurrent_host_calls_with_runs(lib):
+    """Host calls from several threads at once (the C ABI releases the GIL via
+    ctypes): run scans share the copy pool and its reused buffers, so every
+    thread's result must still match its own device-resident call."""
+    import threading
+    n = 400_000
+    results = {}
+
+    def work(k):
+        flag, t, K, rng = _chain(n, 100 + k, t_run=4_000 + 1_000 * k)
+        S, r, q = np.full(1, 100.0), np.full(n, 0.01 * k), np.zeros(1)
+        sig = np.repeat(rng.uniform(0.1, 0.5, n // 8_000 + 1), 8_000)[:n]
+        cols = [flag, S, K, t, r, q, sig]
+        want = _call(lib, "pg", cols, n, host=False)
+        got = [_call(lib, "pg", cols, n, host=True) for _ in range(3)]
+        results[k] = (want, got)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert len(results) == 4
+    for k, (want, got) in results.items():
+        for g in got:
+            assert g[0] == want[0] == 0
+            for a, b in zip(g[2], want[2]):
+                assert_bits(a, b, "thread %d" % k)
