@@ -37,6 +37,13 @@ def main():
     if os.environ.get("AB_LIBS"):                     # e.g. AB_LIBS=a,b: only variants/lib_a.so, lib_b.so
         paths = [os.path.join(REPO, "variants", "lib_%s.so" % x) for x in os.environ["AB_LIBS"].split(",")]
     libs = [(os.path.basename(p)[4:-3], load(p)) for p in paths]
+    # AB_CHUNKS=name:rows,...: a build's host-pipeline chunk rows (copies of one .so
+    # under several names keep separate settings)
+    for spec in filter(None, os.environ.get("AB_CHUNKS", "").split(",")):
+        name, rows = spec.split(":")
+        for nm, lib in libs:
+            if nm == name:
+                lib.fv_set_chunk_rows(int(rows))
     ref = _native.lib_for_compute()
     dev = torch.device("cuda", 0)
     for wl in wls:
