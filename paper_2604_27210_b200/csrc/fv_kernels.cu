@@ -1489,6 +1489,7 @@ struct DevWork {
   cudaEvent_t fork2_ev[FV_NSLOT] = {}, join2_ev[FV_NSLOT] = {};   // LBR far-high solve
   FvDevStatus* st = nullptr;            // device, [2]: call (or price stage), IV stage of fv_price_iv
   FvDevStatus* st_host = nullptr;       // pinned mirror [2]
+  bool st_armed = false;                // st holds the all-ones "nothing failed" state
   // chunk buffers for host-pointer calls
   char* chunk[FV_NSLOT] = {};
   int64_t chunk_cap_rows[FV_NSLOT] = {};
@@ -2084,6 +2085,37 @@ KArgs base_args(const Call& c, DevWork* w) {
 }
 
 
+// A call's outcome block: every pass folds its first failing rows into w->st
+// (atomicMin on all-ones), and the call reads it back at the end.
+// FV_STATUS_KERNEL: one warp copies the block into the pinned host mirror
+// through its UVA address and re-arms it for the next call (which then skips
+// its reset), instead of a D2H copy at the end and a memset at the start.
+#ifndef FV_STATUS_KERNEL
+#define FV_STATUS_KERNEL 1
+#endif
+__global__ void k_publish_status(unsigned long long* st, unsigned long long* host) {
+  constexpr int kWords = (int)(2 * sizeof(FvDevStatus) / 8);
+  for (int i = threadIdx.x; i < kWords; i += blockDim.x) {
+    host[i] = st[i];
+    st[i] = ~0ull;
+  }
+}
+cudaError_t arm_status(DevWork* w, cudaStream_t s) {
+  cudaError_t ce = cudaSuccess;
+  if (!(FV_STATUS_KERNEL && w->st_armed)) ce = cudaMemsetAsync(w->st, 0xff, 2 * sizeof(FvDevStatus), s);
+  w->st_armed = false;                     // re-armed only by a call that completes
+  return ce;
+}
+cudaError_t read_status(DevWork* w, cudaStream_t s) {
+#if FV_STATUS_KERNEL
+  k_publish_status<<<1, 32, 0, s>>>((unsigned long long*)w->st, (unsigned long long*)w->st_host);
+  ++t_launches;
+  return cudaGetLastError();
+#else
+  return cudaMemcpyAsync(w->st_host, w->st, 2 * sizeof(FvDevStatus), cudaMemcpyDeviceToHost, s);
+#endif
+}
+
 int run_device(DevWork* w, const Call& c, cudaStream_t s, uint32_t bcast_bits, fv_error* e1,
                fv_error* e2) {
   cudaError_t ce;
@@ -2105,12 +2137,12 @@ int run_device(DevWork* w, const Call& c, cudaStream_t s, uint32_t bcast_bits, f
     cudaEventCreate(&sp1);
     cudaEventRecord(sp0, s);
   }
-  if ((ce = cudaMemsetAsync(w->st, 0xff, 2 * sizeof(FvDevStatus), s)) != cudaSuccess) return set_cuda_err(e1, ce);
+  if ((ce = arm_status(w, s)) != cudaSuccess) return set_cuda_err(e1, ce);
   if ((ce = launch(w, c, a, 0, s)) != cudaSuccess) return set_cuda_err(e1, ce);
   if (t_span) cudaEventRecord(sp1, s);
-  if ((ce = cudaMemcpyAsync(w->st_host, w->st, 2 * sizeof(FvDevStatus), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-    return set_cuda_err(e1, ce);
+  if ((ce = read_status(w, s)) != cudaSuccess) return set_cuda_err(e1, ce);
   if ((ce = cudaStreamSynchronize(s)) != cudaSuccess) return set_cuda_err(e1, ce);
+  w->st_armed = true;
   if (t_span) {
     t_span_ms = -1.0f;
     cudaEventElapsedTime(&t_span_ms, sp0, sp1);
@@ -2636,8 +2668,7 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
     par_memcpy_batch(segs);
     slot_chunk[s] = -1;
   };
-  if ((ce = cudaMemsetAsync(w->st, 0xff, 2 * sizeof(FvDevStatus), w->streams[0])) != cudaSuccess)
-    return set_cuda_err(e1, ce);
+  if ((ce = arm_status(w, w->streams[0])) != cudaSuccess) return set_cuda_err(e1, ce);
   cudaEvent_t ready;
   cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
   cudaEventRecord(ready, w->streams[0]);
@@ -2770,12 +2801,12 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
   }
   cudaEventDestroy(ready);
   cudaStream_t s0 = w->streams[0];
-  if ((ce = cudaMemcpyAsync(w->st_host, w->st, 2 * sizeof(FvDevStatus), cudaMemcpyDeviceToHost, s0)) != cudaSuccess)
-    return set_cuda_err(e1, ce);
+  if ((ce = read_status(w, s0)) != cudaSuccess) return set_cuda_err(e1, ce);
   if ((ce = cudaStreamSynchronize(s0)) != cudaSuccess) return set_cuda_err(e1, ce);
   for (int s = 1; s < FV_NSLOT; ++s)
     if ((ce = cudaStreamSynchronize(w->streams[s])) != cudaSuccess) return set_cuda_err(e1, ce);
   if ((ce = cudaGetLastError()) != cudaSuccess) return set_cuda_err(e1, ce);
+  w->st_armed = true;
   TR_MARK("synced");
   // exceptions in later chunks: the explain kernel needs that chunk's inputs;
   // re-stage the offending row alone (fv_price_iv: the IV stage's row, its
