@@ -1422,6 +1422,17 @@ thread_local cudaStream_t t_user_stream = nullptr;
 thread_local bool t_user_stream_set = false;   // fv_set_stream called (NULL = legacy default stream)
 thread_local int64_t t_launches = 0;
 thread_local int64_t t_h2d_bytes = 0;       // host calls: bytes this thread's last call moved host -> device
+#ifndef FV_CALL_TRACE
+#define FV_CALL_TRACE 0
+#endif
+#if FV_CALL_TRACE
+thread_local std::chrono::steady_clock::time_point t_ct0;
+thread_local double t_ct[16];
+thread_local int t_ctn = 0;
+#define CT_MARK() do { if (t_ctn < 16) t_ct[t_ctn++] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_ct0).count(); } while (0)
+#else
+#define CT_MARK() ((void)0)
+#endif
 
 // Optional per-kernel timing (fv_set_kernel_timing): CUDA events around every
 // launch on the launching stream, summed per kernel by fv_kernel_times.
@@ -2137,11 +2148,15 @@ int run_device(DevWork* w, const Call& c, cudaStream_t s, uint32_t bcast_bits, f
     cudaEventCreate(&sp1);
     cudaEventRecord(sp0, s);
   }
+  CT_MARK();                                   // [2] run_device entered
   if ((ce = arm_status(w, s)) != cudaSuccess) return set_cuda_err(e1, ce);
   if ((ce = launch(w, c, a, 0, s)) != cudaSuccess) return set_cuda_err(e1, ce);
+  CT_MARK();                                   // [3] kernels launched
   if (t_span) cudaEventRecord(sp1, s);
   if ((ce = read_status(w, s)) != cudaSuccess) return set_cuda_err(e1, ce);
+  CT_MARK();                                   // [4] status kernel launched
   if ((ce = cudaStreamSynchronize(s)) != cudaSuccess) return set_cuda_err(e1, ce);
+  CT_MARK();                                   // [5] synchronised
   w->st_armed = true;
   if (t_span) {
     t_span_ms = -1.0f;
@@ -2998,6 +3013,10 @@ int merge_shards(Kind kind, const std::vector<ShardOut>& outs, const std::vector
 
 // For host calls, broadcast columns must be readable on the device.
 int dispatch(Call c, fv_error* e1, fv_error* e2) {
+#if FV_CALL_TRACE
+  t_ct0 = std::chrono::steady_clock::now();
+  t_ctn = 0;
+#endif
   t_launches = 0;
   t_h2d_bytes = 0;
   // fv_last_outcome describes THIS call, even when it fails before finish()
@@ -3060,10 +3079,12 @@ int dispatch(Call c, fv_error* e1, fv_error* e2) {
     std::vector<int> devs = devices_for_host_calls();
     if (devs.size() > 1 && c.n >= (int64_t)devs.size() * kMinShardRows) return dispatch_sharded(c, devs, e1, e2);
   }
+  CT_MARK();                                   // [0] pointer classification done
   DevWork* w = nullptr;
   cudaError_t ce = get_work(&w);
   if (ce != cudaSuccess) return set_cuda_err(e1, ce);
   std::lock_guard<std::mutex> g(w->mu);
+  CT_MARK();                                   // [1] work + lock
   // broadcast scalars of a host call: checked once on the host and copied
   // into the device's scalar slot.  A device call does not read them back
   // (a synchronous device -> host copy per column, ~10 us each, before any
@@ -3351,6 +3372,14 @@ FV_API int fv_set_chunk_rows(int64_t rows) {
 FV_API int64_t fv_last_launch_count(void) { return t_launches; }
 
 FV_API int64_t fv_last_h2d_bytes(void) { return t_h2d_bytes; }
+
+#if FV_CALL_TRACE
+// diagnostic builds only: the last device call's host-side stage timestamps (us)
+FV_API int fv_call_trace(double* out, int cap) {
+  for (int i = 0; i < t_ctn && i < cap; ++i) out[i] = t_ct[i];
+  return t_ctn;
+}
+#endif
 
 FV_API int fv_host_find_runs(const void* data, int elem, int64_t n, int64_t budget, int32_t* starts, void* vals,
                              int64_t* nruns) {
