@@ -39,7 +39,9 @@
 
 namespace {
 
-const int64_t kRowsPerThread = 1 << 20;
+// rows per host thread: a thread costs ~30-50 us to start, a row ~1-3 ns, so
+// a 1M-row column (the reference bench harness's size) already splits 8 ways
+const int64_t kRowsPerThread = 1 << 17;
 
 template <class F>
 void par_rows(int64_t n, F fn) {
@@ -77,6 +79,21 @@ PyObject* parse_flags_u(PyObject*, PyObject* args) {
   Py_BEGIN_ALLOW_THREADS
   par_rows(n, [&](int k, int64_t a, int64_t b) {
     int64_t bad = -1;
+    if (width == 1) {                          // 'U1': a branch-free pass, then the first bad row if any
+      uint32_t any_bad = 0;
+      for (int64_t i = a; i < b; ++i) {
+        const uint32_t low = cp[i] | 0x20u;
+        o[i] = (int8_t)(low == 0x63u ? 1 : -1);
+        any_bad |= (uint32_t)(low != 0x63u) & (uint32_t)(low != 0x70u);
+      }
+      if (any_bad)
+        for (int64_t i = a; i < b; ++i) {
+          const uint32_t low = cp[i] | 0x20u;
+          if (low != 0x63u && low != 0x70u) { bad = i; break; }
+        }
+      first[k] = bad;
+      return;
+    }
     for (int64_t i = a; i < b; ++i) {
       const uint32_t* e = cp + i * width;
       const uint32_t low = e[0] | 0x20u;

@@ -2508,6 +2508,9 @@ bool is_pageable(const void* p) {
 #ifndef FV_HOST_AUTO_CHUNK
 #define FV_HOST_AUTO_CHUNK 1
 #endif
+#ifndef FV_CAP_BY_CALL
+#define FV_CAP_BY_CALL 0
+#endif
 #ifndef FV_HOST_CHUNK_DIV
 #define FV_HOST_CHUNK_DIV 8
 #endif
@@ -2598,7 +2601,11 @@ int run_host(DevWork* w, const Call& c, uint32_t bcast_bits, fv_error* e1, fv_er
   // for the three staging slots of 2^22 rows)
   // (sized for the configured chunk, so smaller auto-sized chunks of a
   // mid-size call never shrink the buffers a large call needs)
+#if FV_CAP_BY_CALL
+  const int64_t cap_rows = chunk;
+#else
   const int64_t cap_rows = g_chunk_rows > chunk ? g_chunk_rows : chunk;
+#endif
   const size_t max_slot = align(cap_rows) + 6 * align(8 * cap_rows) + 6 * align(8 * cap_rows) + 2 * align(cap_rows);
   for (int s = 0; s < FV_NSLOT; ++s) {
     if (w->chunk_cap_rows[s] < (int64_t)slot_bytes) {
