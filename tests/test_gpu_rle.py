@@ -220,3 +220,31 @@ def test_concurrent_host_calls_with_runs(lib):
             assert g[0] == want[0] == 0
             for a, b in zip(g[2], want[2]):
                 assert_bits(a, b, "thread %d" % k)
+
+
+def test_outcome_block_rearmed_between_calls(lib):
+    """The call's outcome block is read back and re-armed in place by the last
+    kernel of each call (k_publish_status): a call that fails validation, or
+    raises mid-batch, must not leak its failing rows into the next call's
+    outcome -- alternate failing and clean calls on device and host pointers."""
+    from paper_2604_27210_b200 import _native
+    n = 50_000
+    rng = np.random.default_rng(9)
+    flag = np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8)
+    S, r, q = np.full(n, 100.0), np.full(n, 0.01), np.zeros(n)
+    K = 100.0 * np.exp(rng.uniform(-0.3, 0.3, n))
+    t = rng.uniform(0.1, 2.0, n)
+    sig = rng.uniform(0.1, 0.6, n)
+    bad_sig = sig.copy()
+    bad_sig[31_337] = -1.0                                  # DomainError: negative sigma at row 31337
+    clean = [flag, S, K, t, r, q, sig]
+    broken = [flag, S, K, t, r, q, bad_sig]
+    want = _call(lib, "pg", clean, n, host=False)
+    assert want[0] == 0
+    for host in (False, True, False, True):
+        b = _call(lib, "pg", broken, n, host=host)
+        assert b[0] == _native.FV_ERR_BATCH and b[1][2] == 31_337, b[1]
+        g = _call(lib, "pg", clean, n, host=host)
+        assert g[0] == 0 and g[1][0] == 0, g[1]
+        for a, w in zip(g[2], want[2]):
+            assert_bits(a, w, "clean call after a failing one (host=%s)" % host)
