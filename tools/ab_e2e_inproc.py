@@ -58,12 +58,17 @@ def main():
         if method >= 0 and not roundtrip:
             cols["price"] = bench.price_on_device(ref, model, cols, n)
             last = "price"
-        h = {k: (v.cpu().pin_memory() if v.numel() > 1 else v.cpu()) for k, v in cols.items() if torch.is_tensor(v)}
+        pin = not os.environ.get("AB_PAGEABLE")         # AB_PAGEABLE=1: pageable host buffers
+        h = {k: (v.cpu().pin_memory() if (v.numel() > 1 and pin) else v.cpu()) for k, v in cols.items()
+             if torch.is_tensor(v)}
         del cols
         torch.cuda.empty_cache()
         hn = bench.native_cols(h, last)
-        outs = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(6 if method < 0 else 2)]
-        st = torch.empty(n, dtype=torch.int8).pin_memory()
+        outs = [torch.empty(n, dtype=torch.float64) for _ in range(6 if method < 0 else 2)]
+        st = torch.empty(n, dtype=torch.int8)
+        if pin:
+            outs = [o.pin_memory() for o in outs]
+            st = st.pin_memory()
 
         def call(lib):
             e1, e2 = _native.fv_error(), _native.fv_error()
